@@ -1,0 +1,143 @@
+"""ctypes binding of libgpuim.so (include/gpuim.h).
+
+The product path has no CPU fallback: if the shared library is missing or a
+call fails, this module raises.  Build with `python -m paper_2510_12196_b200.build`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libgpuim.so"
+MAX_LEVELS = 8
+
+GIM_OK = 0
+GIM_E_INVALID = 1
+GIM_E_CUDA = 2
+GIM_E_UNSUPPORTED = 3
+GIM_E_OVERFLOW = 4
+GIM_E_INTERNAL = 5
+GIM_E_EMPTY = 6
+
+
+class GimGraph(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32),
+        ("m2", C.c_int64),
+        ("offsets", C.c_void_p),
+        ("targets", C.c_void_p),
+        ("weights", C.c_void_p),
+        ("vweights", C.c_void_p),
+        ("sources", C.c_void_p),
+    ]
+
+
+class GimTopology(C.Structure):
+    _fields_ = [
+        ("levels", C.c_int32),
+        ("hierarchy", C.c_int64 * MAX_LEVELS),
+        ("distances", C.c_int64 * MAX_LEVELS),
+    ]
+
+
+class GimImParams(C.Structure):
+    _fields_ = [
+        ("coarsest_factor", C.c_int64),
+        ("phi", C.c_double),
+        ("rho", C.c_int32),
+        ("filter_mode", C.c_int32),
+        ("jet_filter_c", C.c_double),
+        ("sigma_coarse", C.c_double),
+        ("sigma_fine", C.c_double),
+        ("iw_max_finest", C.c_int32),
+    ]
+
+
+class GimImStats(C.Structure):
+    _fields_ = [
+        ("n_levels", C.c_int32),
+        ("level_n", C.c_int64 * 64),
+        ("level_m2", C.c_int64 * 64),
+        ("refine_iterations", C.c_int64),
+        ("lp_passes", C.c_int64),
+        ("weak_passes", C.c_int64),
+        ("strong_passes", C.c_int64),
+        ("init_refine_iterations", C.c_int64),
+        ("partitioner_calls", C.c_int64),
+        ("kernel_launches", C.c_int64),
+        ("final_j", C.c_int64),
+        ("max_block_weight", C.c_int64),
+        ("l_max", C.c_double),
+        ("ms_coarsen", C.c_double),
+        ("ms_initial", C.c_double),
+        ("ms_refine", C.c_double),
+        ("ms_total", C.c_double),
+    ]
+
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+U64 = C.c_uint64
+DBL = C.c_double
+GP = C.POINTER(GimGraph)
+TP = C.POINTER(GimTopology)
+
+# name -> argtypes; every symbol declared in include/gpuim.h appears here
+SIGNATURES: dict[str, list] = {
+    "gim_version": [],
+    "gim_last_error": [],
+    "gim_total_cost": [GP, P, TP, P, P],
+    "gim_block_weights": [GP, P, I32, P, P],
+}
+
+_lib = None
+
+
+class GimError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libgpuim error {status}: {msg}")
+        self.status = status
+
+
+def load():
+    """Load libgpuim.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2510_12196_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL if hasattr(os, "RTLD_LOCAL") else 0)
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = C.c_char_p if name == "gim_last_error" else C.c_int
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != GIM_OK:
+        msg = load().gim_last_error()
+        msg = msg.decode() if msg else ""
+        if status == GIM_E_EMPTY:
+            raise ValueError(msg)
+        raise GimError(status, msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+def topology_struct(hierarchy, distances) -> GimTopology:
+    if len(hierarchy) > MAX_LEVELS:
+        raise ValueError(f"at most {MAX_LEVELS} hierarchy levels are supported")
+    t = GimTopology()
+    t.levels = len(hierarchy)
+    for i, (a, d) in enumerate(zip(hierarchy, distances)):
+        t.hierarchy[i] = int(a)
+        t.distances[i] = int(d)
+    return t

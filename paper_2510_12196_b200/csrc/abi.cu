@@ -1,0 +1,120 @@
+// Library-level plumbing: error state, memory pool, topology upload.
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <map>
+#include <mutex>
+
+namespace gim {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void* dmalloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes == 0) return nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess)
+    throw Error{GIM_E_CUDA, std::string("cudaMallocAsync(") + std::to_string(bytes) +
+                                ") failed: " + cudaGetErrorString(e)};
+  return p;
+}
+
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);  // never throws from a destructor
+}
+
+static std::mutex g_topo_mu;
+static std::map<std::vector<long long>, Topo> g_topo_cache;
+
+Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances) {
+  GIM_CHECK(levels >= 1 && levels <= GIM_MAX_LEVELS, GIM_E_INVALID,
+            "hierarchy must have 1.." + std::to_string(GIM_MAX_LEVELS) + " levels");
+  std::vector<long long> key;
+  long long k = 1;
+  for (int i = 0; i < levels; ++i) {
+    GIM_CHECK(hierarchy[i] >= 1, GIM_E_INVALID, "hierarchy factors must be >= 1");
+    GIM_CHECK(distances[i] >= 0, GIM_E_INVALID, "distances must be nonnegative");
+    if (i) GIM_CHECK(distances[i] >= distances[i - 1], GIM_E_INVALID,
+                     "distances must be nondecreasing");
+    k *= hierarchy[i];
+    GIM_CHECK(k < (1ll << 30), GIM_E_OVERFLOW, "k too large for int32 block ids");
+    key.push_back(hierarchy[i]);
+    key.push_back(distances[i]);
+  }
+  std::lock_guard<std::mutex> lk(g_topo_mu);
+  auto it = g_topo_cache.find(key);
+  if (it != g_topo_cache.end()) return it->second;
+  // bit field layout: level 0 (least significant digit) in the low bits
+  int shift[GIM_MAX_LEVELS];
+  int bits = 0;
+  std::vector<long long> dbit(64, 0);
+  for (int i = 0; i < levels; ++i) {
+    int wdt = 0;
+    while ((1ll << wdt) < hierarchy[i]) ++wdt;
+    shift[i] = bits;
+    for (int b = bits; b < bits + wdt && b < 64; ++b) dbit[b] = distances[i];
+    bits += wdt;
+  }
+  GIM_CHECK(bits <= 64, GIM_E_UNSUPPORTED, "hierarchy digit codes exceed 64 bits");
+  std::vector<unsigned long long> code((size_t)k);
+  for (long long b = 0; b < k; ++b) {
+    long long x = b;
+    unsigned long long c = 0;
+    for (int i = 0; i < levels; ++i) {
+      c |= (unsigned long long)(x % hierarchy[i]) << shift[i];
+      x /= hierarchy[i];
+    }
+    code[(size_t)b] = c;
+  }
+  void* p = nullptr;
+  size_t bytes = sizeof(unsigned long long) * (size_t)k + sizeof(long long) * 64;
+  GIM_CUDA(cudaMalloc(&p, bytes));
+  GIM_CUDA(cudaMemcpy(p, code.data(), sizeof(unsigned long long) * (size_t)k,
+                      cudaMemcpyHostToDevice));
+  GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + sizeof(unsigned long long) * (size_t)k,
+                      dbit.data(), sizeof(long long) * 64, cudaMemcpyHostToDevice));
+  Topo t;
+  t.L = levels;
+  t.k = (int)k;
+  t.code = static_cast<const unsigned long long*>(p);
+  t.dbit = reinterpret_cast<const long long*>(static_cast<char*>(p) +
+                                              sizeof(unsigned long long) * (size_t)k);
+  g_topo_cache.emplace(key, t);
+  return t;
+}
+
+Topo get_flat_topo(int k) {
+  int64_t h[1] = {k}, d[1] = {1};
+  return get_topo(1, h, d);
+}
+
+// one-time pool configuration: keep freed blocks cached (no OS round trips
+// between refinement iterations / levels)
+static void configure_pool_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
+static thread_local long long g_launches = 0;
+void count_launch(long long n) { g_launches += n; }
+long long launches() { return g_launches; }
+void reset_launches() { g_launches = 0; }
+
+}  // namespace gim
+
+extern "C" int gim_version(void) {
+  gim::configure_pool_once();
+  return 1;
+}
+
+extern "C" const char* gim_last_error(void) { return gim::last_error(); }

@@ -1,0 +1,187 @@
+// Shared device/host helpers for libgpuim (GPU-IM on sm_100a).
+//
+// Device layout: every CSR level lives in HBM as int32
+// offsets/targets/weights/vertex weights plus an int32 edge-source array
+// (the reference's `edge_sources`, graph.py:25-38 / PAPER.md:411-418).
+// Block ids are int32, block weights / gains / J are int64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/gpuim.h"
+
+namespace gim {
+
+// ---------------------------------------------------------------------------
+// error state (thread-local string + status codes from gpuim.h)
+
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define GIM_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      throw ::gim::Error{GIM_E_CUDA, std::string(#call) + ": " +              \
+                                         cudaGetErrorString(_e) + " @" +      \
+                                         __FILE__ + ":" +                     \
+                                         std::to_string(__LINE__)};           \
+  } while (0)
+
+#define GIM_CHECK(cond, code, msg)                                            \
+  do {                                                                        \
+    if (!(cond)) throw ::gim::Error{(code), (msg)};                           \
+  } while (0)
+
+#define GIM_LAUNCH_CHECK() GIM_CUDA(cudaGetLastError())
+
+// run `body` translating exceptions to a status code (C-ABI boundary)
+template <class F>
+int guard(F&& body) {
+  try {
+    body();
+    return GIM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal error: ") + e.what());
+    return GIM_E_INTERNAL;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// topology: D[x,y] from mixed-radix digits, no k x k matrix
+// (topology.py:112-129: d_j for the highest differing digit j, 0 if x == y)
+
+// Each block id b gets a 64-bit "digit code": its mixed-radix digits packed
+// into fixed bit fields, highest hierarchy level in the most significant
+// field.  The highest set bit of code[x] ^ code[y] then lies in the field of
+// the highest differing digit, and dbit[bit] holds that level's distance.
+// Both tables live in one small device array (L1-resident), built once per
+// topology by get_topo() — two cached loads + xor + clz per distance.
+struct Topo {
+  int L;                                // hierarchy levels
+  int k;                                // number of PEs
+  const unsigned long long* code;       // [k]
+  const long long* dbit;                // [64]
+};
+
+// cached per (hierarchy, distances); device tables are never freed
+Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances);
+Topo get_flat_topo(int k);
+
+__device__ __forceinline__ long long dist(const Topo& t, int x, int y) {
+  unsigned long long c = __ldg(t.code + x) ^ __ldg(t.code + y);
+  return c ? __ldg(t.dbit + (63 - __clzll(c))) : 0ll;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic mixers (util.py:13-24), uint64 arithmetic
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t hash2(uint64_t seed, uint64_t a, uint64_t b) {
+  return splitmix64(splitmix64(seed ^ splitmix64(a)) ^ b);
+}
+
+// ---------------------------------------------------------------------------
+// launch accounting (per host thread; reset by the driver)
+
+void count_launch(long long n = 1);
+long long launches();
+void reset_launches();
+
+// ---------------------------------------------------------------------------
+// launch geometry
+
+constexpr int kSMs = 148;
+
+inline int grid_for(long long work, int block, int max_blocks = kSMs * 16) {
+  long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// block-wide int64 sum into *out with one atomic per block
+template <int BLOCK>
+__device__ __forceinline__ void block_sum_atomic(long long v, long long* out) {
+  __shared__ long long s[BLOCK / 32];
+  v = warp_sum_ll(v);
+  if (lane_id() == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long x = threadIdx.x < BLOCK / 32 ? s[threadIdx.x] : 0;
+    x = warp_sum_ll(x);
+    if (threadIdx.x == 0 && x != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stream-ordered device memory (cudaMallocAsync pool)
+
+void* dmalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) : n(count), s(st) {
+    p = count ? static_cast<T*>(dmalloc(count * sizeof(T), st)) : nullptr;
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) dfree(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+}  // namespace gim

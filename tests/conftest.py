@@ -1,0 +1,56 @@
+"""Shared pytest setup: the `gpu` marker, repo on sys.path, golden loaders."""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libgpuim.so")
+
+
+class Case(dict):
+    """One golden case: dict of arrays plus a graph builder."""
+
+    def graph(self):
+        from oracle.promap_np import OGraph
+        return OGraph(self["offsets"], self["targets"], self["weights"], self["vweights"])
+
+    def topology(self):
+        from oracle.promap_np import OTopology
+        return OTopology(tuple(int(x) for x in self["hierarchy"]),
+                         tuple(int(x) for x in self["distances"]))
+
+    def scalar(self, key):
+        return self[key].item()
+
+
+def load_golden(name: str) -> list[Case]:
+    z = np.load(GOLDEN / f"{name}.npz")
+    cases = [Case() for _ in range(int(z["count"]))]
+    for key in z.files:
+        if key == "count":
+            continue
+        i, field = key.split("/", 1)
+        cases[int(i)][field] = z[key]
+    return cases
+
+
+@pytest.fixture(scope="session")
+def golden():
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = load_golden(name)
+        return cache[name]
+    return get
