@@ -102,6 +102,111 @@ int gim_total_cost(const gim_graph* g, const int32_t* assignment,
 int gim_block_weights(const gim_graph* g, const int32_t* assignment, int32_t k,
                       int64_t* bw_out, void* stream);
 
+/* ---- coarsening (coarsening.py) --------------------------------------- */
+/* One heavy-edge matching round (coarsening.py:63-95).  partner[n] in/out
+ * (-1 = unmatched), preferred[n] out; *matched_inout (host) is the matched
+ * vertex count before/after.  Synchronizes `stream`. */
+int gim_hem_round(const gim_graph* g, int32_t* partner, int32_t* preferred, double l_max,
+                  uint64_t seed, int64_t* matched_inout, void* stream);
+
+/* match_graph (coarsening.py:164-173): <= 2 HEM rounds, then two-hop
+ * (leaves, twins, relatives; :113-161).  partner[n] out. Synchronizes. */
+int gim_match_graph(const gim_graph* g, double l_max, uint64_t seed, int32_t* partner,
+                    int64_t* matched_out, void* stream);
+
+/* coarse_map_from_matching (coarsening.py:176-188); *n_c_out host. Syncs. */
+int gim_coarse_map(int32_t n, const int32_t* partner, int32_t* coarse_map, int32_t* n_c_out,
+                   void* stream);
+
+/* contract (coarsening.py:191-249) by radix sort on (cu, cv) + segmented
+ * reduce.  Output rows are sorted by target.  out_targets/out_weights/
+ * out_sources need >= g->m2 slots, out_offsets n_c+1, out_vweights n_c.
+ * *m2_out (host) = coarse directed slots.  Synchronizes. */
+int gim_contract(const gim_graph* g, const int32_t* coarse_map, int32_t n_c,
+                 int32_t* out_offsets, int32_t* out_targets, int32_t* out_weights,
+                 int32_t* out_vweights, int32_t* out_sources, int64_t* m2_out, void* stream);
+
+/* project (coarsening.py:269-277): fine_part[v] = coarse_part[coarse_map[v]]. */
+int gim_project(int32_t n, const int32_t* coarse_map, const int32_t* coarse_part,
+                int32_t* fine_part, void* stream);
+
+/* ---- refinement (refinement.py, mapping.py) ---------------------------- */
+/* BlockConnectivity values (mapping.py:141-158): per vertex the (block,
+ * conn) list sorted by block.  out_blocks/out_weights need >= g->m2 slots.
+ * *total_out (host) = number of entries.  Synchronizes. */
+int gim_conn_build(const gim_graph* g, const int32_t* assignment, int32_t k,
+                   int32_t* out_offsets, int32_t* out_blocks, int32_t* out_weights,
+                   int64_t* total_out, void* stream);
+
+/* label_propagation_pass (refinement.py:201-270) -> MoveProposal arrays.
+ * locked may be NULL (no locks); jet = filter_mode "jet".  Synchronizes. */
+int gim_lp_pass(const gim_graph* g, const int32_t* assignment, const uint8_t* locked,
+                const gim_topology* t, int32_t jet, double jet_c, uint8_t* out_cand,
+                int32_t* out_dest, uint8_t* out_to_move, int64_t* movers_out, void* stream);
+
+/* weak_rebalance / strong_rebalance (refinement.py:312-386).  block_weights
+ * is the device int64[k] of the current mapping.  Synchronizes. */
+int gim_rebalance(const gim_graph* g, const int32_t* assignment, const int64_t* block_weights,
+                  const gim_topology* t, int32_t strong, double sigma, double l_max, int32_t rho,
+                  uint64_t seed, int64_t pass_counter, uint8_t* out_cand, int32_t* out_dest,
+                  uint8_t* out_to_move, int32_t* incomplete_out, void* stream);
+
+/* apply_moves (mapping.py:252-282): assignment/block_weights updated in
+ * place, *delta_j_out (host) = exact change of J.  Synchronizes. */
+int gim_apply_moves(const gim_graph* g, int32_t* assignment, int64_t* block_weights,
+                    const uint8_t* to_move, const int32_t* dest, const gim_topology* t,
+                    int64_t* delta_j_out, void* stream);
+
+/* refine (Alg. 4, refinement.py:389-464) with an explicit RefinementConfig
+ * (refinement.py:50-71).  assignment/block_weights are replaced by the best
+ * mapping found.  Synchronizes. */
+int gim_refine(const gim_graph* g, const gim_topology* t, int32_t* assignment,
+               int64_t* block_weights, double phi, int32_t i_max, int32_t i_w_max,
+               double sigma_fraction, int32_t rho, int32_t jet, double jet_c, uint64_t seed,
+               double l_max, void* stream);
+
+/* ---- initial mapping (pipelines.py) ------------------------------------ */
+/* greedy_graph_growing (pipelines.py:132-188); requires n > k or k == 1. */
+int gim_greedy_graph_growing(const gim_graph* g, int32_t k, int32_t* part, void* stream);
+
+/* internal_partitioner (pipelines.py:191-218). Synchronizes. */
+int gim_internal_partitioner(const gim_graph* g, int32_t k, double eps_local, uint64_t seed,
+                             int32_t* part, void* stream);
+
+/* hierarchical_multisection with the internal partitioner
+ * (pipelines.py:49-110).  Synchronizes. */
+int gim_hierarchical_multisection(const gim_graph* g, const gim_topology* t, double eps,
+                                  uint64_t seed, int32_t* assignment, void* stream);
+
+/* ---- the drop-in ------------------------------------------------------- */
+/* Default keyword arguments of integrated_map. */
+int gim_default_params(gim_im_params* out);
+
+/* integrated_map on a device-resident level-0 graph (pipelines.py:221-269).
+ * out_assignment int32[n], out_block_weights int64[k] (device).  params may
+ * be NULL (defaults); stats may be NULL.  Synchronizes. */
+int gim_integrated_map_device(const gim_graph* g, const gim_topology* t, double eps,
+                              uint64_t seed, const gim_im_params* params,
+                              int32_t* out_assignment, int64_t* out_block_weights,
+                              gim_im_stats* stats, void* stream);
+
+/* integrated_map on HOST int64 CSR arrays (graph.py:17-39 layout, no
+ * edge_sources needed): upload, map, download.  out_assignment int64[n],
+ * out_block_weights int64[k] are HOST arrays.  Returns GIM_E_EMPTY for n == 0
+ * (reference: ValueError).  Synchronizes. */
+int gim_integrated_map(int64_t n, const int64_t* offsets, const int64_t* targets,
+                       const int64_t* edge_weights, const int64_t* vertex_weights,
+                       const gim_topology* t, double eps, uint64_t seed,
+                       const gim_im_params* params, int64_t* out_assignment,
+                       int64_t* out_block_weights, gim_im_stats* stats, void* stream);
+
+/* edge_sources from offsets (graph.py:32-36). */
+int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream);
+
+/* kernels launched by this host thread since the last reset (evidence). */
+int64_t gim_launch_count(void);
+void gim_reset_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,12 +85,38 @@ GP = C.POINTER(GimGraph)
 TP = C.POINTER(GimTopology)
 
 # name -> argtypes; every symbol declared in include/gpuim.h appears here
+PI32 = C.POINTER(C.c_int32)
+PI64 = C.POINTER(C.c_int64)
+PARP = C.POINTER(GimImParams)
+PSTP = C.POINTER(GimImStats)
+
 SIGNATURES: dict[str, list] = {
     "gim_version": [],
     "gim_last_error": [],
     "gim_total_cost": [GP, P, TP, P, P],
     "gim_block_weights": [GP, P, I32, P, P],
+    "gim_hem_round": [GP, P, P, DBL, U64, PI64, P],
+    "gim_match_graph": [GP, DBL, U64, P, PI64, P],
+    "gim_coarse_map": [I32, P, P, PI32, P],
+    "gim_contract": [GP, P, I32, P, P, P, P, P, PI64, P],
+    "gim_project": [I32, P, P, P, P],
+    "gim_conn_build": [GP, P, I32, P, P, P, PI64, P],
+    "gim_lp_pass": [GP, P, P, TP, I32, DBL, P, P, P, PI64, P],
+    "gim_rebalance": [GP, P, P, TP, I32, DBL, DBL, I32, U64, I64, P, P, P, PI32, P],
+    "gim_apply_moves": [GP, P, P, P, P, TP, PI64, P],
+    "gim_refine": [GP, TP, P, P, DBL, I32, I32, DBL, I32, I32, DBL, U64, DBL, P],
+    "gim_greedy_graph_growing": [GP, I32, P, P],
+    "gim_internal_partitioner": [GP, I32, DBL, U64, P, P],
+    "gim_hierarchical_multisection": [GP, TP, DBL, U64, P, P],
+    "gim_default_params": [PARP],
+    "gim_integrated_map_device": [GP, TP, DBL, U64, PARP, P, P, PSTP, P],
+    "gim_integrated_map": [I64, P, P, P, P, TP, DBL, U64, PARP, P, P, PSTP, P],
+    "gim_fill_sources": [I32, P, P, P],
+    "gim_launch_count": [],
+    "gim_reset_launch_count": [],
 }
+RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
+            "gim_reset_launch_count": None}
 
 _lib = None
 
@@ -114,7 +140,7 @@ def load():
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = C.c_char_p if name == "gim_last_error" else C.c_int
+        fn.restype = RESTYPES.get(name, C.c_int)
     _lib = lib
     return lib
 

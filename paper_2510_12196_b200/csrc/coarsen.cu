@@ -1,0 +1,509 @@
+// Coarsening: heavy-edge matching (K3/K4), two-hop matching (K5), coarse ids,
+// contraction by hand-rolled radix sort + segmented reduce (K6), projection (K7).
+//
+// Reference: coarsening.py (match rounds :63-95, two-hop :98-161,
+// match_graph :164-173, coarse ids :176-188, contract :191-249, project
+// :269-277, build_level_stack :280-295).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+
+namespace gim {
+
+// ---------------------------------------------------------------------------
+// K3 heavy-edge preference: per unmatched v, argmax over eligible unmatched
+// neighbours u (c_v + c_u <= l_max) of (w^2/(c_v c_u), hash2(seed,min,max)),
+// first CSR slot on a full tie (coarsening.py:72-90).  The rational is
+// compared exactly by 128-bit cross multiplication (c_v cancels).
+
+struct HemCand {
+  int w, c, slot, u;
+  unsigned long long h;
+};
+
+__device__ __forceinline__ bool hem_better(const HemCand& a, const HemCand& b) {
+  if (a.u < 0) return false;
+  if (b.u < 0) return true;
+  unsigned long long aw2 = (unsigned long long)a.w * (unsigned long long)a.w;
+  unsigned long long bw2 = (unsigned long long)b.w * (unsigned long long)b.w;
+  unsigned __int128 lhs = (unsigned __int128)aw2 * (unsigned)b.c;
+  unsigned __int128 rhs = (unsigned __int128)bw2 * (unsigned)a.c;
+  if (lhs != rhs) return lhs > rhs;
+  if (a.h != b.h) return a.h > b.h;
+  return a.slot < b.slot;
+}
+
+__device__ __forceinline__ HemCand hem_shfl(const HemCand& x, int o) {
+  HemCand y;
+  y.w = __shfl_xor_sync(0xffffffffu, x.w, o);
+  y.c = __shfl_xor_sync(0xffffffffu, x.c, o);
+  y.slot = __shfl_xor_sync(0xffffffffu, x.slot, o);
+  y.u = __shfl_xor_sync(0xffffffffu, x.u, o);
+  y.h = __shfl_xor_sync(0xffffffffu, x.h, o);
+  return y;
+}
+
+// VW lanes per vertex; loop bounds are warp-uniform so the shuffles in the
+// group reduction always run with the full mask
+template <int VW>
+__global__ void __launch_bounds__(256) k_hem_pref(int n, const int* __restrict__ off,
+                                                  const int* __restrict__ tgt,
+                                                  const int* __restrict__ w,
+                                                  const int* __restrict__ vw,
+                                                  const int* __restrict__ partner, double l_max,
+                                                  unsigned long long seed, int* __restrict__ pref) {
+  constexpr int GPW = 32 / VW;
+  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int gi = lane / VW, li = lane % VW;
+  for (long long vb = wid * GPW; vb < n; vb += nw * GPW) {
+    const int v = (int)(vb + gi);
+    HemCand best;
+    best.u = -1;
+    best.w = best.c = best.slot = 0;
+    best.h = 0;
+    const bool active = v < n && partner[v] < 0;
+    if (active) {
+      const long long cv = vw[v];
+      const int e1 = off[v + 1];
+      for (int e = off[v] + li; e < e1; e += VW) {
+        int u = tgt[e];
+        if (partner[u] >= 0) continue;
+        int cu = vw[u];
+        if ((double)(cv + cu) > l_max) continue;
+        HemCand c;
+        c.w = w[e];
+        c.c = cu;
+        c.slot = e;
+        c.u = u;
+        c.h = hash2(seed, (unsigned long long)min(v, u), (unsigned long long)max(v, u));
+        if (hem_better(c, best)) best = c;
+      }
+    }
+#pragma unroll
+    for (int o = VW / 2; o > 0; o >>= 1) {
+      HemCand y = hem_shfl(best, o);
+      if (hem_better(y, best)) best = y;
+    }
+    if (li == 0 && v < n) pref[v] = active ? best.u : -1;
+  }
+}
+
+// K4 mutual matching: v and u match iff they prefer each other (snapshot
+// semantics: preferences were all computed first, coarsening.py:91-94)
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restrict__ pref,
+                                                      int* __restrict__ partner,
+                                                      long long* __restrict__ matched) {
+  long long cnt = 0;
+  for (int v = blockIdx.x * BLOCK + threadIdx.x; v < n; v += gridDim.x * BLOCK) {
+    int u = pref[v];
+    if (u >= 0 && v < u && pref[u] == v) {
+      partner[v] = u;
+      partner[u] = v;
+      cnt += 2;
+    }
+  }
+  block_sum_atomic<BLOCK>(cnt, matched);
+}
+
+static int pick_vw(long long m2, int n) {
+  double avg = n ? (double)m2 / n : 0.0;
+  if (avg <= 3.0) return 4;
+  if (avg <= 7.0) return 8;
+  if (avg <= 20.0) return 16;
+  return 32;
+}
+
+void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
+               unsigned long long seed, long long* matched, cudaStream_t s) {
+  if (g.n == 0) return;
+  constexpr int B = 256;
+  int vw = pick_vw(g.m2, g.n);
+  long long groups = (long long)g.n * vw;
+  int grid = grid_for(groups, B, kSMs * 16);
+  switch (vw) {
+    case 4: k_hem_pref<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
+    case 8: k_hem_pref<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
+    case 16: k_hem_pref<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
+    default: k_hem_pref<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
+  }
+  k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched);
+  GIM_LAUNCH_CHECK();
+  count_launch(2);
+}
+
+// ---------------------------------------------------------------------------
+// K5 two-hop matching (coarsening.py:98-161).  Leaves and twins form
+// disjoint groups: group members are compacted in vertex order, stably
+// sorted by group key, and each group runs the sequential `_pair_up`
+// automaton on one thread.  Relatives have overlapping groups visited in
+// matchmaker order, so they run as one sequential device thread.
+
+__device__ void pair_up_seq(const int* grp, int len, int* partner, const int* vw, double l_max,
+                            long long* cnt) {
+  int i = 0;
+  while (i + 1 < len) {
+    int a = grp[i], b = grp[i + 1];
+    if (partner[a] >= 0) { ++i; continue; }
+    if (partner[b] >= 0 || (double)((long long)vw[a] + vw[b]) > l_max) { ++i; continue; }
+    partner[a] = b;
+    partner[b] = a;
+    *cnt += 2;
+    i += 2;
+  }
+}
+
+struct LeafFlag {
+  const int* off;
+  const int* partner;
+  __device__ int operator()(long long v) const {
+    return (off[v + 1] - off[v] == 1 && partner[v] < 0) ? 1 : 0;
+  }
+};
+struct TwinFlag {
+  const int* off;
+  const int* partner;
+  __device__ int operator()(long long v) const {
+    return (off[v + 1] - off[v] >= 1 && partner[v] < 0) ? 1 : 0;
+  }
+};
+template <class Flag>
+struct CompactOut {
+  Flag f;
+  int* out;
+  __device__ void operator()(long long v, int pos) const {
+    if (f(v)) out[pos] = (int)v;
+  }
+};
+
+// group key per compacted member: leaves -> the single neighbour;
+// twins -> order-independent 64-bit hash of the neighbourhood (+ degree)
+__global__ void k_leaf_keys(int cnt, const int* __restrict__ mem, const int* __restrict__ off,
+                            const int* __restrict__ tgt, unsigned long long* keys, int* vals) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    int v = mem[i];
+    keys[i] = (unsigned long long)tgt[off[v]];
+    vals[i] = v;
+  }
+}
+
+__global__ void k_twin_keys(int cnt, const int* __restrict__ mem, const int* __restrict__ off,
+                            const int* __restrict__ tgt, unsigned long long* keys, int* vals) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    int v = mem[i];
+    unsigned long long h1 = 0, h2 = 0;
+    for (int e = off[v]; e < off[v + 1]; ++e) {
+      unsigned long long x = splitmix64((unsigned long long)tgt[e]);
+      h1 += x;
+      h2 ^= splitmix64(x ^ 0x5851F42D4C957F2Dull);
+    }
+    keys[i] = splitmix64(h1 ^ (h2 * 0x9E3779B97F4A7C15ull) ^ (unsigned long long)(off[v + 1] - off[v]));
+    vals[i] = v;
+  }
+}
+
+__device__ bool same_neighbourhood(int a, int b, const int* off, const int* tgt) {
+  int da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+  if (da != db) return false;
+  for (int e = off[a]; e < off[a + 1]; ++e) {
+    int x = tgt[e];
+    bool found = false;
+    for (int f = off[b]; f < off[b + 1]; ++f)
+      if (tgt[f] == x) { found = true; break; }
+    if (!found) return false;
+  }
+  return true;
+}
+
+// one thread per group start (head of a run of equal keys)
+__global__ void k_pair_groups(int cnt, const unsigned long long* __restrict__ keys,
+                              const int* __restrict__ mem, int* partner, const int* vw,
+                              double l_max, int verify_twins, const int* off, const int* tgt,
+                              long long* matched, int* collision) {
+  long long local = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    if (i > 0 && keys[i] == keys[i - 1]) continue;
+    int j = i + 1;
+    while (j < cnt && keys[j] == keys[i]) ++j;
+    if (verify_twins)
+      for (int q = i + 1; q < j; ++q)
+        if (!same_neighbourhood(mem[i], mem[q], off, tgt)) atomicExch(collision, 1);
+    pair_up_seq(mem + i, j - i, partner, vw, l_max, &local);
+  }
+  if (local) atomicAdd(reinterpret_cast<unsigned long long*>(matched), (unsigned long long)local);
+}
+
+// relatives (coarsening.py:148-158): sequential over matchmakers with degree
+// <= 8; each sorts its currently unmatched neighbours and pairs them up
+__global__ void k_relatives(int n, const int* __restrict__ off, const int* __restrict__ tgt,
+                            int* partner, const int* vw, double l_max, long long* matched,
+                            int* progressed) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  long long local = 0;
+  int prog = 0;
+  int grp[8];
+  for (int mm = 0; mm < n; ++mm) {
+    int d = off[mm + 1] - off[mm];
+    if (d > 8) continue;
+    int len = 0;
+    for (int e = off[mm]; e < off[mm + 1]; ++e) {
+      int u = tgt[e];
+      if (partner[u] < 0) {
+        int p = len++;
+        while (p > 0 && grp[p - 1] > u) { grp[p] = grp[p - 1]; --p; }  // insertion sort
+        grp[p] = u;
+      }
+    }
+    long long before = local;
+    pair_up_seq(grp, len, partner, vw, l_max, &local);
+    if (local > before) prog = 1;
+  }
+  *matched += local;
+  *progressed = prog;
+}
+
+// sort-and-pair one two-hop phase; returns after the pairing kernel
+static void two_hop_phase(const DevGraph& g, int* partner, double l_max, long long* matched,
+                          bool twins, int* collision, cudaStream_t s) {
+  DBuf<int> cnt_d(1, s);
+  DBuf<int> mem((size_t)g.n, s);
+  if (twins) {
+    TwinFlag f{g.off, partner};
+    exclusive_scan<int>(g.n, f, CompactOut<TwinFlag>{f, mem.get()}, cnt_d.get(), s);
+  } else {
+    LeafFlag f{g.off, partner};
+    exclusive_scan<int>(g.n, f, CompactOut<LeafFlag>{f, mem.get()}, cnt_d.get(), s);
+  }
+  int cnt = 0;
+  GIM_CUDA(cudaMemcpyAsync(&cnt, cnt_d.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  if (cnt < 2) return;
+  DBuf<unsigned long long> keys(cnt, s), keys2(cnt, s);
+  DBuf<int> vals(cnt, s), vals2(cnt, s);
+  int grid = grid_for(cnt, 256);
+  if (twins)
+    k_twin_keys<<<grid, 256, 0, s>>>(cnt, mem.get(), g.off, g.tgt, keys.get(), vals.get());
+  else
+    k_leaf_keys<<<grid, 256, 0, s>>>(cnt, mem.get(), g.off, g.tgt, keys.get(), vals.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  radix_sort_pairs<unsigned long long, int>(cnt, keys.get(), vals.get(), keys2.get(),
+                                            vals2.get(), twins ? 64 : bit_length(g.n), s);
+  k_pair_groups<<<grid, 256, 0, s>>>(cnt, keys.get(), vals.get(), partner, g.vw, l_max,
+                                     twins ? 1 : 0, g.off, g.tgt, matched, collision);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+// returns the matched count after two-hop (coarsening.py:113-161)
+long long two_hop(const DevGraph& g, int* partner, double l_max, long long matched_now,
+                  long long* matched_d, cudaStream_t s) {
+  const double target = 0.40;
+  auto frac = [&](long long m) { return g.n ? (double)m / (double)g.n : 1.0; };
+  DBuf<int> flags(2, s);  // [collision, progressed]
+  GIM_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int), s));
+  auto read = [&]() {
+    long long m = 0;
+    GIM_CUDA(cudaMemcpyAsync(&m, matched_d, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    return m;
+  };
+  GIM_CUDA(cudaMemcpyAsync(matched_d, &matched_now, sizeof(long long), cudaMemcpyHostToDevice, s));
+  long long m = matched_now;
+  for (int rep = 0; rep < 3; ++rep) {
+    if (frac(m) >= target) return m;
+    two_hop_phase(g, partner, l_max, matched_d, false, flags.get(), s);
+    m = read();
+    if (frac(m) >= target) return m;
+    two_hop_phase(g, partner, l_max, matched_d, true, flags.get(), s);
+    m = read();
+    int coll = 0;
+    GIM_CUDA(cudaMemcpy(&coll, flags.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    GIM_CHECK(coll == 0, GIM_E_INTERNAL, "two-hop twin hash collision (non-identical "
+                                         "neighbourhoods share a 64-bit key)");
+    if (frac(m) >= target) return m;
+    k_relatives<<<1, 1, 0, s>>>(g.n, g.off, g.tgt, partner, g.vw, l_max, matched_d,
+                                flags.get() + 1);
+    count_launch();
+    GIM_LAUNCH_CHECK();
+    m = read();
+    int prog = 0;
+    GIM_CUDA(cudaMemcpy(&prog, flags.get() + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!prog) return m;
+  }
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// coarse ids (coarsening.py:176-188): root = min(v, partner); ids by an
+// exclusive scan over is_root in vertex order
+
+struct IsRoot {
+  const int* partner;
+  __device__ int operator()(long long v) const {
+    int p = partner[v];
+    return (p < 0 || v < p) ? 1 : 0;
+  }
+};
+
+__global__ void k_coarse_map(int n, const int* __restrict__ partner, const int* __restrict__ ids,
+                             int* __restrict__ cmap) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int p = partner[v];
+    cmap[v] = (p >= 0 && p < v) ? ids[p] : ids[v];
+  }
+}
+
+int coarse_map(int n, const int* partner, int* cmap, cudaStream_t s) {
+  if (n == 0) return 0;
+  DBuf<int> ids((size_t)n, s), tot(1, s);
+  exclusive_scan<int>(n, IsRoot{partner}, StoreTo<int>{ids.get()}, tot.get(), s);
+  k_coarse_map<<<grid_for(n, 256), 256, 0, s>>>(n, partner, ids.get(), cmap);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  int n_c = 0;
+  GIM_CUDA(cudaMemcpyAsync(&n_c, tot.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  return n_c;
+}
+
+// ---------------------------------------------------------------------------
+// K6 contraction (coarsening.py:191-249): key (cu, cv) = cu * n_c + cv per
+// fine slot, self loops keyed past the end, radix sort, segmented sum of
+// equal keys -> coarse CSR sorted by (source, target).
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_contract_keys(long long m2, const int* __restrict__ src,
+                                                         const int* __restrict__ tgt,
+                                                         const int* __restrict__ w,
+                                                         const int* __restrict__ cmap, int n_c,
+                                                         unsigned long long* __restrict__ keys,
+                                                         int* __restrict__ vals,
+                                                         long long* __restrict__ selfloops) {
+  const unsigned long long sent = (unsigned long long)n_c * (unsigned long long)n_c;
+  long long cnt = 0;
+  for (long long e = (long long)blockIdx.x * BLOCK + threadIdx.x; e < m2;
+       e += (long long)gridDim.x * BLOCK) {
+    int cu = cmap[src[e]], cv = cmap[tgt[e]];
+    if (cu == cv) {
+      keys[e] = sent;
+      ++cnt;
+    } else {
+      keys[e] = (unsigned long long)cu * (unsigned long long)n_c + (unsigned long long)cv;
+    }
+    vals[e] = w[e];
+  }
+  block_sum_atomic<BLOCK>(cnt, selfloops);
+}
+
+struct KeyHead {
+  const unsigned long long* keys;
+  __device__ int operator()(long long i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0; }
+};
+
+struct KeyHeadOut {
+  const unsigned long long* keys;
+  const int* vals;
+  long long valid;
+  int n_c;
+  int* ctgt;
+  int* cw;
+  int* csrc;
+  int* deg;
+  __device__ void operator()(long long i, int uid) const {
+    if (i > 0 && keys[i] == keys[i - 1]) return;
+    long long sum = 0;
+    long long j = i;
+    while (j < valid && keys[j] == keys[i]) sum += vals[j++];
+    unsigned long long k = keys[i];
+    int cu = (int)(k / (unsigned long long)n_c);
+    ctgt[uid] = (int)(k % (unsigned long long)n_c);
+    cw[uid] = (int)sum;
+    csrc[uid] = cu;
+    atomicAdd(&deg[cu], 1);
+  }
+};
+
+__global__ void k_coarse_vw(int n, const int* __restrict__ cmap, const int* __restrict__ vw,
+                            int* __restrict__ cvw) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicAdd(&cvw[cmap[v]], vw[v]);
+}
+
+// returns m2 of the coarse graph; out arrays must hold >= g.m2 slots
+long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off, int* c_tgt,
+                        int* c_w, int* c_vw, int* c_src, cudaStream_t s) {
+  GIM_CUDA(cudaMemsetAsync(c_vw, 0, sizeof(int) * (size_t)n_c, s));
+  if (n_c > 0) {
+    k_coarse_vw<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, cmap, g.vw, c_vw);
+    count_launch();
+  }
+  if (g.m2 == 0) {
+    GIM_CUDA(cudaMemsetAsync(c_off, 0, sizeof(int) * ((size_t)n_c + 1), s));
+    return 0;
+  }
+  DBuf<unsigned long long> keys((size_t)g.m2, s), keys2((size_t)g.m2, s);
+  DBuf<int> vals((size_t)g.m2, s), vals2((size_t)g.m2, s);
+  DBuf<long long> selfl(1, s);
+  GIM_CUDA(cudaMemsetAsync(selfl.get(), 0, sizeof(long long), s));
+  constexpr int B = 256;
+  k_contract_keys<B><<<grid_for(g.m2, B, kSMs * 8), B, 0, s>>>(
+      g.m2, g.src, g.tgt, g.w, cmap, n_c, keys.get(), vals.get(), selfl.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  int bits = bit_length((unsigned long long)n_c * (unsigned long long)n_c);
+  radix_sort_pairs<unsigned long long, int>(g.m2, keys.get(), vals.get(), keys2.get(),
+                                            vals2.get(), bits, s);
+  long long self = 0;
+  GIM_CUDA(cudaMemcpyAsync(&self, selfl.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  long long valid = g.m2 - self;
+  DBuf<int> deg((size_t)n_c + 1, s), m2c_d(1, s);
+  GIM_CUDA(cudaMemsetAsync(deg.get(), 0, sizeof(int) * ((size_t)n_c + 1), s));
+  KeyHeadOut out{keys.get(), vals.get(), valid, n_c, c_tgt, c_w, c_src, deg.get()};
+  exclusive_scan<int>(valid, KeyHead{keys.get()}, out, m2c_d.get(), s);
+  exclusive_scan<int>((long long)n_c + 1, LoadAs<int, int>{deg.get()}, StoreTo<int>{c_off},
+                      (int*)nullptr, s);
+  int m2c = 0;
+  GIM_CUDA(cudaMemcpyAsync(&m2c, m2c_d.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  return m2c;
+}
+
+void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cudaStream_t s) {
+  DBuf<int> t((size_t)std::max<long long>(g.m2, 1), s), w((size_t)std::max<long long>(g.m2, 1), s),
+      sr((size_t)std::max<long long>(g.m2, 1), s);
+  out.n = n_c;
+  out.off = DBuf<int>((size_t)n_c + 1, s);
+  out.vw = DBuf<int>((size_t)std::max(n_c, 1), s);
+  long long m2c = contract_into(g, cmap, n_c, out.off.get(), t.get(), w.get(), out.vw.get(),
+                                sr.get(), s);
+  out.m2 = m2c;
+  out.tgt = DBuf<int>((size_t)std::max<long long>(m2c, 1), s);
+  out.w = DBuf<int>((size_t)std::max<long long>(m2c, 1), s);
+  out.src = DBuf<int>((size_t)std::max<long long>(m2c, 1), s);
+  if (m2c) {
+    GIM_CUDA(cudaMemcpyAsync(out.tgt.get(), t.get(), sizeof(int) * m2c, cudaMemcpyDeviceToDevice, s));
+    GIM_CUDA(cudaMemcpyAsync(out.w.get(), w.get(), sizeof(int) * m2c, cudaMemcpyDeviceToDevice, s));
+    GIM_CUDA(cudaMemcpyAsync(out.src.get(), sr.get(), sizeof(int) * m2c, cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+// K7 projection (coarsening.py:269-277): Pi_f = Pi_c[M]
+__global__ void k_project(int n, const int* __restrict__ cmap, const int* __restrict__ pc,
+                          int* __restrict__ pf) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    pf[v] = pc[cmap[v]];
+}
+
+void project(int n, const int* cmap, const int* pc, int* pf, cudaStream_t s) {
+  if (n == 0) return;
+  k_project<<<grid_for(n, 256), 256, 0, s>>>(n, cmap, pc, pf);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+}  // namespace gim

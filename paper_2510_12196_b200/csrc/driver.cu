@@ -1,0 +1,878 @@
+// Host driver (native runtime): level stack, Alg. 4 refinement control,
+// hierarchical multisection with the internal partitioner, integrated_map —
+// plus the C-ABI entry points of include/gpuim.h.
+//
+// All float threshold math (l_max, sigma, excess/room, phi * J, match
+// fractions, Eq. 2) is evaluated on the host in IEEE double with the same
+// operation order as the reference's Python float expressions, so control
+// decisions agree bit-for-bit; kernels only see the resulting doubles.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "scan.cuh"
+
+namespace gim {
+
+void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s);
+void extract_subgraphs(const DevGraph& g, const int* part, int parts,
+                       std::vector<OwnedGraph>& subs, std::vector<DBuf<int>>& ids,
+                       cudaStream_t s);
+void gather(int n, const int* idx, const int* src, int* dst, cudaStream_t s);
+void scatter_const(int n, const int* idx, int value, int* dst, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// run statistics
+
+struct RunStats {
+  long long refine_iterations = 0, lp = 0, weak = 0, strong = 0;
+  long long init_refine_iterations = 0, partitioner_calls = 0;
+  bool in_initial = false;
+};
+
+// pinned host scratch, one per host thread
+struct Pinned {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      bytes = std::max(need, (size_t)1 << 16);
+      if (cudaMallocHost(&p, bytes) != cudaSuccess) throw Error{GIM_E_CUDA, "cudaMallocHost failed"};
+    }
+    return p;
+  }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+static thread_local Pinned g_pin;
+
+template <class T>
+static T read_scalar(const T* d, cudaStream_t s) {
+  T* h = static_cast<T*>(g_pin.get(sizeof(T)));
+  GIM_CUDA(cudaMemcpyAsync(h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  return *h;
+}
+
+__global__ void k_sum_vw(int n, const int* __restrict__ vw, long long* out) {
+  long long acc = 0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    acc += vw[v];
+  block_sum_atomic<256>(acc, out);
+}
+
+static long long total_vertex_weight(const DevGraph& g, cudaStream_t s) {
+  DBuf<long long> d(1, s);
+  GIM_CUDA(cudaMemsetAsync(d.get(), 0, sizeof(long long), s));
+  if (g.n) {
+    k_sum_vw<<<grid_for(g.n, 256, kSMs * 2), 256, 0, s>>>(g.n, g.vw, d.get());
+    count_launch();
+  }
+  return read_scalar(d.get(), s);
+}
+
+__global__ void k_iota(int n, int* p) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) p[v] = v;
+}
+
+// ---------------------------------------------------------------------------
+// refinement config (refinement.py:50-101)
+
+struct RefCfg {
+  double phi = 0.999;
+  int i_max = 12;
+  int i_w_max = 2;
+  double sigma_fraction = 0.005;
+  int rho = 2;
+  int jet = 0;
+  double jet_c = 0.25;
+  unsigned long long seed = 0;
+};
+
+static RefCfg config_for_level(int level, int n_levels, double phi, int rho, int jet,
+                               double jet_c, double sigma_coarse, double sigma_fine,
+                               int iw_max_finest, unsigned long long seed) {
+  int span = std::max(n_levels - 1, 1);
+  double frac = n_levels > 1 ? (double)level / (double)span : 0.0;
+  double delta = sigma_fine + (sigma_coarse - sigma_fine) * frac;
+  RefCfg c;
+  c.phi = phi;
+  c.i_max = 12 + level;
+  c.i_w_max = level == 0 ? iw_max_finest : 2;
+  c.sigma_fraction = delta;
+  c.rho = rho;
+  c.jet = jet;
+  c.jet_c = jet_c;
+  c.seed = seed;
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 4 (refinement.py:389-464).  `part`/`bw` are consumed and replaced by
+// the best mapping seen.
+
+static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, const RefCfg& cfg,
+                   double l_max, RunStats& st, cudaStream_t s) {
+  const int n = L.g.n, k = t.k;
+  if (L.heavy.get() == nullptr) prepare_level(L, k, s);
+  RefineBuffers rb;
+  alloc_refine_buffers(rb, n, k, s);
+  // host mirrors
+  size_t pin_bytes = sizeof(long long) * ((size_t)k + 2) + (size_t)k * 2 + sizeof(int) * (size_t)k;
+  char* pin = static_cast<char*>(g_pin.get(pin_bytes));
+  long long* h_bw = reinterpret_cast<long long*>(pin);
+  long long* h_mv = h_bw + k;
+  long long* h_dj = h_mv + 1;
+  unsigned char* h_ovl = reinterpret_cast<unsigned char*>(h_dj + 1);
+  unsigned char* h_elig = h_ovl + k;
+  int* h_elist = reinterpret_cast<int*>(h_elig + k);
+  DBuf<unsigned char> d_masks((size_t)k * 2, s);
+  DBuf<int> d_elist((size_t)k, s);
+  DBuf<long long> d_j(1, s);
+
+  total_cost(L.g, part, t, d_j.get(), s);
+  GIM_CUDA(cudaMemcpyAsync(h_dj, d_j.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  long long J = *h_dj;
+  std::vector<long long> bw(h_bw, h_bw + k);
+  auto maxof = [&](const std::vector<long long>& x) {
+    long long m = 0;
+    for (long long y : x) m = std::max(m, y);
+    return m;
+  };
+  const double sigma = l_max * (1.0 - cfg.sigma_fraction);
+  DBuf<int> best((size_t)std::max(n, 1), s);
+  GIM_CUDA(cudaMemcpyAsync(best.get(), part, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  std::vector<long long> best_bw = bw;
+  long long maxw = maxof(bw);
+  bool best_balanced = (double)maxw <= l_max;
+  long long best_j = J;
+  long long best_maxw = maxw;
+  bool locks_nonempty = false;
+  int i = 0, i_w = 0;
+  long long pass_counter = 0;
+  while (i < cfg.i_max) {
+    const bool balanced_now = (double)maxw <= l_max;
+    const bool entry_locks_empty = !locks_nonempty;
+    bool incomplete = false;
+    bool is_lp = balanced_now;
+    if (balanced_now) {
+      lp_pass(L, t, part, locks_nonempty ? rb.locks.get() : nullptr, cfg.jet, cfg.jet_c, rb, s);
+      i_w = 0;
+      ++st.lp;
+    } else {
+      locks_nonempty = false;
+      int ne = 0;
+      for (int b = 0; b < k; ++b) {
+        h_ovl[b] = (double)bw[b] > l_max;
+        h_elig[b] = (double)bw[b] < sigma;
+        if (h_elig[b]) h_elist[ne++] = b;
+      }
+      incomplete = ne == 0;
+      GIM_CUDA(cudaMemcpyAsync(d_masks.get(), h_ovl, (size_t)k * 2, cudaMemcpyHostToDevice, s));
+      if (ne)
+        GIM_CUDA(cudaMemcpyAsync(d_elist.get(), h_elist, sizeof(int) * ne, cudaMemcpyHostToDevice, s));
+      bool strong = !(i_w < cfg.i_w_max);
+      rebalance_pass(L, t, part, bw_d, strong, l_max, cfg.rho, cfg.seed, pass_counter,
+                     d_masks.get(), d_masks.get() + k, d_elist.get(), ne, rb, s);
+      if (strong) {
+        i_w = 0;
+        ++st.strong;
+      } else {
+        ++i_w;
+        ++st.weak;
+      }
+      ++pass_counter;
+    }
+    apply_moves(L, t, part, bw_d, rb, s);
+    GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(h_mv, rb.movers.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(h_dj, rb.dj.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    if (st.in_initial) ++st.init_refine_iterations;
+    else ++st.refine_iterations;
+    const long long movers = *h_mv;
+    if (movers == 0) {
+      if (balanced_now && entry_locks_empty) break;   // fixed point
+      if (!balanced_now && incomplete) break;         // rebalancing is stuck
+    }
+    J += *h_dj;
+    bw.assign(h_bw, h_bw + k);
+    maxw = maxof(bw);
+    if (is_lp) {
+      std::swap(rb.locks, rb.to_move);  // locks for the next pass = the moved set
+      locks_nonempty = movers > 0;
+    } else {
+      locks_nonempty = false;
+    }
+    bool reset = false;
+    bool take = false;
+    if ((double)maxw <= l_max) {
+      if (!best_balanced) {
+        best_balanced = true;
+        best_j = J;
+        best_maxw = maxw;
+        reset = take = true;
+      } else if (J < best_j) {
+        reset = (double)J < cfg.phi * (double)best_j;
+        best_j = J;
+        best_maxw = maxw;
+        take = true;
+      }
+    } else if (!best_balanced && maxw < best_maxw) {
+      best_maxw = maxw;
+      reset = take = true;
+    }
+    if (take) {
+      GIM_CUDA(cudaMemcpyAsync(best.get(), part, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+      best_bw = bw;
+    }
+    i = reset ? 0 : i + 1;
+  }
+  GIM_CUDA(cudaMemcpyAsync(part, best.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  std::copy(best_bw.begin(), best_bw.end(), h_bw);
+  GIM_CUDA(cudaMemcpyAsync(bw_d, h_bw, sizeof(long long) * k, cudaMemcpyHostToDevice, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// level stack (coarsening.py:164-173, 280-295)
+
+struct Level {
+  OwnedGraph own;       // empty for the input level
+  DevGraph g;
+  DBuf<int> cmap;       // fine -> coarse (absent on the coarsest level)
+  int n_c = 0;
+  RefineLevel rl;
+};
+
+static long long match_graph(const DevGraph& g, double l_max, unsigned long long seed,
+                             int* partner, cudaStream_t s) {
+  GIM_CUDA(cudaMemsetAsync(partner, 0xff, sizeof(int) * (size_t)std::max(g.n, 1), s));
+  DBuf<int> pref((size_t)std::max(g.n, 1), s);
+  DBuf<long long> matched(1, s);
+  GIM_CUDA(cudaMemsetAsync(matched.get(), 0, sizeof(long long), s));
+  long long m = 0;
+  auto frac = [&](long long x) { return g.n ? (double)x / (double)g.n : 1.0; };
+  for (int r = 0; r < 2; ++r) {
+    if (frac(m) >= 0.40) break;
+    hem_round(g, partner, pref.get(), l_max, splitmix64(seed ^ (unsigned long long)(r + 1)),
+              matched.get(), s);
+    m = read_scalar(matched.get(), s);
+  }
+  if (frac(m) < 0.40) m = two_hop(g, partner, l_max, m, matched.get(), s);
+  return m;
+}
+
+static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, long long threshold,
+                                            unsigned long long seed, cudaStream_t s) {
+  std::vector<Level> levels;
+  levels.emplace_back();
+  levels.back().g = g0;
+  for (;;) {
+    Level& cur = levels.back();
+    if ((long long)cur.g.n < threshold) break;
+    DBuf<int> partner((size_t)std::max(cur.g.n, 1), s);
+    unsigned long long lseed = splitmix64(seed ^ (unsigned long long)(levels.size() - 1));
+    match_graph(cur.g, l_max, lseed, partner.get(), s);
+    DBuf<int> cmap((size_t)std::max(cur.g.n, 1), s);
+    int n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
+    if ((double)n_c * 1.02 > (double)cur.g.n) break;  // stall guard
+    Level next;
+    contract(cur.g, cmap.get(), n_c, next.own, s);
+    next.g = next.own.view();
+    cur.cmap = std::move(cmap);
+    cur.n_c = n_c;
+    levels.push_back(std::move(next));
+  }
+  return levels;
+}
+
+// ---------------------------------------------------------------------------
+// internal partitioner (pipelines.py:191-218)
+
+static void internal_partitioner(const DevGraph& g, long long total, int parts, double eps_local,
+                                 unsigned long long seed, int* part, RunStats& st, cudaStream_t s) {
+  const int n = g.n;
+  ++st.partitioner_calls;
+  if (parts <= 1 || n == 0) {
+    GIM_CUDA(cudaMemsetAsync(part, 0, sizeof(int) * (size_t)std::max(n, 1), s));
+    return;
+  }
+  if (n <= parts) {
+    k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, part);
+    count_launch();
+    return;
+  }
+  Topo tf = get_flat_topo(parts);
+  const double l_max = (1.0 + eps_local) * (double)total / (double)parts;
+  std::vector<Level> levels =
+      build_level_stack(g, l_max, std::max<long long>(64ll * parts, 2), seed, s);
+  const int nl = (int)levels.size();
+  DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
+  greedy_graph_growing(levels.back().g, parts, cur.get(), s);
+  DBuf<long long> bw((size_t)parts, s);
+  for (int li = nl - 1; li >= 0; --li) {
+    Level& L = levels[li];
+    if (li < nl - 1) {
+      DBuf<int> fine((size_t)std::max(L.g.n, 1), s);
+      project(L.g.n, L.cmap.get(), cur.get(), fine.get(), s);
+      cur = std::move(fine);
+    }
+    block_weights(L.g.n, L.g.vw, cur.get(), parts, bw.get(), s);
+    RefCfg cfg = config_for_level(li, nl, 0.999, 2, 1, 0.25, 0.065, 0.005, 10,
+                                  hash2(seed, 101, (unsigned long long)li));
+    L.rl.g = L.g;
+    refine(L.rl, tf, cur.get(), bw.get(), cfg, l_max, st, s);
+  }
+  GIM_CUDA(cudaMemcpyAsync(part, cur.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+}
+
+// ---------------------------------------------------------------------------
+// hierarchical multisection (pipelines.py:49-110)
+
+struct MsCtx {
+  std::vector<long long> h, d;
+  long long k;
+  long long total;
+  double eps;
+  int* assignment;
+  RunStats* st;
+  cudaStream_t s;
+};
+
+static double adaptive_imbalance(double eps, long long total, long long sub, long long k,
+                                 long long k_sub, int depth) {
+  double value = std::pow((1.0 + eps) * (double)(k_sub * total) / (double)(k * sub),
+                          1.0 / (double)depth) - 1.0;
+  return std::max(value, 0.0);
+}
+
+static int calc_id(const std::vector<long long>& h, const std::vector<int>& ident) {
+  const int ell = (int)h.size();
+  long long out = 0, place = 1;
+  for (int i = 0; i < ell; ++i) {
+    out += ident[ell - 1 - i] * place;
+    place *= h[i];
+  }
+  return (int)out;
+}
+
+static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int level,
+                    std::vector<int>& ident, const int* translation, unsigned long long node_seed) {
+  cudaStream_t s = C.s;
+  if (sub.n == 0) return;
+  if (level == 0) {
+    scatter_const(sub.n, translation, calc_id(C.h, ident), C.assignment, s);
+    return;
+  }
+  const int parts = (int)C.h[level - 1];
+  long long k_sub = 1;
+  for (int i = 0; i < level; ++i) k_sub *= C.h[i];
+  double eps_local = adaptive_imbalance(C.eps, C.total, sub_total, C.k, k_sub, level);
+  DBuf<int> part((size_t)std::max(sub.n, 1), s);
+  if (parts == 1)
+    GIM_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(int) * sub.n, s));
+  else
+    internal_partitioner(sub, sub_total, parts, eps_local, node_seed, part.get(), *C.st, s);
+  DBuf<long long> bw((size_t)parts, s);
+  block_weights(sub.n, sub.vw, part.get(), parts, bw.get(), s);
+  std::vector<long long> child_total((size_t)parts);
+  GIM_CUDA(cudaMemcpyAsync(child_total.data(), bw.get(), sizeof(long long) * parts,
+                           cudaMemcpyDeviceToHost, s));
+  std::vector<OwnedGraph> subs;
+  std::vector<DBuf<int>> ids;
+  extract_subgraphs(sub, part.get(), parts, subs, ids, s);  // synchronizes s
+  for (int j = 0; j < parts; ++j) {
+    DBuf<int> trans((size_t)std::max(subs[j].n, 1), s);
+    gather(subs[j].n, ids[j].get(), translation, trans.get(), s);
+    ids[j].release();
+    ident.push_back(j);
+    descend(C, subs[j].view(), child_total[j], level - 1, ident, trans.get(),
+            hash2(node_seed, (unsigned long long)level, (unsigned long long)j));
+    ident.pop_back();
+    subs[j] = OwnedGraph();
+  }
+}
+
+static void hierarchical_multisection(const DevGraph& g, long long total,
+                                      const std::vector<long long>& h,
+                                      const std::vector<long long>& d, double eps,
+                                      unsigned long long seed, int* assignment, RunStats& st,
+                                      cudaStream_t s) {
+  GIM_CHECK(g.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+  MsCtx C;
+  C.h = h;
+  C.d = d;
+  C.k = 1;
+  for (long long a : h) C.k *= a;
+  C.total = total;
+  C.eps = eps;
+  C.assignment = assignment;
+  C.st = &st;
+  C.s = s;
+  GIM_CUDA(cudaMemsetAsync(assignment, 0, sizeof(int) * g.n, s));
+  DBuf<int> ident_ids((size_t)g.n, s);
+  k_iota<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, ident_ids.get());
+  count_launch();
+  std::vector<int> ident;
+  descend(C, g, total, (int)h.size(), ident, ident_ids.get(), seed);
+}
+
+// ---------------------------------------------------------------------------
+// integrated_map (pipelines.py:221-269)
+
+struct ImTimes {
+  cudaEvent_t e[4];
+};
+
+static void integrated_map_device(const DevGraph& g0, long long total, const gim_topology& tt,
+                                  double eps, unsigned long long seed, const gim_im_params& P,
+                                  int* out_part, long long* out_bw, gim_im_stats* stats,
+                                  cudaStream_t s) {
+  GIM_CHECK(g0.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+  Topo t = get_topo(tt.levels, tt.hierarchy, tt.distances);
+  std::vector<long long> h(tt.hierarchy, tt.hierarchy + tt.levels);
+  std::vector<long long> d(tt.distances, tt.distances + tt.levels);
+  const long long k = t.k;
+  RunStats st;
+  reset_launches();
+  cudaEvent_t ev[4];
+  for (auto& e : ev) GIM_CUDA(cudaEventCreate(&e));
+  GIM_CUDA(cudaEventRecord(ev[0], s));
+  const double l_max = (1.0 + eps) * (double)total / (double)k;
+  std::vector<Level> levels = build_level_stack(
+      g0, l_max, std::max<long long>(P.coarsest_factor * k, 1), seed, s);
+  const int nl = (int)levels.size();
+  GIM_CUDA(cudaEventRecord(ev[1], s));
+  DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
+  st.in_initial = true;
+  hierarchical_multisection(levels.back().g, levels.size() == 1 ? total : total, h, d, eps,
+                            hash2(seed, 7, 7), cur.get(), st, s);
+  st.in_initial = false;
+  GIM_CUDA(cudaEventRecord(ev[2], s));
+  for (int li = nl - 1; li >= 0; --li) {
+    Level& L = levels[li];
+    if (li < nl - 1) {
+      DBuf<int> fine((size_t)std::max(L.g.n, 1), s);
+      project(L.g.n, L.cmap.get(), cur.get(), fine.get(), s);
+      cur = std::move(fine);
+      levels[li + 1] = Level();  // release the coarser level
+    }
+    block_weights(L.g.n, L.g.vw, cur.get(), (int)k, out_bw, s);
+    RefCfg cfg = config_for_level(li, nl, P.phi, P.rho, P.filter_mode, P.jet_filter_c,
+                                  P.sigma_coarse, P.sigma_fine, P.iw_max_finest,
+                                  hash2(seed, 211, (unsigned long long)li));
+    L.rl.g = L.g;
+    refine(L.rl, t, cur.get(), out_bw, cfg, l_max, st, s);
+  }
+  GIM_CUDA(cudaMemcpyAsync(out_part, cur.get(), sizeof(int) * g0.n, cudaMemcpyDeviceToDevice, s));
+  GIM_CUDA(cudaEventRecord(ev[3], s));
+  GIM_CUDA(cudaEventSynchronize(ev[3]));
+  if (stats) {
+    float a = 0, b = 0, c = 0, tot = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    cudaEventElapsedTime(&tot, ev[0], ev[3]);
+    stats->n_levels = nl;
+    stats->ms_coarsen = a;
+    stats->ms_initial = b;
+    stats->ms_refine = c;
+    stats->ms_total = tot;
+    stats->refine_iterations = st.refine_iterations;
+    stats->lp_passes = st.lp;
+    stats->weak_passes = st.weak;
+    stats->strong_passes = st.strong;
+    stats->init_refine_iterations = st.init_refine_iterations;
+    stats->partitioner_calls = st.partitioner_calls;
+    stats->kernel_launches = launches();
+    stats->l_max = l_max;
+    DBuf<long long> dj(1, s);
+    total_cost(g0, out_part, t, dj.get(), s);
+    stats->final_j = read_scalar(dj.get(), s);
+    std::vector<long long> bw((size_t)k);
+    GIM_CUDA(cudaMemcpy(bw.data(), out_bw, sizeof(long long) * k, cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (long long x : bw) mx = std::max(mx, x);
+    stats->max_block_weight = mx;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
+// host-array upload (graph.py:17-39 int64 CSR) -> int32 device level
+__global__ void k_narrow(long long n, const long long* __restrict__ in, int* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = (int)in[i];
+}
+
+__global__ void k_fill_sources(int n, const int* __restrict__ off, int* __restrict__ src) {
+  // one warp per vertex row
+  const int lane = lane_id();
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
+       w += ((long long)gridDim.x * blockDim.x) >> 5) {
+    int v = (int)w;
+    for (int e = off[v] + lane; e < off[v + 1]; e += 32) src[e] = v;
+  }
+}
+
+void fill_sources(int n, const int* off, int* src, cudaStream_t s) {
+  if (n == 0) return;
+  k_fill_sources<<<grid_for((long long)n * 32, 256, kSMs * 16), 256, 0, s>>>(n, off, src);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, const int64_t* ew,
+                         const int64_t* vw, OwnedGraph& G, cudaStream_t s) {
+  GIM_CHECK(n >= 0 && n < INT32_MAX, GIM_E_OVERFLOW, "n must be < 2^31");
+  long long m2 = off[n];
+  GIM_CHECK(m2 >= 0 && m2 < INT32_MAX, GIM_E_OVERFLOW, "2m must be < 2^31");
+  long long tv = 0, te = 0;
+  for (long long v = 0; v < n; ++v) {
+    GIM_CHECK(vw[v] > 0, GIM_E_INVALID, "vertex weights must be positive");
+    tv += vw[v];
+  }
+  GIM_CHECK(tv < INT32_MAX, GIM_E_OVERFLOW, "total vertex weight must be < 2^31");
+  for (long long e = 0; e < m2; ++e) te += ew[e];
+  GIM_CHECK(te < INT32_MAX, GIM_E_OVERFLOW, "total edge weight must be < 2^31");
+  G.n = (int)n;
+  G.m2 = m2;
+  G.total_vw = tv;
+  G.off = DBuf<int>((size_t)n + 1, s);
+  G.tgt = DBuf<int>((size_t)std::max(m2, 1ll), s);
+  G.w = DBuf<int>((size_t)std::max(m2, 1ll), s);
+  G.vw = DBuf<int>((size_t)std::max(n, 1ll), s);
+  G.src = DBuf<int>((size_t)std::max(m2, 1ll), s);
+  long long biggest = std::max(m2, n + 1);
+  DBuf<long long> stage((size_t)std::max(biggest, 1ll), s);
+  auto up = [&](const int64_t* h, long long cnt, int* d) {
+    if (cnt == 0) return;
+    GIM_CUDA(cudaMemcpyAsync(stage.get(), h, sizeof(long long) * cnt, cudaMemcpyHostToDevice, s));
+    k_narrow<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, stage.get(), d);
+    count_launch();
+  };
+  up(off, n + 1, G.off.get());
+  up(tgt, m2, G.tgt.get());
+  up(ew, m2, G.w.get());
+  up(vw, n, G.vw.get());
+  fill_sources((int)n, G.off.get(), G.src.get(), s);
+  GIM_LAUNCH_CHECK();
+}
+
+__global__ void k_widen(int n, const int* __restrict__ in, long long* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+}  // namespace gim
+
+// ===========================================================================
+// C ABI
+
+using namespace gim;
+
+static gim_im_params default_params() {
+  gim_im_params p;
+  p.coarsest_factor = 128;
+  p.phi = 0.999;
+  p.rho = 2;
+  p.filter_mode = 0;
+  p.jet_filter_c = 0.25;
+  p.sigma_coarse = 0.065;
+  p.sigma_fine = 0.005;
+  p.iw_max_finest = 10;
+  return p;
+}
+
+extern "C" int gim_default_params(gim_im_params* out) {
+  return guard([&] {
+    GIM_CHECK(out, GIM_E_INVALID, "null argument");
+    *out = default_params();
+  });
+}
+
+extern "C" int gim_hem_round(const gim_graph* g, int32_t* partner, int32_t* preferred,
+                             double l_max, uint64_t seed, int64_t* matched_inout, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && partner && preferred && matched_inout, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    DBuf<long long> m(1, s);
+    long long h = *matched_inout;
+    GIM_CUDA(cudaMemcpyAsync(m.get(), &h, sizeof(long long), cudaMemcpyHostToDevice, s));
+    hem_round(view(*g), partner, preferred, l_max, seed, m.get(), s);
+    *matched_inout = read_scalar(m.get(), s);
+  });
+}
+
+extern "C" int gim_match_graph(const gim_graph* g, double l_max, uint64_t seed, int32_t* partner,
+                               int64_t* matched_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && partner, GIM_E_INVALID, "null argument");
+    long long m = match_graph(view(*g), l_max, seed, partner, (cudaStream_t)stream);
+    if (matched_out) *matched_out = m;
+  });
+}
+
+extern "C" int gim_coarse_map(int32_t n, const int32_t* partner, int32_t* cmap_out,
+                              int32_t* n_c_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(n >= 0 && n_c_out, GIM_E_INVALID, "bad argument");
+    *n_c_out = gim::coarse_map(n, partner, cmap_out, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int gim_contract(const gim_graph* g, const int32_t* coarse_map, int32_t n_c,
+                            int32_t* out_offsets, int32_t* out_targets, int32_t* out_weights,
+                            int32_t* out_vweights, int32_t* out_sources, int64_t* m2_out,
+                            void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && m2_out && n_c >= 0, GIM_E_INVALID, "bad argument");
+    *m2_out = contract_into(view(*g), coarse_map, n_c, out_offsets, out_targets, out_weights,
+                            out_vweights, out_sources, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int gim_project(int32_t n, const int32_t* coarse_map, const int32_t* coarse_part,
+                           int32_t* fine_part, void* stream) {
+  return guard([&] { project(n, coarse_map, coarse_part, fine_part, (cudaStream_t)stream); });
+}
+
+extern "C" int gim_conn_build(const gim_graph* g, const int32_t* assignment, int32_t k,
+                              int32_t* out_offsets, int32_t* out_blocks, int32_t* out_weights,
+                              int64_t* total_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && total_out && k >= 1, GIM_E_INVALID, "bad argument");
+    *total_out = conn_build(view(*g), assignment, k, out_offsets, out_blocks, out_weights,
+                            (cudaStream_t)stream);
+  });
+}
+
+__global__ void k_lp_export(int n, const unsigned char* tm, unsigned char* out) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    out[v] = tm[v];
+}
+
+extern "C" int gim_lp_pass(const gim_graph* g, const int32_t* assignment, const uint8_t* locked,
+                           const gim_topology* t, int32_t jet, double jet_c, uint8_t* out_cand,
+                           int32_t* out_dest, uint8_t* out_to_move, int64_t* movers_out,
+                           void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    RefineLevel L;
+    L.g = view(*g);
+    prepare_level(L, tp.k, s);
+    RefineBuffers rb;
+    alloc_refine_buffers(rb, g->n, tp.k, s);
+    lp_pass(L, tp, assignment, locked, jet, jet_c, rb, s);
+    if (g->n) {
+      GIM_CUDA(cudaMemcpyAsync(out_cand, rb.cand.get(), g->n, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(out_dest, rb.dest.get(), sizeof(int) * g->n, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(out_to_move, rb.to_move.get(), g->n, cudaMemcpyDeviceToDevice, s));
+    }
+    long long mv = read_scalar(rb.movers.get(), s);
+    if (movers_out) *movers_out = mv;
+  });
+}
+
+__global__ void k_rb_export(int n, const int* part, const unsigned char* ovl, const int* target,
+                            const unsigned char* tm, const int* dest, unsigned char* cand,
+                            int* odest, unsigned char* otm) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    bool c = ovl[part[v]] && target[v] >= 0;
+    cand[v] = c;
+    odest[v] = c ? target[v] : part[v];
+    otm[v] = tm[v];
+    (void)dest;
+  }
+}
+
+extern "C" int gim_rebalance(const gim_graph* g, const int32_t* assignment,
+                             const int64_t* block_weights, const gim_topology* t, int32_t strong,
+                             double sigma, double l_max, int32_t rho, uint64_t seed,
+                             int64_t pass_counter, uint8_t* out_cand, int32_t* out_dest,
+                             uint8_t* out_to_move, int32_t* incomplete_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t && block_weights, GIM_E_INVALID, "null argument");
+    GIM_CHECK(rho >= 1, GIM_E_INVALID, "rho must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    const int k = tp.k;
+    std::vector<long long> bw((size_t)k);
+    GIM_CUDA(cudaMemcpyAsync(bw.data(), block_weights, sizeof(long long) * k,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    std::vector<unsigned char> masks((size_t)k * 2);
+    std::vector<int> el;
+    for (int b = 0; b < k; ++b) {
+      masks[b] = (double)bw[b] > l_max;
+      masks[k + b] = (double)bw[b] < sigma;
+      if (masks[k + b]) el.push_back(b);
+    }
+    DBuf<unsigned char> dm((size_t)k * 2, s);
+    DBuf<int> de((size_t)k, s);
+    GIM_CUDA(cudaMemcpyAsync(dm.get(), masks.data(), (size_t)k * 2, cudaMemcpyHostToDevice, s));
+    if (!el.empty())
+      GIM_CUDA(cudaMemcpyAsync(de.get(), el.data(), sizeof(int) * el.size(), cudaMemcpyHostToDevice, s));
+    RefineLevel L;
+    L.g = view(*g);
+    prepare_level(L, k, s);
+    RefineBuffers rb;
+    alloc_refine_buffers(rb, g->n, k, s);
+    rebalance_pass(L, tp, assignment, reinterpret_cast<const long long*>(block_weights),
+                   strong != 0, l_max, rho, seed, pass_counter,
+                   dm.get(), dm.get() + k, de.get(), (int)el.size(), rb, s);
+    if (g->n) {
+      k_rb_export<<<grid_for(g->n, 256), 256, 0, s>>>(g->n, assignment, dm.get(), rb.dest2.get(),
+                                                       rb.to_move.get(), rb.dest.get(), out_cand,
+                                                       out_dest, out_to_move);
+      GIM_LAUNCH_CHECK();
+    }
+    GIM_CUDA(cudaStreamSynchronize(s));
+    if (incomplete_out) *incomplete_out = el.empty() ? 1 : 0;
+  });
+}
+
+extern "C" int gim_apply_moves(const gim_graph* g, int32_t* assignment, int64_t* block_weights,
+                               const uint8_t* to_move, const int32_t* dest, const gim_topology* t,
+                               int64_t* delta_j_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    RefineLevel L;
+    L.g = view(*g);
+    prepare_level(L, tp.k, s);
+    RefineBuffers rb;
+    alloc_refine_buffers(rb, g->n, tp.k, s);
+    if (g->n) {
+      GIM_CUDA(cudaMemcpyAsync(rb.to_move.get(), to_move, g->n, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(rb.dest.get(), dest, sizeof(int) * g->n, cudaMemcpyDeviceToDevice, s));
+    }
+    apply_moves(L, tp, assignment, reinterpret_cast<long long*>(block_weights), rb, s);
+    long long dj = read_scalar(rb.dj.get(), s);
+    if (delta_j_out) *delta_j_out = dj;
+  });
+}
+
+extern "C" int gim_refine(const gim_graph* g, const gim_topology* t, int32_t* assignment,
+                          int64_t* block_weights, double phi, int32_t i_max, int32_t i_w_max,
+                          double sigma_fraction, int32_t rho, int32_t jet, double jet_c,
+                          uint64_t seed, double l_max, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    RefineLevel L;
+    L.g = view(*g);
+    RefCfg c;
+    c.phi = phi;
+    c.i_max = i_max;
+    c.i_w_max = i_w_max;
+    c.sigma_fraction = sigma_fraction;
+    c.rho = rho;
+    c.jet = jet;
+    c.jet_c = jet_c;
+    c.seed = seed;
+    RunStats st;
+    refine(L, tp, assignment, reinterpret_cast<long long*>(block_weights), c, l_max, st, s);
+  });
+}
+
+extern "C" int gim_greedy_graph_growing(const gim_graph* g, int32_t k, int32_t* part,
+                                        void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && k >= 1, GIM_E_INVALID, "bad argument");
+    GIM_CHECK(g->n > k || k == 1, GIM_E_INVALID, "greedy graph growing needs n > k");
+    greedy_graph_growing(view(*g), k, part, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int gim_internal_partitioner(const gim_graph* g, int32_t k, double eps_local,
+                                        uint64_t seed, int32_t* part, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && k >= 1, GIM_E_INVALID, "bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevGraph dg = view(*g);
+    long long total = total_vertex_weight(dg, s);
+    RunStats st;
+    internal_partitioner(dg, total, k, eps_local, seed, part, st, s);
+    GIM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int gim_hierarchical_multisection(const gim_graph* g, const gim_topology* t, double eps,
+                                             uint64_t seed, int32_t* assignment, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevGraph dg = view(*g);
+    GIM_CHECK(dg.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+    (void)get_topo(t->levels, t->hierarchy, t->distances);
+    long long total = total_vertex_weight(dg, s);
+    std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
+    std::vector<long long> d(t->distances, t->distances + t->levels);
+    RunStats st;
+    hierarchical_multisection(dg, total, h, d, eps, seed, assignment, st, s);
+    GIM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int gim_integrated_map_device(const gim_graph* g, const gim_topology* t, double eps,
+                                         uint64_t seed, const gim_im_params* params,
+                                         int32_t* out_assignment, int64_t* out_block_weights,
+                                         gim_im_stats* stats, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t && out_assignment && out_block_weights, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevGraph dg = view(*g);
+    GIM_CHECK(dg.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+    gim_im_params P = params ? *params : default_params();
+    long long total = total_vertex_weight(dg, s);
+    integrated_map_device(dg, total, *t, eps, seed, P, out_assignment,
+                          reinterpret_cast<long long*>(out_block_weights), stats, s);
+  });
+}
+
+extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64_t* targets,
+                                  const int64_t* edge_weights, const int64_t* vertex_weights,
+                                  const gim_topology* t, double eps, uint64_t seed,
+                                  const gim_im_params* params, int64_t* out_assignment,
+                                  int64_t* out_block_weights, gim_im_stats* stats, void* stream) {
+  return guard([&] {
+    GIM_CHECK(t && offsets && out_assignment && out_block_weights, GIM_E_INVALID,
+              "null argument");
+    GIM_CHECK(n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+    cudaStream_t s = (cudaStream_t)stream;
+    gim_im_params P = params ? *params : default_params();
+    OwnedGraph G;
+    upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    DBuf<int> part((size_t)n, s);
+    DBuf<long long> bw((size_t)tp.k, s);
+    integrated_map_device(G.view(), G.total_vw, *t, eps, seed, P, part.get(), bw.get(), stats, s);
+    DBuf<long long> wide((size_t)n, s);
+    k_widen<<<grid_for(n, 256), 256, 0, s>>>((int)n, part.get(), wide.get());
+    count_launch();
+    GIM_CUDA(cudaMemcpyAsync(out_assignment, wide.get(), sizeof(long long) * n,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(out_block_weights, bw.get(), sizeof(long long) * tp.k,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    if (stats) stats->kernel_launches = launches();
+  });
+}
+
+extern "C" int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream) {
+  return guard([&] { fill_sources(n, offsets, sources, (cudaStream_t)stream); });
+}
+
+extern "C" int64_t gim_launch_count(void) { return launches(); }
+extern "C" void gim_reset_launch_count(void) { reset_launches(); }

@@ -1,0 +1,345 @@
+// Initial mapping kernels: greedy graph growing (K15), subgraph extraction
+// (K14) and the leaf scatter of the hierarchical multisection.
+//
+// Reference: pipelines.py (_multi_source_bfs :113-129, greedy_graph_growing
+// :132-188, hierarchical_multisection leaf :78-80), graph.py
+// (extract_subgraphs :357-389).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+
+namespace gim {
+
+// ---------------------------------------------------------------------------
+// K15 greedy graph growing, one warp per subgraph (the coarsest partitioner
+// graphs hold a few hundred vertices).  Semantics of pipelines.py:132-188:
+//  * seeds: farthest-first over hop distances (BFS from {0}; then from the
+//    seed set), preferring the lowest unreachable vertex, else the first
+//    vertex of maximum distance;
+//  * growth: the lightest block (ties: lowest id) claims, among unassigned
+//    vertices it is connected to, the one with maximum connectivity (ties:
+//    lowest id) — exactly the entry its lazy max-heap would pop — or the
+//    lowest unassigned vertex when it has none.
+// Scratch per subgraph: dist[n], conn[k][n] (global, L1/L2 resident).
+
+__device__ void warp_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
+                         int ns) {
+  const int lane = lane_id();
+  for (int v = lane; v < n; v += 32) dist[v] = -1;
+  __syncwarp();
+  for (int i = lane; i < ns; i += 32) dist[seeds[i]] = 0;
+  __syncwarp();
+  for (int d = 0;; ++d) {
+    bool changed = false;
+    for (int v = lane; v < n; v += 32) {
+      if (dist[v] != d) continue;
+      for (int e = off[v]; e < off[v + 1]; ++e) {
+        int u = tgt[e];
+        if (dist[u] < 0) {
+          dist[u] = d + 1;  // benign race: every writer stores d + 1
+          changed = true;
+        }
+      }
+    }
+    __syncwarp();
+    if (!__any_sync(0xffffffffu, changed)) break;
+  }
+}
+
+// farthest-first seed: lowest unreached vertex if any, else first argmax
+__device__ int warp_pick_seed(int n, const int* dist) {
+  const int lane = lane_id();
+  int unreached = INT_MAX;
+  int bd = -1, bv = INT_MAX;
+  for (int v = lane; v < n; v += 32) {
+    int d = dist[v];
+    if (d < 0) unreached = min(unreached, v);
+    else if (d > bd) { bd = d; bv = v; }  // ascending v per lane: first max
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unreached = min(unreached, __shfl_xor_sync(0xffffffffu, unreached, o));
+    int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+    int v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    if (d2 > bd || (d2 == bd && v2 < bv)) { bd = d2; bv = v2; }
+  }
+  return unreached != INT_MAX ? unreached : bv;
+}
+
+struct GggJob {
+  int n;
+  int k;
+  const int* off;
+  const int* tgt;
+  const int* w;
+  const int* vw;
+  int* part;        // out [n]
+  int* scratch;     // dist[n] + seeds[k] + conn[k*n]
+  long long* bwork; // [k]
+};
+
+__global__ void __launch_bounds__(32) k_ggg(const GggJob* jobs, int njobs) {
+  const int j = blockIdx.x;
+  if (j >= njobs) return;
+  const GggJob J = jobs[j];
+  const int n = J.n, k = J.k;
+  const int lane = lane_id();
+  int* dist = J.scratch;
+  int* seeds = dist + n;
+  int* conn = seeds + k;
+  if (k == 1) {
+    for (int v = lane; v < n; v += 32) J.part[v] = 0;
+    return;
+  }
+  // seeds (pipelines.py:143-153)
+  int zero = 0;
+  warp_bfs(n, J.off, J.tgt, dist, &zero, 1);
+  int s0 = warp_pick_seed(n, dist);
+  if (lane == 0) seeds[0] = s0;
+  __syncwarp();
+  for (int ns = 1; ns < k; ++ns) {
+    warp_bfs(n, J.off, J.tgt, dist, seeds, ns);
+    int sv = warp_pick_seed(n, dist);
+    if (lane == 0) seeds[ns] = sv;
+    __syncwarp();
+  }
+  // growth (pipelines.py:155-188)
+  for (int v = lane; v < n; v += 32) J.part[v] = -1;
+  for (long long i = lane; i < (long long)k * n; i += 32) conn[i] = 0;
+  for (int b = lane; b < k; b += 32) J.bwork[b] = 0;
+  __syncwarp();
+  int assigned = 0;
+  int next_free = 0;
+  auto claim = [&](int v, int b) {
+    if (lane == 0) {
+      J.part[v] = b;
+      J.bwork[b] += J.vw[v];
+    }
+    __syncwarp();
+    for (int e = J.off[v] + lane; e < J.off[v + 1]; e += 32) {
+      int u = J.tgt[e];
+      if (J.part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per lane
+    }
+    __syncwarp();
+    ++assigned;
+  };
+  for (int b = 0; b < k; ++b) claim(seeds[b], b);
+  while (assigned < n) {
+    // lightest block, lowest id on ties
+    long long bwv = LLONG_MAX;
+    int bb = INT_MAX;
+    for (int b = lane; b < k; b += 32) {
+      long long x = J.bwork[b];
+      if (x < bwv) { bwv = x; bb = b; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
+      int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+      if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
+    }
+    const int* cb = conn + (long long)bb * n;
+    int bc = 0, bv = INT_MAX;
+    for (int u = lane; u < n; u += 32) {
+      int c = cb[u];
+      if (c > bc && J.part[u] < 0) { bc = c; bv = u; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+      int v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      if (c2 > bc || (c2 == bc && v2 < bv)) { bc = c2; bv = v2; }
+    }
+    int v = bv;
+    if (bc == 0) {  // frontier dried up: lowest unassigned vertex
+      while (J.part[next_free] >= 0) ++next_free;
+      v = next_free;
+    }
+    claim(v, bb);
+  }
+}
+
+void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
+  DBuf<int> scratch((size_t)g.n + k + (size_t)k * g.n, s);
+  DBuf<long long> bwork((size_t)k, s);
+  GggJob job{g.n, k, g.off, g.tgt, g.w, g.vw, part, scratch.get(), bwork.get()};
+  DBuf<GggJob> dj(1, s);
+  GIM_CUDA(cudaMemcpyAsync(dj.get(), &job, sizeof(GggJob), cudaMemcpyHostToDevice, s));
+  k_ggg<<<1, 32, 0, s>>>(dj.get(), 1);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  GIM_CUDA(cudaStreamSynchronize(s));  // job struct lives on this stack frame
+}
+
+// ---------------------------------------------------------------------------
+// K14 extract_subgraphs (graph.py:357-389): vertices of part j keep their
+// relative order (local ids), edges internal to a part keep CSR order.
+// Stable radix sort of (part, v) gives the concatenated vertex order; each
+// row's surviving slots are copied in order.
+
+__global__ void k_local_ids(int n, const int* __restrict__ order, const int* __restrict__ part,
+                            const int* __restrict__ pstart, int* __restrict__ local) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int v = order[i];
+    local[v] = i - pstart[part[v]];
+  }
+}
+
+__global__ void k_part_starts(int n, const unsigned* __restrict__ keys, int* __restrict__ pstart) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (i == 0 || keys[i] != keys[i - 1]) pstart[keys[i]] = i;
+}
+
+__global__ void k_iota_keys(int n, const int* __restrict__ part, unsigned* keys, int* vals) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    keys[i] = (unsigned)part[i];
+    vals[i] = i;
+  }
+}
+
+struct KeptDeg {
+  const int* order;
+  const int* off;
+  const int* tgt;
+  const int* part;
+  __device__ int operator()(long long i) const {
+    int v = order[i];
+    int pv = part[v], c = 0;
+    for (int e = off[v]; e < off[v + 1]; ++e) c += part[tgt[e]] == pv;
+    return c;
+  }
+};
+
+__global__ void k_copy_rows(int n, const int* __restrict__ order, const int* __restrict__ off,
+                            const int* __restrict__ tgt, const int* __restrict__ w,
+                            const int* __restrict__ vw, const int* __restrict__ part,
+                            const int* __restrict__ local, const int* __restrict__ pstart,
+                            const int* __restrict__ noff, int* __restrict__ ntgt,
+                            int* __restrict__ nw, int* __restrict__ nsrc, int* __restrict__ nvw) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int v = order[i];
+    int pv = part[v];
+    int pos = noff[i];
+    int li = i - pstart[pv];
+    for (int e = off[v]; e < off[v + 1]; ++e) {
+      int u = tgt[e];
+      if (part[u] != pv) continue;
+      ntgt[pos] = local[u];
+      nw[pos] = w[e];
+      nsrc[pos] = li;
+      ++pos;
+    }
+    nvw[i] = vw[v];
+  }
+}
+
+__global__ void k_rebase(int cnt, const int* __restrict__ src, int base, int* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    dst[i] = src[i] - base;
+}
+
+__global__ void k_gather(int n, const int* __restrict__ idx, const int* __restrict__ src,
+                         int* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void k_scatter_const(int n, const int* __restrict__ idx, int value, int* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[idx[i]] = value;
+}
+
+void gather(int n, const int* idx, const int* src, int* dst, cudaStream_t s) {
+  if (n == 0) return;
+  k_gather<<<grid_for(n, 256), 256, 0, s>>>(n, idx, src, dst);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+void scatter_const(int n, const int* idx, int value, int* dst, cudaStream_t s) {
+  if (n == 0) return;
+  k_scatter_const<<<grid_for(n, 256), 256, 0, s>>>(n, idx, value, dst);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+// splits g by part[] into `parts` owned subgraphs + their global ids
+void extract_subgraphs(const DevGraph& g, const int* part, int parts,
+                       std::vector<OwnedGraph>& subs, std::vector<DBuf<int>>& ids,
+                       cudaStream_t s) {
+  const int n = g.n;
+  subs.clear();
+  ids.clear();
+  subs.resize(parts);
+  ids.resize(parts);
+  DBuf<unsigned> keys((size_t)std::max(n, 1), s), keys2((size_t)std::max(n, 1), s);
+  DBuf<int> order((size_t)std::max(n, 1), s), vals2((size_t)std::max(n, 1), s);
+  DBuf<int> pstart((size_t)parts + 1, s), local((size_t)std::max(n, 1), s);
+  DBuf<int> noff((size_t)n + 1, s);
+  int grid = grid_for(n, 256);
+  k_iota_keys<<<grid, 256, 0, s>>>(n, part, keys.get(), order.get());
+  count_launch();
+  radix_sort_pairs<unsigned, int>(n, keys.get(), order.get(), keys2.get(), vals2.get(),
+                                  bit_length((unsigned long long)parts), s);
+  // pstart[j] = first index of part j (parts without vertices: fixed below)
+  GIM_CUDA(cudaMemsetAsync(pstart.get(), 0xff, sizeof(int) * ((size_t)parts + 1), s));
+  k_part_starts<<<grid, 256, 0, s>>>(n, keys.get(), pstart.get());
+  count_launch();
+  std::vector<int> hs((size_t)parts + 1);
+  GIM_CUDA(cudaMemcpyAsync(hs.data(), pstart.get(), sizeof(int) * ((size_t)parts + 1),
+                           cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  hs[parts] = n;
+  for (int j = parts - 1; j >= 0; --j)
+    if (hs[j] < 0) hs[j] = hs[j + 1];
+  GIM_CUDA(cudaMemcpyAsync(pstart.get(), hs.data(), sizeof(int) * ((size_t)parts + 1),
+                           cudaMemcpyHostToDevice, s));
+  k_local_ids<<<grid, 256, 0, s>>>(n, order.get(), part, pstart.get(), local.get());
+  count_launch();
+  DBuf<int> m2tot(1, s);
+  exclusive_scan<int>(n, KeptDeg{order.get(), g.off, g.tgt, part}, StoreTo<int>{noff.get()},
+                      m2tot.get(), s);
+  int m2 = 0;
+  GIM_CUDA(cudaMemcpyAsync(&m2, m2tot.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaMemcpyAsync(noff.get() + n, m2tot.get(), sizeof(int), cudaMemcpyDeviceToDevice, s));
+  DBuf<int> ntgt((size_t)std::max(m2, 1), s), nw((size_t)std::max(m2, 1), s),
+      nsrc((size_t)std::max(m2, 1), s), nvw((size_t)std::max(n, 1), s);
+  k_copy_rows<<<grid, 256, 0, s>>>(n, order.get(), g.off, g.tgt, g.w, g.vw, part, local.get(),
+                                   pstart.get(), noff.get(), ntgt.get(), nw.get(), nsrc.get(),
+                                   nvw.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  std::vector<int> hoff((size_t)n + 1);
+  GIM_CUDA(cudaMemcpyAsync(hoff.data(), noff.get(), sizeof(int) * ((size_t)n + 1),
+                           cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  for (int j = 0; j < parts; ++j) {
+    int v0 = hs[j], v1 = hs[j + 1];
+    int nj = v1 - v0;
+    int e0 = hoff[v0], e1 = hoff[v1];
+    OwnedGraph& sg = subs[j];
+    sg.n = nj;
+    sg.m2 = e1 - e0;
+    sg.off = DBuf<int>((size_t)nj + 1, s);
+    sg.tgt = DBuf<int>((size_t)std::max(e1 - e0, 1), s);
+    sg.w = DBuf<int>((size_t)std::max(e1 - e0, 1), s);
+    sg.src = DBuf<int>((size_t)std::max(e1 - e0, 1), s);
+    sg.vw = DBuf<int>((size_t)std::max(nj, 1), s);
+    ids[j] = DBuf<int>((size_t)std::max(nj, 1), s);
+    k_rebase<<<grid_for(nj + 1, 256), 256, 0, s>>>(nj + 1, noff.get() + v0, e0, sg.off.get());
+    count_launch();
+    if (e1 > e0) {
+      GIM_CUDA(cudaMemcpyAsync(sg.tgt.get(), ntgt.get() + e0, sizeof(int) * (e1 - e0), cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(sg.w.get(), nw.get() + e0, sizeof(int) * (e1 - e0), cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(sg.src.get(), nsrc.get() + e0, sizeof(int) * (e1 - e0), cudaMemcpyDeviceToDevice, s));
+    }
+    if (nj) {
+      GIM_CUDA(cudaMemcpyAsync(sg.vw.get(), nvw.get() + v0, sizeof(int) * nj, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(ids[j].get(), order.get() + v0, sizeof(int) * nj, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  GIM_LAUNCH_CHECK();
+}
+
+}  // namespace gim

@@ -53,4 +53,49 @@ void total_cost(const DevGraph& g, const int* part, const Topo& t, long long* j_
 void block_weights(int n, const int* vw, const int* part, int k, long long* bw,
                    cudaStream_t s);
 
+// ---- coarsen.cu
+void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
+               unsigned long long seed, long long* matched, cudaStream_t s);
+long long two_hop(const DevGraph& g, int* partner, double l_max, long long matched_now,
+                  long long* matched_d, cudaStream_t s);
+int coarse_map(int n, const int* partner, int* cmap, cudaStream_t s);
+long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off, int* c_tgt,
+                        int* c_w, int* c_vw, int* c_src, cudaStream_t s);
+void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cudaStream_t s);
+void project(int n, const int* cmap, const int* pc, int* pf, cudaStream_t s);
+
+// ---- refine.cu
+// one CSR level prepared for refinement: group width + heavy-vertex list
+struct RefineLevel {
+  DevGraph g;
+  int vw = 32;       // lanes per vertex on the register path
+  int n_heavy = 0;   // vertices with degree > vw (shared-memory path)
+  DBuf<int> heavy;
+};
+
+// scratch of one refinement (sized for the finest level it serves)
+struct RefineBuffers {
+  DBuf<unsigned char> cand, to_move, locks;
+  DBuf<int> dest, dest2;
+  DBuf<long long> gkey;
+  DBuf<unsigned int> rkeys, rkeys2;
+  DBuf<int> rvals, rvals2;
+  DBuf<long long> rexcl;
+  DBuf<int> gstart, count;
+  DBuf<long long> movers, dj;
+};
+
+void prepare_level(RefineLevel& L, int k, cudaStream_t s);
+void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s);
+void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigned char* locked,
+             int jet, double jet_c, RefineBuffers& rb, cudaStream_t s);
+void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const long long* bw,
+                    bool strong, double l_max, int rho, unsigned long long seed,
+                    long long pass_counter, const unsigned char* ovl, const unsigned char* elig,
+                    const int* elig_list, int n_elig, RefineBuffers& rb, cudaStream_t s);
+void apply_moves(const RefineLevel& L, const Topo& t, int* part, long long* bw,
+                 RefineBuffers& rb, cudaStream_t s);
+long long conn_build(const DevGraph& g, const int* part, int k, int* c_off, int* c_blocks,
+                     int* c_w, cudaStream_t s);
+
 }  // namespace gim

@@ -1,0 +1,774 @@
+// Refinement kernels: Jet-style label propagation (K9/K10), weak/strong
+// rebalancing (K11/K12), move application with exact J delta (K13), and the
+// block-connectivity table (K8, parity unit).
+//
+// Reference: refinement.py (_best_target :168-190, _gain_to :193-198,
+// label_propagation_pass :201-270, _rebalance_candidates :273-309,
+// weak_rebalance :312-347, strong_rebalance :350-386), mapping.py
+// (BlockConnectivity :124-249, apply_moves :252-282).
+//
+// Per-vertex connectivity is never stored between iterations: every pass
+// rebuilds conn(v, .) on chip from the CSR row and Pi (registers for
+// degree <= VW, a per-warp shared-memory block table otherwise), which is
+// exact and keeps the HBM traffic at one row sweep per pass.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+
+namespace gim {
+
+constexpr long long kGainNone = LLONG_MIN;
+
+// distance between two digit codes (see Topo)
+__device__ __forceinline__ long long cdist(const long long* dbit, unsigned long long a,
+                                           unsigned long long b) {
+  unsigned long long c = a ^ b;
+  return c ? dbit[63 - __clzll(c)] : 0ll;
+}
+
+struct Best {
+  long long gain;
+  int b;
+};
+
+// (gain desc, block asc); b < 0 = none
+__device__ __forceinline__ bool best_better(long long g1, int b1, long long g2, int b2) {
+  if (b1 < 0) return false;
+  if (b2 < 0) return true;
+  if (g1 != g2) return g1 > g2;
+  return b1 < b2;
+}
+
+// shared per-block copy of dbit
+__device__ __forceinline__ void load_dbit(long long* s_dbit, const Topo& t) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_dbit[i] = t.dbit[i];
+}
+
+// ---------------------------------------------------------------------------
+// Per-vertex gain evaluation, register path (degree <= VW).
+// Lane j of the group holds neighbour j: its block code and edge weight.
+// cost(b_j) = sum_i w_i D(b_j, b_i) by a VW-step shuffle broadcast;
+// gain(b_j) = cur - cost(b_j), cur = cost(own)  (Eq. 1, refinement.py:171-186).
+
+struct VertexEval {
+  long long cur;       // sum_u w D(own, Pi u)
+  long long conn_own;  // conn(v, own)
+  long long best_gain;
+  int best_b;          // -1: no admissible adjacent block
+};
+
+template <int VW>
+__device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, int myw,
+                                                const Topo& t, const long long* s_dbit,
+                                                const unsigned char* allowed) {
+  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
+  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
+  long long wv = valid ? myw : 0;
+  long long cur = wv * cdist(s_dbit, ocode, mycode);
+  long long co = (valid && myb == own) ? wv : 0;
+  long long cost = 0;
+#pragma unroll 4
+  for (int i = 0; i < VW; ++i) {
+    unsigned long long ci = __shfl_sync(0xffffffffu, mycode, i, VW);
+    long long wi = __shfl_sync(0xffffffffu, wv, i, VW);
+    cost += wi * cdist(s_dbit, mycode, ci);
+  }
+#pragma unroll
+  for (int o = VW / 2; o > 0; o >>= 1) {
+    cur += __shfl_xor_sync(0xffffffffu, cur, o);
+    co += __shfl_xor_sync(0xffffffffu, co, o);
+  }
+  bool cand = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
+  long long g = cand ? cur - cost : kGainNone;
+  int b = cand ? myb : -1;
+#pragma unroll
+  for (int o = VW / 2; o > 0; o >>= 1) {
+    long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
+    int b2 = __shfl_xor_sync(0xffffffffu, b, o);
+    if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
+  }
+  VertexEval r;
+  r.cur = cur;
+  r.conn_own = co;
+  r.best_gain = g;
+  r.best_b = b;
+  return r;
+}
+
+// cost of moving to a fixed block `tb` (for the rebalance hash fallback)
+template <int VW>
+__device__ __forceinline__ long long cost_regs(bool valid, int myb, int myw, int tb,
+                                               const Topo& t, const long long* s_dbit) {
+  unsigned long long tc = __ldg(t.code + (tb < 0 ? 0 : tb));
+  unsigned long long mc = myb >= 0 ? __ldg(t.code + myb) : 0ull;
+  long long c = valid ? (long long)myw * cdist(s_dbit, tc, mc) : 0;
+#pragma unroll
+  for (int o = VW / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Per-vertex gain evaluation, shared-memory path (degree > VW): one warp per
+// vertex, conn(v, b) accumulated into a dense per-warp block table with
+// shared atomics, compacted to the nonzero (block, conn) list, then
+// cost(b) = sum_j conn_j D(b, b_j) over the list.
+
+struct WarpTable {
+  int* tab;    // [k]
+  int* lb;     // [k] nonzero blocks
+  int* lw;     // [k] their conn
+};
+
+__device__ __forceinline__ int warp_build_table(const WarpTable& wt, int k, int e0, int e1,
+                                                const int* __restrict__ tgt,
+                                                const int* __restrict__ w,
+                                                const int* __restrict__ part) {
+  const int lane = lane_id();
+  for (int i = lane; i < k; i += 32) wt.tab[i] = 0;
+  __syncwarp();
+  for (int e = e0 + lane; e < e1; e += 32) atomicAdd(&wt.tab[part[tgt[e]]], w[e]);
+  __syncwarp();
+  int s = 0;
+  for (int base = 0; base < k; base += 32) {
+    int i = base + lane;
+    int x = i < k ? wt.tab[i] : 0;
+    unsigned m = __ballot_sync(0xffffffffu, x != 0);
+    if (x != 0) {
+      int pos = s + __popc(m & ((1u << lane) - 1u));
+      wt.lb[pos] = i;
+      wt.lw[pos] = x;
+    }
+    s += __popc(m);
+  }
+  __syncwarp();
+  return s;
+}
+
+__device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int own,
+                                                 const Topo& t, const long long* s_dbit,
+                                                 const unsigned char* allowed) {
+  const int lane = lane_id();
+  const unsigned long long oc = __ldg(t.code + own);
+  long long cur = 0;
+  for (int j = lane; j < s; j += 32)
+    cur += (long long)wt.lw[j] * cdist(s_dbit, oc, __ldg(t.code + wt.lb[j]));
+  cur = warp_sum_ll(cur);
+  long long g = kGainNone;
+  int b = -1;
+  for (int i = lane; i < s; i += 32) {
+    int bi = wt.lb[i];
+    if (bi == own || (allowed && !allowed[bi])) continue;
+    unsigned long long ci = __ldg(t.code + bi);
+    long long cost = 0;
+    for (int j = 0; j < s; ++j)
+      cost += (long long)wt.lw[j] * cdist(s_dbit, ci, __ldg(t.code + wt.lb[j]));
+    long long gi = cur - cost;
+    if (best_better(gi, bi, g, b)) { g = gi; b = bi; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
+    int b2 = __shfl_xor_sync(0xffffffffu, b, o);
+    if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
+  }
+  VertexEval r;
+  r.cur = cur;
+  r.conn_own = wt.tab[own];
+  r.best_gain = g;
+  r.best_b = b;
+  return r;
+}
+
+__device__ __forceinline__ long long cost_table(const WarpTable& wt, int s, int tb,
+                                                const Topo& t, const long long* s_dbit) {
+  const unsigned long long tc = __ldg(t.code + tb);
+  long long c = 0;
+  for (int j = lane_id(); j < s; j += 32)
+    c += (long long)wt.lw[j] * cdist(s_dbit, tc, __ldg(t.code + wt.lb[j]));
+  return warp_sum_ll(c);
+}
+
+// ---------------------------------------------------------------------------
+// shared per-vertex decisions
+
+struct LpOut {
+  unsigned char* cand;
+  int* dest;
+  long long* gkey;  // gain for candidates, kGainNone otherwise
+};
+
+struct LpParams {
+  const unsigned char* locked;  // null = no locks
+  int jet;
+  double jet_c;
+};
+
+__device__ __forceinline__ void lp_decide(int v, int own, const VertexEval& r,
+                                          const LpParams& p, const LpOut& o) {
+  bool ok = false;
+  if (r.best_b >= 0) {
+    if (r.best_gain >= 0) ok = true;
+    else if (p.jet) ok = (double)(-r.best_gain) < floor(p.jet_c * (double)r.conn_own);
+  }
+  o.cand[v] = ok ? 1 : 0;
+  o.dest[v] = ok ? r.best_b : own;
+  o.gkey[v] = ok ? r.best_gain : kGainNone;
+}
+
+struct RbParams {
+  const unsigned char* ovl;    // [k] overloaded blocks
+  const unsigned char* elig;   // [k] eligible blocks (bw < sigma)
+  const int* elig_list;        // ascending eligible ids
+  int n_elig;
+  unsigned long long seed;
+  long long pass_counter;
+};
+
+struct RbOut {
+  int* target;      // -1: not a rebalance candidate
+  long long* gain;
+};
+
+// ---------------------------------------------------------------------------
+// K9 first filter / K11 candidates, register path.  mode 0 = LP, 1 = rebalance
+
+template <int VW>
+__global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* __restrict__ off,
+                                                   const int* __restrict__ tgt,
+                                                   const int* __restrict__ w,
+                                                   const int* __restrict__ part, Topo t,
+                                                   LpParams lp, LpOut lo, RbParams rb, RbOut ro) {
+  __shared__ long long s_dbit[64];
+  load_dbit(s_dbit, t);
+  __syncthreads();
+  constexpr int GPW = 32 / VW;
+  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int gi = lane / VW, li = lane % VW;
+  for (long long vb = wid * GPW; vb < n; vb += nw * GPW) {
+    const int v = (int)(vb + gi);
+    bool live = v < n;
+    int e0 = 0, d = 0, own = 0;
+    if (live) {
+      e0 = off[v];
+      d = off[v + 1] - e0;
+      own = part[v];
+      if (d > VW) live = false;  // handled by the shared-memory path
+      else if (mode == 0 && lp.locked && lp.locked[v]) {
+        live = false;
+        if (li == 0) { lo.cand[v] = 0; lo.dest[v] = own; lo.gkey[v] = kGainNone; }
+      } else if (mode == 1 && !rb.ovl[own]) {
+        live = false;
+        if (li == 0) ro.target[v] = -1;
+      }
+    }
+    const bool valid = live && li < d;
+    int myb = -1, myw = 0;
+    if (valid) {
+      myb = part[tgt[e0 + li]];
+      myw = w[e0 + li];
+    }
+    VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, t, s_dbit,
+                                 mode == 1 ? rb.elig : nullptr);
+    if (mode == 0) {
+      if (live && li == 0) lp_decide(v, own, r, lp, lo);
+    } else {
+      // fallback target: eligible[hash2(seed, v, pass) % n_elig] (refinement.py:302-307)
+      bool need = live && r.best_b < 0 && rb.n_elig > 0;
+      unsigned any = __ballot_sync(0xffffffffu, need);
+      int tb = -1;
+      if (need) {
+        unsigned long long h = hash2(rb.seed, (unsigned long long)v,
+                                     (unsigned long long)rb.pass_counter);
+        tb = rb.elig_list[h % (unsigned long long)rb.n_elig];
+      }
+      long long cost = 0;
+      if (any) cost = cost_regs<VW>(valid && need, myb, myw, need ? tb : 0, t, s_dbit);
+      if (live && li == 0) {
+        if (r.best_b >= 0) {
+          ro.target[v] = r.best_b;
+          ro.gain[v] = r.best_gain;
+        } else if (need) {
+          ro.target[v] = tb;
+          ro.gain[v] = r.cur - cost;
+        } else {
+          ro.target[v] = -1;  // no eligible block anywhere: incomplete
+        }
+      }
+    }
+  }
+}
+
+// K9/K11 for heavy vertices (degree > VW): one warp per listed vertex
+__global__ void __launch_bounds__(128) k_eval_table(int mode, int n_heavy,
+                                                    const int* __restrict__ heavy, int k,
+                                                    const int* __restrict__ off,
+                                                    const int* __restrict__ tgt,
+                                                    const int* __restrict__ w,
+                                                    const int* __restrict__ part, Topo t,
+                                                    LpParams lp, LpOut lo, RbParams rb,
+                                                    RbOut ro) {
+  extern __shared__ int smem[];
+  __shared__ long long s_dbit[64];
+  load_dbit(s_dbit, t);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  WarpTable wt;
+  wt.tab = smem + (size_t)warp * 3 * k;
+  wt.lb = wt.tab + k;
+  wt.lw = wt.lb + k;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_heavy; i += nwarps) {
+    const int v = heavy[i];
+    const int own = part[v];
+    if (mode == 0 && lp.locked && lp.locked[v]) {
+      if (lane == 0) { lo.cand[v] = 0; lo.dest[v] = own; lo.gkey[v] = kGainNone; }
+      continue;
+    }
+    if (mode == 1 && !rb.ovl[own]) {
+      if (lane == 0) ro.target[v] = -1;
+      continue;
+    }
+    int s = warp_build_table(wt, k, off[v], off[v + 1], tgt, w, part);
+    VertexEval r = eval_table(wt, s, own, t, s_dbit, mode == 1 ? rb.elig : nullptr);
+    if (mode == 0) {
+      if (lane == 0) lp_decide(v, own, r, lp, lo);
+    } else {
+      if (r.best_b >= 0) {
+        if (lane == 0) { ro.target[v] = r.best_b; ro.gain[v] = r.best_gain; }
+      } else if (rb.n_elig > 0) {
+        unsigned long long h = hash2(rb.seed, (unsigned long long)v,
+                                     (unsigned long long)rb.pass_counter);
+        int tb = rb.elig_list[h % (unsigned long long)rb.n_elig];
+        long long cost = cost_table(wt, s, tb, t, s_dbit);
+        if (lane == 0) { ro.target[v] = tb; ro.gain[v] = r.cur - cost; }
+      } else if (lane == 0) {
+        ro.target[v] = -1;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K10 second filter (refinement.py:246-269): candidate v is re-evaluated as if
+// every candidate neighbour ordered before it (higher gain, then lower id)
+// had moved; kept iff the re-evaluated gain is >= 0.
+
+template <int VW>
+__global__ void __launch_bounds__(256) k_lp_second(int n, const int* __restrict__ off,
+                                                   const int* __restrict__ tgt,
+                                                   const int* __restrict__ w,
+                                                   const int* __restrict__ part, Topo t,
+                                                   const unsigned char* __restrict__ cand,
+                                                   const int* __restrict__ dest,
+                                                   const long long* __restrict__ gkey,
+                                                   unsigned char* __restrict__ to_move,
+                                                   long long* __restrict__ movers) {
+  __shared__ long long s_dbit[64];
+  load_dbit(s_dbit, t);
+  __syncthreads();
+  constexpr int GPW = 32 / VW;
+  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int gi = lane / VW, li = lane % VW;
+  long long moved = 0;
+  for (long long vb = wid * GPW; vb < n; vb += nw * GPW) {
+    const int v = (int)(vb + gi);
+    const bool c = v < n && cand[v];
+    long long fut = 0;
+    if (c) {
+      const long long gv = gkey[v];
+      const unsigned long long oc = __ldg(t.code + part[v]);
+      const unsigned long long dc = __ldg(t.code + dest[v]);
+      for (int e = off[v] + li; e < off[v + 1]; e += VW) {
+        int u = tgt[e];
+        long long gu = gkey[u];
+        bool earlier = gu > gv || (gu == gv && u < v);  // kGainNone never earlier
+        int pos = earlier ? dest[u] : part[u];
+        unsigned long long pc = __ldg(t.code + pos);
+        fut += (long long)w[e] * (cdist(s_dbit, oc, pc) - cdist(s_dbit, dc, pc));
+      }
+    }
+#pragma unroll
+    for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
+    if (v < n && li == 0) {
+      bool m = c && fut >= 0;
+      to_move[v] = m ? 1 : 0;
+      moved += m;
+    }
+  }
+  block_sum_atomic<256>(moved, movers);
+}
+
+// ---------------------------------------------------------------------------
+// K13 apply moves (mapping.py:252-282) with the exact J delta:
+// dJ = sum over movers v, neighbours u of w (D(new v, new u) - D(old v, old u)),
+// doubled when u stays (its mirror slot (u, v) changes identically).
+// Block weights by warp-aggregated atomics.
+
+template <int VW>
+__global__ void __launch_bounds__(256) k_apply_delta(int n, const int* __restrict__ off,
+                                                     const int* __restrict__ tgt,
+                                                     const int* __restrict__ w,
+                                                     const int* __restrict__ vw,
+                                                     const int* __restrict__ part, Topo t,
+                                                     const unsigned char* __restrict__ to_move,
+                                                     const int* __restrict__ dest,
+                                                     long long* __restrict__ bw,
+                                                     long long* __restrict__ dj) {
+  __shared__ long long s_dbit[64];
+  load_dbit(s_dbit, t);
+  __syncthreads();
+  constexpr int GPW = 32 / VW;
+  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int gi = lane / VW, li = lane % VW;
+  long long acc = 0;
+  for (long long vb = wid * GPW; vb < n; vb += nw * GPW) {
+    const int v = (int)(vb + gi);
+    if (v < n && to_move[v]) {
+      const int ov = part[v], nv = dest[v];
+      const unsigned long long oc = __ldg(t.code + ov), nc = __ldg(t.code + nv);
+      for (int e = off[v] + li; e < off[v + 1]; e += VW) {
+        int u = tgt[e];
+        bool um = to_move[u];
+        int ou = part[u];
+        int nu = um ? dest[u] : ou;
+        long long d = cdist(s_dbit, nc, __ldg(t.code + nu)) - cdist(s_dbit, oc, __ldg(t.code + ou));
+        acc += (long long)w[e] * d * (um ? 1 : 2);
+      }
+      if (li == 0 && ov != nv) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&bw[ov]), (unsigned long long)(-(long long)vw[v]));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&bw[nv]), (unsigned long long)(long long)vw[v]);
+      }
+    }
+  }
+  block_sum_atomic<256>(acc, dj);
+}
+
+__global__ void k_commit(int n, const unsigned char* __restrict__ to_move,
+                         const int* __restrict__ dest, int* __restrict__ part) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (to_move[v]) part[v] = dest[v];
+}
+
+// ---------------------------------------------------------------------------
+// K12 rebalance selection (refinement.py:333-346 weak, 371-385 strong).
+// Candidates are compacted in vertex order (the reference visits source
+// blocks ascending, vertices ascending; since the sort key starts with the
+// block this is equivalent), stably radix-sorted by
+//   weak:   (source, cell)            cell = slot(gain) * rho + v % rho
+//   strong: (target, cell, source)
+// and a segmented prefix of vertex weights selects the taken prefix:
+//   weak: exclusive prefix < bw[src] - l_max;  strong: inclusive <= l_max - bw[tgt].
+
+__device__ __forceinline__ int slot_for_gain(long long g) {
+  if (g > 0) return 0;
+  if (g <= -1000) return 30;
+  long long x = -g;  // bisect_right over [0,1..10,20..100,200..1000]
+  if (x <= 10) return (int)x + 1;
+  if (x < 100) return 11 + (int)(x / 10);
+  if (x < 1000) return 20 + (int)(x / 100);
+  return 30;
+}
+
+struct RbFlag {
+  const int* part;
+  const unsigned char* ovl;
+  const int* target;
+  __device__ int operator()(long long v) const { return (ovl[part[v]] && target[v] >= 0) ? 1 : 0; }
+};
+
+struct RbKeyOut {
+  RbFlag f;
+  const long long* gain;
+  int rho, k, strong;
+  unsigned int* keys;
+  int* vals;
+  __device__ void operator()(long long v, int pos) const {
+    if (!f(v)) return;
+    int src = f.part[v];
+    int tb = f.target[v];
+    unsigned cell = (unsigned)(slot_for_gain(gain[v]) * rho + (int)(v % rho));
+    unsigned ncell = 31u * (unsigned)rho;
+    unsigned key = strong ? ((unsigned)tb * ncell + cell) * (unsigned)k + (unsigned)src
+                          : (unsigned)src * ncell + cell;
+    keys[pos] = key;
+    vals[pos] = (int)v;
+  }
+};
+
+struct RbWeight {
+  const int* vals;
+  const int* vw;
+  __device__ long long operator()(long long i) const { return vw[vals[i]]; }
+};
+
+__global__ void k_rb_group_start(int cnt, const unsigned int* __restrict__ keys, unsigned div,
+                                 int* __restrict__ gstart) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    unsigned gcur = keys[i] / div;
+    if (i == 0 || keys[i - 1] / div != gcur) gstart[gcur] = i;
+  }
+}
+
+__global__ void k_rb_select(int cnt, int strong, const unsigned int* __restrict__ keys,
+                            unsigned div, const int* __restrict__ vals,
+                            const long long* __restrict__ excl, const int* __restrict__ vw,
+                            const int* __restrict__ gstart, const long long* __restrict__ bw,
+                            double l_max, const int* __restrict__ target,
+                            unsigned char* __restrict__ to_move, int* __restrict__ dest,
+                            long long* __restrict__ movers) {
+  long long moved = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    unsigned grp = keys[i] / div;
+    long long before = excl[i] - excl[gstart[grp]];
+    int v = vals[i];
+    bool take;
+    if (strong) {
+      double room = l_max - (double)bw[grp];
+      take = (double)(before + vw[v]) <= room;
+    } else {
+      double excess = (double)bw[grp] - l_max;
+      take = (double)before < excess;
+    }
+    if (take) {
+      to_move[v] = 1;
+      dest[v] = target[v];
+      ++moved;
+    }
+  }
+  if (moved) atomicAdd(reinterpret_cast<unsigned long long*>(movers), (unsigned long long)moved);
+}
+
+// ---------------------------------------------------------------------------
+// host wrappers
+
+static void launch_eval(const RefineLevel& L, int mode, const Topo& t, const int* part,
+                        const LpParams& lp, const LpOut& lo, const RbParams& rb,
+                        const RbOut& ro, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  constexpr int B = 256;
+  long long groups = (long long)g.n * L.vw;
+  int grid = grid_for(groups, B, kSMs * 8);
+  switch (L.vw) {
+    case 4: k_eval_regs<4><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
+    case 8: k_eval_regs<8><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
+    case 16: k_eval_regs<16><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
+    default: k_eval_regs<32><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
+  }
+  count_launch();
+  if (L.n_heavy > 0) {
+    int k = t.k;
+    size_t smem = (size_t)4 * 3 * k * sizeof(int);
+    static int configured_smem = 0;
+    if ((int)smem > 48 * 1024 && (int)smem > configured_smem) {
+      GIM_CUDA(cudaFuncSetAttribute(k_eval_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      configured_smem = (int)smem;
+    }
+    int hgrid = grid_for((long long)L.n_heavy * 32, 128, kSMs * 4);
+    k_eval_table<<<hgrid, 128, smem, s>>>(mode, L.n_heavy, L.heavy.get(), k, g.off, g.tgt, g.w,
+                                          part, t, lp, lo, rb, ro);
+    count_launch();
+  }
+  GIM_LAUNCH_CHECK();
+}
+
+struct HeavyFlag {
+  const int* off;
+  int vw;
+  __device__ int operator()(long long v) const { return off[v + 1] - off[v] > vw ? 1 : 0; }
+};
+struct HeavyOut {
+  HeavyFlag f;
+  int* out;
+  __device__ void operator()(long long v, int pos) const {
+    if (f(v)) out[pos] = (int)v;
+  }
+};
+
+void prepare_level(RefineLevel& L, int k, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  double avg = g.n ? (double)g.m2 / g.n : 0.0;
+  L.vw = avg <= 3.0 ? 4 : avg <= 6.0 ? 8 : avg <= 12.0 ? 16 : 32;
+  GIM_CHECK((long long)k * 12 * 4 <= 200 * 1024 || g.n == 0, GIM_E_UNSUPPORTED,
+            "k too large for the shared-memory connectivity table (k <= 4266)");
+  L.heavy = DBuf<int>((size_t)std::max(g.n, 1), s);
+  DBuf<int> cnt(1, s);
+  HeavyFlag f{g.off, L.vw};
+  exclusive_scan<int>(g.n, f, HeavyOut{f, L.heavy.get()}, cnt.get(), s);
+  int h = 0;
+  if (g.n) {
+    GIM_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+  }
+  L.n_heavy = h;
+}
+
+void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigned char* locked,
+             int jet, double jet_c, RefineBuffers& rb, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  LpParams lp{locked, jet, jet_c};
+  LpOut lo{rb.cand.get(), rb.dest.get(), rb.gkey.get()};
+  RbParams rp{};
+  RbOut ro{};
+  launch_eval(L, 0, t, part, lp, lo, rp, ro, s);
+  GIM_CUDA(cudaMemsetAsync(rb.movers.get(), 0, sizeof(long long), s));
+  constexpr int B = 256;
+  int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
+  switch (L.vw) {
+    case 4: k_lp_second<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
+    case 8: k_lp_second<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
+    case 16: k_lp_second<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
+    default: k_lp_second<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
+  }
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
+void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const long long* bw,
+                    bool strong, double l_max, int rho, unsigned long long seed,
+                    long long pass_counter, const unsigned char* ovl, const unsigned char* elig,
+                    const int* elig_list, int n_elig, RefineBuffers& rb, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  const int k = t.k;
+  LpParams lp{};
+  LpOut lo{};
+  RbParams rp{ovl, elig, elig_list, n_elig, seed, pass_counter};
+  RbOut ro{rb.dest2.get(), rb.gkey.get()};
+  launch_eval(L, 1, t, part, lp, lo, rp, ro, s);
+  GIM_CUDA(cudaMemsetAsync(rb.to_move.get(), 0, (size_t)g.n, s));
+  GIM_CUDA(cudaMemsetAsync(rb.movers.get(), 0, sizeof(long long), s));
+  // compaction in vertex order + keys
+  RbFlag f{part, ovl, rb.dest2.get()};
+  RbKeyOut ko{f, rb.gkey.get(), rho, k, strong ? 1 : 0, rb.rkeys.get(), rb.rvals.get()};
+  exclusive_scan<int>(g.n, f, ko, rb.count.get(), s);
+  int cnt = 0;
+  GIM_CUDA(cudaMemcpyAsync(&cnt, rb.count.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  if (cnt == 0) return;
+  unsigned ncell = 31u * (unsigned)rho;
+  unsigned long long maxkey = strong ? (unsigned long long)k * ncell * k : (unsigned long long)k * ncell;
+  GIM_CHECK(maxkey < (1ull << 32), GIM_E_UNSUPPORTED, "rebalance key exceeds 32 bits");
+  radix_sort_pairs<unsigned int, int>(cnt, rb.rkeys.get(), rb.rvals.get(), rb.rkeys2.get(),
+                                      rb.rvals2.get(), bit_length(maxkey), s);
+  unsigned div = strong ? ncell * (unsigned)k : ncell;
+  exclusive_scan<long long>(cnt, RbWeight{rb.rvals.get(), g.vw}, StoreTo<long long>{rb.rexcl.get()},
+                            (long long*)nullptr, s);
+  int grid = grid_for(cnt, 256);
+  k_rb_group_start<<<grid, 256, 0, s>>>(cnt, rb.rkeys.get(), div, rb.gstart.get());
+  k_rb_select<<<grid, 256, 0, s>>>(cnt, strong ? 1 : 0, rb.rkeys.get(), div, rb.rvals.get(),
+                                   rb.rexcl.get(), g.vw, rb.gstart.get(), bw, l_max,
+                                   rb.dest2.get(), rb.to_move.get(), rb.dest.get(),
+                                   rb.movers.get());
+  count_launch(2);
+  GIM_LAUNCH_CHECK();
+}
+
+void apply_moves(const RefineLevel& L, const Topo& t, int* part, long long* bw,
+                 RefineBuffers& rb, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  GIM_CUDA(cudaMemsetAsync(rb.dj.get(), 0, sizeof(long long), s));
+  constexpr int B = 256;
+  int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
+  switch (L.vw) {
+    case 4: k_apply_delta<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
+    case 8: k_apply_delta<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
+    case 16: k_apply_delta<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
+    default: k_apply_delta<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
+  }
+  k_commit<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, rb.to_move.get(), rb.dest.get(), part);
+  count_launch(2);
+  GIM_LAUNCH_CHECK();
+}
+
+void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
+  size_t nn = (size_t)std::max(n, 1);
+  rb.cand = DBuf<unsigned char>(nn, s);
+  rb.to_move = DBuf<unsigned char>(nn, s);
+  rb.locks = DBuf<unsigned char>(nn, s);
+  rb.dest = DBuf<int>(nn, s);
+  rb.dest2 = DBuf<int>(nn, s);
+  rb.gkey = DBuf<long long>(nn, s);
+  rb.rkeys = DBuf<unsigned int>(nn, s);
+  rb.rkeys2 = DBuf<unsigned int>(nn, s);
+  rb.rvals = DBuf<int>(nn, s);
+  rb.rvals2 = DBuf<int>(nn, s);
+  rb.rexcl = DBuf<long long>(nn, s);
+  rb.gstart = DBuf<int>((size_t)k * 31 * 8 + 1, s);
+  rb.count = DBuf<int>(1, s);
+  rb.movers = DBuf<long long>(1, s);
+  rb.dj = DBuf<long long>(1, s);
+}
+
+// ---------------------------------------------------------------------------
+// K8 connectivity table (parity unit; mapping.py:141-158): per vertex the
+// sorted (block, conn) list, built by the same key-sort + segmented reduce
+// as contraction with key (v, Pi(u)).
+
+__global__ void k_conn_keys(long long m2, const int* __restrict__ src, const int* __restrict__ tgt,
+                            const int* __restrict__ w, const int* __restrict__ part, int k,
+                            unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m2;
+       e += (long long)gridDim.x * blockDim.x) {
+    keys[e] = (unsigned long long)src[e] * (unsigned long long)k + (unsigned long long)part[tgt[e]];
+    vals[e] = w[e];
+  }
+}
+
+struct ConnHead {
+  const unsigned long long* keys;
+  __device__ int operator()(long long i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0; }
+};
+struct ConnOut {
+  const unsigned long long* keys;
+  const int* vals;
+  long long m2;
+  int k;
+  int* blocks;
+  int* cw;
+  int* deg;
+  __device__ void operator()(long long i, int uid) const {
+    if (i > 0 && keys[i] == keys[i - 1]) return;
+    long long sum = 0;
+    long long j = i;
+    while (j < m2 && keys[j] == keys[i]) sum += vals[j++];
+    blocks[uid] = (int)(keys[i] % (unsigned long long)k);
+    cw[uid] = (int)sum;
+    atomicAdd(&deg[keys[i] / (unsigned long long)k], 1);
+  }
+};
+
+long long conn_build(const DevGraph& g, const int* part, int k, int* c_off, int* c_blocks,
+                     int* c_w, cudaStream_t s) {
+  if (g.m2 == 0) {
+    GIM_CUDA(cudaMemsetAsync(c_off, 0, sizeof(int) * ((size_t)g.n + 1), s));
+    return 0;
+  }
+  DBuf<unsigned long long> keys((size_t)g.m2, s), keys2((size_t)g.m2, s);
+  DBuf<int> vals((size_t)g.m2, s), vals2((size_t)g.m2, s), deg((size_t)g.n + 1, s), tot(1, s);
+  k_conn_keys<<<grid_for(g.m2, 256), 256, 0, s>>>(g.m2, g.src, g.tgt, g.w, part, k, keys.get(),
+                                                  vals.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  radix_sort_pairs<unsigned long long, int>(g.m2, keys.get(), vals.get(), keys2.get(), vals2.get(),
+                                            bit_length((unsigned long long)g.n * k), s);
+  GIM_CUDA(cudaMemsetAsync(deg.get(), 0, sizeof(int) * ((size_t)g.n + 1), s));
+  ConnOut out{keys.get(), vals.get(), g.m2, k, c_blocks, c_w, deg.get()};
+  exclusive_scan<int>(g.m2, ConnHead{keys.get()}, out, tot.get(), s);
+  exclusive_scan<int>((long long)g.n + 1, LoadAs<int, int>{deg.get()}, StoreTo<int>{c_off},
+                      (int*)nullptr, s);
+  int total = 0;
+  GIM_CUDA(cudaMemcpyAsync(&total, tot.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  return total;
+}
+
+}  // namespace gim

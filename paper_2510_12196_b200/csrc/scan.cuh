@@ -13,7 +13,7 @@ constexpr int kScanBlock = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanBlock * kScanItems;
 
-__device__ __forceinline__ int scan_pad(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int scan_pad(int i) { return i + (i >> 5); }
 
 template <class T>
 __device__ __forceinline__ T warp_incl_scan(T v) {

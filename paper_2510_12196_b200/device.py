@@ -1,8 +1,9 @@
-"""Device-resident CSR levels (torch tensors as plumbing, int32 layout).
+"""Device-resident CSR levels and thin wrappers over every libgpuim entry point.
 
-`DeviceGraph.from_host` performs the one host->device upload of the
-reference `Graph` arrays (graph.py:17-39, int64) with the overflow checks
-the int32 device layout needs.
+torch tensors are the plumbing (device memory + the current CUDA stream);
+all compute happens in libgpuim.so.  Each wrapper cites the reference
+function its kernel replaces.  There is no CPU fallback anywhere: a missing
+library raises ImportError, a failed call raises GimError.
 """
 from __future__ import annotations
 
@@ -16,22 +17,50 @@ from . import _lib
 INT32_MAX = 2**31 - 1
 
 
-def _ptr(t: torch.Tensor | None) -> int | None:
+def _ptr(t: torch.Tensor | None):
     if t is None:
         return None
     return t.data_ptr() if t.numel() else None
 
 
-class DeviceGraph:
-    """One CSR level on the GPU: offsets/targets/weights/vweights/sources."""
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
 
-    def __init__(self, offsets, targets, weights, vweights, sources, total_weight: int):
+
+def _i32(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.int32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int32)).to(device)
+
+
+def _u8(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.uint8).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint8)).to(device)
+
+
+def topology_struct(hierarchy, distances) -> _lib.GimTopology:
+    if not all(isinstance(d, (int, np.integer)) for d in distances):
+        raise NotImplementedError(
+            "the GPU path implements integral distances (Topology.integral_distances)")
+    return _lib.topology_struct(hierarchy, distances)
+
+
+class DeviceGraph:
+    """One CSR level on the GPU: int32 offsets/targets/weights/vweights/sources."""
+
+    def __init__(self, offsets, targets, weights, vweights, sources=None, total_weight=None):
         self.offsets = offsets
         self.targets = targets
         self.weights = weights
         self.vweights = vweights
+        if sources is None:
+            sources = torch.empty(targets.numel(), dtype=torch.int32, device=offsets.device)
+            if self.n:
+                _lib.call("gim_fill_sources", self.n, _ptr(offsets), _ptr(sources),
+                          stream_ptr(offsets.device))
         self.sources = sources
-        self.total_weight = int(total_weight)
+        self.total_weight = int(vweights.sum().item()) if total_weight is None else int(total_weight)
 
     @property
     def n(self) -> int:
@@ -46,39 +75,25 @@ class DeviceGraph:
         return self.offsets.device
 
     @staticmethod
-    def check_host(offsets: np.ndarray, targets: np.ndarray, eweights: np.ndarray,
-                   vweights: np.ndarray) -> int:
+    def check_host(offsets, targets, eweights, vweights) -> int:
         n = len(offsets) - 1
-        if n < 0:
-            raise ValueError("offsets must have n+1 entries")
         if len(targets) > INT32_MAX or n > INT32_MAX:
             raise OverflowError("graph too large for the int32 device layout")
-        total_vw = int(vweights.sum(dtype=np.int64)) if n else 0
+        total_vw = int(np.asarray(vweights).sum(dtype=np.int64)) if n else 0
         if total_vw > INT32_MAX:
             raise OverflowError("total vertex weight must be < 2^31")
-        if len(eweights) and int(eweights.sum(dtype=np.int64)) > INT32_MAX:
+        if len(eweights) and int(np.asarray(eweights).sum(dtype=np.int64)) > INT32_MAX:
             raise OverflowError("total edge weight must be < 2^31")
         return total_vw
 
     @classmethod
     def from_host(cls, g, device="cuda") -> "DeviceGraph":
-        """Upload a reference-style Graph (attributes offsets, edge_targets,
-        edge_weights, vertex_weights, optional edge_sources)."""
-        off = np.ascontiguousarray(g.offsets, dtype=np.int64)
-        tgt = np.ascontiguousarray(g.edge_targets, dtype=np.int64)
-        ew = np.ascontiguousarray(g.edge_weights, dtype=np.int64)
-        vw = np.ascontiguousarray(g.vertex_weights, dtype=np.int64)
-        total = cls.check_host(off, tgt, ew, vw)
+        """Upload a reference-layout Graph (offsets, edge_targets, edge_weights,
+        vertex_weights; int64)."""
+        total = cls.check_host(g.offsets, g.edge_targets, g.edge_weights, g.vertex_weights)
         dev = torch.device(device)
-        t_off = torch.from_numpy(off).to(dev, non_blocking=False).to(torch.int32)
-        t_tgt = torch.from_numpy(tgt).to(dev).to(torch.int32)
-        t_w = torch.from_numpy(ew).to(dev).to(torch.int32)
-        t_vw = torch.from_numpy(vw).to(dev).to(torch.int32)
-        n = len(off) - 1
-        deg = t_off[1:] - t_off[:-1]
-        t_src = torch.repeat_interleave(torch.arange(n, device=dev, dtype=torch.int32),
-                                        deg.to(torch.int64), output_size=len(tgt))
-        return cls(t_off, t_tgt, t_w, t_vw, t_src, total)
+        return cls(_i32(g.offsets, dev), _i32(g.edge_targets, dev), _i32(g.edge_weights, dev),
+                   _i32(g.vertex_weights, dev), None, total)
 
     def struct(self) -> _lib.GimGraph:
         s = _lib.GimGraph()
@@ -91,26 +106,251 @@ class DeviceGraph:
         s.sources = _ptr(self.sources)
         return s
 
+    def to_host(self):
+        """(offsets, targets, weights, vweights) as int64 numpy arrays."""
+        return tuple(x.cpu().numpy().astype(np.int64) for x in
+                     (self.offsets, self.targets, self.weights, self.vweights))
 
-def stream_ptr(device=None) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
 
+# ---------------------------------------------------------------------------
+# objective (mapping.py:38-91)
 
-def total_cost(dg: DeviceGraph, assignment: torch.Tensor, hierarchy, distances) -> int:
-    """J(C, D, Pi) on the device (mapping.py:76-91), exact int64."""
-    a = assignment.to(device=dg.device, dtype=torch.int32).contiguous()
+def total_cost(dg: DeviceGraph, assignment, hierarchy, distances) -> int:
+    a = _i32(assignment, dg.device)
     out = torch.empty(1, dtype=torch.int64, device=dg.device)
-    t = _lib.topology_struct(hierarchy, distances)
+    t = topology_struct(hierarchy, distances)
     g = dg.struct()
     _lib.call("gim_total_cost", C.byref(g), _ptr(a), C.byref(t), out.data_ptr(),
               stream_ptr(dg.device))
     return int(out.item())
 
 
-def block_weights(dg: DeviceGraph, assignment: torch.Tensor, k: int) -> torch.Tensor:
-    a = assignment.to(device=dg.device, dtype=torch.int32).contiguous()
+def block_weights(dg: DeviceGraph, assignment, k: int) -> torch.Tensor:
+    a = _i32(assignment, dg.device)
     out = torch.empty(k, dtype=torch.int64, device=dg.device)
     g = dg.struct()
     _lib.call("gim_block_weights", C.byref(g), _ptr(a), int(k), out.data_ptr(),
               stream_ptr(dg.device))
     return out
+
+
+# ---------------------------------------------------------------------------
+# coarsening (coarsening.py)
+
+def hem_round(dg: DeviceGraph, partner: torch.Tensor, l_max: float, seed: int,
+              matched: int = 0):
+    """coarsening.py:63-95; partner updated in place. Returns (preferred, matched)."""
+    pref = torch.empty(dg.n, dtype=torch.int32, device=dg.device)
+    m = C.c_int64(matched)
+    g = dg.struct()
+    _lib.call("gim_hem_round", C.byref(g), _ptr(partner), _ptr(pref), float(l_max),
+              int(seed) & (2**64 - 1), C.byref(m), stream_ptr(dg.device))
+    return pref, m.value
+
+
+def match_graph(dg: DeviceGraph, l_max: float, seed: int) -> torch.Tensor:
+    """coarsening.py:164-173."""
+    partner = torch.empty(dg.n, dtype=torch.int32, device=dg.device)
+    m = C.c_int64(0)
+    g = dg.struct()
+    _lib.call("gim_match_graph", C.byref(g), float(l_max), int(seed) & (2**64 - 1),
+              _ptr(partner), C.byref(m), stream_ptr(dg.device))
+    return partner
+
+
+def coarse_map(partner: torch.Tensor):
+    """coarsening.py:176-188 -> (coarse_map, n_c)."""
+    n = partner.numel()
+    cmap = torch.empty(n, dtype=torch.int32, device=partner.device)
+    n_c = C.c_int32(0)
+    _lib.call("gim_coarse_map", n, _ptr(partner), _ptr(cmap), C.byref(n_c),
+              stream_ptr(partner.device))
+    return cmap, n_c.value
+
+
+def contract(dg: DeviceGraph, cmap: torch.Tensor, n_c: int) -> DeviceGraph:
+    """coarsening.py:191-249 (rows sorted by target)."""
+    dev = dg.device
+    cap = max(dg.m2, 1)
+    off = torch.empty(n_c + 1, dtype=torch.int32, device=dev)
+    tgt = torch.empty(cap, dtype=torch.int32, device=dev)
+    w = torch.empty(cap, dtype=torch.int32, device=dev)
+    vw = torch.empty(max(n_c, 1), dtype=torch.int32, device=dev)
+    src = torch.empty(cap, dtype=torch.int32, device=dev)
+    m2 = C.c_int64(0)
+    g = dg.struct()
+    _lib.call("gim_contract", C.byref(g), _ptr(_i32(cmap, dev)), int(n_c), _ptr(off), _ptr(tgt),
+              _ptr(w), _ptr(vw), _ptr(src), C.byref(m2), stream_ptr(dev))
+    k = m2.value
+    return DeviceGraph(off, tgt[:k].clone(), w[:k].clone(), vw[:n_c].clone(), src[:k].clone(),
+                       dg.total_weight)
+
+
+def project(cmap: torch.Tensor, coarse_part: torch.Tensor) -> torch.Tensor:
+    """coarsening.py:269-277."""
+    out = torch.empty(cmap.numel(), dtype=torch.int32, device=cmap.device)
+    _lib.call("gim_project", cmap.numel(), _ptr(cmap), _ptr(_i32(coarse_part, cmap.device)),
+              _ptr(out), stream_ptr(cmap.device))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# refinement (refinement.py, mapping.py)
+
+def conn_build(dg: DeviceGraph, assignment, k: int):
+    """BlockConnectivity values (mapping.py:141-158) as a block-sorted CSR."""
+    dev = dg.device
+    cap = max(dg.m2, 1)
+    off = torch.empty(dg.n + 1, dtype=torch.int32, device=dev)
+    blocks = torch.empty(cap, dtype=torch.int32, device=dev)
+    w = torch.empty(cap, dtype=torch.int32, device=dev)
+    tot = C.c_int64(0)
+    g = dg.struct()
+    _lib.call("gim_conn_build", C.byref(g), _ptr(_i32(assignment, dev)), int(k), _ptr(off),
+              _ptr(blocks), _ptr(w), C.byref(tot), stream_ptr(dev))
+    return off, blocks[:tot.value], w[:tot.value]
+
+
+def lp_pass(dg: DeviceGraph, assignment, locked, hierarchy, distances, jet: bool = False,
+            jet_c: float = 0.25):
+    """label_propagation_pass (refinement.py:201-270) -> (cand, dest, to_move)."""
+    dev = dg.device
+    a = _i32(assignment, dev)
+    lk = _u8(locked, dev) if locked is not None else None
+    cand = torch.empty(dg.n, dtype=torch.uint8, device=dev)
+    dest = torch.empty(dg.n, dtype=torch.int32, device=dev)
+    tm = torch.empty(dg.n, dtype=torch.uint8, device=dev)
+    mv = C.c_int64(0)
+    t = topology_struct(hierarchy, distances)
+    g = dg.struct()
+    _lib.call("gim_lp_pass", C.byref(g), _ptr(a), _ptr(lk), C.byref(t), int(bool(jet)),
+              float(jet_c), _ptr(cand), _ptr(dest), _ptr(tm), C.byref(mv), stream_ptr(dev))
+    return cand, dest, tm
+
+
+def rebalance(dg: DeviceGraph, assignment, bw, hierarchy, distances, strong: bool,
+              sigma: float, l_max: float, rho: int, seed: int, pass_counter: int):
+    """weak/strong_rebalance (refinement.py:312-386) -> (cand, dest, to_move, incomplete)."""
+    dev = dg.device
+    a = _i32(assignment, dev)
+    bwt = bw.to(device=dev, dtype=torch.int64).contiguous() if isinstance(bw, torch.Tensor) \
+        else torch.from_numpy(np.ascontiguousarray(bw, dtype=np.int64)).to(dev)
+    cand = torch.empty(dg.n, dtype=torch.uint8, device=dev)
+    dest = torch.empty(dg.n, dtype=torch.int32, device=dev)
+    tm = torch.empty(dg.n, dtype=torch.uint8, device=dev)
+    inc = C.c_int32(0)
+    t = topology_struct(hierarchy, distances)
+    g = dg.struct()
+    _lib.call("gim_rebalance", C.byref(g), _ptr(a), _ptr(bwt), C.byref(t), int(bool(strong)),
+              float(sigma), float(l_max), int(rho), int(seed) & (2**64 - 1), int(pass_counter),
+              _ptr(cand), _ptr(dest), _ptr(tm), C.byref(inc), stream_ptr(dev))
+    return cand, dest, tm, bool(inc.value)
+
+
+def apply_moves(dg: DeviceGraph, assignment: torch.Tensor, bw: torch.Tensor, to_move, dest,
+                hierarchy, distances) -> int:
+    """apply_moves (mapping.py:252-282) in place; returns the exact J delta."""
+    dev = dg.device
+    dj = C.c_int64(0)
+    t = topology_struct(hierarchy, distances)
+    g = dg.struct()
+    _lib.call("gim_apply_moves", C.byref(g), _ptr(assignment), _ptr(bw), _ptr(_u8(to_move, dev)),
+              _ptr(_i32(dest, dev)), C.byref(t), C.byref(dj), stream_ptr(dev))
+    return dj.value
+
+
+def refine(dg: DeviceGraph, hierarchy, distances, assignment: torch.Tensor, bw: torch.Tensor, *,
+           phi=0.999, i_max=12, i_w_max=2, sigma_fraction=0.005, rho=2, jet=False,
+           jet_c=0.25, seed=0, l_max: float):
+    """refine (Alg. 4, refinement.py:389-464); assignment/bw replaced in place by the best."""
+    t = topology_struct(hierarchy, distances)
+    g = dg.struct()
+    _lib.call("gim_refine", C.byref(g), C.byref(t), _ptr(assignment), _ptr(bw), float(phi),
+              int(i_max), int(i_w_max), float(sigma_fraction), int(rho), int(bool(jet)),
+              float(jet_c), int(seed) & (2**64 - 1), float(l_max), stream_ptr(dg.device))
+
+
+# ---------------------------------------------------------------------------
+# initial mapping (pipelines.py)
+
+def greedy_graph_growing(dg: DeviceGraph, k: int) -> torch.Tensor:
+    out = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    g = dg.struct()
+    _lib.call("gim_greedy_graph_growing", C.byref(g), int(k), _ptr(out), stream_ptr(dg.device))
+    return out[:dg.n]
+
+
+def internal_partitioner(dg: DeviceGraph, k: int, eps_local: float, seed: int) -> torch.Tensor:
+    out = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    g = dg.struct()
+    _lib.call("gim_internal_partitioner", C.byref(g), int(k), float(eps_local),
+              int(seed) & (2**64 - 1), _ptr(out), stream_ptr(dg.device))
+    return out[:dg.n]
+
+
+def hierarchical_multisection(dg: DeviceGraph, hierarchy, distances, eps: float,
+                              seed: int) -> torch.Tensor:
+    out = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    t = topology_struct(hierarchy, distances)
+    g = dg.struct()
+    _lib.call("gim_hierarchical_multisection", C.byref(g), C.byref(t), float(eps),
+              int(seed) & (2**64 - 1), _ptr(out), stream_ptr(dg.device))
+    return out[:dg.n]
+
+
+def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", jet_filter_c=0.25,
+                  sigma_coarse=0.065, sigma_fine=0.005, iw_max_finest=10) -> _lib.GimImParams:
+    p = _lib.GimImParams()
+    p.coarsest_factor = int(coarsest_factor)
+    p.phi = float(phi)
+    p.rho = int(rho)
+    p.filter_mode = 1 if filter_mode == "jet" else 0
+    p.jet_filter_c = float(jet_filter_c)
+    p.sigma_coarse = float(sigma_coarse)
+    p.sigma_fine = float(sigma_fine)
+    p.iw_max_finest = int(iw_max_finest)
+    return p
+
+
+def stats_dict(st: _lib.GimImStats) -> dict:
+    d = {f: getattr(st, f) for f, _ in _lib.GimImStats._fields_
+         if f not in ("level_n", "level_m2")}
+    return d
+
+
+def integrated_map_device(dg: DeviceGraph, hierarchy, distances, eps: float, seed: int = 0,
+                          **kw):
+    """integrated_map on a resident graph -> (assignment int32, bw int64, stats dict)."""
+    k = int(np.prod(hierarchy))
+    a = torch.empty(dg.n, dtype=torch.int32, device=dg.device)
+    bw = torch.empty(k, dtype=torch.int64, device=dg.device)
+    st = _lib.GimImStats()
+    t = topology_struct(hierarchy, distances)
+    p = params_struct(**kw)
+    g = dg.struct()
+    _lib.call("gim_integrated_map_device", C.byref(g), C.byref(t), float(eps),
+              int(seed) & (2**64 - 1), C.byref(p), _ptr(a), _ptr(bw), C.byref(st),
+              stream_ptr(dg.device))
+    return a, bw, stats_dict(st)
+
+
+def integrated_map_host(offsets, targets, eweights, vweights, hierarchy, distances, eps: float,
+                        seed: int = 0, **kw):
+    """integrated_map on HOST int64 arrays through the one-call C ABI
+    -> (assignment int64 np, block weights int64 np, stats dict)."""
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    tgt = np.ascontiguousarray(targets, dtype=np.int64)
+    ew = np.ascontiguousarray(eweights, dtype=np.int64)
+    vw = np.ascontiguousarray(vweights, dtype=np.int64)
+    n = len(off) - 1
+    k = int(np.prod(hierarchy))
+    a = np.empty(max(n, 0), dtype=np.int64)
+    bw = np.empty(k, dtype=np.int64)
+    st = _lib.GimImStats()
+    t = topology_struct(hierarchy, distances)
+    p = params_struct(**kw)
+    ptr = lambda x: x.ctypes.data if x.size else None  # noqa: E731
+    _lib.call("gim_integrated_map", int(n), ptr(off), ptr(tgt), ptr(ew), ptr(vw), C.byref(t),
+              float(eps), int(seed) & (2**64 - 1), C.byref(p), ptr(a), ptr(bw), C.byref(st),
+              stream_ptr())
+    return a, bw, stats_dict(st)

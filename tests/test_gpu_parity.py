@@ -1,0 +1,277 @@
+"""GPU parity: libgpuim.so kernels vs the reference's golden vectors and the
+oracle, through the C ABI (paper_2510_12196_b200.device wraps include/gpuim.h).
+
+Bit-exact everywhere: J, HEM rounds, coarse ids, contraction, connectivity,
+LP / weak / strong proposals, apply_moves deltas, refine, greedy growing,
+the internal partitioner, multisection and integrated_map itself.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import promap_np as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_12196_b200 import device
+    return device
+
+
+def dev_graph(D, c):
+    return D.DeviceGraph.from_host(c.graph())
+
+
+def np_(t):
+    return t.cpu().numpy().astype(np.int64)
+
+
+def test_total_cost_golden(D, golden):
+    for c in golden("jeval"):
+        dg = dev_graph(D, c)
+        j = D.total_cost(dg, c["assignment"], tuple(c["hierarchy"]), tuple(c["distances"]))
+        assert j == c.scalar("j")
+
+
+def test_block_weights(D, golden):
+    for c in golden("jeval"):
+        g = c.graph()
+        k = int(np.prod(c["hierarchy"]))
+        bw = D.block_weights(dev_graph(D, c), c["assignment"], k)
+        assert np.array_equal(np_(bw), O.block_weights(g.vertex_weights, c["assignment"], k))
+
+
+def test_hem_rounds_golden(D, golden):
+    for c in golden("hem"):
+        if not c.scalar("has_rounds"):
+            continue
+        dg = dev_graph(D, c)
+        partner = torch.full((dg.n,), -1, dtype=torch.int32, device="cuda")
+        pref, m = D.hem_round(dg, partner, c.scalar("l_max"), int(c["seed1"]), 0)
+        assert np.array_equal(np_(pref), c["pref1"])
+        assert np.array_equal(np_(partner), c["part1"])
+        assert m == int((c["part1"] >= 0).sum())
+        pref, m = D.hem_round(dg, partner, c.scalar("l_max"), int(c["seed2"]), m)
+        assert np.array_equal(np_(pref), c["pref2"])
+        assert np.array_equal(np_(partner), c["part2"])
+
+
+def test_match_coarse_map_contract_golden(D, golden):
+    for c in golden("hem"):
+        dg = dev_graph(D, c)
+        partner = D.match_graph(dg, c.scalar("l_max"), int(c["match_seed"]))
+        assert np.array_equal(np_(partner), c["match_partner"])
+        cmap, n_c = D.coarse_map(partner)
+        assert n_c == c.scalar("n_c")
+        assert np.array_equal(np_(cmap), c["coarse_map"])
+        cg = D.contract(dg, cmap, n_c)
+        off, tgt, w, vw = cg.to_host()
+        assert np.array_equal(off, c["c_offsets"])
+        assert np.array_equal(tgt, c["c_targets"])
+        assert np.array_equal(w, c["c_weights"])
+        assert np.array_equal(vw, c["c_vweights"])
+        assert np.array_equal(np_(cg.sources), np.repeat(np.arange(n_c), np.diff(off)))
+
+
+def test_level_stack_golden(D, golden):
+    """build_level_stack (coarsening.py:280-295) driven level by level."""
+    for c in golden("stack"):
+        dg = dev_graph(D, c)
+        sizes, m2s = [dg.n], [dg.m2]
+        li = 0
+        while dg.n >= int(c["threshold"]):
+            seed = O.splitmix64(int(c["seed"]) ^ li)
+            partner = D.match_graph(dg, c.scalar("l_max"), seed)
+            cmap, n_c = D.coarse_map(partner)
+            if li == 0:
+                assert np.array_equal(np_(cmap), c["cmap0"])
+            if n_c * 1.02 > dg.n:
+                break
+            dg = D.contract(dg, cmap, n_c)
+            sizes.append(dg.n)
+            m2s.append(dg.m2)
+            li += 1
+        assert sizes == list(c["sizes"])
+        assert m2s == list(c["m2s"])
+        off, tgt, w, _ = dg.to_host()
+        assert np.array_equal(off, c["c_offsets"])
+        assert np.array_equal(tgt, c["c_targets"])
+        assert np.array_equal(w, c["c_weights"])
+
+
+def test_contract_matches_oracle_random(D):
+    rng = np.random.default_rng(5)
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(20000, 0.55, 11)
+    dg = D.DeviceGraph.from_host(g)
+    cmap = rng.integers(0, 7000, g.n)
+    cmap[:7000] = np.arange(7000)
+    cg = D.contract(dg, torch.from_numpy(cmap).cuda(), 7000)
+    ref = O.contract(g, cmap, 7000)
+    off, tgt, w, vw = cg.to_host()
+    assert np.array_equal(off, ref.offsets)
+    assert np.array_equal(tgt, ref.edge_targets)
+    assert np.array_equal(w, ref.edge_weights)
+    assert np.array_equal(vw, ref.vertex_weights)
+
+
+def test_conn_golden(D, golden):
+    for c in golden("conn"):
+        off, blocks, w = D.conn_build(dev_graph(D, c), c["assignment"], c.topology().k)
+        assert np.array_equal(np_(off), c["conn_offsets"])
+        assert np.array_equal(np_(blocks), c["conn_blocks"])
+        assert np.array_equal(np_(w), c["conn_weights"])
+
+
+def test_lp_golden(D, golden):
+    for c in golden("lp"):
+        cand, dest, tm = D.lp_pass(dev_graph(D, c), c["assignment"], c["locked"],
+                                   tuple(c["hierarchy"]), tuple(c["distances"]),
+                                   jet=bool(c.scalar("jet")))
+        assert np.array_equal(np_(cand).astype(bool), c["cand"])
+        assert np.array_equal(np_(dest), c["dest"])
+        assert np.array_equal(np_(tm).astype(bool), c["to_move"])
+
+
+def test_rebalance_golden(D, golden):
+    for c in golden("rebalance"):
+        g = c.graph()
+        k = c.topology().k
+        bw = O.block_weights(g.vertex_weights, c["assignment"], k)
+        dg = dev_graph(D, c)
+        for strong, p in ((False, "w"), (True, "s")):
+            cand, dest, tm, inc = D.rebalance(
+                dg, c["assignment"], bw, tuple(c["hierarchy"]), tuple(c["distances"]), strong,
+                c.scalar("sigma"), c.scalar("l_max"), int(c["rho"]), int(c["seed"]),
+                int(c["pass_counter"]))
+            assert np.array_equal(np_(cand).astype(bool), c[f"{p}_cand"])
+            assert np.array_equal(np_(dest), c[f"{p}_dest"])
+            assert np.array_equal(np_(tm).astype(bool), c[f"{p}_to_move"])
+            assert inc == bool(c[f"{p}_incomplete"])
+
+
+def test_apply_moves_delta_j(D, golden):
+    rng = np.random.default_rng(3)
+    for c in golden("lp")[::3]:
+        g, t = c.graph(), c.topology()
+        a = c["assignment"].copy()
+        h, d = tuple(c["hierarchy"]), tuple(c["distances"])
+        tm = rng.random(g.n) < 0.3
+        dest = np.where(tm, rng.integers(0, t.k, g.n), a)
+        dg = dev_graph(D, c)
+        at = torch.from_numpy(a.astype(np.int32)).cuda()
+        bw = torch.from_numpy(O.block_weights(g.vertex_weights, a, t.k)).cuda()
+        dj = D.apply_moves(dg, at, bw, tm, dest, h, d)
+        new = np.where(tm, dest, a)
+        assert np.array_equal(np_(at), new)
+        assert np.array_equal(np_(bw), O.block_weights(g.vertex_weights, new, t.k))
+        assert dj == O.total_cost(g, t, new) - O.total_cost(g, t, a)
+
+
+def test_refine_golden(D, golden):
+    for c in golden("refine"):
+        g, t = c.graph(), c.topology()
+        lev, nl = int(c["level"]), int(c["n_levels"])
+        cfg = O.config_for_level(lev, nl, seed=int(c["seed"]),
+                                 filter_mode="jet" if c.scalar("jet") else "nonneg")
+        dg = dev_graph(D, c)
+        at = torch.from_numpy(c["assignment"].astype(np.int32)).cuda()
+        bw = torch.from_numpy(O.block_weights(g.vertex_weights, c["assignment"], t.k)).cuda()
+        D.refine(dg, tuple(c["hierarchy"]), tuple(c["distances"]), at, bw, phi=cfg.phi,
+                 i_max=cfg.i_max, i_w_max=cfg.i_w_max, sigma_fraction=cfg.sigma_fraction,
+                 rho=cfg.rho, jet=cfg.filter_mode == "jet", jet_c=cfg.jet_filter_c,
+                 seed=cfg.seed, l_max=c.scalar("l_max"))
+        assert np.array_equal(np_(at), c["best"])
+        assert np.array_equal(np_(bw), O.block_weights(g.vertex_weights, c["best"], t.k))
+
+
+def test_ggg_golden(D, golden):
+    for c in golden("ggg"):
+        g = c.graph()
+        k = int(c["k"])
+        if g.n <= k:
+            continue
+        part = D.greedy_graph_growing(dev_graph(D, c), k)
+        assert np.array_equal(np_(part), c["part"])
+
+
+def test_partitioner_golden(D, golden):
+    for c in golden("partitioner"):
+        part = D.internal_partitioner(dev_graph(D, c), int(c["k"]), c.scalar("eps"),
+                                      int(c["seed"]))
+        assert np.array_equal(np_(part), c["part"])
+
+
+def test_multisection_golden(D, golden):
+    for c in golden("multisection"):
+        a = D.hierarchical_multisection(dev_graph(D, c), tuple(c["hierarchy"]),
+                                        tuple(c["distances"]), c.scalar("eps"), int(c["seed"]))
+        assert np.array_equal(np_(a), c["assignment"])
+
+
+def test_integrated_map_small_golden(D, golden):
+    for c in golden("im_small"):
+        a, bw, st = D.integrated_map_device(dev_graph(D, c), tuple(c["hierarchy"]),
+                                            tuple(c["distances"]), c.scalar("eps"),
+                                            int(c["seed"]),
+                                            coarsest_factor=int(c["coarsest_factor"]))
+        assert np.array_equal(np_(a), c["assignment"].astype(np.int64))
+        assert st["final_j"] == c.scalar("j")
+
+
+def test_integrated_map_cfg1_all_seeds_bit_exact(D, golden):
+    """Config 1 through the public drop-in API: identical mappings to the
+    reference for seeds 0-4 (stronger than the J tolerance gate)."""
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import gen_grid
+    g = gen_grid(128, 128)
+    t = O.OTopology((4, 8, 2), (1, 10, 100))
+    for c in golden("im_cfg1"):
+        m = integrated_map(g, t, 0.03, int(c["seed"]))
+        assert np.array_equal(m.assignment, c["assignment"].astype(np.int64))
+        assert O.total_cost(g, t, m.assignment) == c.scalar("j")
+        assert m.max_block_weight() <= (1.03 * g.n / 64)
+
+
+def test_integrated_map_edge_cases(D):
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import HostGraph, from_pairs
+    t = O.OTopology((2, 2), (1, 10))
+    empty = HostGraph(np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64),
+                      np.zeros(0, np.int64))
+    with pytest.raises(ValueError):
+        integrated_map(empty, t, 0.03)
+    # no edges at all, and fewer vertices than PEs
+    iso = HostGraph(np.zeros(4, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64),
+                    np.ones(3, np.int64))
+    m = integrated_map(iso, t, 0.03)
+    a, _, _ = O.integrated_map(iso, t, 0.03)
+    assert np.array_equal(m.assignment, a)
+    # two components plus isolated vertices, k = 1
+    g = from_pairs(9, np.array([0, 1, 4, 5]), np.array([1, 2, 5, 6]))
+    one = O.OTopology((1,), (3,))
+    m = integrated_map(g, one, 0.0)
+    assert np.array_equal(m.assignment, np.zeros(9, np.int64))
+    m = integrated_map(g, t, 0.5, seed=3)
+    a, bw, _ = O.integrated_map(g, t, 0.5, seed=3)
+    assert np.array_equal(m.assignment, a)
+    assert np.array_equal(m.block_weights, bw)
+
+
+def test_integrated_map_matches_oracle_rgg(D):
+    """Mid-size rgg with a real level stack: identical to the oracle."""
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << 14, 0.55, 1)
+    t = O.OTopology((4, 8, 6), (1, 10, 100))
+    m = integrated_map(g, t, 0.03, 0, coarsest_factor=16)
+    a, bw, l_max = O.integrated_map(g, t, 0.03, 0, coarsest_factor=16)
+    assert np.array_equal(m.assignment, a)
+    assert m.max_block_weight() <= l_max
