@@ -1,0 +1,367 @@
+"""Benchmark: GPU-IM end-to-end mapping throughput on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[1]): random geometric
+graph, n = 2^20, radius 0.55*sqrt(ln n / n), graph seed 1 (m = 6,896,118,
+generator identical to the reference's gen_rgg), mapped to H = 4:8:6
+(k = 192), D = 1:10:100, eps = 0.03.  One "step" = one complete
+integrated_map (coarsening, initial multisection, refinement of every level)
+with a fresh mapping seed.
+
+  value  = undirected edges mapped per second, graph resident in HBM,
+           CUDA events on the mapping stream, L2 flushed between steps
+  e2e    = the same through the public drop-in API
+           (paper_2510_12196_b200.integrated_map) from pinned host int64 CSR
+           arrays: H2D, mapping, D2H of the Mapping, per step
+
+Multi-GPU (torchrun): independent replicas (refinement does not shard, see
+DESIGN.md §6); every rank maps the graph with its own seeds, the timing is
+the max over ranks and value = all edges mapped / that time.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, oracle/promap_np.py) on this box's host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "end-to-end mapping time (s) and edges/s at H=4:8:6; comm cost J vs CPU ref"
+UNIT = "edges/s"
+H = (4, 8, 6)
+DIST = (1, 10, 100)
+EPS = 0.03
+RADIUS = 0.55
+GRAPH_SEED = 1
+# J of the reference package (promap) on this exact workload, mapping seed 0,
+# measured in the build container: the quality yardstick
+REF_J_SEED0 = {20: 2893838}
+
+
+def workload(logn: int) -> dict:
+    return {"workload": f"rgg n=2^{logn} (radius {RADIUS}*sqrt(ln n/n), graph seed "
+                        f"{GRAPH_SEED}) -> H=4:8:6 (k=192), D=1:10:100, eps={EPS}",
+            "n": 1 << logn, "hierarchy": "4:8:6", "distances": "1:10:100", "eps": EPS}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port) — reference arm and cpu_baseline
+
+def _cpu_map_once(args):
+    logn, seed = args
+    from oracle import promap_np as O
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << logn, RADIUS, GRAPH_SEED)
+    t0 = time.perf_counter()
+    a, bw, l_max = O.integrated_map(g, O.OTopology(H, DIST), EPS, seed)
+    dt = time.perf_counter() - t0
+    return g.m, dt, O.total_cost(g, O.OTopology(H, DIST), a), int(bw.max()) <= l_max
+
+
+# measured oracle seconds per full map at these sizes (build container, 1 core)
+_CPU_EST_S = {12: 8.0, 13: 12.0, 14: 19.0, 15: 30.0, 16: 45.0}
+
+
+def cpu_sample_logn(budget_s: float) -> int:
+    best = 12
+    for logn, s in sorted(_CPU_EST_S.items()):
+        if s <= budget_s:
+            best = logn
+    return best
+
+
+def run_reference(args) -> dict:
+    """The reference algorithm on the host cores: one oracle integrated_map
+    per core per step (distinct seeds), aggregate edges/s."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    logn = cpu_sample_logn(180.0 / max(args.steps + args.warmup, 1))
+    ctx = mp.get_context("spawn")
+    times, js, ok = [], [], True
+    with ctx.Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            jobs = [(logn, step * cores + c) for c in range(cores)]
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_map_once, jobs)
+            wall = time.perf_counter() - t0
+            if step >= args.warmup:
+                times.append(wall)
+                js += [r[2] for r in res]
+                ok &= all(r[3] for r in res)
+            m = res[0][0]
+    total = sum(times)
+    value = m * cores * len(times) / total
+    sample = (f"oracle integrated_map on rgg n=2^{logn} (same recipe/H/D/eps), one map per "
+              f"core per step, {cores} processes in parallel")
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {**workload(args.logn), "sample_logn": logn, "parallelism": f"{cores} procs"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "quality": {"J_geomean": float(np.exp(np.mean(np.log(js)))), "balanced": bool(ok)},
+    }
+
+
+def cpu_baseline_single() -> dict:
+    logn = 14
+    m, dt, j, ok = _cpu_map_once((logn, 0))
+    return {"value": m / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle (numpy port of the reference) integrated_map on rgg n=2^{logn}, "
+                      f"same recipe/H/D/eps, seed 0, 1 core: {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+class Clocks:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [x for x in sm if x > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:  # noqa: BLE001
+            pass
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(cls: str):
+    """dram bytes per launch of the dominant kernel class from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), if any."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(cls)
+        except Exception:  # noqa: BLE001
+            return None
+    return None
+
+
+def run_gpu(args) -> dict | None:
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2510_12196_b200 import device as D
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import HostGraph, gen_rgg
+
+    g = gen_rgg(1 << args.logn, RADIUS, GRAPH_SEED)
+    dg = D.DeviceGraph.from_host(g)
+    k = math.prod(H)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def seed_of(step):
+        return rank * 100003 + step
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxed(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (also JIT-free: libgpuim is prebuilt)
+    for w in range(args.warmup):
+        D.integrated_map_device(dg, H, DIST, EPS, seed_of(10**6 + w))
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    D.set_profiling(True)
+    step_ms, js, balanced, launches, prof = [], [], True, 0, {}
+    barrier()
+    with Clocks(local) as clk:
+        for step in range(args.steps):
+            flush.fill_(step & 0xff)  # L2 flush, outside the events
+            a_ev = torch.cuda.Event(enable_timing=True)
+            b_ev = torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            a, bw, st = D.integrated_map_device(dg, H, DIST, EPS, seed_of(step))
+            b_ev.record(stream)
+            b_ev.synchronize()
+            step_ms.append(a_ev.elapsed_time(b_ev))
+            js.append(st["final_j"])
+            balanced &= st["max_block_weight"] <= st["l_max"]
+            launches += st["kernel_launches"]
+            for name, p in st["profile"].items():
+                q = prof.setdefault(name, {"ms": 0.0, "bytes": 0.0, "count": 0})
+                for f in q:
+                    q[f] += p[f]
+            last = st
+    barrier()
+    D.set_profiling(False)
+    total_ms = maxed(sum(step_ms))
+    value = g.m * args.steps * world / (total_ms / 1000.0)
+
+    # ---- end to end through the public API, pinned host buffers
+    def pinned(x):
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).pin_memory()
+        return t, t.numpy()
+    keep = [pinned(x) for x in (g.offsets, g.edge_targets, g.edge_weights, g.vertex_weights)]
+    hg = HostGraph(*[kp[1] for kp in keep])
+
+    class Topo:
+        hierarchy = H
+        distances = DIST
+    e2e_ms = []
+    barrier()
+    for step in range(args.steps):
+        flush.fill_((step + 7) & 0xff)
+        a_ev = torch.cuda.Event(enable_timing=True)
+        b_ev = torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        m = integrated_map(hg, Topo(), EPS, seed_of(step))
+        b_ev.record(stream)
+        b_ev.synchronize()
+        e2e_ms.append(a_ev.elapsed_time(b_ev))
+        assert m.max_block_weight() <= (1.0 + EPS) * g.total_weight / k
+    barrier()
+    e2e_total = maxed(sum(e2e_ms))
+    e2e_value = g.m * args.steps * world / (e2e_total / 1000.0)
+    h2d = 8 * (g.n + 1) + 8 * len(g.edge_targets) * 2 + 8 * g.n
+    d2h = 8 * g.n + 8 * k
+
+    if rank != 0:
+        return None
+
+    # roofline of the dominant kernel class (largest device time in the step)
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    name, p = dom
+    per_launch_bytes = p["bytes"] / max(p["count"], 1)
+    per_launch_ms = p["ms"] / max(p["count"], 1)
+    achieved = (p["bytes"] / 1e9) / (p["ms"] / 1e3) if p["ms"] > 0 else 0.0
+    peak, peak_kind = peaks()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (rgg generator identical to the reference's gen_rgg)",
+        "config": {**workload(args.logn), "m": g.m, "levels": last["n_levels"],
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB write outside the events)"},
+        "seconds_per_map": total_ms / args.steps / 1000.0,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "seconds_per_map": e2e_total / args.steps / 1000.0},
+        "quality": {"J": js, "J_geomean": float(np.exp(np.mean(np.log(js)))),
+                    "balanced": bool(balanced),
+                    "J_reference_seed0": REF_J_SEED0.get(args.logn)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(name),
+                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+                     "launches_timed": p["count"]},
+        "profile_ms_per_step": {k2: v["ms"] / args.steps for k2, v in prof.items()},
+        "phases_ms_last_step": {"coarsen": last["ms_coarsen"], "initial": last["ms_initial"],
+                                "refine": last["ms_refine"], "total": last["ms_total"]},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline_single()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--logn", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", 0)) != 0:
+            return
+        print(json.dumps(run_reference(args)), flush=True)
+        return
+    out = run_gpu(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

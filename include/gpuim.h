@@ -86,6 +86,14 @@ typedef struct gim_im_stats {
   int64_t max_block_weight;
   double l_max;
   double ms_coarsen, ms_initial, ms_refine, ms_total; /* device-event times */
+  /* per kernel class (only when profiling is on, see gim_set_profiling):
+   * 0 J-eval, 1 HEM, 2 contraction, 3 LP first filter, 4 LP second filter,
+   * 5 apply moves, 6 rebalance, 7 greedy growing, 8 subgraph extraction,
+   * 9 two-hop matching.  ms from CUDA events on the launching stream,
+   * bytes = algorithmic bytes, count = timed scopes. */
+  double prof_ms[16];
+  double prof_bytes[16];
+  int64_t prof_count[16];
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -202,6 +210,9 @@ int gim_integrated_map(int64_t n, const int64_t* offsets, const int64_t* targets
 
 /* edge_sources from offsets (graph.py:32-36). */
 int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream);
+
+/* Per-kernel-class CUDA-event timing for integrated_map stats (thread-local). */
+void gim_set_profiling(int32_t on);
 
 /* kernels launched by this host thread since the last reset (evidence). */
 int64_t gim_launch_count(void);

@@ -73,6 +73,9 @@ class GimImStats(C.Structure):
         ("ms_initial", C.c_double),
         ("ms_refine", C.c_double),
         ("ms_total", C.c_double),
+        ("prof_ms", C.c_double * 16),
+        ("prof_bytes", C.c_double * 16),
+        ("prof_count", C.c_int64 * 16),
     ]
 
 
@@ -112,11 +115,12 @@ SIGNATURES: dict[str, list] = {
     "gim_integrated_map_device": [GP, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_integrated_map": [I64, P, P, P, P, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_fill_sources": [I32, P, P, P],
+    "gim_set_profiling": [I32],
     "gim_launch_count": [],
     "gim_reset_launch_count": [],
 }
 RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
-            "gim_reset_launch_count": None}
+            "gim_reset_launch_count": None, "gim_set_profiling": None}
 
 _lib = None
 

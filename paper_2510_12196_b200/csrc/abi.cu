@@ -110,7 +110,64 @@ void count_launch(long long n) { g_launches += n; }
 long long launches() { return g_launches; }
 void reset_launches() { g_launches = 0; }
 
+// ---- profiling registry (per host thread)
+struct ProfRec {
+  int cls;
+  double bytes;
+  cudaEvent_t a, b;
+};
+static thread_local bool g_prof = false;
+static thread_local std::vector<ProfRec> g_recs;
+static thread_local std::vector<cudaEvent_t> g_evpool;
+
+static cudaEvent_t ev_get() {
+  if (!g_evpool.empty()) {
+    cudaEvent_t e = g_evpool.back();
+    g_evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GIM_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+bool prof_on() { return g_prof; }
+void prof_set(bool on) { g_prof = on; }
+
+void prof_begin(int cls, double bytes, cudaStream_t s, void** token) {
+  ProfRec r{cls, bytes, ev_get(), ev_get()};
+  GIM_CUDA(cudaEventRecord(r.a, s));
+  g_recs.push_back(r);
+  *token = reinterpret_cast<void*>(g_recs.size());  // 1-based index
+}
+
+void prof_end(void* token, cudaStream_t s, double extra_bytes) {
+  size_t i = reinterpret_cast<size_t>(token) - 1;
+  if (i < g_recs.size()) {
+    g_recs[i].bytes += extra_bytes;
+    cudaEventRecord(g_recs[i].b, s);
+  }
+}
+
+void prof_collect(double* ms, double* bytes, long long* count) {
+  for (auto& r : g_recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cls >= 0 && r.cls < P_COUNT) {
+      ms[r.cls] += t;
+      bytes[r.cls] += r.bytes;
+      count[r.cls] += 1;
+    }
+    g_evpool.push_back(r.a);
+    g_evpool.push_back(r.b);
+  }
+  g_recs.clear();
+}
+
 }  // namespace gim
+
+extern "C" void gim_set_profiling(int32_t on) { gim::prof_set(on != 0); }
 
 extern "C" int gim_version(void) {
   gim::configure_pool_once();

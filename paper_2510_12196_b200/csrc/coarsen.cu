@@ -120,6 +120,7 @@ static int pick_vw(long long m2, int n) {
 void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
                unsigned long long seed, long long* matched, cudaStream_t s) {
   if (g.n == 0) return;
+  ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
   int vw = pick_vw(g.m2, g.n);
   long long groups = (long long)g.n * vw;
@@ -313,6 +314,7 @@ long long two_hop(const DevGraph& g, int* partner, double l_max, long long match
   };
   GIM_CUDA(cudaMemcpyAsync(matched_d, &matched_now, sizeof(long long), cudaMemcpyHostToDevice, s));
   long long m = matched_now;
+  ProfScope prof(P_TWO_HOP, 0.0, s);
   for (int rep = 0; rep < 3; ++rep) {
     if (frac(m) >= target) return m;
     two_hop_phase(g, partner, l_max, matched_d, false, flags.get(), s);
@@ -436,6 +438,7 @@ __global__ void k_coarse_vw(int n, const int* __restrict__ cmap, const int* __re
 // returns m2 of the coarse graph; out arrays must hold >= g.m2 slots
 long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off, int* c_tgt,
                         int* c_w, int* c_vw, int* c_src, cudaStream_t s) {
+  ProfScope prof(P_CONTRACT, 12.0 * g.n + 12.0 * g.m2 + 8.0 * n_c, s);
   GIM_CUDA(cudaMemsetAsync(c_vw, 0, sizeof(int) * (size_t)n_c, s));
   if (n_c > 0) {
     k_coarse_vw<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, cmap, g.vw, c_vw);
@@ -470,6 +473,7 @@ long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off,
   int m2c = 0;
   GIM_CUDA(cudaMemcpyAsync(&m2c, m2c_d.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   GIM_CUDA(cudaStreamSynchronize(s));
+  prof.extra = 8.0 * m2c;
   return m2c;
 }
 

@@ -106,6 +106,36 @@ long long launches();
 void reset_launches();
 
 // ---------------------------------------------------------------------------
+// kernel-class profiling with CUDA events on the launching stream (off by
+// default; bench.py turns it on for the timed region).  Each scope records
+// a start/stop event pair plus the algorithmic bytes of what it launched;
+// prof_collect() resolves the pairs once at the end (no per-scope syncs).
+
+enum ProfClass {
+  P_JEVAL = 0, P_HEM, P_CONTRACT, P_LP_EVAL, P_LP_SECOND, P_APPLY, P_REBALANCE, P_GGG,
+  P_EXTRACT, P_TWO_HOP, P_COUNT
+};
+
+bool prof_on();
+void prof_set(bool on);
+void prof_begin(int cls, double bytes, cudaStream_t s, void** token);
+void prof_end(void* token, cudaStream_t s, double extra_bytes);
+// accumulate totals per class (ms, bytes, launches); clears the records
+void prof_collect(double* ms, double* bytes, long long* count);
+
+struct ProfScope {
+  void* tok = nullptr;
+  cudaStream_t s;
+  double extra = 0.0;  // bytes only known after the launches (e.g. output size)
+  ProfScope(int cls, double bytes, cudaStream_t st) : s(st) {
+    if (prof_on()) prof_begin(cls, bytes, st, &tok);
+  }
+  ~ProfScope() {
+    if (tok) prof_end(tok, s, extra);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // launch geometry
 
 constexpr int kSMs = 148;

@@ -448,6 +448,11 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   std::vector<Level> levels = build_level_stack(
       g0, l_max, std::max<long long>(P.coarsest_factor * k, 1), seed, s);
   const int nl = (int)levels.size();
+  std::vector<long long> level_n, level_m2;
+  for (auto& L : levels) {
+    level_n.push_back(L.g.n);
+    level_m2.push_back(L.g.m2);
+  }
   GIM_CUDA(cudaEventRecord(ev[1], s));
   DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
   st.in_initial = true;
@@ -480,6 +485,10 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     cudaEventElapsedTime(&c, ev[2], ev[3]);
     cudaEventElapsedTime(&tot, ev[0], ev[3]);
     stats->n_levels = nl;
+    for (int i = 0; i < 64; ++i) {
+      stats->level_n[i] = i < nl ? level_n[i] : 0;
+      stats->level_m2[i] = i < nl ? level_m2[i] : 0;
+    }
     stats->ms_coarsen = a;
     stats->ms_initial = b;
     stats->ms_refine = c;
@@ -492,6 +501,14 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     stats->partitioner_calls = st.partitioner_calls;
     stats->kernel_launches = launches();
     stats->l_max = l_max;
+    double pms[P_COUNT] = {0}, pby[P_COUNT] = {0};
+    long long pct[P_COUNT] = {0};
+    prof_collect(pms, pby, pct);
+    for (int c = 0; c < 16; ++c) {
+      stats->prof_ms[c] = c < P_COUNT ? pms[c] : 0.0;
+      stats->prof_bytes[c] = c < P_COUNT ? pby[c] : 0.0;
+      stats->prof_count[c] = c < P_COUNT ? pct[c] : 0;
+    }
     DBuf<long long> dj(1, s);
     total_cost(g0, out_part, t, dj.get(), s);
     stats->final_j = read_scalar(dj.get(), s);

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(32) k_ggg(const GggJob* jobs, int njobs) {
 }
 
 void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
+  ProfScope prof(P_GGG, 0.0, s);
   DBuf<int> scratch((size_t)g.n + k + (size_t)k * g.n, s);
   DBuf<long long> bwork((size_t)k, s);
   GggJob job{g.n, k, g.off, g.tgt, g.w, g.vw, part, scratch.get(), bwork.get()};
@@ -269,6 +270,7 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
                        std::vector<OwnedGraph>& subs, std::vector<DBuf<int>>& ids,
                        cudaStream_t s) {
   const int n = g.n;
+  ProfScope prof(P_EXTRACT, 12.0 * n + 12.0 * g.m2, s);
   subs.clear();
   ids.clear();
   subs.resize(parts);

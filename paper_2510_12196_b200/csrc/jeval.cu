@@ -41,6 +41,9 @@ void total_cost(const DevGraph& g, const int* part, const Topo& t, long long* j_
                 cudaStream_t s) {
   GIM_CUDA(cudaMemsetAsync(j_out, 0, sizeof(long long), s));
   if (g.m2 == 0) return;
+  // algorithmic bytes: offsets + Pi[v] per vertex, target +
+  // weight + Pi[target] per slot
+  ProfScope prof(P_JEVAL, 8.0 * g.n + 12.0 * g.m2, s);
   constexpr int B = 256;
   int grid = grid_for((g.m2 + 3) / 4, B, kSMs * 8);
   k_total_cost<B><<<grid, B, 0, s>>>(g.m2, g.src, g.tgt, g.w, part, t, j_out);

@@ -473,8 +473,8 @@ __device__ __forceinline__ int slot_for_gain(long long g) {
   if (g <= -1000) return 30;
   long long x = -g;  // bisect_right over [0,1..10,20..100,200..1000]
   if (x <= 10) return (int)x + 1;
-  if (x < 100) return 11 + (int)(x / 10);
-  if (x < 1000) return 20 + (int)(x / 100);
+  if (x < 100) return 10 + (int)(x / 10);
+  if (x < 1000) return 19 + (int)(x / 100);
   return 30;
 }
 
@@ -554,6 +554,10 @@ static void launch_eval(const RefineLevel& L, int mode, const Topo& t, const int
                         const LpParams& lp, const LpOut& lo, const RbParams& rb,
                         const RbOut& ro, cudaStream_t s) {
   const DevGraph& g = L.g;
+  // LP first filter / rebalance candidates: every CSR row once (target,
+  // weight, Pi[target] = 12 B/slot) + offsets, Pi, lock and the three
+  // per-vertex outputs (22 B/vertex)
+  ProfScope prof(mode == 0 ? P_LP_EVAL : P_REBALANCE, 22.0 * g.n + 12.0 * g.m2, s);
   constexpr int B = 256;
   long long groups = (long long)g.n * L.vw;
   int grid = grid_for(groups, B, kSMs * 8);
@@ -621,6 +625,7 @@ void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigne
   RbOut ro{};
   launch_eval(L, 0, t, part, lp, lo, rp, ro, s);
   GIM_CUDA(cudaMemsetAsync(rb.movers.get(), 0, sizeof(long long), s));
+  ProfScope prof(P_LP_SECOND, 6.0 * g.n, s);  // lower bound: candidate rows not counted
   constexpr int B = 256;
   int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
   switch (L.vw) {
@@ -676,6 +681,7 @@ void apply_moves(const RefineLevel& L, const Topo& t, int* part, long long* bw,
                  RefineBuffers& rb, cudaStream_t s) {
   const DevGraph& g = L.g;
   GIM_CUDA(cudaMemsetAsync(rb.dj.get(), 0, sizeof(long long), s));
+  ProfScope prof(P_APPLY, 6.0 * g.n, s);  // lower bound: mover rows not counted
   constexpr int B = 256;
   int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
   switch (L.vw) {

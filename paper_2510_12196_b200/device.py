@@ -312,10 +312,26 @@ def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", j
     return p
 
 
+PROF_CLASSES = ("jeval", "hem", "contract", "lp_eval", "lp_second", "apply", "rebalance",
+                "ggg", "extract", "two_hop")
+
+
 def stats_dict(st: _lib.GimImStats) -> dict:
     d = {f: getattr(st, f) for f, _ in _lib.GimImStats._fields_
-         if f not in ("level_n", "level_m2")}
+         if f not in ("level_n", "level_m2", "prof_ms", "prof_bytes", "prof_count")}
+    d["level_n"] = [st.level_n[i] for i in range(min(st.n_levels, 64))]
+    d["level_m2"] = [st.level_m2[i] for i in range(min(st.n_levels, 64))]
+    prof = {}
+    for i, name in enumerate(PROF_CLASSES):
+        if st.prof_count[i]:
+            prof[name] = {"ms": st.prof_ms[i], "bytes": st.prof_bytes[i],
+                          "count": st.prof_count[i]}
+    d["profile"] = prof
     return d
+
+
+def set_profiling(on: bool) -> None:
+    _lib.load().gim_set_profiling(1 if on else 0)
 
 
 def integrated_map_device(dg: DeviceGraph, hierarchy, distances, eps: float, seed: int = 0,

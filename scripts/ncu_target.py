@@ -1,0 +1,52 @@
+"""ncu targets (run under `ncu --profile-from-start off ...`).
+
+  --mode step : warm-up map, then ONE integrated_map inside the capture
+                window (launch list / per-kernel share of a step)
+  --mode lp   : warm-up map, then the level-0 LP / J / HEM / contraction
+                kernels on the final mapping inside the window (full sets)
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2510_12196_b200 import device as D  # noqa: E402
+from paper_2510_12196_b200.generators import gen_rgg  # noqa: E402
+
+H, DIST = (4, 8, 6), (1, 10, 100)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", choices=["step", "lp"], default="step")
+    ap.add_argument("--logn", type=int, default=20)
+    args = ap.parse_args()
+    g = gen_rgg(1 << args.logn, 0.55, 1)
+    dg = D.DeviceGraph.from_host(g)
+    a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, 0)
+    torch.cuda.synchronize()
+    prof = torch.cuda.profiler
+    if args.mode == "step":
+        prof.start()
+        D.integrated_map_device(dg, H, DIST, 0.03, 1)
+        torch.cuda.synchronize()
+        prof.stop()
+    else:
+        locked = torch.zeros(dg.n, dtype=torch.uint8, device="cuda")
+        prof.start()
+        for _ in range(3):
+            D.lp_pass(dg, a, locked, H, DIST)
+        D.total_cost(dg, a, H, DIST)
+        partner = torch.full((dg.n,), -1, dtype=torch.int32, device="cuda")
+        D.hem_round(dg, partner, 1e9, 12345, 0)
+        cmap, n_c = D.coarse_map(partner)
+        D.contract(dg, cmap, n_c)
+        torch.cuda.synchronize()
+        prof.stop()
+    print("done", st["final_j"])
+
+
+if __name__ == "__main__":
+    main()
