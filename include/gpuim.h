@@ -211,8 +211,12 @@ int gim_integrated_map(int64_t n, const int64_t* offsets, const int64_t* targets
 /* edge_sources from offsets (graph.py:32-36). */
 int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream);
 
-/* Per-kernel-class CUDA-event timing for integrated_map stats (thread-local). */
+/* Per-kernel-class CUDA-event timing for integrated_map stats. */
 void gim_set_profiling(int32_t on);
+
+/* Run sibling multisection subtrees on concurrent host threads / CUDA
+ * streams (default 1).  Results are identical either way. */
+void gim_set_fanout(int32_t on);
 
 /* kernels launched by this host thread since the last reset (evidence). */
 int64_t gim_launch_count(void);

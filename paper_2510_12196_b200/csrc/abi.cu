@@ -2,6 +2,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <atomic>
 #include <map>
 #include <mutex>
 
@@ -105,10 +106,12 @@ static void configure_pool_once() {
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
-static thread_local long long g_launches = 0;
-void count_launch(long long n) { g_launches += n; }
-long long launches() { return g_launches; }
-void reset_launches() { g_launches = 0; }
+// process-wide (the multisection drives sibling subtrees from worker
+// threads; their launches belong to the same integrated_map call)
+static std::atomic<long long> g_launches{0};
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launches() { return g_launches.load(); }
+void reset_launches() { g_launches.store(0); }
 
 // ---- profiling registry (per host thread)
 struct ProfRec {
@@ -116,11 +119,12 @@ struct ProfRec {
   double bytes;
   cudaEvent_t a, b;
 };
-static thread_local bool g_prof = false;
-static thread_local std::vector<ProfRec> g_recs;
-static thread_local std::vector<cudaEvent_t> g_evpool;
+static std::atomic<bool> g_prof{false};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_evpool;
 
-static cudaEvent_t ev_get() {
+static cudaEvent_t ev_get() {  // caller holds g_prof_mu
   if (!g_evpool.empty()) {
     cudaEvent_t e = g_evpool.back();
     g_evpool.pop_back();
@@ -135,6 +139,7 @@ bool prof_on() { return g_prof; }
 void prof_set(bool on) { g_prof = on; }
 
 void prof_begin(int cls, double bytes, cudaStream_t s, void** token) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   ProfRec r{cls, bytes, ev_get(), ev_get()};
   GIM_CUDA(cudaEventRecord(r.a, s));
   g_recs.push_back(r);
@@ -142,6 +147,7 @@ void prof_begin(int cls, double bytes, cudaStream_t s, void** token) {
 }
 
 void prof_end(void* token, cudaStream_t s, double extra_bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   size_t i = reinterpret_cast<size_t>(token) - 1;
   if (i < g_recs.size()) {
     g_recs[i].bytes += extra_bytes;
@@ -150,6 +156,7 @@ void prof_end(void* token, cudaStream_t s, double extra_bytes) {
 }
 
 void prof_collect(double* ms, double* bytes, long long* count) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& r : g_recs) {
     cudaEventSynchronize(r.b);
     float t = 0.f;

@@ -6,7 +6,10 @@
 // fractions, Eq. 2) is evaluated on the host in IEEE double with the same
 // operation order as the reference's Python float expressions, so control
 // decisions agree bit-for-bit; kernels only see the resulting doubles.
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -25,10 +28,10 @@ void scatter_const(int n, const int* idx, int value, int* dst, cudaStream_t s);
 // ---------------------------------------------------------------------------
 // run statistics
 
-struct RunStats {
-  long long refine_iterations = 0, lp = 0, weak = 0, strong = 0;
-  long long init_refine_iterations = 0, partitioner_calls = 0;
-  bool in_initial = false;
+struct RunStats {  // shared by the multisection worker threads
+  std::atomic<long long> refine_iterations{0}, lp{0}, weak{0}, strong{0};
+  std::atomic<long long> init_refine_iterations{0}, partitioner_calls{0};
+  std::atomic<bool> in_initial{false};
 };
 
 // pinned host scratch, one per host thread
@@ -115,10 +118,9 @@ static RefCfg config_for_level(int level, int n_levels, double phi, int rho, int
 // the best mapping seen.
 
 static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, const RefCfg& cfg,
-                   double l_max, RunStats& st, cudaStream_t s) {
+                   double l_max, RunStats& st, RefineBuffers& rb, cudaStream_t s) {
   const int n = L.g.n, k = t.k;
   if (L.heavy.get() == nullptr) prepare_level(L, k, s);
-  RefineBuffers rb;
   alloc_refine_buffers(rb, n, k, s);
   // host mirrors
   size_t pin_bytes = sizeof(long long) * ((size_t)k + 2) + (size_t)k * 2 + sizeof(int) * (size_t)k;
@@ -129,12 +131,11 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
   unsigned char* h_ovl = reinterpret_cast<unsigned char*>(h_dj + 1);
   unsigned char* h_elig = h_ovl + k;
   int* h_elist = reinterpret_cast<int*>(h_elig + k);
-  DBuf<unsigned char> d_masks((size_t)k * 2, s);
-  DBuf<int> d_elist((size_t)k, s);
-  DBuf<long long> d_j(1, s);
+  unsigned char* d_masks = rb.masks.get();
+  int* d_elist = rb.elist.get();
 
-  total_cost(L.g, part, t, d_j.get(), s);
-  GIM_CUDA(cudaMemcpyAsync(h_dj, d_j.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+  total_cost(L.g, part, t, rb.jtmp.get(), s);
+  GIM_CUDA(cudaMemcpyAsync(h_dj, rb.jtmp.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
   GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
   GIM_CUDA(cudaStreamSynchronize(s));
   long long J = *h_dj;
@@ -173,12 +174,12 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
         if (h_elig[b]) h_elist[ne++] = b;
       }
       incomplete = ne == 0;
-      GIM_CUDA(cudaMemcpyAsync(d_masks.get(), h_ovl, (size_t)k * 2, cudaMemcpyHostToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(d_masks, h_ovl, (size_t)k * 2, cudaMemcpyHostToDevice, s));
       if (ne)
-        GIM_CUDA(cudaMemcpyAsync(d_elist.get(), h_elist, sizeof(int) * ne, cudaMemcpyHostToDevice, s));
+        GIM_CUDA(cudaMemcpyAsync(d_elist, h_elist, sizeof(int) * ne, cudaMemcpyHostToDevice, s));
       bool strong = !(i_w < cfg.i_w_max);
       rebalance_pass(L, t, part, bw_d, strong, l_max, cfg.rho, cfg.seed, pass_counter,
-                     d_masks.get(), d_masks.get() + k, d_elist.get(), ne, rb, s);
+                     d_masks, d_masks + k, d_elist, ne, rb, s);
       if (strong) {
         i_w = 0;
         ++st.strong;
@@ -190,8 +191,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
     }
     apply_moves(L, t, part, bw_d, rb, s);
     GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaMemcpyAsync(h_mv, rb.movers.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaMemcpyAsync(h_dj, rb.dj.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(h_mv, rb.ctr.get(), 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaStreamSynchronize(s));
     if (st.in_initial) ++st.init_refine_iterations;
     else ++st.refine_iterations;
@@ -316,6 +316,8 @@ static void internal_partitioner(const DevGraph& g, long long total, int parts, 
   DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
   greedy_graph_growing(levels.back().g, parts, cur.get(), s);
   DBuf<long long> bw((size_t)parts, s);
+  RefineBuffers rb;
+  alloc_refine_buffers(rb, g.n, parts, s);  // finest level: serves all levels
   for (int li = nl - 1; li >= 0; --li) {
     Level& L = levels[li];
     if (li < nl - 1) {
@@ -327,7 +329,7 @@ static void internal_partitioner(const DevGraph& g, long long total, int parts, 
     RefCfg cfg = config_for_level(li, nl, 0.999, 2, 1, 0.25, 0.065, 0.005, 10,
                                   hash2(seed, 101, (unsigned long long)li));
     L.rl.g = L.g;
-    refine(L.rl, tf, cur.get(), bw.get(), cfg, l_max, st, s);
+    refine(L.rl, tf, cur.get(), bw.get(), cfg, l_max, st, rb, s);
   }
   GIM_CUDA(cudaMemcpyAsync(part, cur.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
 }
@@ -342,8 +344,12 @@ struct MsCtx {
   double eps;
   int* assignment;
   RunStats* st;
-  cudaStream_t s;
+  bool threads;
+  int device;
 };
+
+// sibling-subtree fan-out over host threads (gim_set_fanout; default on)
+static std::atomic<bool> g_fanout{true};
 
 static double adaptive_imbalance(double eps, long long total, long long sub, long long k,
                                  long long k_sub, int depth) {
@@ -362,9 +368,13 @@ static int calc_id(const std::vector<long long>& h, const std::vector<int>& iden
   return (int)out;
 }
 
+// Sibling subtrees are independent (disjoint vertex sets, seeds derived from
+// the parent only), so each child subtree that still has partitioning work
+// runs on its own host thread and CUDA stream; the result is identical to
+// the reference's sequential recursion.
 static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int level,
-                    std::vector<int>& ident, const int* translation, unsigned long long node_seed) {
-  cudaStream_t s = C.s;
+                    std::vector<int>& ident, const int* translation, unsigned long long node_seed,
+                    cudaStream_t s) {
   if (sub.n == 0) return;
   if (level == 0) {
     scatter_const(sub.n, translation, calc_id(C.h, ident), C.assignment, s);
@@ -387,16 +397,44 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
   std::vector<OwnedGraph> subs;
   std::vector<DBuf<int>> ids;
   extract_subgraphs(sub, part.get(), parts, subs, ids, s);  // synchronizes s
+  std::vector<DBuf<int>> trans((size_t)parts);
   for (int j = 0; j < parts; ++j) {
-    DBuf<int> trans((size_t)std::max(subs[j].n, 1), s);
-    gather(subs[j].n, ids[j].get(), translation, trans.get(), s);
-    ids[j].release();
-    ident.push_back(j);
-    descend(C, subs[j].view(), child_total[j], level - 1, ident, trans.get(),
-            hash2(node_seed, (unsigned long long)level, (unsigned long long)j));
-    ident.pop_back();
-    subs[j] = OwnedGraph();
+    trans[j] = DBuf<int>((size_t)std::max(subs[j].n, 1), s);
+    gather(subs[j].n, ids[j].get(), translation, trans[j].get(), s);
   }
+  const bool fan_out = level - 1 >= 1 && parts > 1 && C.threads;
+  if (!fan_out) {
+    for (int j = 0; j < parts; ++j) {
+      ident.push_back(j);
+      descend(C, subs[j].view(), child_total[j], level - 1, ident, trans[j].get(),
+              hash2(node_seed, (unsigned long long)level, (unsigned long long)j), s);
+      ident.pop_back();
+    }
+    return;
+  }
+  GIM_CUDA(cudaStreamSynchronize(s));  // children read subs/trans from other streams
+  std::vector<std::thread> workers;
+  std::vector<std::exception_ptr> errs((size_t)parts);
+  for (int j = 0; j < parts; ++j) {
+    workers.emplace_back([&, j] {
+      cudaStream_t cs = nullptr;
+      try {
+        GIM_CUDA(cudaSetDevice(C.device));
+        GIM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        std::vector<int> id2 = ident;
+        id2.push_back(j);
+        descend(C, subs[j].view(), child_total[j], level - 1, id2, trans[j].get(),
+                hash2(node_seed, (unsigned long long)level, (unsigned long long)j), cs);
+        GIM_CUDA(cudaStreamSynchronize(cs));
+      } catch (...) {
+        errs[j] = std::current_exception();
+      }
+      if (cs) cudaStreamDestroy(cs);
+    });
+  }
+  for (auto& w : workers) w.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
 }
 
 static void hierarchical_multisection(const DevGraph& g, long long total,
@@ -414,13 +452,14 @@ static void hierarchical_multisection(const DevGraph& g, long long total,
   C.eps = eps;
   C.assignment = assignment;
   C.st = &st;
-  C.s = s;
+  C.threads = g_fanout;
+  GIM_CUDA(cudaGetDevice(&C.device));
   GIM_CUDA(cudaMemsetAsync(assignment, 0, sizeof(int) * g.n, s));
   DBuf<int> ident_ids((size_t)g.n, s);
   k_iota<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, ident_ids.get());
   count_launch();
   std::vector<int> ident;
-  descend(C, g, total, (int)h.size(), ident, ident_ids.get(), seed);
+  descend(C, g, total, (int)h.size(), ident, ident_ids.get(), seed, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,6 +499,8 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
                             hash2(seed, 7, 7), cur.get(), st, s);
   st.in_initial = false;
   GIM_CUDA(cudaEventRecord(ev[2], s));
+  RefineBuffers rb;
+  alloc_refine_buffers(rb, g0.n, (int)k, s);  // sized for level 0, reused by every level
   for (int li = nl - 1; li >= 0; --li) {
     Level& L = levels[li];
     if (li < nl - 1) {
@@ -473,7 +514,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
                                   P.sigma_coarse, P.sigma_fine, P.iw_max_finest,
                                   hash2(seed, 211, (unsigned long long)li));
     L.rl.g = L.g;
-    refine(L.rl, t, cur.get(), out_bw, cfg, l_max, st, s);
+    refine(L.rl, t, cur.get(), out_bw, cfg, l_max, st, rb, s);
   }
   GIM_CUDA(cudaMemcpyAsync(out_part, cur.get(), sizeof(int) * g0.n, cudaMemcpyDeviceToDevice, s));
   GIM_CUDA(cudaEventRecord(ev[3], s));
@@ -694,7 +735,7 @@ extern "C" int gim_lp_pass(const gim_graph* g, const int32_t* assignment, const 
       GIM_CUDA(cudaMemcpyAsync(out_dest, rb.dest.get(), sizeof(int) * g->n, cudaMemcpyDeviceToDevice, s));
       GIM_CUDA(cudaMemcpyAsync(out_to_move, rb.to_move.get(), g->n, cudaMemcpyDeviceToDevice, s));
     }
-    long long mv = read_scalar(rb.movers.get(), s);
+    long long mv = read_scalar(rb.movers, s);
     if (movers_out) *movers_out = mv;
   });
 }
@@ -774,7 +815,7 @@ extern "C" int gim_apply_moves(const gim_graph* g, int32_t* assignment, int64_t*
       GIM_CUDA(cudaMemcpyAsync(rb.dest.get(), dest, sizeof(int) * g->n, cudaMemcpyDeviceToDevice, s));
     }
     apply_moves(L, tp, assignment, reinterpret_cast<long long*>(block_weights), rb, s);
-    long long dj = read_scalar(rb.dj.get(), s);
+    long long dj = read_scalar(rb.dj, s);
     if (delta_j_out) *delta_j_out = dj;
   });
 }
@@ -799,7 +840,8 @@ extern "C" int gim_refine(const gim_graph* g, const gim_topology* t, int32_t* as
     c.jet_c = jet_c;
     c.seed = seed;
     RunStats st;
-    refine(L, tp, assignment, reinterpret_cast<long long*>(block_weights), c, l_max, st, s);
+    RefineBuffers rb;
+    refine(L, tp, assignment, reinterpret_cast<long long*>(block_weights), c, l_max, st, rb, s);
   });
 }
 
@@ -893,3 +935,5 @@ extern "C" int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sour
 
 extern "C" int64_t gim_launch_count(void) { return launches(); }
 extern "C" void gim_reset_launch_count(void) { reset_launches(); }
+
+extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }

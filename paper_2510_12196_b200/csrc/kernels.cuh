@@ -82,7 +82,13 @@ struct RefineBuffers {
   DBuf<int> rvals, rvals2;
   DBuf<long long> rexcl;
   DBuf<int> gstart, count;
-  DBuf<long long> movers, dj;
+  DBuf<long long> ctr;           // [movers, dJ] — zeroed by each candidate pass
+  long long* movers = nullptr;   // ctr + 0
+  long long* dj = nullptr;       // ctr + 1
+  DBuf<unsigned char> masks;     // [ovl | elig] per block (rebalance)
+  DBuf<int> elist;               // eligible block list (rebalance)
+  DBuf<long long> jtmp;          // J scratch
+  int cap_n = 0, cap_k = 0;      // sizes the buffers were allocated for
 };
 
 void prepare_level(RefineLevel& L, int k, cudaStream_t s);

@@ -58,18 +58,30 @@ struct VertexEval {
   int best_b;          // -1: no admissible adjacent block
 };
 
+// `dmax` = max degree over the warp's groups (warp-uniform loop bound).
+// Interior vertices (every neighbour in the own block) are the common case
+// after the first iterations: a warp whose groups have no candidate lane
+// skips the whole evaluation, so the pass degenerates to one row sweep.
 template <int VW>
-__device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, int myw,
+__device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, int myw, int dmax,
                                                 const Topo& t, const long long* s_dbit,
-                                                const unsigned char* allowed) {
+                                                const unsigned char* allowed, bool need_conn) {
+  VertexEval r;
+  r.cur = 0;
+  r.conn_own = 0;
+  r.best_gain = kGainNone;
+  r.best_b = -1;
+  const bool cand = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
+  if (!__any_sync(0xffffffffu, cand)) return r;
   const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
   const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
   long long wv = valid ? myw : 0;
   long long cur = wv * cdist(s_dbit, ocode, mycode);
-  long long co = (valid && myb == own) ? wv : 0;
+  long long co = (need_conn && valid && myb == own) ? wv : 0;
   long long cost = 0;
+  const int lim = min(dmax, VW);
 #pragma unroll 4
-  for (int i = 0; i < VW; ++i) {
+  for (int i = 0; i < lim; ++i) {
     unsigned long long ci = __shfl_sync(0xffffffffu, mycode, i, VW);
     long long wi = __shfl_sync(0xffffffffu, wv, i, VW);
     cost += wi * cdist(s_dbit, mycode, ci);
@@ -77,9 +89,8 @@ __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, in
 #pragma unroll
   for (int o = VW / 2; o > 0; o >>= 1) {
     cur += __shfl_xor_sync(0xffffffffu, cur, o);
-    co += __shfl_xor_sync(0xffffffffu, co, o);
+    if (need_conn) co += __shfl_xor_sync(0xffffffffu, co, o);
   }
-  bool cand = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
   long long g = cand ? cur - cost : kGainNone;
   int b = cand ? myb : -1;
 #pragma unroll
@@ -88,12 +99,23 @@ __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, in
     int b2 = __shfl_xor_sync(0xffffffffu, b, o);
     if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
   }
-  VertexEval r;
   r.cur = cur;
   r.conn_own = co;
   r.best_gain = g;
   r.best_b = b;
   return r;
+}
+
+// cur = sum_u w D(own, Pi u) alone (rebalance fallback when no candidate)
+template <int VW>
+__device__ __forceinline__ long long cur_regs(bool valid, int own, int myb, int myw,
+                                              const Topo& t, const long long* s_dbit) {
+  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
+  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
+  long long cur = valid ? (long long)myw * cdist(s_dbit, ocode, mycode) : 0;
+#pragma unroll
+  for (int o = VW / 2; o > 0; o >>= 1) cur += __shfl_xor_sync(0xffffffffu, cur, o);
+  return cur;
 }
 
 // cost of moving to a fixed block `tb` (for the rebalance hash fallback)
@@ -228,6 +250,7 @@ struct RbParams {
 struct RbOut {
   int* target;      // -1: not a rebalance candidate
   long long* gain;
+  unsigned char* to_move;  // zeroed by the candidate pass
 };
 
 // ---------------------------------------------------------------------------
@@ -238,7 +261,8 @@ __global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* _
                                                    const int* __restrict__ tgt,
                                                    const int* __restrict__ w,
                                                    const int* __restrict__ part, Topo t,
-                                                   LpParams lp, LpOut lo, RbParams rb, RbOut ro) {
+                                                   LpParams lp, LpOut lo, RbParams rb, RbOut ro,
+                                                   long long* __restrict__ ctr) {
   __shared__ long long s_dbit[64];
   load_dbit(s_dbit, t);
   __syncthreads();
@@ -247,6 +271,8 @@ __global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* _
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
   const int gi = lane / VW, li = lane % VW;
+  // per-iteration counters are zeroed here instead of by separate memsets
+  if (ctr && blockIdx.x == 0 && threadIdx.x < 2) ctr[threadIdx.x] = 0;
   for (long long vb = wid * GPW; vb < n; vb += nw * GPW) {
     const int v = (int)(vb + gi);
     bool live = v < n;
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* _
       e0 = off[v];
       d = off[v + 1] - e0;
       own = part[v];
+      if (mode == 1 && li == 0) ro.to_move[v] = 0;
       if (d > VW) live = false;  // handled by the shared-memory path
       else if (mode == 0 && lp.locked && lp.locked[v]) {
         live = false;
@@ -270,8 +297,9 @@ __global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* _
       myb = part[tgt[e0 + li]];
       myw = w[e0 + li];
     }
-    VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, t, s_dbit,
-                                 mode == 1 ? rb.elig : nullptr);
+    const int dmax = __reduce_max_sync(0xffffffffu, live ? d : 0);
+    VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, dmax, t, s_dbit,
+                                 mode == 1 ? rb.elig : nullptr, mode == 0 && lp.jet);
     if (mode == 0) {
       if (live && li == 0) lp_decide(v, own, r, lp, lo);
     } else {
@@ -284,15 +312,18 @@ __global__ void __launch_bounds__(256) k_eval_regs(int mode, int n, const int* _
                                      (unsigned long long)rb.pass_counter);
         tb = rb.elig_list[h % (unsigned long long)rb.n_elig];
       }
-      long long cost = 0;
-      if (any) cost = cost_regs<VW>(valid && need, myb, myw, need ? tb : 0, t, s_dbit);
+      long long cost = 0, cur = 0;
+      if (any) {
+        cost = cost_regs<VW>(valid && need, myb, myw, need ? tb : 0, t, s_dbit);
+        cur = cur_regs<VW>(valid && need, own, myb, myw, t, s_dbit);
+      }
       if (live && li == 0) {
         if (r.best_b >= 0) {
           ro.target[v] = r.best_b;
           ro.gain[v] = r.best_gain;
         } else if (need) {
           ro.target[v] = tb;
-          ro.gain[v] = r.cur - cost;
+          ro.gain[v] = cur - cost;
         } else {
           ro.target[v] = -1;  // no eligible block anywhere: incomplete
         }
@@ -552,7 +583,7 @@ __global__ void k_rb_select(int cnt, int strong, const unsigned int* __restrict_
 
 static void launch_eval(const RefineLevel& L, int mode, const Topo& t, const int* part,
                         const LpParams& lp, const LpOut& lo, const RbParams& rb,
-                        const RbOut& ro, cudaStream_t s) {
+                        const RbOut& ro, long long* ctr, cudaStream_t s) {
   const DevGraph& g = L.g;
   // LP first filter / rebalance candidates: every CSR row once (target,
   // weight, Pi[target] = 12 B/slot) + offsets, Pi, lock and the three
@@ -562,10 +593,10 @@ static void launch_eval(const RefineLevel& L, int mode, const Topo& t, const int
   long long groups = (long long)g.n * L.vw;
   int grid = grid_for(groups, B, kSMs * 8);
   switch (L.vw) {
-    case 4: k_eval_regs<4><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
-    case 8: k_eval_regs<8><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
-    case 16: k_eval_regs<16><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
-    default: k_eval_regs<32><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro); break;
+    case 4: k_eval_regs<4><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro, ctr); break;
+    case 8: k_eval_regs<8><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro, ctr); break;
+    case 16: k_eval_regs<16><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro, ctr); break;
+    default: k_eval_regs<32><<<grid, B, 0, s>>>(mode, g.n, g.off, g.tgt, g.w, part, t, lp, lo, rb, ro, ctr); break;
   }
   count_launch();
   if (L.n_heavy > 0) {
@@ -623,16 +654,15 @@ void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigne
   LpOut lo{rb.cand.get(), rb.dest.get(), rb.gkey.get()};
   RbParams rp{};
   RbOut ro{};
-  launch_eval(L, 0, t, part, lp, lo, rp, ro, s);
-  GIM_CUDA(cudaMemsetAsync(rb.movers.get(), 0, sizeof(long long), s));
+  launch_eval(L, 0, t, part, lp, lo, rp, ro, rb.ctr.get(), s);
   ProfScope prof(P_LP_SECOND, 6.0 * g.n, s);  // lower bound: candidate rows not counted
   constexpr int B = 256;
   int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
   switch (L.vw) {
-    case 4: k_lp_second<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
-    case 8: k_lp_second<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
-    case 16: k_lp_second<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
-    default: k_lp_second<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers.get()); break;
+    case 4: k_lp_second<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers); break;
+    case 8: k_lp_second<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers); break;
+    case 16: k_lp_second<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers); break;
+    default: k_lp_second<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, part, t, rb.cand.get(), rb.dest.get(), rb.gkey.get(), rb.to_move.get(), rb.movers); break;
   }
   count_launch();
   GIM_LAUNCH_CHECK();
@@ -647,10 +677,8 @@ void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const 
   LpParams lp{};
   LpOut lo{};
   RbParams rp{ovl, elig, elig_list, n_elig, seed, pass_counter};
-  RbOut ro{rb.dest2.get(), rb.gkey.get()};
-  launch_eval(L, 1, t, part, lp, lo, rp, ro, s);
-  GIM_CUDA(cudaMemsetAsync(rb.to_move.get(), 0, (size_t)g.n, s));
-  GIM_CUDA(cudaMemsetAsync(rb.movers.get(), 0, sizeof(long long), s));
+  RbOut ro{rb.dest2.get(), rb.gkey.get(), rb.to_move.get()};
+  launch_eval(L, 1, t, part, lp, lo, rp, ro, rb.ctr.get(), s);
   // compaction in vertex order + keys
   RbFlag f{part, ovl, rb.dest2.get()};
   RbKeyOut ko{f, rb.gkey.get(), rho, k, strong ? 1 : 0, rb.rkeys.get(), rb.rvals.get()};
@@ -672,7 +700,7 @@ void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const 
   k_rb_select<<<grid, 256, 0, s>>>(cnt, strong ? 1 : 0, rb.rkeys.get(), div, rb.rvals.get(),
                                    rb.rexcl.get(), g.vw, rb.gstart.get(), bw, l_max,
                                    rb.dest2.get(), rb.to_move.get(), rb.dest.get(),
-                                   rb.movers.get());
+                                   rb.movers);
   count_launch(2);
   GIM_LAUNCH_CHECK();
 }
@@ -680,22 +708,27 @@ void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const 
 void apply_moves(const RefineLevel& L, const Topo& t, int* part, long long* bw,
                  RefineBuffers& rb, cudaStream_t s) {
   const DevGraph& g = L.g;
-  GIM_CUDA(cudaMemsetAsync(rb.dj.get(), 0, sizeof(long long), s));
+  // rb.dj was zeroed by the candidate pass of this iteration
   ProfScope prof(P_APPLY, 6.0 * g.n, s);  // lower bound: mover rows not counted
   constexpr int B = 256;
   int grid = grid_for((long long)g.n * L.vw, B, kSMs * 8);
   switch (L.vw) {
-    case 4: k_apply_delta<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
-    case 8: k_apply_delta<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
-    case 16: k_apply_delta<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
-    default: k_apply_delta<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj.get()); break;
+    case 4: k_apply_delta<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj); break;
+    case 8: k_apply_delta<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj); break;
+    case 16: k_apply_delta<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj); break;
+    default: k_apply_delta<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, part, t, rb.to_move.get(), rb.dest.get(), bw, rb.dj); break;
   }
   k_commit<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, rb.to_move.get(), rb.dest.get(), part);
   count_launch(2);
   GIM_LAUNCH_CHECK();
 }
 
+// (re)allocate only when the buffers are smaller than needed, so one set
+// serves every level of a mapping (finest level first in size order)
 void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
+  if (rb.cap_n >= std::max(n, 1) && rb.cap_k >= k && rb.ctr.get()) return;
+  rb.cap_n = std::max(n, 1);
+  rb.cap_k = k;
   size_t nn = (size_t)std::max(n, 1);
   rb.cand = DBuf<unsigned char>(nn, s);
   rb.to_move = DBuf<unsigned char>(nn, s);
@@ -710,8 +743,13 @@ void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
   rb.rexcl = DBuf<long long>(nn, s);
   rb.gstart = DBuf<int>((size_t)k * 31 * 8 + 1, s);
   rb.count = DBuf<int>(1, s);
-  rb.movers = DBuf<long long>(1, s);
-  rb.dj = DBuf<long long>(1, s);
+  rb.ctr = DBuf<long long>(2, s);
+  rb.movers = rb.ctr.get();
+  rb.dj = rb.ctr.get() + 1;
+  GIM_CUDA(cudaMemsetAsync(rb.ctr.get(), 0, 2 * sizeof(long long), s));
+  rb.masks = DBuf<unsigned char>((size_t)k * 2, s);
+  rb.elist = DBuf<int>((size_t)k, s);
+  rb.jtmp = DBuf<long long>(1, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -179,7 +179,8 @@ def contract(dg: DeviceGraph, cmap: torch.Tensor, n_c: int) -> DeviceGraph:
     src = torch.empty(cap, dtype=torch.int32, device=dev)
     m2 = C.c_int64(0)
     g = dg.struct()
-    _lib.call("gim_contract", C.byref(g), _ptr(_i32(cmap, dev)), int(n_c), _ptr(off), _ptr(tgt),
+    cm = _i32(cmap, dev)  # keep every argument tensor alive across the call
+    _lib.call("gim_contract", C.byref(g), _ptr(cm), int(n_c), _ptr(off), _ptr(tgt),
               _ptr(w), _ptr(vw), _ptr(src), C.byref(m2), stream_ptr(dev))
     k = m2.value
     return DeviceGraph(off, tgt[:k].clone(), w[:k].clone(), vw[:n_c].clone(), src[:k].clone(),
@@ -189,7 +190,8 @@ def contract(dg: DeviceGraph, cmap: torch.Tensor, n_c: int) -> DeviceGraph:
 def project(cmap: torch.Tensor, coarse_part: torch.Tensor) -> torch.Tensor:
     """coarsening.py:269-277."""
     out = torch.empty(cmap.numel(), dtype=torch.int32, device=cmap.device)
-    _lib.call("gim_project", cmap.numel(), _ptr(cmap), _ptr(_i32(coarse_part, cmap.device)),
+    cp = _i32(coarse_part, cmap.device)
+    _lib.call("gim_project", cmap.numel(), _ptr(cmap), _ptr(cp),
               _ptr(out), stream_ptr(cmap.device))
     return out
 
@@ -206,7 +208,8 @@ def conn_build(dg: DeviceGraph, assignment, k: int):
     w = torch.empty(cap, dtype=torch.int32, device=dev)
     tot = C.c_int64(0)
     g = dg.struct()
-    _lib.call("gim_conn_build", C.byref(g), _ptr(_i32(assignment, dev)), int(k), _ptr(off),
+    a = _i32(assignment, dev)
+    _lib.call("gim_conn_build", C.byref(g), _ptr(a), int(k), _ptr(off),
               _ptr(blocks), _ptr(w), C.byref(tot), stream_ptr(dev))
     return off, blocks[:tot.value], w[:tot.value]
 
@@ -254,8 +257,10 @@ def apply_moves(dg: DeviceGraph, assignment: torch.Tensor, bw: torch.Tensor, to_
     dj = C.c_int64(0)
     t = topology_struct(hierarchy, distances)
     g = dg.struct()
-    _lib.call("gim_apply_moves", C.byref(g), _ptr(assignment), _ptr(bw), _ptr(_u8(to_move, dev)),
-              _ptr(_i32(dest, dev)), C.byref(t), C.byref(dj), stream_ptr(dev))
+    tm = _u8(to_move, dev)
+    de = _i32(dest, dev)
+    _lib.call("gim_apply_moves", C.byref(g), _ptr(assignment), _ptr(bw), _ptr(tm), _ptr(de),
+              C.byref(t), C.byref(dj), stream_ptr(dev))
     return dj.value
 
 
@@ -370,3 +375,8 @@ def integrated_map_host(offsets, targets, eweights, vweights, hierarchy, distanc
               float(eps), int(seed) & (2**64 - 1), C.byref(p), ptr(a), ptr(bw), C.byref(st),
               stream_ptr())
     return a, bw, stats_dict(st)
+
+
+def set_fanout(on: bool) -> None:
+    """Sibling multisection subtrees on concurrent host threads/streams."""
+    _lib.load().gim_set_fanout(1 if on else 0)

@@ -16,7 +16,11 @@ def main():
     ap.add_argument("--logn", type=int, nargs="+", default=[16, 20])
     ap.add_argument("--oracle", type=int, default=16, help="compare with oracle up to this logn")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--no-fanout", action="store_true")
+    ap.add_argument("--profile", action="store_true")
     args = ap.parse_args()
+    D.set_fanout(not args.no_fanout)
+    D.set_profiling(args.profile)
     h, d = (4, 8, 6), (1, 10, 100)
     for logn in args.logn:
         t0 = time.time()
