@@ -13,9 +13,12 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
+static void configure_pool_once();
+
 void* dmalloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes == 0) return nullptr;
+  configure_pool_once();
   cudaError_t e = cudaMallocAsync(&p, bytes, s);
   if (e != cudaSuccess)
     throw Error{GIM_E_CUDA, std::string("cudaMallocAsync(") + std::to_string(bytes) +
@@ -95,11 +98,12 @@ Topo get_flat_topo(int k) {
 // one-time pool configuration: keep freed blocks cached (no OS round trips
 // between refinement iterations / levels)
 static void configure_pool_once() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::atomic<unsigned long long> done{0};  // bit per device
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  const unsigned long long bit = 1ull << dev;
+  if (done.load(std::memory_order_acquire) & bit) return;
+  done.fetch_or(bit);
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
   uint64_t thr = UINT64_MAX;
