@@ -218,6 +218,10 @@ void gim_set_profiling(int32_t on);
  * streams (default 1).  Results are identical either way. */
 void gim_set_fanout(int32_t on);
 
+/* Run Alg. 4 as one persistent cooperative kernel per level (default 1) or
+ * as per-phase launches with host control.  Results are identical. */
+void gim_set_fused(int32_t on);
+
 /* kernels launched by this host thread since the last reset (evidence). */
 int64_t gim_launch_count(void);
 void gim_reset_launch_count(void);

@@ -177,6 +177,7 @@ __device__ __forceinline__ void block_sum_atomic(long long v, long long* out) {
     if (threadIdx.x == 0 && x != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)x);
   }
+  __syncthreads();  // s[] is reusable by the next call (persistent kernels)
 }
 
 // ---------------------------------------------------------------------------

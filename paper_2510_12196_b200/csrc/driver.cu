@@ -117,11 +117,137 @@ static RefCfg config_for_level(int level, int n_levels, double phi, int rho, int
 // Alg. 4 (refinement.py:389-464).  `part`/`bw` are consumed and replaced by
 // the best mapping seen.
 
+// device-resident loop on/off (gim_set_fused; default on); both give identical results
+static std::atomic<bool> g_fused{true};
+
+static long long max_of(const std::vector<long long>& x) {
+  long long m = 0;
+  for (long long y : x) m = std::max(m, y);
+  return m;
+}
+
+// Alg. 4 with the persistent cooperative kernel (refine_fused.cu); the host
+// only performs the rare strong passes the kernel hands back.
+static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long long* bw_d,
+                               const RefCfg& cfg, double l_max, RunStats& st, RefineBuffers& rb,
+                               cudaStream_t s) {
+  const int n = L.g.n, k = t.k;
+  FusedBuffers fb;
+  fb.cand = rb.cand.get();
+  fb.tm0 = rb.to_move.get();
+  fb.tm1 = rb.locks.get();
+  fb.rcell = rb.rcell.get();
+  fb.dest = rb.dest.get();
+  fb.rtgt = rb.dest2.get();
+  fb.best = rb.best.get();
+  fb.gkey = rb.gkey.get();
+  fb.best_bw = rb.best_bw.get();
+  fb.ctr = rb.fctr.get();
+  fb.state = reinterpret_cast<FusedState*>(rb.fstate.get());
+  FusedState hs{};
+  fb.h_state = &hs;
+  FusedCfg fc;
+  fc.l_max = l_max;
+  fc.sigma = l_max * (1.0 - cfg.sigma_fraction);
+  fc.phi = cfg.phi;
+  fc.jet_c = cfg.jet_c;
+  fc.jet = cfg.jet;
+  fc.rho = cfg.rho;
+  fc.i_max = cfg.i_max;
+  fc.i_w_max = cfg.i_w_max;
+  fc.seed = cfg.seed;
+  GIM_CUDA(cudaMemsetAsync(fb.state, 0, sizeof(FusedState), s));
+  GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 5 * sizeof(long long), s));
+  long long strong = 0;
+  bool host_finished = false;
+  std::vector<long long> bw((size_t)k);
+  std::vector<unsigned char> masks((size_t)k * 2);
+  std::vector<int> el((size_t)k);
+  for (;;) {
+    if (refine_fused_run(L, t, part, bw_d, fc, fb, s)) break;
+    // strong pass (refinement.py:350-386) + the same Alg. 4 bookkeeping
+    GIM_CUDA(cudaMemcpyAsync(bw.data(), bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    int ne = 0;
+    for (int b = 0; b < k; ++b) {
+      masks[b] = (double)bw[b] > l_max;
+      masks[k + b] = (double)bw[b] < fc.sigma;
+      if (masks[k + b]) el[ne++] = b;
+    }
+    const bool incomplete = ne == 0;
+    GIM_CUDA(cudaMemcpyAsync(rb.masks.get(), masks.data(), (size_t)k * 2, cudaMemcpyHostToDevice, s));
+    if (ne)
+      GIM_CUDA(cudaMemcpyAsync(rb.elist.get(), el.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, s));
+    rebalance_pass(L, t, part, bw_d, true, l_max, cfg.rho, cfg.seed, hs.pass_counter,
+                   rb.masks.get(), rb.masks.get() + k, rb.elist.get(), ne, rb, s);
+    apply_moves(L, t, part, bw_d, rb, s);
+    long long ctr[2];
+    GIM_CUDA(cudaMemcpyAsync(bw.data(), bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(ctr, rb.ctr.get(), 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    ++strong;
+    ++hs.iters;
+    hs.i_w = 0;
+    ++hs.pass_counter;
+    if (ctr[0] == 0 && incomplete) {
+      host_finished = true;
+      break;
+    }
+    hs.J += ctr[1];
+    hs.maxw = max_of(bw);
+    hs.locks_nonempty = 0;
+    bool reset = false, take = false;
+    if ((double)hs.maxw <= l_max) {
+      if (!hs.best_balanced) {
+        hs.best_balanced = 1;
+        hs.best_j = hs.J;
+        hs.best_maxw = hs.maxw;
+        reset = take = true;
+      } else if (hs.J < hs.best_j) {
+        reset = (double)hs.J < cfg.phi * (double)hs.best_j;
+        hs.best_j = hs.J;
+        hs.best_maxw = hs.maxw;
+        take = true;
+      }
+    } else if (!hs.best_balanced && hs.maxw < hs.best_maxw) {
+      hs.best_maxw = hs.maxw;
+      reset = take = true;
+    }
+    if (take) {
+      GIM_CUDA(cudaMemcpyAsync(fb.best, part, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(fb.best_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToDevice, s));
+    }
+    hs.i = reset ? 0 : hs.i + 1;
+    if (hs.i >= cfg.i_max) {
+      host_finished = true;
+      break;
+    }
+    hs.status = 0;
+    hs.started = 1;
+    GIM_CUDA(cudaMemcpyAsync(fb.state, &hs, sizeof(FusedState), cudaMemcpyHostToDevice, s));
+    GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 5 * sizeof(long long), s));
+  }
+  if (host_finished) {  // restore the best mapping (the kernel does this itself otherwise)
+    GIM_CUDA(cudaMemcpyAsync(part, fb.best, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    GIM_CUDA(cudaMemcpyAsync(bw_d, fb.best_bw, sizeof(long long) * k, cudaMemcpyDeviceToDevice, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+  }
+  st.lp += hs.lp;
+  st.weak += hs.weak;
+  st.strong += strong;
+  if (st.in_initial) st.init_refine_iterations += hs.iters;
+  else st.refine_iterations += hs.iters;
+}
+
 static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, const RefCfg& cfg,
                    double l_max, RunStats& st, RefineBuffers& rb, cudaStream_t s) {
   const int n = L.g.n, k = t.k;
   if (L.heavy.get() == nullptr) prepare_level(L, k, s);
   alloc_refine_buffers(rb, n, k, s);
+  if (g_fused.load() && fused_supported(k, cfg.rho) && n > 0) {
+    refine_device_loop(L, t, part, bw_d, cfg, l_max, st, rb, s);
+    return;
+  }
   // host mirrors
   size_t pin_bytes = sizeof(long long) * ((size_t)k + 2) + (size_t)k * 2 + sizeof(int) * (size_t)k;
   char* pin = static_cast<char*>(g_pin.get(pin_bytes));
@@ -937,3 +1063,4 @@ extern "C" int64_t gim_launch_count(void) { return launches(); }
 extern "C" void gim_reset_launch_count(void) { reset_launches(); }
 
 extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }
+extern "C" void gim_set_fused(int32_t on) { gim::g_fused.store(on != 0); }

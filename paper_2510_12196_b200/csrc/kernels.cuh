@@ -88,6 +88,11 @@ struct RefineBuffers {
   DBuf<unsigned char> masks;     // [ovl | elig] per block (rebalance)
   DBuf<int> elist;               // eligible block list (rebalance)
   DBuf<long long> jtmp;          // J scratch
+  // device-resident loop (refine_fused.cu)
+  DBuf<int> best;                // best mapping seen
+  DBuf<long long> best_bw, fctr; // its block weights; [movers0, dj0, movers1, dj1, J]
+  DBuf<unsigned char> rcell;     // weak-rebalance cell per vertex
+  DBuf<unsigned char> fstate;    // FusedState (device)
   int cap_n = 0, cap_k = 0;      // sizes the buffers were allocated for
 };
 
@@ -103,5 +108,36 @@ void apply_moves(const RefineLevel& L, const Topo& t, int* part, long long* bw,
                  RefineBuffers& rb, cudaStream_t s);
 long long conn_build(const DevGraph& g, const int* part, int k, int* c_off, int* c_blocks,
                      int* c_w, cudaStream_t s);
+
+// ---- refine_fused.cu: device-resident Alg. 4
+// control state shared between the persistent kernel and the host (which
+// performs the rare strong passes between launches)
+struct FusedState {
+  long long J, best_j, best_maxw, maxw, pass_counter;
+  long long iters, lp, weak;
+  int i, i_w, best_balanced, locks_nonempty, lp_par, status, started;
+};
+
+struct FusedCfg {
+  double l_max, sigma, phi, jet_c;
+  int jet, rho, i_max, i_w_max;
+  unsigned long long seed;
+};
+
+struct FusedBuffers {
+  // aliases into RefineBuffers
+  unsigned char *cand = nullptr, *tm0 = nullptr, *tm1 = nullptr, *rcell = nullptr;
+  int *dest = nullptr, *rtgt = nullptr, *best = nullptr;
+  long long *gkey = nullptr, *best_bw = nullptr, *ctr = nullptr;
+  // owned
+  DBuf<long long> W, S;
+  long long W_cap = 0, S_cap = 0;
+  FusedState* state = nullptr;    // device
+  FusedState* h_state = nullptr;  // pinned host mirror
+};
+
+bool fused_supported(int k, int rho);
+bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long* bw,
+                      const FusedCfg& cfg, FusedBuffers& fb, cudaStream_t s);
 
 }  // namespace gim

@@ -14,244 +14,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "radix.cuh"
+#include "refine_dev.cuh"
 #include "scan.cuh"
 
 namespace gim {
-
-constexpr long long kGainNone = LLONG_MIN;
-
-// distance between two digit codes (see Topo)
-__device__ __forceinline__ long long cdist(const long long* dbit, unsigned long long a,
-                                           unsigned long long b) {
-  unsigned long long c = a ^ b;
-  return c ? dbit[63 - __clzll(c)] : 0ll;
-}
-
-struct Best {
-  long long gain;
-  int b;
-};
-
-// (gain desc, block asc); b < 0 = none
-__device__ __forceinline__ bool best_better(long long g1, int b1, long long g2, int b2) {
-  if (b1 < 0) return false;
-  if (b2 < 0) return true;
-  if (g1 != g2) return g1 > g2;
-  return b1 < b2;
-}
-
-// shared per-block copy of dbit
-__device__ __forceinline__ void load_dbit(long long* s_dbit, const Topo& t) {
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_dbit[i] = t.dbit[i];
-}
-
-// ---------------------------------------------------------------------------
-// Per-vertex gain evaluation, register path (degree <= VW).
-// Lane j of the group holds neighbour j: its block code and edge weight.
-// cost(b_j) = sum_i w_i D(b_j, b_i) by a VW-step shuffle broadcast;
-// gain(b_j) = cur - cost(b_j), cur = cost(own)  (Eq. 1, refinement.py:171-186).
-
-struct VertexEval {
-  long long cur;       // sum_u w D(own, Pi u)
-  long long conn_own;  // conn(v, own)
-  long long best_gain;
-  int best_b;          // -1: no admissible adjacent block
-};
-
-// `dmax` = max degree over the warp's groups (warp-uniform loop bound).
-// Interior vertices (every neighbour in the own block) are the common case
-// after the first iterations: a warp whose groups have no candidate lane
-// skips the whole evaluation, so the pass degenerates to one row sweep.
-template <int VW>
-__device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, int myw, int dmax,
-                                                const Topo& t, const long long* s_dbit,
-                                                const unsigned char* allowed, bool need_conn) {
-  VertexEval r;
-  r.cur = 0;
-  r.conn_own = 0;
-  r.best_gain = kGainNone;
-  r.best_b = -1;
-  const bool cand = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
-  if (!__any_sync(0xffffffffu, cand)) return r;
-  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
-  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
-  long long wv = valid ? myw : 0;
-  long long cur = wv * cdist(s_dbit, ocode, mycode);
-  long long co = (need_conn && valid && myb == own) ? wv : 0;
-  long long cost = 0;
-  const int lim = min(dmax, VW);
-#pragma unroll 4
-  for (int i = 0; i < lim; ++i) {
-    unsigned long long ci = __shfl_sync(0xffffffffu, mycode, i, VW);
-    long long wi = __shfl_sync(0xffffffffu, wv, i, VW);
-    cost += wi * cdist(s_dbit, mycode, ci);
-  }
-#pragma unroll
-  for (int o = VW / 2; o > 0; o >>= 1) {
-    cur += __shfl_xor_sync(0xffffffffu, cur, o);
-    if (need_conn) co += __shfl_xor_sync(0xffffffffu, co, o);
-  }
-  long long g = cand ? cur - cost : kGainNone;
-  int b = cand ? myb : -1;
-#pragma unroll
-  for (int o = VW / 2; o > 0; o >>= 1) {
-    long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
-    int b2 = __shfl_xor_sync(0xffffffffu, b, o);
-    if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
-  }
-  r.cur = cur;
-  r.conn_own = co;
-  r.best_gain = g;
-  r.best_b = b;
-  return r;
-}
-
-// cur = sum_u w D(own, Pi u) alone (rebalance fallback when no candidate)
-template <int VW>
-__device__ __forceinline__ long long cur_regs(bool valid, int own, int myb, int myw,
-                                              const Topo& t, const long long* s_dbit) {
-  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
-  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
-  long long cur = valid ? (long long)myw * cdist(s_dbit, ocode, mycode) : 0;
-#pragma unroll
-  for (int o = VW / 2; o > 0; o >>= 1) cur += __shfl_xor_sync(0xffffffffu, cur, o);
-  return cur;
-}
-
-// cost of moving to a fixed block `tb` (for the rebalance hash fallback)
-template <int VW>
-__device__ __forceinline__ long long cost_regs(bool valid, int myb, int myw, int tb,
-                                               const Topo& t, const long long* s_dbit) {
-  unsigned long long tc = __ldg(t.code + (tb < 0 ? 0 : tb));
-  unsigned long long mc = myb >= 0 ? __ldg(t.code + myb) : 0ull;
-  long long c = valid ? (long long)myw * cdist(s_dbit, tc, mc) : 0;
-#pragma unroll
-  for (int o = VW / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  return c;
-}
-
-// ---------------------------------------------------------------------------
-// Per-vertex gain evaluation, shared-memory path (degree > VW): one warp per
-// vertex, conn(v, b) accumulated into a dense per-warp block table with
-// shared atomics, compacted to the nonzero (block, conn) list, then
-// cost(b) = sum_j conn_j D(b, b_j) over the list.
-
-struct WarpTable {
-  int* tab;    // [k]
-  int* lb;     // [k] nonzero blocks
-  int* lw;     // [k] their conn
-};
-
-__device__ __forceinline__ int warp_build_table(const WarpTable& wt, int k, int e0, int e1,
-                                                const int* __restrict__ tgt,
-                                                const int* __restrict__ w,
-                                                const int* __restrict__ part) {
-  const int lane = lane_id();
-  for (int i = lane; i < k; i += 32) wt.tab[i] = 0;
-  __syncwarp();
-  for (int e = e0 + lane; e < e1; e += 32) atomicAdd(&wt.tab[part[tgt[e]]], w[e]);
-  __syncwarp();
-  int s = 0;
-  for (int base = 0; base < k; base += 32) {
-    int i = base + lane;
-    int x = i < k ? wt.tab[i] : 0;
-    unsigned m = __ballot_sync(0xffffffffu, x != 0);
-    if (x != 0) {
-      int pos = s + __popc(m & ((1u << lane) - 1u));
-      wt.lb[pos] = i;
-      wt.lw[pos] = x;
-    }
-    s += __popc(m);
-  }
-  __syncwarp();
-  return s;
-}
-
-__device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int own,
-                                                 const Topo& t, const long long* s_dbit,
-                                                 const unsigned char* allowed) {
-  const int lane = lane_id();
-  const unsigned long long oc = __ldg(t.code + own);
-  long long cur = 0;
-  for (int j = lane; j < s; j += 32)
-    cur += (long long)wt.lw[j] * cdist(s_dbit, oc, __ldg(t.code + wt.lb[j]));
-  cur = warp_sum_ll(cur);
-  long long g = kGainNone;
-  int b = -1;
-  for (int i = lane; i < s; i += 32) {
-    int bi = wt.lb[i];
-    if (bi == own || (allowed && !allowed[bi])) continue;
-    unsigned long long ci = __ldg(t.code + bi);
-    long long cost = 0;
-    for (int j = 0; j < s; ++j)
-      cost += (long long)wt.lw[j] * cdist(s_dbit, ci, __ldg(t.code + wt.lb[j]));
-    long long gi = cur - cost;
-    if (best_better(gi, bi, g, b)) { g = gi; b = bi; }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
-    int b2 = __shfl_xor_sync(0xffffffffu, b, o);
-    if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
-  }
-  VertexEval r;
-  r.cur = cur;
-  r.conn_own = wt.tab[own];
-  r.best_gain = g;
-  r.best_b = b;
-  return r;
-}
-
-__device__ __forceinline__ long long cost_table(const WarpTable& wt, int s, int tb,
-                                                const Topo& t, const long long* s_dbit) {
-  const unsigned long long tc = __ldg(t.code + tb);
-  long long c = 0;
-  for (int j = lane_id(); j < s; j += 32)
-    c += (long long)wt.lw[j] * cdist(s_dbit, tc, __ldg(t.code + wt.lb[j]));
-  return warp_sum_ll(c);
-}
-
-// ---------------------------------------------------------------------------
-// shared per-vertex decisions
-
-struct LpOut {
-  unsigned char* cand;
-  int* dest;
-  long long* gkey;  // gain for candidates, kGainNone otherwise
-};
-
-struct LpParams {
-  const unsigned char* locked;  // null = no locks
-  int jet;
-  double jet_c;
-};
-
-__device__ __forceinline__ void lp_decide(int v, int own, const VertexEval& r,
-                                          const LpParams& p, const LpOut& o) {
-  bool ok = false;
-  if (r.best_b >= 0) {
-    if (r.best_gain >= 0) ok = true;
-    else if (p.jet) ok = (double)(-r.best_gain) < floor(p.jet_c * (double)r.conn_own);
-  }
-  o.cand[v] = ok ? 1 : 0;
-  o.dest[v] = ok ? r.best_b : own;
-  o.gkey[v] = ok ? r.best_gain : kGainNone;
-}
-
-struct RbParams {
-  const unsigned char* ovl;    // [k] overloaded blocks
-  const unsigned char* elig;   // [k] eligible blocks (bw < sigma)
-  const int* elig_list;        // ascending eligible ids
-  int n_elig;
-  unsigned long long seed;
-  long long pass_counter;
-};
-
-struct RbOut {
-  int* target;      // -1: not a rebalance candidate
-  long long* gain;
-  unsigned char* to_move;  // zeroed by the candidate pass
-};
 
 // ---------------------------------------------------------------------------
 // K9 first filter / K11 candidates, register path.  mode 0 = LP, 1 = rebalance
@@ -499,15 +265,6 @@ __global__ void k_commit(int n, const unsigned char* __restrict__ to_move,
 // and a segmented prefix of vertex weights selects the taken prefix:
 //   weak: exclusive prefix < bw[src] - l_max;  strong: inclusive <= l_max - bw[tgt].
 
-__device__ __forceinline__ int slot_for_gain(long long g) {
-  if (g > 0) return 0;
-  if (g <= -1000) return 30;
-  long long x = -g;  // bisect_right over [0,1..10,20..100,200..1000]
-  if (x <= 10) return (int)x + 1;
-  if (x < 100) return 10 + (int)(x / 10);
-  if (x < 1000) return 19 + (int)(x / 100);
-  return 30;
-}
 
 struct RbFlag {
   const int* part;
@@ -750,6 +507,11 @@ void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
   rb.masks = DBuf<unsigned char>((size_t)k * 2, s);
   rb.elist = DBuf<int>((size_t)k, s);
   rb.jtmp = DBuf<long long>(1, s);
+  rb.best = DBuf<int>(nn, s);
+  rb.best_bw = DBuf<long long>((size_t)k, s);
+  rb.fctr = DBuf<long long>(5, s);
+  rb.rcell = DBuf<unsigned char>(nn, s);
+  rb.fstate = DBuf<unsigned char>(sizeof(FusedState), s);
 }
 
 // ---------------------------------------------------------------------------

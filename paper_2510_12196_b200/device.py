@@ -380,3 +380,8 @@ def integrated_map_host(offsets, targets, eweights, vweights, hierarchy, distanc
 def set_fanout(on: bool) -> None:
     """Sibling multisection subtrees on concurrent host threads/streams."""
     _lib.load().gim_set_fanout(1 if on else 0)
+
+
+def set_fused(on: bool) -> None:
+    """Device-resident Alg. 4 (one cooperative kernel per level) vs per-phase launches."""
+    _lib.load().gim_set_fused(1 if on else 0)

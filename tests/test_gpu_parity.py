@@ -25,6 +25,15 @@ def D():
     return device
 
 
+@pytest.fixture(params=["fused", "phased"])
+def mode(request, D):
+    """Alg. 4 as one persistent cooperative kernel per level ("fused") or as
+    per-phase launches with host control ("phased"); both must be exact."""
+    D.set_fused(request.param == "fused")
+    yield request.param
+    D.set_fused(True)
+
+
 def dev_graph(D, c):
     return D.DeviceGraph.from_host(c.graph())
 
@@ -175,7 +184,7 @@ def test_apply_moves_delta_j(D, golden):
         assert dj == O.total_cost(g, t, new) - O.total_cost(g, t, a)
 
 
-def test_refine_golden(D, golden):
+def test_refine_golden(D, mode, golden):
     for c in golden("refine"):
         g, t = c.graph(), c.topology()
         lev, nl = int(c["level"]), int(c["n_levels"])
@@ -202,21 +211,21 @@ def test_ggg_golden(D, golden):
         assert np.array_equal(np_(part), c["part"])
 
 
-def test_partitioner_golden(D, golden):
+def test_partitioner_golden(D, mode, golden):
     for c in golden("partitioner"):
         part = D.internal_partitioner(dev_graph(D, c), int(c["k"]), c.scalar("eps"),
                                       int(c["seed"]))
         assert np.array_equal(np_(part), c["part"])
 
 
-def test_multisection_golden(D, golden):
+def test_multisection_golden(D, mode, golden):
     for c in golden("multisection"):
         a = D.hierarchical_multisection(dev_graph(D, c), tuple(c["hierarchy"]),
                                         tuple(c["distances"]), c.scalar("eps"), int(c["seed"]))
         assert np.array_equal(np_(a), c["assignment"])
 
 
-def test_integrated_map_small_golden(D, golden):
+def test_integrated_map_small_golden(D, mode, golden):
     for c in golden("im_small"):
         a, bw, st = D.integrated_map_device(dev_graph(D, c), tuple(c["hierarchy"]),
                                             tuple(c["distances"]), c.scalar("eps"),
@@ -226,7 +235,7 @@ def test_integrated_map_small_golden(D, golden):
         assert st["final_j"] == c.scalar("j")
 
 
-def test_integrated_map_cfg1_all_seeds_bit_exact(D, golden):
+def test_integrated_map_cfg1_all_seeds_bit_exact(D, mode, golden):
     """Config 1 through the public drop-in API: identical mappings to the
     reference for seeds 0-4 (stronger than the J tolerance gate)."""
     from paper_2510_12196_b200 import integrated_map
@@ -265,7 +274,7 @@ def test_integrated_map_edge_cases(D):
     assert np.array_equal(m.block_weights, bw)
 
 
-def test_integrated_map_matches_oracle_rgg(D):
+def test_integrated_map_matches_oracle_rgg(D, mode):
     """Mid-size rgg with a real level stack: identical to the oracle."""
     from paper_2510_12196_b200 import integrated_map
     from paper_2510_12196_b200.generators import gen_rgg
