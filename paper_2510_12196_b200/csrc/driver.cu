@@ -143,6 +143,13 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   fb.gkey = rb.gkey.get();
   fb.best_bw = rb.best_bw.get();
   fb.ctr = rb.fctr.get();
+  fb.bstamp = rb.bstamp.get();
+  const size_t nn = (size_t)rb.cap_n;
+  fb.lsmall = rb.lists.get();
+  fb.lheavy = fb.lsmall + nn;
+  fb.lcand = fb.lheavy + nn;
+  fb.lmov0 = fb.lcand + nn;
+  fb.lmov1 = fb.lmov0 + nn;
   fb.state = reinterpret_cast<FusedState*>(rb.fstate.get());
   FusedState hs{};
   fb.h_state = &hs;
@@ -157,7 +164,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   fc.i_w_max = cfg.i_w_max;
   fc.seed = cfg.seed;
   GIM_CUDA(cudaMemsetAsync(fb.state, 0, sizeof(FusedState), s));
-  GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 5 * sizeof(long long), s));
+  GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 17 * sizeof(long long), s));
   long long strong = 0;
   bool host_finished = false;
   std::vector<long long> bw((size_t)k);
@@ -224,8 +231,10 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
     }
     hs.status = 0;
     hs.started = 1;
+    hs.reinit = 1;  // the host pass reused the per-vertex arrays
+    hs.prev_n = 0;  // no locks after a rebalance pass
     GIM_CUDA(cudaMemcpyAsync(fb.state, &hs, sizeof(FusedState), cudaMemcpyHostToDevice, s));
-    GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 5 * sizeof(long long), s));
+    GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 17 * sizeof(long long), s));
   }
   if (host_finished) {  // restore the best mapping (the kernel does this itself otherwise)
     GIM_CUDA(cudaMemcpyAsync(part, fb.best, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
@@ -244,7 +253,9 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
   const int n = L.g.n, k = t.k;
   if (L.heavy.get() == nullptr) prepare_level(L, k, s);
   alloc_refine_buffers(rb, n, k, s);
-  if (g_fused.load() && fused_supported(k, cfg.rho) && n > 0) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(L.g.src) |
+                         reinterpret_cast<uintptr_t>(L.g.tgt)) & 15) == 0;
+  if (g_fused.load() && fused_supported(k, cfg.rho) && n > 0 && aligned) {
     refine_device_loop(L, t, part, bw_d, cfg, l_max, st, rb, s);
     return;
   }

@@ -93,6 +93,7 @@ struct RefineBuffers {
   DBuf<long long> best_bw, fctr; // its block weights; [movers0, dj0, movers1, dj1, J]
   DBuf<unsigned char> rcell;     // weak-rebalance cell per vertex
   DBuf<unsigned char> fstate;    // FusedState (device)
+  DBuf<int> bstamp, lists;       // boundary stamps; 5 work lists of n entries
   int cap_n = 0, cap_k = 0;      // sizes the buffers were allocated for
 };
 
@@ -115,7 +116,10 @@ long long conn_build(const DevGraph& g, const int* part, int k, int* c_off, int*
 struct FusedState {
   long long J, best_j, best_maxw, maxw, pass_counter;
   long long iters, lp, weak;
-  int i, i_w, best_balanced, locks_nonempty, lp_par, status, started;
+  int i, i_w, best_balanced, locks_nonempty, lp_par, prev_n, stamp;
+  int status;   // 0 = finished, 1 = strong pass due (host)
+  int started;  // 0 = first launch of this refinement
+  int reinit;   // 1 = re-establish the per-vertex list invariants on entry
 };
 
 struct FusedCfg {
@@ -129,6 +133,9 @@ struct FusedBuffers {
   unsigned char *cand = nullptr, *tm0 = nullptr, *tm1 = nullptr, *rcell = nullptr;
   int *dest = nullptr, *rtgt = nullptr, *best = nullptr;
   long long *gkey = nullptr, *best_bw = nullptr, *ctr = nullptr;
+  int *bstamp = nullptr, *lsmall = nullptr, *lheavy = nullptr, *lcand = nullptr;
+  int *lmov0 = nullptr, *lmov1 = nullptr;
+  long long lp_seen = 0, weak_seen = 0;
   // owned
   DBuf<long long> W, S;
   long long W_cap = 0, S_cap = 0;

@@ -509,7 +509,9 @@ void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
   rb.jtmp = DBuf<long long>(1, s);
   rb.best = DBuf<int>(nn, s);
   rb.best_bw = DBuf<long long>((size_t)k, s);
-  rb.fctr = DBuf<long long>(5, s);
+  rb.fctr = DBuf<long long>(17, s);
+  rb.bstamp = DBuf<int>(nn, s);
+  rb.lists = DBuf<int>(nn * 5, s);
   rb.rcell = DBuf<unsigned char>(nn, s);
   rb.fstate = DBuf<unsigned char>(sizeof(FusedState), s);
 }

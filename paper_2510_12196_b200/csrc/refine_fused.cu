@@ -4,6 +4,19 @@
 // J tracking and best-mapping bookkeeping — with grid-wide barriers between
 // phases and no host round trip per iteration.
 //
+// Work lists.  Every phase starts from a compact list instead of sweeping
+// all vertices with one warp each: an edge-parallel, vectorised sweep stamps
+// boundary vertices (some neighbour in another block — only they can have a
+// label-propagation candidate, refinement.py:187-190), a vertex sweep
+// compacts them, and the gain evaluation, second filter, move application
+// and commit then run over the boundary / candidate / mover lists.  Lists
+// are appended with warp-aggregated atomics (order is irrelevant: every
+// per-vertex result and every reduction is order-independent integer math).
+// Invariants kept between iterations: gkey = LLONG_MIN and rtgt = -1 for
+// every non-candidate; move flags are set only for the current movers and
+// the lock set (= previous LP movers), both listed, so resets touch only
+// listed vertices.
+//
 // The Alg. 4 control state (i, i_w, pass counter, best J / max weight, locks)
 // is replicated in every CTA and updated identically from the same global
 // counters after each barrier, so every CTA takes the same branch.  All float
@@ -16,8 +29,8 @@
 // before c* is taken whole, every cell after it not at all, and inside c* a
 // vertex is taken iff P_{c*} + (weight of earlier c*-vertices of b) < excess_b.
 // That in-cell prefix is a per-block running sum in vertex order: CTAs own
-// contiguous vertex ranges, publish per-block partial sums, and one warp per
-// CTA walks its range with __match_any_sync ranking.
+// contiguous vertex ranges, publish per-block partial sums (scanned across
+// CTAs), and one warp per CTA walks its range with __match_any_sync ranking.
 //
 // Strong passes (rare: 7 of ~3,000 passes on rgg 2^20) exit the kernel
 // ("yield"); the host runs the sort-based strong pass and relaunches.
@@ -33,6 +46,8 @@ namespace gim {
 
 constexpr int kFusedBlock = 256;
 constexpr int kFusedWarps = kFusedBlock / 32;
+constexpr int kCtrStride = 8;  // per-iteration-parity counters
+enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ };
 
 struct FusedArgs {
   int n;
@@ -48,29 +63,32 @@ struct FusedArgs {
   long long* bw;
   int* best;
   long long* best_bw;
-  unsigned char* cand;
   int* dest;
   long long* gkey;
-  unsigned char* tm0;
-  unsigned char* tm1;
-  int* rtgt;             // rebalance target per vertex (-1 = none)
-  unsigned char* rcell;  // rebalance cell per vertex
-  long long* W;          // [k * C] candidate weight per (source block, cell)
-  long long* S;          // [G * k] per-CTA partial sums of c*-cell weights
-  long long* ctr;        // [movers0, dj0, movers1, dj1, J]
-  const int* heavy;
-  int n_heavy;
+  unsigned char* flags0;
+  unsigned char* flags1;
+  int* rtgt;
+  unsigned char* rcell;
+  int* bstamp;         // boundary stamp per vertex
+  int* lsmall;         // work lists
+  int* lheavy;
+  int* lcand;
+  int* lmov0;
+  int* lmov1;
+  long long* W;        // [k * NC]
+  long long* S;        // [k * G]
+  long long* ctr;      // [2 * kCtrStride] per-parity counters, [16] = J at entry
   FusedState* st;
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
   unsigned long long seed;
 };
 
-// per-CTA replicated control state
 struct Ctl {
   long long J, best_j, best_maxw, maxw, pass_counter;
-  int i, i_w, best_balanced, locks_nonempty, lp_par, it, brk, take, strong_yield;
   long long iters, lp, weak;
+  int i, i_w, best_balanced, locks_nonempty, lp_par, prev_n, it, stamp;
+  int brk, take, strong_yield;
 };
 
 __device__ __forceinline__ long long block_max_bw(const long long* bw, int k) {
@@ -87,6 +105,20 @@ __device__ __forceinline__ long long block_max_bw(const long long* bw, int k) {
   return r;
 }
 
+// warp-aggregated append; every lane of the warp must call it
+__device__ __forceinline__ void warp_append(bool pred, int val, int* list, long long* counter) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return;
+  const int lane = lane_id();
+  const int leader = __ffs(m) - 1;
+  long long base = 0;
+  if (lane == leader)
+    base = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(counter),
+                                (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
 template <int VW>
 __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   cg::grid_group grid = cg::this_grid();
@@ -97,7 +129,8 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   const int k = A.k;
   const int NC = 31 * A.rho;
   const int n = A.n;
-  // dynamic smem: warp tables | ovl[k] | elig[k] | elist[k] | cstar[k] | pstar[k] | run[k]
+  const int G = gridDim.x;
+  // dynamic smem: warp tables | pstar[k] | run[k] | elist[k] | cstar[k] | ovl[k] | elig[k]
   int* tables = reinterpret_cast<int*>(dsm);
   long long* pstar = reinterpret_cast<long long*>(tables + (size_t)kFusedWarps * 3 * k);
   long long* run = pstar + k;
@@ -113,30 +146,43 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   const long long NW = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long GT = (long long)gridDim.x * blockDim.x;
+  const long long wt0 = gt - lane;  // first thread of this warp (warp-uniform loops)
   constexpr int GPW = 32 / VW;
   const int gi = lane / VW, li = lane % VW;
   WarpTable wt;
   wt.tab = tables + (size_t)warp * 3 * k;
   wt.lb = wt.tab + k;
   wt.lw = wt.lb + k;
-  // contiguous vertex range of this CTA (weak selection walk)
-  const int R = (n + gridDim.x - 1) / gridDim.x;
+  const int R = (n + G - 1) / G;  // contiguous vertex range of this CTA
   const int r0 = min(n, (int)blockIdx.x * R), r1 = min(n, r0 + R);
 
-  // ---- entry: J, best := current (first launch only)
-  if (!A.st->started) {
+  // ---- entry
+  const bool first = !A.st->started;
+  const bool reinit = first || A.st->reinit;
+  if (reinit) {  // (re)establish the list invariants
+    for (long long v = gt; v < n; v += GT) {
+      A.gkey[v] = kGainNone;
+      A.rtgt[v] = -1;
+      A.flags0[v] = 0;
+      A.flags1[v] = 0;
+      A.bstamp[v] = 0;
+    }
+    for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
+  }
+  if (first) {
     long long acc = 0;
     for (long long e = gt; e < A.m2; e += GT)
       acc += (long long)A.w[e] * dist(A.t, A.part[A.src[e]], A.part[A.tgt[e]]);
-    block_sum_atomic<kFusedBlock>(acc, A.ctr + 4);
+    block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
     for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
-    for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
     if (blockIdx.x == 0)
       for (int b = threadIdx.x; b < k; b += blockDim.x) A.best_bw[b] = A.bw[b];
-    grid.sync();
+  }
+  grid.sync();
+  if (first) {
     long long mx = block_max_bw(A.bw, k);
     if (threadIdx.x == 0) {
-      C.J = A.ctr[4];
+      C.J = A.ctr[16];
       C.maxw = mx;
       C.best_balanced = (double)mx <= A.l_max;
       C.best_j = C.J;
@@ -145,8 +191,8 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       C.pass_counter = 0;
       C.locks_nonempty = 0;
       C.lp_par = 0;
-      C.it = 0;
-      C.iters = C.lp = C.weak = 0;
+      C.prev_n = 0;
+      C.stamp = 0;
     }
   } else if (threadIdx.x == 0) {
     const FusedState& S0 = *A.st;
@@ -160,10 +206,12 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
     C.best_balanced = S0.best_balanced;
     C.locks_nonempty = S0.locks_nonempty;
     C.lp_par = S0.lp_par;
-    C.it = 0;
-    C.iters = C.lp = C.weak = 0;
+    C.prev_n = S0.prev_n;
+    C.stamp = S0.stamp;
   }
   if (threadIdx.x == 0) {
+    C.it = 0;
+    C.iters = C.lp = C.weak = 0;
     C.brk = 0;
     C.strong_yield = 0;
   }
@@ -178,28 +226,58 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       break;
     }
     const int q = C.it & 1;
-    long long* movers = A.ctr + 2 * q;
-    long long* dj = A.ctr + 2 * q + 1;
-    unsigned char* tm = C.lp_par ? A.tm1 : A.tm0;
-    const unsigned char* locks = C.locks_nonempty ? (C.lp_par ? A.tm0 : A.tm1) : nullptr;
+    long long* cnt = A.ctr + q * kCtrStride;          // this iteration (zeroed beforehand)
+    long long* cnt_next = A.ctr + (q ^ 1) * kCtrStride;
+    unsigned char* tmf = C.lp_par ? A.flags1 : A.flags0;   // to_move flags
+    unsigned char* lkf = C.lp_par ? A.flags0 : A.flags1;   // lock flags (= previous movers)
+    int* lmov = C.lp_par ? A.lmov1 : A.lmov0;
+    const int* lprev = C.lp_par ? A.lmov0 : A.lmov1;
+    const int prev_n = C.prev_n;
+    const bool use_locks = C.locks_nonempty != 0;
+    const int stamp = C.stamp + 1;
     bool incomplete = false;
     if (balanced_now) {
-      // ---- K9 first filter
-      LpParams lp{locks, A.jet, A.jet_c};
-      LpOut lo{A.cand, A.dest, A.gkey};
-      for (long long vb = gw * GPW; vb < n; vb += NW * GPW) {
-        const int v = (int)(vb + gi);
-        bool live = v < n;
+      // ---- boundary stamps: edge-parallel, int4-vectorised over E_u
+      {
+        const long long m4 = A.m2 & ~3ll;
+        for (long long e = gt * 4; e < m4; e += GT * 4) {
+          int4 s4 = *reinterpret_cast<const int4*>(A.src + e);
+          int4 t4 = *reinterpret_cast<const int4*>(A.tgt + e);
+          int ps0 = A.part[s4.x], ps1 = A.part[s4.y], ps2 = A.part[s4.z], ps3 = A.part[s4.w];
+          int pt0 = A.part[t4.x], pt1 = A.part[t4.y], pt2 = A.part[t4.z], pt3 = A.part[t4.w];
+          if (ps0 != pt0) A.bstamp[s4.x] = stamp;
+          if (ps1 != pt1) A.bstamp[s4.y] = stamp;
+          if (ps2 != pt2) A.bstamp[s4.z] = stamp;
+          if (ps3 != pt3) A.bstamp[s4.w] = stamp;
+        }
+        for (long long e = m4 + gt; e < A.m2; e += GT)
+          if (A.part[A.src[e]] != A.part[A.tgt[e]]) A.bstamp[A.src[e]] = stamp;
+      }
+      grid.sync();
+      // ---- boundary list (unlocked), split by degree
+      for (long long b0 = wt0; b0 < n; b0 += GT) {
+        const long long v = b0 + lane;
+        bool bnd = false, heavy = false;
+        if (v < n && A.bstamp[v] == stamp && !(use_locks && lkf[v])) {
+          bnd = true;
+          heavy = A.off[v + 1] - A.off[v] > VW;
+        }
+        warp_append(bnd && !heavy, (int)v, A.lsmall, cnt + C_SMALL);
+        warp_append(bnd && heavy, (int)v, A.lheavy, cnt + C_HEAVY);
+      }
+      grid.sync();
+      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
+      // ---- K9 first filter over the boundary list
+      const long long ns = cnt[C_SMALL], nh = cnt[C_HEAVY];
+      for (long long ib = gw * GPW; ib < ns; ib += NW * GPW) {
+        const long long idx = ib + gi;
+        const bool live = idx < ns;
+        const int v = live ? A.lsmall[idx] : 0;
         int e0 = 0, d = 0, own = 0;
         if (live) {
           e0 = A.off[v];
           d = A.off[v + 1] - e0;
           own = A.part[v];
-          if (d > VW) live = false;
-          else if (locks && locks[v]) {
-            live = false;
-            if (li == 0) { lo.cand[v] = 0; lo.dest[v] = own; lo.gkey[v] = kGainNone; }
-          }
         }
         const bool valid = live && li < d;
         int myb = -1, myw = 0;
@@ -210,29 +288,42 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         const int dmax = __reduce_max_sync(0xffffffffu, live ? d : 0);
         VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, dmax, A.t, s_dbit, nullptr,
                                      A.jet != 0);
-        if (live && li == 0) lp_decide(v, own, r, lp, lo);
-      }
-      for (long long hi = gw; hi < A.n_heavy; hi += NW) {
-        const int v = A.heavy[hi];
-        const int own = A.part[v];
-        if (locks && locks[v]) {
-          if (lane == 0) { lo.cand[v] = 0; lo.dest[v] = own; lo.gkey[v] = kGainNone; }
-          continue;
+        bool ok = false;
+        if (live && r.best_b >= 0) {
+          if (r.best_gain >= 0) ok = true;
+          else if (A.jet) ok = (double)(-r.best_gain) < floor(A.jet_c * (double)r.conn_own);
         }
+        if (ok && li == 0) {
+          A.dest[v] = r.best_b;
+          A.gkey[v] = r.best_gain;
+        }
+        warp_append(ok && li == 0, v, A.lcand, cnt + C_CAND);
+      }
+      for (long long hi = gw; hi < nh; hi += NW) {
+        const int v = A.lheavy[hi];
+        const int own = A.part[v];
         int s = warp_build_table(wt, k, A.off[v], A.off[v + 1], A.tgt, A.w, A.part);
         VertexEval r = eval_table(wt, s, own, A.t, s_dbit, nullptr);
-        if (lane == 0) lp_decide(v, own, r, lp, lo);
-        __syncwarp();
+        bool ok = false;
+        if (r.best_b >= 0) {
+          if (r.best_gain >= 0) ok = true;
+          else if (A.jet) ok = (double)(-r.best_gain) < floor(A.jet_c * (double)r.conn_own);
+        }
+        if (ok && lane == 0) {
+          A.dest[v] = r.best_b;
+          A.gkey[v] = r.best_gain;
+        }
+        warp_append(ok && lane == 0, v, A.lcand, cnt + C_CAND);
       }
       grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x < 2) A.ctr[2 * (q ^ 1) + threadIdx.x] = 0;
-      // ---- K10 second filter
-      long long moved = 0;
-      for (long long vb = gw * GPW; vb < n; vb += NW * GPW) {
-        const int v = (int)(vb + gi);
-        const bool c = v < n && A.cand[v];
+      // ---- K10 second filter over the candidates
+      const long long nc = cnt[C_CAND];
+      for (long long ib = gw * GPW; ib < nc; ib += NW * GPW) {
+        const long long idx = ib + gi;
+        const bool live = idx < nc;
+        const int v = live ? A.lcand[idx] : 0;
         long long fut = 0;
-        if (c) {
+        if (live) {
           const long long gv = A.gkey[v];
           const unsigned long long oc = __ldg(A.t.code + A.part[v]);
           const unsigned long long dc = __ldg(A.t.code + A.dest[v]);
@@ -247,17 +338,13 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         }
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
-        if (v < n && li == 0) {
-          bool m = c && fut >= 0;
-          tm[v] = m ? 1 : 0;
-          moved += m;
-        }
+        const bool m = live && li == 0 && fut >= 0;
+        if (m) tmf[v] = 1;
+        warp_append(m, v, lmov, cnt + C_MOV);
       }
-      block_sum_atomic<kFusedBlock>(moved, movers);
       grid.sync();
     } else {
-      // ---- K11 weak rebalance candidates (refinement.py:273-309); locks are
-      // cleared by the control update below (locks_nonempty = 0)
+      // ---- K11 weak rebalance candidates (refinement.py:273-309)
       for (int b = threadIdx.x; b < k; b += blockDim.x) {
         ovl[b] = (double)A.bw[b] > A.l_max;
         elig[b] = (double)A.bw[b] < A.sigma;
@@ -272,21 +359,28 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       __syncthreads();
       const int n_elig = s_nelig;
       incomplete = n_elig == 0;
-      RbParams rp{ovl, elig, elist, n_elig, A.seed, C.pass_counter};
-      for (long long vb = gw * GPW; vb < n; vb += NW * GPW) {
-        const int v = (int)(vb + gi);
-        bool live = v < n;
+      for (long long b0 = wt0; b0 < n; b0 += GT) {  // vertices of overloaded blocks
+        const long long v = b0 + lane;
+        bool inb = false, heavy = false;
+        if (v < n && ovl[A.part[v]]) {
+          inb = true;
+          heavy = A.off[v + 1] - A.off[v] > VW;
+        }
+        warp_append(inb && !heavy, (int)v, A.lsmall, cnt + C_SMALL);
+        warp_append(inb && heavy, (int)v, A.lheavy, cnt + C_HEAVY);
+      }
+      grid.sync();
+      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
+      const long long ns = cnt[C_SMALL], nh = cnt[C_HEAVY];
+      for (long long ib = gw * GPW; ib < ns; ib += NW * GPW) {
+        const long long idx = ib + gi;
+        const bool live = idx < ns;
+        const int v = live ? A.lsmall[idx] : 0;
         int e0 = 0, d = 0, own = 0;
         if (live) {
           e0 = A.off[v];
           d = A.off[v + 1] - e0;
           own = A.part[v];
-          if (li == 0) tm[v] = 0;
-          if (d > VW) live = false;
-          else if (!ovl[own]) {
-            live = false;
-            if (li == 0) A.rtgt[v] = -1;
-          }
         }
         const bool valid = live && li < d;
         int myb = -1, myw = 0;
@@ -301,8 +395,8 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         unsigned any = __ballot_sync(0xffffffffu, need);
         int tb = -1;
         if (need) {
-          unsigned long long h = hash2(rp.seed, (unsigned long long)v,
-                                       (unsigned long long)rp.pass_counter);
+          unsigned long long h = hash2(A.seed, (unsigned long long)v,
+                                       (unsigned long long)C.pass_counter);
           tb = elist[h % (unsigned long long)n_elig];
         }
         long long cost = 0, cur = 0;
@@ -310,9 +404,9 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           cost = cost_regs<VW>(valid && need, myb, myw, need ? tb : 0, A.t, s_dbit);
           cur = cur_regs<VW>(valid && need, own, myb, myw, A.t, s_dbit);
         }
-        if (live && li == 0) {
-          int target = -1;
-          long long gain = 0;
+        int target = -1;
+        long long gain = 0;
+        if (live) {
           if (r.best_b >= 0) {
             target = r.best_b;
             gain = r.best_gain;
@@ -320,22 +414,20 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
             target = tb;
             gain = cur - cost;
           }
+        }
+        const bool isc = li == 0 && target >= 0;
+        if (isc) {
           A.rtgt[v] = target;
-          if (target >= 0) {
-            int cell = slot_for_gain(gain) * A.rho + v % A.rho;
-            A.rcell[v] = (unsigned char)cell;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
-                      (unsigned long long)(long long)A.vw[v]);
-          }
+          int cell = slot_for_gain(gain) * A.rho + v % A.rho;
+          A.rcell[v] = (unsigned char)cell;
+          atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
+                    (unsigned long long)(long long)A.vw[v]);
         }
+        warp_append(isc, v, A.lcand, cnt + C_CAND);
       }
-      for (long long hi = gw; hi < A.n_heavy; hi += NW) {
-        const int v = A.heavy[hi];
+      for (long long hi = gw; hi < nh; hi += NW) {
+        const int v = A.lheavy[hi];
         const int own = A.part[v];
-        if (!ovl[own]) {
-          if (lane == 0) A.rtgt[v] = -1;
-          continue;
-        }
         int s = warp_build_table(wt, k, A.off[v], A.off[v + 1], A.tgt, A.w, A.part);
         VertexEval r = eval_table(wt, s, own, A.t, s_dbit, elig);
         int target = -1;
@@ -344,26 +436,26 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           target = r.best_b;
           gain = r.best_gain;
         } else if (n_elig > 0) {
-          unsigned long long h = hash2(rp.seed, (unsigned long long)v,
-                                       (unsigned long long)rp.pass_counter);
+          unsigned long long h = hash2(A.seed, (unsigned long long)v,
+                                       (unsigned long long)C.pass_counter);
           target = elist[h % (unsigned long long)n_elig];
           gain = r.cur - cost_table(wt, s, target, A.t, s_dbit);
         }
-        if (lane == 0) {
+        const bool isc = lane == 0 && target >= 0;
+        if (isc) {
           A.rtgt[v] = target;
-          if (target >= 0) {
-            int cell = slot_for_gain(gain) * A.rho + v % A.rho;
-            A.rcell[v] = (unsigned char)cell;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
-                      (unsigned long long)(long long)A.vw[v]);
-          }
+          int cell = slot_for_gain(gain) * A.rho + v % A.rho;
+          A.rcell[v] = (unsigned char)cell;
+          atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
+                    (unsigned long long)(long long)A.vw[v]);
         }
-        __syncwarp();
+        warp_append(isc, v, A.lcand, cnt + C_CAND);
       }
+      // the lock set is cleared on every rebalance pass (refinement.py:425)
+      for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;
       grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x < 2) A.ctr[2 * (q ^ 1) + threadIdx.x] = 0;
-      // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block and
-      // this CTA's per-block weight of c*-cell candidates
+      // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block (every
+      // CTA redundantly) and this CTA's per-block weight of c*-cell vertices
       for (int b = threadIdx.x; b < k; b += blockDim.x) {
         run[b] = 0;
         if (!ovl[b]) { cstar[b] = NC; pstar[b] = 0; continue; }
@@ -380,93 +472,107 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       }
       __syncthreads();
       for (int v = r0 + threadIdx.x; v < r1; v += blockDim.x) {
-        int tb = A.rtgt[v];
-        if (tb < 0) continue;
-        int b = A.part[v];
+        if (A.rtgt[v] < 0) continue;
+        const int b = A.part[v];
         if ((int)A.rcell[v] == cstar[b])
           atomicAdd(reinterpret_cast<unsigned long long*>(&run[b]), (unsigned long long)(long long)A.vw[v]);
       }
       __syncthreads();
-      for (int b = threadIdx.x; b < k; b += blockDim.x) A.S[(size_t)blockIdx.x * k + b] = run[b];
+      for (int b = threadIdx.x; b < k; b += blockDim.x) A.S[(size_t)b * G + blockIdx.x] = run[b];
       grid.sync();
-      // step B: in-cell prefix in vertex order, then the take decisions
-      for (int b = threadIdx.x; b < k; b += blockDim.x) {
-        long long base = 0;
-        for (int c2 = 0; c2 < (int)blockIdx.x; ++c2) base += A.S[(size_t)c2 * k + b];
-        run[b] = base;
+      // step B: exclusive scan of S over CTAs, one warp per block
+      for (long long b = gw; b < k; b += NW) {
+        long long carry = 0;
+        long long* row = A.S + (size_t)b * G;
+        for (int c0 = 0; c0 < G; c0 += 32) {
+          const int c = c0 + lane;
+          long long x = c < G ? row[c] : 0;
+          long long incl = x;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (c < G) row[c] = carry + incl - x;
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
       }
+      grid.sync();
+      // step C: in-cell prefix in vertex order (warp 0 walks the CTA range),
+      // whole cells before c* everywhere else
+      for (int b = threadIdx.x; b < k; b += blockDim.x) run[b] = A.S[(size_t)b * G + blockIdx.x];
       __syncthreads();
-      long long moved = 0;
       if (warp == 0) {
         for (int v0 = r0; v0 < r1; v0 += 32) {
           const int v = v0 + lane;
           bool partial = false;
           int b = 0;
           long long wv = 0;
-          if (v < r1) {
-            int tb = A.rtgt[v];
-            if (tb >= 0) {
-              b = A.part[v];
-              partial = (int)A.rcell[v] == cstar[b];
-              wv = A.vw[v];
-            }
+          if (v < r1 && A.rtgt[v] >= 0) {
+            b = A.part[v];
+            partial = (int)A.rcell[v] == cstar[b];
+            wv = A.vw[v];
           }
-          unsigned act = __ballot_sync(0xffffffffu, partial);
+          const unsigned act = __ballot_sync(0xffffffffu, partial);
+          bool take = false;
           if (partial) {
-            unsigned peers = __match_any_sync(act, b);
-            int leader = __ffs(peers) - 1;
+            const unsigned peers = __match_any_sync(act, b);
+            const int leader = __ffs(peers) - 1;
             long long before = 0, total = 0;
-            unsigned m = peers;
-            while (m) {
-              int l = __ffs(m) - 1;
-              m &= m - 1;
-              long long x = __shfl_sync(peers, wv, l);
-              if (l < (int)lane) before += x;
+            unsigned mm = peers;
+            while (mm) {
+              const int l = __ffs(mm) - 1;
+              mm &= mm - 1;
+              const long long x = __shfl_sync(peers, wv, l);
+              if (l < lane) before += x;
               total += x;
             }
-            const long long q0 = run[b] + before;
             const double excess = (double)A.bw[b] - A.l_max;
-            if ((double)(pstar[b] + q0) < excess) {
-              tm[v] = 1;
-              A.dest[v] = A.rtgt[v];
-              ++moved;
-            }
+            take = (double)(pstar[b] + run[b] + before) < excess;
             __syncwarp(peers);
-            if ((int)lane == leader) run[b] += total;
+            if (lane == leader) run[b] += total;
           }
-          __syncwarp();
-        }
-      } else {
-        for (int v = r0 + threadIdx.x - 32; v < r1; v += blockDim.x - 32) {
-          int tb = A.rtgt[v];
-          if (tb < 0) continue;
-          int b = A.part[v];
-          if ((int)A.rcell[v] < cstar[b]) {
-            tm[v] = 1;
-            A.dest[v] = tb;
-            ++moved;
+          if (take) {
+            tmf[v] = 1;
+            A.dest[v] = A.rtgt[v];
           }
+          warp_append(take, v, lmov, cnt + C_MOV);
         }
       }
-      block_sum_atomic<kFusedBlock>(moved, movers);
+      const long long nc = cnt[C_CAND];
+      for (long long b0 = wt0; b0 < nc; b0 += GT) {
+        const long long idx = b0 + lane;
+        bool take = false;
+        int v = 0;
+        if (idx < nc) {
+          v = A.lcand[idx];
+          take = (int)A.rcell[v] < cstar[A.part[v]];
+          if (take) {
+            tmf[v] = 1;
+            A.dest[v] = A.rtgt[v];
+          }
+        }
+        warp_append(take, v, lmov, cnt + C_MOV);
+      }
       grid.sync();
-      for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;  // next weak pass
     }
-    // ---- K13 apply moves: exact dJ + block weights
+    // ---- K13 apply moves over the movers: exact dJ + block weights
     {
+      const long long nm = cnt[C_MOV];
       long long acc = 0;
-      for (long long vb = gw * GPW; vb < n; vb += NW * GPW) {
-        const int v = (int)(vb + gi);
-        if (v < n && tm[v]) {
+      for (long long ib = gw * GPW; ib < nm; ib += NW * GPW) {
+        const long long idx = ib + gi;
+        if (idx < nm) {
+          const int v = lmov[idx];
           const int ov = A.part[v], nv = A.dest[v];
           const unsigned long long oc = __ldg(A.t.code + ov), nc = __ldg(A.t.code + nv);
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
-            int u = A.tgt[e];
-            bool um = tm[u];
-            int ou = A.part[u];
-            int nu = um ? A.dest[u] : ou;
-            long long dd = cdist(s_dbit, nc, __ldg(A.t.code + nu)) -
-                           cdist(s_dbit, oc, __ldg(A.t.code + ou));
+            const int u = A.tgt[e];
+            const bool um = tmf[u];
+            const int ou = A.part[u];
+            const int nu = um ? A.dest[u] : ou;
+            const long long dd = cdist(s_dbit, nc, __ldg(A.t.code + nu)) -
+                                 cdist(s_dbit, oc, __ldg(A.t.code + ou));
             acc += (long long)A.w[e] * dd * (um ? 1 : 2);
           }
           if (li == 0 && ov != nv) {
@@ -477,31 +583,55 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           }
         }
       }
-      block_sum_atomic<kFusedBlock>(acc, dj);
+      block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
     }
     grid.sync();
-    for (long long v = gt; v < n; v += GT)
-      if (tm[v]) A.part[v] = A.dest[v];
+    // ---- commit + restore the list invariants
+    {
+      const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
+      for (long long i = gt; i < nm; i += GT) {
+        const int v = lmov[i];
+        A.part[v] = A.dest[v];
+        if (!balanced_now) tmf[v] = 0;  // no locks after a rebalance pass
+      }
+      if (balanced_now) {
+        for (long long i = gt; i < nc; i += GT) A.gkey[A.lcand[i]] = kGainNone;
+        for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;  // old locks
+      } else {
+        for (long long i = gt; i < nc; i += GT) A.rtgt[A.lcand[i]] = -1;
+        for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
+      }
+    }
     grid.sync();
     // ---- Alg. 4 control (refinement.py:433-463), replicated per CTA
-    long long mx = block_max_bw(A.bw, k);
+    const long long mx = block_max_bw(A.bw, k);
     if (threadIdx.x == 0) {
-      const long long mv = *movers;
+      const long long mv = cnt[C_MOV];
       C.take = 0;
       C.iters++;
-      if (balanced_now) C.lp++; else { C.weak++; C.i_w++; C.pass_counter++; }
-      if (balanced_now) C.i_w = 0;
+      C.stamp = stamp;
+      if (balanced_now) {
+        C.lp++;
+        C.i_w = 0;
+      } else {
+        C.weak++;
+        C.i_w++;
+        C.pass_counter++;
+      }
+      // the move flags of this pass become the next locks (LP) or are gone
+      if (balanced_now) {
+        C.locks_nonempty = mv > 0;
+        C.lp_par ^= 1;
+        C.prev_n = (int)mv;
+      } else {
+        C.locks_nonempty = 0;
+        C.prev_n = 0;
+      }
       if (mv == 0 && ((balanced_now && entry_locks_empty) || (!balanced_now && incomplete))) {
         C.brk = 1;
       } else {
-        C.J += *dj;
+        C.J += cnt[C_DJ];
         C.maxw = mx;
-        if (balanced_now) {
-          C.locks_nonempty = mv > 0;
-          C.lp_par ^= 1;
-        } else {
-          C.locks_nonempty = 0;
-        }
         int reset = 0;
         if ((double)C.maxw <= A.l_max) {
           if (!C.best_balanced) {
@@ -520,8 +650,8 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           reset = C.take = 1;
         }
         C.i = reset ? 0 : C.i + 1;
-        C.it++;
       }
+      C.it++;
     }
     __syncthreads();
     if (C.brk) break;
@@ -536,6 +666,7 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     FusedState& S1 = *A.st;
     S1.started = 1;
+    S1.reinit = 0;
     S1.J = C.J;
     S1.best_j = C.best_j;
     S1.best_maxw = C.best_maxw;
@@ -546,6 +677,8 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
     S1.best_balanced = C.best_balanced;
     S1.locks_nonempty = C.locks_nonempty;
     S1.lp_par = C.lp_par;
+    S1.prev_n = C.prev_n;
+    S1.stamp = C.stamp;
     S1.status = C.strong_yield ? 1 : 0;
     S1.iters += C.iters;
     S1.lp += C.lp;
@@ -592,8 +725,9 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     case 16: maxb = coop_max_blocks<16>(smem); break;
     default: maxb = coop_max_blocks<32>(smem); break;
   }
-  // ~2K vertices per CTA, at most one full co-resident wave
-  int G = (int)std::min<long long>((long long)maxb, std::max<long long>(1, ((long long)g.n + 2047) / 2048));
+  // ~1K vertices per CTA, at most one full co-resident wave
+  const int G = (int)std::min<long long>(
+      (long long)maxb, std::max<long long>(1, ((long long)g.n + 1023) / 1024));
   if (fb.S_cap < (long long)G * k) {
     fb.S = DBuf<long long>((size_t)G * k, s);
     fb.S_cap = (long long)G * k;
@@ -616,18 +750,21 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.bw = bw;
   A.best = fb.best;
   A.best_bw = fb.best_bw;
-  A.cand = fb.cand;
   A.dest = fb.dest;
   A.gkey = fb.gkey;
-  A.tm0 = fb.tm0;
-  A.tm1 = fb.tm1;
+  A.flags0 = fb.tm0;
+  A.flags1 = fb.tm1;
   A.rtgt = fb.rtgt;
   A.rcell = fb.rcell;
+  A.bstamp = fb.bstamp;
+  A.lsmall = fb.lsmall;
+  A.lheavy = fb.lheavy;
+  A.lcand = fb.lcand;
+  A.lmov0 = fb.lmov0;
+  A.lmov1 = fb.lmov1;
   A.W = fb.W.get();
   A.S = fb.S.get();
   A.ctr = fb.ctr;
-  A.heavy = L.heavy.get();
-  A.n_heavy = L.n_heavy;
   A.st = fb.state;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
@@ -647,12 +784,18 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     default: fn = (void*)k_refine_fused<32>; break;
   }
   {
+    // one launch = many Alg. 4 iterations; per-iteration algorithmic bytes
+    // are accounted by the host from the iteration count
     ProfScope prof(P_LP_EVAL, 0.0, s);
     GIM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kFusedBlock), args, smem, s));
+    count_launch();
+    GIM_CUDA(cudaMemcpyAsync(fb.h_state, fb.state, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaStreamSynchronize(s));
+    prof.extra = (double)(fb.h_state->lp + fb.h_state->weak - fb.lp_seen - fb.weak_seen) *
+                 (12.0 * (double)g.m2 + 8.0 * (double)g.n);
+    fb.lp_seen = fb.h_state->lp;
+    fb.weak_seen = fb.h_state->weak;
   }
-  count_launch();
-  GIM_CUDA(cudaMemcpyAsync(fb.h_state, fb.state, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
   return fb.h_state->status == 0;
 }
 
