@@ -222,6 +222,10 @@ void gim_set_fanout(int32_t on);
  * as per-phase launches with host control.  Results are identical. */
 void gim_set_fused(int32_t on);
 
+/* Contract level-stack matchings row-wise (default 1) or always with the
+ * radix-sort path.  The coarse graphs are identical. */
+void gim_set_rowwise_contraction(int32_t on);
+
 /* kernels launched by this host thread since the last reset (evidence). */
 int64_t gim_launch_count(void);
 void gim_reset_launch_count(void);

@@ -496,6 +496,184 @@ void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cuda
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6' contraction of a MATCHING (the level-stack case): every coarse vertex c
+// has one or two members, so its row is the union of <= 2 fine rows mapped
+// through M.  One warp per coarse vertex stages those L = deg(v1) + deg(v2)
+// (cv, w) pairs in shared memory, drops the self loop cv == c, and
+// deduplicates / ranks them in O(L^2 / 32): the output row is sorted by
+// target and parallel edges are summed — the same labelled graph as the
+// sort path, with two row sweeps instead of six radix passes.  Rows longer
+// than kRowCap (hubs, R-MAT) route the whole level to the radix-sort path.
+
+constexpr int kRowCap = 256;
+constexpr int kRowWarps = 8;
+
+__global__ void k_members(int n, const int* __restrict__ partner, const int* __restrict__ cmap,
+                          const int* __restrict__ off, const int* __restrict__ vw,
+                          int* __restrict__ mem, int* __restrict__ rowlen, int* __restrict__ cvw,
+                          int* __restrict__ maxlen) {
+  int mx = 0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int p = partner[v];
+    if (p >= 0 && p < v) continue;  // not the root of its pair
+    const int c = cmap[v];
+    int L = off[v + 1] - off[v];
+    int wsum = vw[v];
+    if (p >= 0) {
+      L += off[p + 1] - off[p];
+      wsum += vw[p];
+    }
+    mem[2 * c] = v;
+    mem[2 * c + 1] = p;
+    rowlen[c] = L;
+    cvw[c] = wsum;
+    mx = max(mx, L);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane_id() == 0 && mx) atomicMax(maxlen, mx);
+}
+
+// stage the row of coarse vertex c in K/Wt (self loops -> INT_MAX)
+__device__ __forceinline__ int stage_row(int c, const int* mem, const int* off, const int* tgt,
+                                         const int* w, const int* cmap, int* K, int* Wt) {
+  const int v0 = mem[2 * c], v1 = mem[2 * c + 1];
+  const int b0 = off[v0], d0 = off[v0 + 1] - b0;
+  const int b1 = v1 >= 0 ? off[v1] : 0, d1 = v1 >= 0 ? off[v1 + 1] - b1 : 0;
+  const int L = d0 + d1;
+  for (int i = lane_id(); i < L; i += 32) {
+    const int e = i < d0 ? b0 + i : b1 + (i - d0);
+    const int key = cmap[tgt[e]];
+    K[i] = key == c ? INT_MAX : key;
+    Wt[i] = w[e];
+  }
+  __syncwarp();
+  return L;
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) k_row_count(int n_c, const int* __restrict__ mem,
+                                                             const int* __restrict__ off,
+                                                             const int* __restrict__ tgt,
+                                                             const int* __restrict__ w,
+                                                             const int* __restrict__ cmap,
+                                                             int* __restrict__ cdeg) {
+  __shared__ int sK[kRowWarps][kRowCap], sW[kRowWarps][kRowCap];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  int* K = sK[warp];
+  int* Wt = sW[warp];
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_c;
+       c += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int L = stage_row((int)c, mem, off, tgt, w, cmap, K, Wt);
+    int cnt = 0;
+    for (int i = lane; i < L; i += 32) {
+      const int key = K[i];
+      if (key == INT_MAX) continue;
+      bool first = true;
+      for (int j = 0; j < i; ++j)
+        if (K[j] == key) { first = false; break; }
+      cnt += first;
+    }
+    cnt = warp_sum_i(cnt);
+    if (lane == 0) cdeg[c] = cnt;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int* __restrict__ mem,
+                                                            const int* __restrict__ off,
+                                                            const int* __restrict__ tgt,
+                                                            const int* __restrict__ w,
+                                                            const int* __restrict__ cmap,
+                                                            const int* __restrict__ c_off,
+                                                            int* __restrict__ c_tgt,
+                                                            int* __restrict__ c_w,
+                                                            int* __restrict__ c_src) {
+  __shared__ int sK[kRowWarps][kRowCap], sW[kRowWarps][kRowCap];
+  __shared__ unsigned char sF[kRowWarps][kRowCap];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  int* K = sK[warp];
+  int* Wt = sW[warp];
+  unsigned char* F = sF[warp];
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_c;
+       c += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int L = stage_row((int)c, mem, off, tgt, w, cmap, K, Wt);
+    for (int i = lane; i < L; i += 32) {
+      const int key = K[i];
+      bool first = key != INT_MAX;
+      for (int j = 0; j < i && first; ++j)
+        if (K[j] == key) first = false;
+      F[i] = first;
+    }
+    __syncwarp();
+    const int base = c_off[c];
+    for (int i = lane; i < L; i += 32) {
+      if (!F[i]) continue;
+      const int key = K[i];
+      long long sum = 0;
+      int rank = 0;
+      for (int j = 0; j < L; ++j) {
+        const int kj = K[j];
+        if (kj == key) sum += Wt[j];
+        rank += (F[j] && kj < key);
+      }
+      c_tgt[base + rank] = key;
+      c_w[base + rank] = (int)sum;
+      c_src[base + rank] = (int)c;
+    }
+    __syncwarp();
+  }
+}
+
+// contraction of a matching (partner[] given); falls back to the radix-sort
+// path when some coarse row exceeds kRowCap
+void contract_matching(const DevGraph& g, const int* cmap, const int* partner, int n_c,
+                       OwnedGraph& out, cudaStream_t s) {
+  if (g.m2 == 0 || n_c == 0) {
+    contract(g, cmap, n_c, out, s);
+    return;
+  }
+  DBuf<int> mem((size_t)2 * n_c, s), rowlen((size_t)n_c, s);
+  DBuf<int> cdeg((size_t)n_c + 1, s), scal(2, s);  // [maxlen, m2c]
+  DBuf<int> cvw((size_t)n_c, s);
+  GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(int), s));
+  GIM_CUDA(cudaMemsetAsync(cdeg.get() + n_c, 0, sizeof(int), s));
+  k_members<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, partner, cmap, g.off, g.vw, mem.get(),
+                                               rowlen.get(), cvw.get(), scal.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  int maxlen = 0;
+  GIM_CUDA(cudaMemcpyAsync(&maxlen, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  if (maxlen > kRowCap) {  // hub rows: radix-sort path for this level
+    contract(g, cmap, n_c, out, s);
+    return;
+  }
+  ProfScope prof(P_CONTRACT, 12.0 * g.n + 12.0 * g.m2 + 8.0 * n_c, s);
+  out.n = n_c;
+  out.vw = std::move(cvw);
+  out.off = DBuf<int>((size_t)n_c + 1, s);
+  const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
+  k_row_count<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), g.off, g.tgt, g.w, cmap,
+                                              cdeg.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  exclusive_scan<int>((long long)n_c + 1, LoadAs<int, int>{cdeg.get()},
+                      StoreTo<int>{out.off.get()}, scal.get() + 1, s);
+  int m2c = 0;
+  GIM_CUDA(cudaMemcpyAsync(&m2c, out.off.get() + n_c, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaStreamSynchronize(s));
+  out.m2 = m2c;
+  out.tgt = DBuf<int>((size_t)std::max(m2c, 1), s);
+  out.w = DBuf<int>((size_t)std::max(m2c, 1), s);
+  out.src = DBuf<int>((size_t)std::max(m2c, 1), s);
+  k_row_fill<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), g.off, g.tgt, g.w, cmap,
+                                             out.off.get(), out.tgt.get(), out.w.get(),
+                                             out.src.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  prof.extra = 8.0 * m2c;
+}
+
 // K7 projection (coarsening.py:269-277): Pi_f = Pi_c[M]
 __global__ void k_project(int n, const int* __restrict__ cmap, const int* __restrict__ pc,
                           int* __restrict__ pf) {

@@ -119,6 +119,8 @@ static RefCfg config_for_level(int level, int n_levels, double phi, int rho, int
 
 // device-resident loop on/off (gim_set_fused; default on); both give identical results
 static std::atomic<bool> g_fused{true};
+// row-wise contraction of matchings (else the radix-sort path); identical graphs
+static std::atomic<bool> g_rowwise{true};
 
 static long long max_of(const std::vector<long long>& x) {
   long long m = 0;
@@ -420,7 +422,10 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
     int n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
     if ((double)n_c * 1.02 > (double)cur.g.n) break;  // stall guard
     Level next;
-    contract(cur.g, cmap.get(), n_c, next.own, s);
+    if (g_rowwise.load())
+      contract_matching(cur.g, cmap.get(), partner.get(), n_c, next.own, s);
+    else
+      contract(cur.g, cmap.get(), n_c, next.own, s);
     next.g = next.own.view();
     cur.cmap = std::move(cmap);
     cur.n_c = n_c;
@@ -1075,3 +1080,4 @@ extern "C" void gim_reset_launch_count(void) { reset_launches(); }
 
 extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }
 extern "C" void gim_set_fused(int32_t on) { gim::g_fused.store(on != 0); }
+extern "C" void gim_set_rowwise_contraction(int32_t on) { gim::g_rowwise.store(on != 0); }

@@ -12,7 +12,7 @@
 namespace gim {
 
 // ---------------------------------------------------------------------------
-// K15 greedy graph growing, one warp per subgraph (the coarsest partitioner
+// K15 greedy graph growing, one CTA per subgraph (the coarsest partitioner
 // graphs hold a few hundred vertices).  Semantics of pipelines.py:132-188:
 //  * seeds: farthest-first over hop distances (BFS from {0}; then from the
 //    seed set), preferring the lowest unreachable vertex, else the first
@@ -21,51 +21,11 @@ namespace gim {
 //    vertices it is connected to, the one with maximum connectivity (ties:
 //    lowest id) — exactly the entry its lazy max-heap would pop — or the
 //    lowest unassigned vertex when it has none.
-// Scratch per subgraph: dist[n], conn[k][n] (global, L1/L2 resident).
+// dist[n], part[n], conn[k][n] live in shared memory when they fit (else in
+// the global scratch); every selection is a CTA-wide argmax/argmin.
 
-__device__ void warp_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
-                         int ns) {
-  const int lane = lane_id();
-  for (int v = lane; v < n; v += 32) dist[v] = -1;
-  __syncwarp();
-  for (int i = lane; i < ns; i += 32) dist[seeds[i]] = 0;
-  __syncwarp();
-  for (int d = 0;; ++d) {
-    bool changed = false;
-    for (int v = lane; v < n; v += 32) {
-      if (dist[v] != d) continue;
-      for (int e = off[v]; e < off[v + 1]; ++e) {
-        int u = tgt[e];
-        if (dist[u] < 0) {
-          dist[u] = d + 1;  // benign race: every writer stores d + 1
-          changed = true;
-        }
-      }
-    }
-    __syncwarp();
-    if (!__any_sync(0xffffffffu, changed)) break;
-  }
-}
-
-// farthest-first seed: lowest unreached vertex if any, else first argmax
-__device__ int warp_pick_seed(int n, const int* dist) {
-  const int lane = lane_id();
-  int unreached = INT_MAX;
-  int bd = -1, bv = INT_MAX;
-  for (int v = lane; v < n; v += 32) {
-    int d = dist[v];
-    if (d < 0) unreached = min(unreached, v);
-    else if (d > bd) { bd = d; bv = v; }  // ascending v per lane: first max
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    unreached = min(unreached, __shfl_xor_sync(0xffffffffu, unreached, o));
-    int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-    int v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-    if (d2 > bd || (d2 == bd && v2 < bv)) { bd = d2; bv = v2; }
-  }
-  return unreached != INT_MAX ? unreached : bv;
-}
+constexpr int kGggBlock = 256;
+constexpr int kGggWarps = kGggBlock / 32;
 
 struct GggJob {
   int n;
@@ -75,99 +35,173 @@ struct GggJob {
   const int* w;
   const int* vw;
   int* part;        // out [n]
-  int* scratch;     // dist[n] + seeds[k] + conn[k*n]
+  int* scratch;     // global fallback: dist[n] + part[n] + seeds[k] + conn[k*n]
   long long* bwork; // [k]
+  int use_smem;
 };
 
-__global__ void __launch_bounds__(32) k_ggg(const GggJob* jobs, int njobs) {
+// CTA-wide lexicographic max of (a, -b): larger a wins, ties -> smaller b
+__device__ __forceinline__ void cta_argmax(int& a, int& b, int* sa, int* sb) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int a2 = __shfl_xor_sync(0xffffffffu, a, o), b2 = __shfl_xor_sync(0xffffffffu, b, o);
+    if (a2 > a || (a2 == a && b2 < b)) { a = a2; b = b2; }
+  }
+  if (lane_id() == 0) { sa[threadIdx.x >> 5] = a; sb[threadIdx.x >> 5] = b; }
+  __syncthreads();
+  a = sa[0];
+  b = sb[0];
+  for (int i = 1; i < kGggWarps; ++i)
+    if (sa[i] > a || (sa[i] == a && sb[i] < b)) { a = sa[i]; b = sb[i]; }
+  __syncthreads();
+}
+
+__device__ void cta_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
+                        int ns) {
+  for (int v = threadIdx.x; v < n; v += blockDim.x) dist[v] = -1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) dist[seeds[i]] = 0;
+  __syncthreads();
+  for (int d = 0;; ++d) {
+    int changed = 0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      if (dist[v] != d) continue;
+      for (int e = off[v]; e < off[v + 1]; ++e) {
+        int u = tgt[e];
+        if (dist[u] < 0) {
+          dist[u] = d + 1;  // benign race: every writer stores d + 1
+          changed = 1;
+        }
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+}
+
+// farthest-first seed: lowest unreached vertex if any, else first argmax
+__device__ int cta_pick_seed(int n, const int* dist, int* sa, int* sb) {
+  int unr = INT_MIN + 1, ubv = INT_MAX;  // max of (-v) over unreached
+  int bd = -1, bv = INT_MAX;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    int d = dist[v];
+    if (d < 0) {
+      if (ubv == INT_MAX) { unr = 1; ubv = v; }
+    } else if (d > bd) {
+      bd = d;
+      bv = v;
+    }
+  }
+  int ua = ubv == INT_MAX ? 0 : 1;
+  cta_argmax(ua, ubv, sa, sb);
+  if (ua) return ubv;
+  cta_argmax(bd, bv, sa, sb);
+  return bv;
+}
+
+__global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs) {
   const int j = blockIdx.x;
   if (j >= njobs) return;
   const GggJob J = jobs[j];
   const int n = J.n, k = J.k;
-  const int lane = lane_id();
-  int* dist = J.scratch;
-  int* seeds = dist + n;
+  extern __shared__ int sm[];
+  __shared__ int sa[kGggWarps], sb[kGggWarps];
+  __shared__ int s_v, s_b, s_next;
+  int* base = J.use_smem ? sm : J.scratch;
+  int* dist = base;
+  int* part = dist + n;
+  int* seeds = part + n;
   int* conn = seeds + k;
   if (k == 1) {
-    for (int v = lane; v < n; v += 32) J.part[v] = 0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
     return;
   }
   // seeds (pipelines.py:143-153)
-  int zero = 0;
-  warp_bfs(n, J.off, J.tgt, dist, &zero, 1);
-  int s0 = warp_pick_seed(n, dist);
-  if (lane == 0) seeds[0] = s0;
-  __syncwarp();
+  if (threadIdx.x == 0) s_v = 0;
+  __syncthreads();
+  cta_bfs(n, J.off, J.tgt, dist, &s_v, 1);
+  int sv = cta_pick_seed(n, dist, sa, sb);
+  if (threadIdx.x == 0) seeds[0] = sv;
+  __syncthreads();
   for (int ns = 1; ns < k; ++ns) {
-    warp_bfs(n, J.off, J.tgt, dist, seeds, ns);
-    int sv = warp_pick_seed(n, dist);
-    if (lane == 0) seeds[ns] = sv;
-    __syncwarp();
+    cta_bfs(n, J.off, J.tgt, dist, seeds, ns);
+    sv = cta_pick_seed(n, dist, sa, sb);
+    if (threadIdx.x == 0) seeds[ns] = sv;
+    __syncthreads();
   }
   // growth (pipelines.py:155-188)
-  for (int v = lane; v < n; v += 32) J.part[v] = -1;
-  for (long long i = lane; i < (long long)k * n; i += 32) conn[i] = 0;
-  for (int b = lane; b < k; b += 32) J.bwork[b] = 0;
-  __syncwarp();
-  int assigned = 0;
-  int next_free = 0;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) part[v] = -1;
+  for (long long i = threadIdx.x; i < (long long)k * n; i += blockDim.x) conn[i] = 0;
+  for (int b = threadIdx.x; b < k; b += blockDim.x) J.bwork[b] = 0;
+  if (threadIdx.x == 0) s_next = 0;
+  __syncthreads();
   auto claim = [&](int v, int b) {
-    if (lane == 0) {
-      J.part[v] = b;
+    if (threadIdx.x == 0) {
+      part[v] = b;
       J.bwork[b] += J.vw[v];
     }
-    __syncwarp();
-    for (int e = J.off[v] + lane; e < J.off[v + 1]; e += 32) {
+    __syncthreads();
+    for (int e = J.off[v] + threadIdx.x; e < J.off[v + 1]; e += blockDim.x) {
       int u = J.tgt[e];
-      if (J.part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per lane
+      if (part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per thread
     }
-    __syncwarp();
-    ++assigned;
+    __syncthreads();
   };
   for (int b = 0; b < k; ++b) claim(seeds[b], b);
-  while (assigned < n) {
-    // lightest block, lowest id on ties
-    long long bwv = LLONG_MAX;
-    int bb = INT_MAX;
-    for (int b = lane; b < k; b += 32) {
-      long long x = J.bwork[b];
-      if (x < bwv) { bwv = x; bb = b; }
-    }
+  for (int assigned = k; assigned < n; ++assigned) {
+    if (threadIdx.x < 32) {  // lightest block, lowest id on ties
+      long long bwv = LLONG_MAX;
+      int bb = INT_MAX;
+      for (int b = threadIdx.x; b < k; b += 32) {
+        long long x = J.bwork[b];
+        if (x < bwv) { bwv = x; bb = b; }
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
-      int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-      if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
+      for (int o = 16; o > 0; o >>= 1) {
+        long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
+        int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+        if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
+      }
+      if (threadIdx.x == 0) s_b = bb;
     }
+    __syncthreads();
+    const int bb = s_b;
     const int* cb = conn + (long long)bb * n;
     int bc = 0, bv = INT_MAX;
-    for (int u = lane; u < n; u += 32) {
+    for (int u = threadIdx.x; u < n; u += blockDim.x) {
       int c = cb[u];
-      if (c > bc && J.part[u] < 0) { bc = c; bv = u; }
+      if (c > bc && part[u] < 0) { bc = c; bv = u; }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
-      int v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      if (c2 > bc || (c2 == bc && v2 < bv)) { bc = c2; bv = v2; }
+    cta_argmax(bc, bv, sa, sb);
+    if (threadIdx.x == 0) {
+      int v = bv;
+      if (bc == 0) {  // frontier dried up: lowest unassigned vertex
+        int f = s_next;
+        while (part[f] >= 0) ++f;
+        s_next = f;
+        v = f;
+      }
+      s_v = v;
     }
-    int v = bv;
-    if (bc == 0) {  // frontier dried up: lowest unassigned vertex
-      while (J.part[next_free] >= 0) ++next_free;
-      v = next_free;
-    }
-    claim(v, bb);
+    __syncthreads();
+    claim(s_v, bb);
   }
+  for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
 
 void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
   ProfScope prof(P_GGG, 0.0, s);
-  DBuf<int> scratch((size_t)g.n + k + (size_t)k * g.n, s);
+  const size_t words = (size_t)2 * g.n + k + (size_t)k * g.n;
+  const size_t smem = words * sizeof(int);
+  const bool use_smem = smem <= 160 * 1024;
+  DBuf<int> scratch(use_smem ? 1 : words, s);
   DBuf<long long> bwork((size_t)k, s);
-  GggJob job{g.n, k, g.off, g.tgt, g.w, g.vw, part, scratch.get(), bwork.get()};
+  GggJob job{g.n, k, g.off, g.tgt, g.w, g.vw, part, scratch.get(), bwork.get(), use_smem ? 1 : 0};
   DBuf<GggJob> dj(1, s);
   GIM_CUDA(cudaMemcpyAsync(dj.get(), &job, sizeof(GggJob), cudaMemcpyHostToDevice, s));
-  k_ggg<<<1, 32, 0, s>>>(dj.get(), 1);
+  if (use_smem && smem > 48 * 1024)
+    GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  160 * 1024));
+  k_ggg<<<1, kGggBlock, use_smem ? smem : 0, s>>>(dj.get(), 1);
   count_launch();
   GIM_LAUNCH_CHECK();
   GIM_CUDA(cudaStreamSynchronize(s));  // job struct lives on this stack frame

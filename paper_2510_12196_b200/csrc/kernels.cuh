@@ -62,6 +62,9 @@ int coarse_map(int n, const int* partner, int* cmap, cudaStream_t s);
 long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off, int* c_tgt,
                         int* c_w, int* c_vw, int* c_src, cudaStream_t s);
 void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cudaStream_t s);
+// contraction of a matching (<= 2 members per coarse vertex), row-wise
+void contract_matching(const DevGraph& g, const int* cmap, const int* partner, int n_c,
+                       OwnedGraph& out, cudaStream_t s);
 void project(int n, const int* cmap, const int* pc, int* pf, cudaStream_t s);
 
 // ---- refine.cu

@@ -36,6 +36,9 @@
 // ("yield"); the host runs the sort-based strong pass and relaunches.
 #include <cooperative_groups.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "refine_dev.cuh"
@@ -119,9 +122,18 @@ __device__ __forceinline__ void warp_append(bool pred, int val, int* list, long 
   if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
 }
 
+// grid-wide barrier; a one-CTA launch (small graphs, launched without the
+// cooperative attribute so many run concurrently) only needs __syncthreads
+struct GridBarrier {
+  __device__ __forceinline__ void sync() const {
+    if (gridDim.x == 1) __syncthreads();
+    else cg::this_grid().sync();
+  }
+};
+
 template <int VW>
 __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
-  cg::grid_group grid = cg::this_grid();
+  const GridBarrier grid;
   extern __shared__ unsigned char dsm[];
   __shared__ long long s_dbit[64];
   __shared__ Ctl C;
@@ -694,17 +706,26 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
 // ---------------------------------------------------------------------------
 // host side
 
+// co-resident CTA capacity per (VW, smem), queried once per device
 template <int VW>
 static int coop_max_blocks(size_t smem) {
-  int dev = 0, sms = 0, per = 0;
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, int> cache;
+  int dev = 0;
   GIM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int sms = 0, per = 0;
   GIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (smem > 48 * 1024)
-    GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max<size_t>(smem, 48 * 1024)));
   GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW>, kFusedBlock,
                                                          smem));
-  return std::max(1, per) * sms;
+  int r = std::max(1, per) * sms;
+  cache.emplace(key, r);
+  return r;
 }
 
 bool fused_supported(int k, int rho) { return k <= 1024 && rho >= 1 && rho <= 8; }
@@ -725,9 +746,11 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     case 16: maxb = coop_max_blocks<16>(smem); break;
     default: maxb = coop_max_blocks<32>(smem); break;
   }
+  // small graphs: one CTA (plain launch, __syncthreads barriers); otherwise
   // ~1K vertices per CTA, at most one full co-resident wave
-  const int G = (int)std::min<long long>(
-      (long long)maxb, std::max<long long>(1, ((long long)g.n + 1023) / 1024));
+  const int G = g.n <= 4096 ? 1
+                            : (int)std::min<long long>((long long)maxb,
+                                                       ((long long)g.n + 1023) / 1024);
   if (fb.S_cap < (long long)G * k) {
     fb.S = DBuf<long long>((size_t)G * k, s);
     fb.S_cap = (long long)G * k;
@@ -787,7 +810,10 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     // one launch = many Alg. 4 iterations; per-iteration algorithmic bytes
     // are accounted by the host from the iteration count
     ProfScope prof(P_LP_EVAL, 0.0, s);
-    GIM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kFusedBlock), args, smem, s));
+    if (G == 1)
+      GIM_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kFusedBlock), args, smem, s));
+    else
+      GIM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kFusedBlock), args, smem, s));
     count_launch();
     GIM_CUDA(cudaMemcpyAsync(fb.h_state, fb.state, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaStreamSynchronize(s));

@@ -385,3 +385,8 @@ def set_fanout(on: bool) -> None:
 def set_fused(on: bool) -> None:
     """Device-resident Alg. 4 (one cooperative kernel per level) vs per-phase launches."""
     _lib.load().gim_set_fused(1 if on else 0)
+
+
+def set_rowwise_contraction(on: bool) -> None:
+    """Row-wise contraction of matchings vs the radix-sort path."""
+    _lib.load().gim_set_rowwise_contraction(1 if on else 0)

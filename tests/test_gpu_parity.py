@@ -27,11 +27,14 @@ def D():
 
 @pytest.fixture(params=["fused", "phased"])
 def mode(request, D):
-    """Alg. 4 as one persistent cooperative kernel per level ("fused") or as
-    per-phase launches with host control ("phased"); both must be exact."""
+    """Alg. 4 as one persistent cooperative kernel per level + row-wise
+    contraction ("fused") or per-phase launches with host control + the
+    radix-sort contraction ("phased"); both must be exact."""
     D.set_fused(request.param == "fused")
+    D.set_rowwise_contraction(request.param == "fused")
     yield request.param
     D.set_fused(True)
+    D.set_rowwise_contraction(True)
 
 
 def dev_graph(D, c):
