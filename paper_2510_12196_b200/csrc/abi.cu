@@ -15,10 +15,30 @@ const char* last_error() { return g_last_error.c_str(); }
 
 static void configure_pool_once();
 
-void* dmalloc(size_t bytes, cudaStream_t s) {
+// ---- per-thread stream arena: a size-class free list in front of the pool.
+// The multisection runs dozens of host threads, each allocating hundreds of
+// small buffers on its own stream; the arena keeps them off the (locked)
+// device pool.  Reuse is safe because a block is only ever handed out again
+// on the stream it was released on (stream order = happens-before).
+static thread_local StreamArena* g_arena = nullptr;
+constexpr size_t kArenaMax = (size_t)64 << 20;  // larger buffers go to the pool
+
+static size_t size_class(size_t b) {
+  size_t c = 256;
+  while (c < b) c <<= 1;
+  return c;
+}
+
+StreamArena::StreamArena(cudaStream_t st) : s(st), prev(g_arena) { g_arena = this; }
+
+StreamArena::~StreamArena() {
+  g_arena = prev;
+  for (auto& kv : free_)
+    for (void* p : kv.second) cudaFreeAsync(p, s);
+}
+
+static void* raw_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
-  if (bytes == 0) return nullptr;
-  configure_pool_once();
   cudaError_t e = cudaMallocAsync(&p, bytes, s);
   if (e != cudaSuccess)
     throw Error{GIM_E_CUDA, std::string("cudaMallocAsync(") + std::to_string(bytes) +
@@ -26,8 +46,38 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
   return p;
 }
 
+void* dmalloc(size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return nullptr;
+  configure_pool_once();
+  StreamArena* a = g_arena;
+  if (a && a->s == s && bytes <= kArenaMax) {
+    const size_t c = size_class(bytes);
+    auto& fl = a->free_[c];
+    void* p;
+    if (!fl.empty()) {
+      p = fl.back();
+      fl.pop_back();
+    } else {
+      p = raw_alloc(c, s);
+    }
+    a->owned_[p] = c;
+    return p;
+  }
+  return raw_alloc(bytes, s);
+}
+
 void dfree(void* p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);  // never throws from a destructor
+  if (!p) return;
+  StreamArena* a = g_arena;
+  if (a && a->s == s) {
+    auto it = a->owned_.find(p);
+    if (it != a->owned_.end()) {
+      a->free_[it->second].push_back(p);
+      a->owned_.erase(it);
+      return;
+    }
+  }
+  cudaFreeAsync(p, s);  // never throws from a destructor
 }
 
 static std::mutex g_topo_mu;

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/gpuim.h"
@@ -185,6 +186,19 @@ __device__ __forceinline__ void block_sum_atomic(long long v, long long* out) {
 
 void* dmalloc(size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
+
+// RAII: while alive on this host thread, dmalloc/dfree on stream `s` go
+// through a size-class free list (released to the pool at destruction).
+struct StreamArena {
+  cudaStream_t s;
+  StreamArena* prev;
+  std::unordered_map<size_t, std::vector<void*>> free_;
+  std::unordered_map<void*, size_t> owned_;
+  explicit StreamArena(cudaStream_t st);
+  ~StreamArena();
+  StreamArena(const StreamArena&) = delete;
+  StreamArena& operator=(const StreamArena&) = delete;
+};
 
 template <class T>
 struct DBuf {

@@ -24,6 +24,7 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
                        cudaStream_t s);
 void gather(int n, const int* idx, const int* src, int* dst, cudaStream_t s);
 void scatter_const(int n, const int* idx, int value, int* dst, cudaStream_t s);
+void leaf_scatter(int n, const int* idx, const int* part, int base, int* dst, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // run statistics
@@ -531,6 +532,15 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     GIM_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(int) * sub.n, s));
   else
     internal_partitioner(sub, sub_total, parts, eps_local, node_seed, part.get(), *C.st, s);
+  if (level == 1) {
+    // the children are leaves (pipelines.py:78-80): vertex v of part j lands
+    // on calc_id(ident + (j,)) = calc_id(ident + (0,)) + j — no subgraphs needed
+    ident.push_back(0);
+    const int base = calc_id(C.h, ident);
+    ident.pop_back();
+    leaf_scatter(sub.n, translation, part.get(), base, C.assignment, s);
+    return;
+  }
   DBuf<long long> bw((size_t)parts, s);
   block_weights(sub.n, sub.vw, part.get(), parts, bw.get(), s);
   std::vector<long long> child_total((size_t)parts);
@@ -563,10 +573,13 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
       try {
         GIM_CUDA(cudaSetDevice(C.device));
         GIM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        std::vector<int> id2 = ident;
-        id2.push_back(j);
-        descend(C, subs[j].view(), child_total[j], level - 1, id2, trans[j].get(),
-                hash2(node_seed, (unsigned long long)level, (unsigned long long)j), cs);
+        {
+          StreamArena arena(cs);  // this subtree's scratch stays off the shared pool
+          std::vector<int> id2 = ident;
+          id2.push_back(j);
+          descend(C, subs[j].view(), child_total[j], level - 1, id2, trans[j].get(),
+                  hash2(node_seed, (unsigned long long)level, (unsigned long long)j), cs);
+        }
         GIM_CUDA(cudaStreamSynchronize(cs));
       } catch (...) {
         errs[j] = std::current_exception();
@@ -620,6 +633,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   std::vector<long long> h(tt.hierarchy, tt.hierarchy + tt.levels);
   std::vector<long long> d(tt.distances, tt.distances + tt.levels);
   const long long k = t.k;
+  StreamArena arena(s);  // released (stream-ordered) when the call returns
   RunStats st;
   reset_launches();
   cudaEvent_t ev[4];

@@ -299,6 +299,20 @@ void scatter_const(int n, const int* idx, int value, int* dst, cudaStream_t s) {
   GIM_LAUNCH_CHECK();
 }
 
+__global__ void k_leaf_scatter(int n, const int* __restrict__ idx, const int* __restrict__ part,
+                               int base, int* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[idx[i]] = base + part[i];
+}
+
+// last multisection level: assignment[idx[i]] = base + part[i]
+void leaf_scatter(int n, const int* idx, const int* part, int base, int* dst, cudaStream_t s) {
+  if (n == 0) return;
+  k_leaf_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, idx, part, base, dst);
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
 // splits g by part[] into `parts` owned subgraphs + their global ids
 void extract_subgraphs(const DevGraph& g, const int* part, int parts,
                        std::vector<OwnedGraph>& subs, std::vector<DBuf<int>>& ids,
