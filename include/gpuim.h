@@ -230,6 +230,10 @@ void gim_set_rowwise_contraction(int32_t on);
 int64_t gim_launch_count(void);
 void gim_reset_launch_count(void);
 
+/* Device scratch is cached per (stream, size class) across calls; this
+ * returns every cached block to the CUDA stream-ordered pool. */
+void gim_release_cached_memory(void);
+
 #ifdef __cplusplus
 }
 #endif

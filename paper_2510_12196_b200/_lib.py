@@ -121,9 +121,11 @@ SIGNATURES: dict[str, list] = {
     "gim_set_rowwise_contraction": [I32],
     "gim_launch_count": [],
     "gim_reset_launch_count": [],
+    "gim_release_cached_memory": [],
 }
 RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
             "gim_reset_launch_count": None, "gim_set_profiling": None,
+            "gim_release_cached_memory": None,
             "gim_set_fanout": None, "gim_set_fused": None,
             "gim_set_rowwise_contraction": None}
 

@@ -2,6 +2,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <sched.h>
+
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -15,13 +17,88 @@ const char* last_error() { return g_last_error.c_str(); }
 
 static void configure_pool_once();
 
-// ---- per-thread stream arena: a size-class free list in front of the pool.
-// The multisection runs dozens of host threads, each allocating hundreds of
-// small buffers on its own stream; the arena keeps them off the (locked)
-// device pool.  Reuse is safe because a block is only ever handed out again
-// on the stream it was released on (stream order = happens-before).
-static thread_local StreamArena* g_arena = nullptr;
-constexpr size_t kArenaMax = (size_t)64 << 20;  // larger buffers go to the pool
+cudaError_t sync_stream(cudaStream_t s) {
+  for (int spin = 0;; ++spin) {
+    cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+    if (spin >= 64) sched_yield();
+  }
+}
+
+// ---- pinned scratch: process-wide free list, per-thread lease
+namespace {
+struct PinnedBlock {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_pin_mu;
+std::vector<PinnedBlock> g_pin_free;
+
+struct PinnedLease {
+  PinnedBlock b;
+  ~PinnedLease() {
+    if (!b.p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(b);
+  }
+};
+thread_local PinnedLease g_pin_lease;
+
+std::mutex g_stream_mu;
+std::vector<cudaStream_t> g_stream_free;
+}  // namespace
+
+void* pinned_scratch(size_t bytes) {
+  PinnedBlock& b = g_pin_lease.b;
+  if (b.bytes >= bytes) return b.p;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (b.p) g_pin_free.push_back(b);  // too small: back to the list
+  b = PinnedBlock{};
+  for (size_t i = 0; i < g_pin_free.size(); ++i) {
+    if (g_pin_free[i].bytes >= bytes) {
+      b = g_pin_free[i];
+      g_pin_free.erase(g_pin_free.begin() + (long)i);
+      return b.p;
+    }
+  }
+  size_t sz = (size_t)1 << 16;
+  while (sz < bytes) sz <<= 1;
+  if (cudaMallocHost(&b.p, sz) != cudaSuccess) {
+    b = PinnedBlock{};
+    throw Error{GIM_E_CUDA, "cudaMallocHost failed"};
+  }
+  b.bytes = sz;
+  return b.p;
+}
+
+cudaStream_t acquire_stream() {
+  {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    if (!g_stream_free.empty()) {
+      cudaStream_t s = g_stream_free.back();
+      g_stream_free.pop_back();
+      return s;
+    }
+  }
+  cudaStream_t s = nullptr;
+  GIM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+void release_stream(cudaStream_t s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  g_stream_free.push_back(s);
+}
+
+// ---- stream-keyed caching allocator in front of the cudaMallocAsync pool.
+// A mapping makes thousands of small allocations (per level, per
+// multisection subtree, on many streams); cudaMallocAsync measured
+// ~150 us per call here whenever the pool had to map memory, which
+// dominated small-graph partitioner calls.  Blocks are cached per
+// (stream, size class) for the life of the process and handed out again
+// only on the stream they were released on (stream order = happens-before).
+constexpr size_t kCacheMax = (size_t)64 << 20;  // larger buffers go to the pool
 
 static size_t size_class(size_t b) {
   size_t c = 256;
@@ -29,13 +106,16 @@ static size_t size_class(size_t b) {
   return c;
 }
 
-StreamArena::StreamArena(cudaStream_t st) : s(st), prev(g_arena) { g_arena = this; }
-
-StreamArena::~StreamArena() {
-  g_arena = prev;
-  for (auto& kv : free_)
-    for (void* p : kv.second) cudaFreeAsync(p, s);
-}
+namespace {
+struct CacheKey {
+  cudaStream_t s;
+  size_t c;
+  bool operator<(const CacheKey& o) const { return s != o.s ? s < o.s : c < o.c; }
+};
+std::mutex g_cache_mu;
+std::map<CacheKey, std::vector<void*>> g_cache_free;
+std::unordered_map<void*, size_t> g_cache_owned;
+}  // namespace
 
 static void* raw_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
@@ -49,35 +129,44 @@ static void* raw_alloc(size_t bytes, cudaStream_t s) {
 void* dmalloc(size_t bytes, cudaStream_t s) {
   if (bytes == 0) return nullptr;
   configure_pool_once();
-  StreamArena* a = g_arena;
-  if (a && a->s == s && bytes <= kArenaMax) {
-    const size_t c = size_class(bytes);
-    auto& fl = a->free_[c];
-    void* p;
-    if (!fl.empty()) {
-      p = fl.back();
-      fl.pop_back();
-    } else {
-      p = raw_alloc(c, s);
+  if (bytes > kCacheMax) return raw_alloc(bytes, s);
+  const size_t c = size_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache_free.find(CacheKey{s, c});
+    if (it != g_cache_free.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      g_cache_owned[p] = c;
+      return p;
     }
-    a->owned_[p] = c;
-    return p;
   }
-  return raw_alloc(bytes, s);
+  void* p = raw_alloc(c, s);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache_owned[p] = c;
+  return p;
 }
 
 void dfree(void* p, cudaStream_t s) {
   if (!p) return;
-  StreamArena* a = g_arena;
-  if (a && a->s == s) {
-    auto it = a->owned_.find(p);
-    if (it != a->owned_.end()) {
-      a->free_[it->second].push_back(p);
-      a->owned_.erase(it);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache_owned.find(p);
+    if (it != g_cache_owned.end()) {
+      g_cache_free[CacheKey{s, it->second}].push_back(p);
+      g_cache_owned.erase(it);
       return;
     }
   }
   cudaFreeAsync(p, s);  // never throws from a destructor
+}
+
+// returns every cached block to the pool (stream-ordered on its stream)
+void release_cached_memory() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& kv : g_cache_free)
+    for (void* p : kv.second) cudaFreeAsync(p, kv.first.s);
+  g_cache_free.clear();
 }
 
 static std::mutex g_topo_mu;

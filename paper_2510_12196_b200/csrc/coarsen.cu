@@ -280,7 +280,7 @@ static void two_hop_phase(const DevGraph& g, int* partner, double l_max, long lo
   }
   int cnt = 0;
   GIM_CUDA(cudaMemcpyAsync(&cnt, cnt_d.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   if (cnt < 2) return;
   DBuf<unsigned long long> keys(cnt, s), keys2(cnt, s);
   DBuf<int> vals(cnt, s), vals2(cnt, s);
@@ -309,7 +309,7 @@ long long two_hop(const DevGraph& g, int* partner, double l_max, long long match
   auto read = [&]() {
     long long m = 0;
     GIM_CUDA(cudaMemcpyAsync(&m, matched_d, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     return m;
   };
   GIM_CUDA(cudaMemcpyAsync(matched_d, &matched_now, sizeof(long long), cudaMemcpyHostToDevice, s));
@@ -368,7 +368,7 @@ int coarse_map(int n, const int* partner, int* cmap, cudaStream_t s) {
   GIM_LAUNCH_CHECK();
   int n_c = 0;
   GIM_CUDA(cudaMemcpyAsync(&n_c, tot.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   return n_c;
 }
 
@@ -462,7 +462,7 @@ long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off,
                                             vals2.get(), bits, s);
   long long self = 0;
   GIM_CUDA(cudaMemcpyAsync(&self, selfl.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   long long valid = g.m2 - self;
   DBuf<int> deg((size_t)n_c + 1, s), m2c_d(1, s);
   GIM_CUDA(cudaMemsetAsync(deg.get(), 0, sizeof(int) * ((size_t)n_c + 1), s));
@@ -472,7 +472,7 @@ long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off,
                       (int*)nullptr, s);
   int m2c = 0;
   GIM_CUDA(cudaMemcpyAsync(&m2c, m2c_d.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   prof.extra = 8.0 * m2c;
   return m2c;
 }
@@ -643,7 +643,7 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
   GIM_LAUNCH_CHECK();
   int maxlen = 0;
   GIM_CUDA(cudaMemcpyAsync(&maxlen, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   if (maxlen > kRowCap) {  // hub rows: radix-sort path for this level
     contract(g, cmap, n_c, out, s);
     return;
@@ -661,7 +661,7 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
                       StoreTo<int>{out.off.get()}, scal.get() + 1, s);
   int m2c = 0;
   GIM_CUDA(cudaMemcpyAsync(&m2c, out.off.get() + n_c, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   out.m2 = m2c;
   out.tgt = DBuf<int>((size_t)std::max(m2c, 1), s);
   out.w = DBuf<int>((size_t)std::max(m2c, 1), s);

@@ -182,23 +182,29 @@ __device__ __forceinline__ void block_sum_atomic(long long v, long long* out) {
 }
 
 // ---------------------------------------------------------------------------
-// stream-ordered device memory (cudaMallocAsync pool)
+// host waits and per-thread host resources
+
+// Wait for `s` by polling (cudaStreamQuery) with a yield between polls: the
+// multisection fan-out keeps dozens of host threads waiting at once, and
+// spinning inside cudaStreamSynchronize starves the threads that launch.
+cudaError_t sync_stream(cudaStream_t s);
+
+// pinned host scratch borrowed from a process-wide free list (cudaMallocHost
+// / cudaFreeHost are device-synchronising, so worker threads must not call
+// them); returned to the list when the owning thread exits
+void* pinned_scratch(size_t bytes);
+
+// non-blocking streams recycled across fan-out workers
+cudaStream_t acquire_stream();
+void release_stream(cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// stream-ordered device memory (cudaMallocAsync pool behind a stream-keyed cache)
 
 void* dmalloc(size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
 
-// RAII: while alive on this host thread, dmalloc/dfree on stream `s` go
-// through a size-class free list (released to the pool at destruction).
-struct StreamArena {
-  cudaStream_t s;
-  StreamArena* prev;
-  std::unordered_map<size_t, std::vector<void*>> free_;
-  std::unordered_map<void*, size_t> owned_;
-  explicit StreamArena(cudaStream_t st);
-  ~StreamArena();
-  StreamArena(const StreamArena&) = delete;
-  StreamArena& operator=(const StreamArena&) = delete;
-};
+void release_cached_memory();
 
 template <class T>
 struct DBuf {

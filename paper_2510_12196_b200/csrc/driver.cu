@@ -35,29 +35,17 @@ struct RunStats {  // shared by the multisection worker threads
   std::atomic<bool> in_initial{false};
 };
 
-// pinned host scratch, one per host thread
+// pinned host scratch (process-wide free list, leased per host thread)
 struct Pinned {
-  void* p = nullptr;
-  size_t bytes = 0;
-  void* get(size_t need) {
-    if (need > bytes) {
-      if (p) cudaFreeHost(p);
-      bytes = std::max(need, (size_t)1 << 16);
-      if (cudaMallocHost(&p, bytes) != cudaSuccess) throw Error{GIM_E_CUDA, "cudaMallocHost failed"};
-    }
-    return p;
-  }
-  ~Pinned() {
-    if (p) cudaFreeHost(p);
-  }
+  void* get(size_t need) { return pinned_scratch(need); }
 };
-static thread_local Pinned g_pin;
+static Pinned g_pin;
 
 template <class T>
 static T read_scalar(const T* d, cudaStream_t s) {
   T* h = static_cast<T*>(g_pin.get(sizeof(T)));
   GIM_CUDA(cudaMemcpyAsync(h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   return *h;
 }
 
@@ -177,7 +165,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
     if (refine_fused_run(L, t, part, bw_d, fc, fb, s)) break;
     // strong pass (refinement.py:350-386) + the same Alg. 4 bookkeeping
     GIM_CUDA(cudaMemcpyAsync(bw.data(), bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     int ne = 0;
     for (int b = 0; b < k; ++b) {
       masks[b] = (double)bw[b] > l_max;
@@ -194,7 +182,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
     long long ctr[2];
     GIM_CUDA(cudaMemcpyAsync(bw.data(), bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaMemcpyAsync(ctr, rb.ctr.get(), 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     ++strong;
     ++hs.iters;
     hs.i_w = 0;
@@ -242,7 +230,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   if (host_finished) {  // restore the best mapping (the kernel does this itself otherwise)
     GIM_CUDA(cudaMemcpyAsync(part, fb.best, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
     GIM_CUDA(cudaMemcpyAsync(bw_d, fb.best_bw, sizeof(long long) * k, cudaMemcpyDeviceToDevice, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
   }
   st.lp += hs.lp;
   st.weak += hs.weak;
@@ -277,7 +265,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
   total_cost(L.g, part, t, rb.jtmp.get(), s);
   GIM_CUDA(cudaMemcpyAsync(h_dj, rb.jtmp.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
   GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   long long J = *h_dj;
   std::vector<long long> bw(h_bw, h_bw + k);
   auto maxof = [&](const std::vector<long long>& x) {
@@ -332,7 +320,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
     apply_moves(L, t, part, bw_d, rb, s);
     GIM_CUDA(cudaMemcpyAsync(h_bw, bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaMemcpyAsync(h_mv, rb.ctr.get(), 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     if (st.in_initial) ++st.init_refine_iterations;
     else ++st.refine_iterations;
     const long long movers = *h_mv;
@@ -376,7 +364,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
   GIM_CUDA(cudaMemcpyAsync(part, best.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
   std::copy(best_bw.begin(), best_bw.end(), h_bw);
   GIM_CUDA(cudaMemcpyAsync(bw_d, h_bw, sizeof(long long) * k, cudaMemcpyHostToDevice, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
 }
 
 // ---------------------------------------------------------------------------
@@ -564,7 +552,7 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     }
     return;
   }
-  GIM_CUDA(cudaStreamSynchronize(s));  // children read subs/trans from other streams
+  GIM_CUDA(sync_stream(s));  // children read subs/trans from other streams
   std::vector<std::thread> workers;
   std::vector<std::exception_ptr> errs((size_t)parts);
   for (int j = 0; j < parts; ++j) {
@@ -572,19 +560,18 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
       cudaStream_t cs = nullptr;
       try {
         GIM_CUDA(cudaSetDevice(C.device));
-        GIM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cs = acquire_stream();
         {
-          StreamArena arena(cs);  // this subtree's scratch stays off the shared pool
           std::vector<int> id2 = ident;
           id2.push_back(j);
           descend(C, subs[j].view(), child_total[j], level - 1, id2, trans[j].get(),
                   hash2(node_seed, (unsigned long long)level, (unsigned long long)j), cs);
         }
-        GIM_CUDA(cudaStreamSynchronize(cs));
+        GIM_CUDA(sync_stream(cs));
       } catch (...) {
         errs[j] = std::current_exception();
       }
-      if (cs) cudaStreamDestroy(cs);
+      release_stream(cs);
     });
   }
   for (auto& w : workers) w.join();
@@ -633,7 +620,6 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   std::vector<long long> h(tt.hierarchy, tt.hierarchy + tt.levels);
   std::vector<long long> d(tt.distances, tt.distances + tt.levels);
   const long long k = t.k;
-  StreamArena arena(s);  // released (stream-ordered) when the call returns
   RunStats st;
   reset_launches();
   cudaEvent_t ev[4];
@@ -922,7 +908,7 @@ extern "C" int gim_rebalance(const gim_graph* g, const int32_t* assignment,
     std::vector<long long> bw((size_t)k);
     GIM_CUDA(cudaMemcpyAsync(bw.data(), block_weights, sizeof(long long) * k,
                              cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     std::vector<unsigned char> masks((size_t)k * 2);
     std::vector<int> el;
     for (int b = 0; b < k; ++b) {
@@ -949,7 +935,7 @@ extern "C" int gim_rebalance(const gim_graph* g, const int32_t* assignment,
                                                        out_dest, out_to_move);
       GIM_LAUNCH_CHECK();
     }
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     if (incomplete_out) *incomplete_out = el.empty() ? 1 : 0;
   });
 }
@@ -1019,7 +1005,7 @@ extern "C" int gim_internal_partitioner(const gim_graph* g, int32_t k, double ep
     long long total = total_vertex_weight(dg, s);
     RunStats st;
     internal_partitioner(dg, total, k, eps_local, seed, part, st, s);
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
   });
 }
 
@@ -1036,7 +1022,7 @@ extern "C" int gim_hierarchical_multisection(const gim_graph* g, const gim_topol
     std::vector<long long> d(t->distances, t->distances + t->levels);
     RunStats st;
     hierarchical_multisection(dg, total, h, d, eps, seed, assignment, st, s);
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
   });
 }
 
@@ -1080,7 +1066,7 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
                              cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaMemcpyAsync(out_block_weights, bw.get(), sizeof(long long) * tp.k,
                              cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     if (stats) stats->kernel_launches = launches();
   });
 }
@@ -1090,6 +1076,7 @@ extern "C" int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sour
 }
 
 extern "C" int64_t gim_launch_count(void) { return launches(); }
+extern "C" void gim_release_cached_memory(void) { gim::release_cached_memory(); }
 extern "C" void gim_reset_launch_count(void) { reset_launches(); }
 
 extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }

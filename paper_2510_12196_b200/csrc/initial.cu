@@ -204,7 +204,7 @@ void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
   k_ggg<<<1, kGggBlock, use_smem ? smem : 0, s>>>(dj.get(), 1);
   count_launch();
   GIM_LAUNCH_CHECK();
-  GIM_CUDA(cudaStreamSynchronize(s));  // job struct lives on this stack frame
+  GIM_CUDA(sync_stream(s));  // job struct lives on this stack frame
 }
 
 // ---------------------------------------------------------------------------
@@ -339,7 +339,7 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
   std::vector<int> hs((size_t)parts + 1);
   GIM_CUDA(cudaMemcpyAsync(hs.data(), pstart.get(), sizeof(int) * ((size_t)parts + 1),
                            cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   hs[parts] = n;
   for (int j = parts - 1; j >= 0; --j)
     if (hs[j] < 0) hs[j] = hs[j + 1];
@@ -363,7 +363,7 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
   std::vector<int> hoff((size_t)n + 1);
   GIM_CUDA(cudaMemcpyAsync(hoff.data(), noff.get(), sizeof(int) * ((size_t)n + 1),
                            cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   for (int j = 0; j < parts; ++j) {
     int v0 = hs[j], v1 = hs[j + 1];
     int nj = v1 - v0;

@@ -399,7 +399,7 @@ void prepare_level(RefineLevel& L, int k, cudaStream_t s) {
   int h = 0;
   if (g.n) {
     GIM_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
   }
   L.n_heavy = h;
 }
@@ -442,7 +442,7 @@ void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const 
   exclusive_scan<int>(g.n, f, ko, rb.count.get(), s);
   int cnt = 0;
   GIM_CUDA(cudaMemcpyAsync(&cnt, rb.count.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   if (cnt == 0) return;
   unsigned ncell = 31u * (unsigned)rho;
   unsigned long long maxkey = strong ? (unsigned long long)k * ncell * k : (unsigned long long)k * ncell;
@@ -575,7 +575,7 @@ long long conn_build(const DevGraph& g, const int* part, int k, int* c_off, int*
                       (int*)nullptr, s);
   int total = 0;
   GIM_CUDA(cudaMemcpyAsync(&total, tot.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  GIM_CUDA(cudaStreamSynchronize(s));
+  GIM_CUDA(sync_stream(s));
   return total;
 }
 

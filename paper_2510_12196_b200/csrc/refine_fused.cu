@@ -36,6 +36,7 @@
 // ("yield"); the host runs the sort-based strong pass and relaunches.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -49,6 +50,7 @@ namespace gim {
 
 constexpr int kFusedBlock = 256;
 constexpr int kFusedWarps = kFusedBlock / 32;
+constexpr int kMaxCluster = 16;  // non-portable cluster size (B200 allows 16)
 constexpr int kCtrStride = 8;  // per-iteration-parity counters
 enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ };
 
@@ -82,6 +84,7 @@ struct FusedArgs {
   long long* S;        // [k * G]
   long long* ctr;      // [2 * kCtrStride] per-parity counters, [16] = J at entry
   FusedState* st;
+  int bar_mode;        // GridBarrier mode
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
   unsigned long long seed;
@@ -122,18 +125,22 @@ __device__ __forceinline__ void warp_append(bool pred, int val, int* list, long 
   if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
 }
 
-// grid-wide barrier; a one-CTA launch (small graphs, launched without the
-// cooperative attribute so many run concurrently) only needs __syncthreads
+// Barrier across the CTAs of one refinement: a one-CTA launch only needs
+// __syncthreads; small graphs run as ONE thread-block cluster (plain launch,
+// hardware cluster barrier with release/acquire semantics, so many
+// refinements run concurrently); large graphs as a cooperative grid.
 struct GridBarrier {
+  int mode;  // 0 one CTA, 1 cluster, 2 cooperative grid
   __device__ __forceinline__ void sync() const {
-    if (gridDim.x == 1) __syncthreads();
+    if (mode == 0) __syncthreads();
+    else if (mode == 1) cg::this_cluster().sync();
     else cg::this_grid().sync();
   }
 };
 
 template <int VW>
 __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
-  const GridBarrier grid;
+  const GridBarrier grid{A.bar_mode};
   extern __shared__ unsigned char dsm[];
   __shared__ long long s_dbit[64];
   __shared__ Ctl C;
@@ -721,11 +728,23 @@ static int coop_max_blocks(size_t smem) {
   GIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)std::max<size_t>(smem, 48 * 1024)));
+  GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>,
+                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW>, kFusedBlock,
                                                          smem));
   int r = std::max(1, per) * sms;
   cache.emplace(key, r);
   return r;
+}
+
+// vertices per CTA of a cluster-mode refinement (GIM_CLUSTER_VPC overrides)
+static int cluster_vertices_per_cta() {
+  static const int v = [] {
+    const char* e = std::getenv("GIM_CLUSTER_VPC");
+    int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : 512;
+  }();
+  return v;
 }
 
 bool fused_supported(int k, int rho) { return k <= 1024 && rho >= 1 && rho <= 8; }
@@ -746,11 +765,21 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     case 16: maxb = coop_max_blocks<16>(smem); break;
     default: maxb = coop_max_blocks<32>(smem); break;
   }
-  // small graphs: one CTA (plain launch, __syncthreads barriers); otherwise
-  // ~1K vertices per CTA, at most one full co-resident wave
-  const int G = g.n <= 4096 ? 1
-                            : (int)std::min<long long>((long long)maxb,
-                                                       ((long long)g.n + 1023) / 1024);
+  // small graphs: one CTA, or one thread-block cluster of up to kMaxCluster
+  // CTAs (plain launches, so the refinements of sibling subgraphs overlap);
+  // otherwise ~1K vertices per CTA, at most one full co-resident wave
+  const int vpc = cluster_vertices_per_cta();
+  int G, mode;
+  if (g.n <= (long long)vpc) {
+    G = 1;
+    mode = 0;
+  } else if (g.n <= (long long)vpc * kMaxCluster) {
+    G = (g.n + vpc - 1) / vpc;
+    mode = 1;
+  } else {
+    G = (int)std::min<long long>((long long)maxb, ((long long)g.n + 1023) / 1024);
+    mode = 2;
+  }
   if (fb.S_cap < (long long)G * k) {
     fb.S = DBuf<long long>((size_t)G * k, s);
     fb.S_cap = (long long)G * k;
@@ -789,6 +818,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.S = fb.S.get();
   A.ctr = fb.ctr;
   A.st = fb.state;
+  A.bar_mode = mode;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
   A.phi = cfg.phi;
@@ -810,13 +840,28 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     // one launch = many Alg. 4 iterations; per-iteration algorithmic bytes
     // are accounted by the host from the iteration count
     ProfScope prof(P_LP_EVAL, 0.0, s);
-    if (G == 1)
+    if (mode == 0) {
       GIM_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kFusedBlock), args, smem, s));
-    else
+    } else if (mode == 1) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(G);
+      lc.blockDim = dim3(kFusedBlock);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      GIM_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+    } else {
       GIM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kFusedBlock), args, smem, s));
+    }
     count_launch();
     GIM_CUDA(cudaMemcpyAsync(fb.h_state, fb.state, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
-    GIM_CUDA(cudaStreamSynchronize(s));
+    GIM_CUDA(sync_stream(s));
     prof.extra = (double)(fb.h_state->lp + fb.h_state->weak - fb.lp_seen - fb.weak_seen) *
                  (12.0 * (double)g.m2 + 8.0 * (double)g.n);
     fb.lp_seen = fb.h_state->lp;
