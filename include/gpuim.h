@@ -94,6 +94,10 @@ typedef struct gim_im_stats {
   double prof_ms[16];
   double prof_bytes[16];
   int64_t prof_count[16];
+  /* the single timed scope with the most algorithmic bytes (profiling on):
+   * its class, device ms and bytes — the finest-level refinement launch */
+  int32_t top_class;
+  double top_ms, top_bytes;
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */

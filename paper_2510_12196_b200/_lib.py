@@ -76,6 +76,9 @@ class GimImStats(C.Structure):
         ("prof_ms", C.c_double * 16),
         ("prof_bytes", C.c_double * 16),
         ("prof_count", C.c_int64 * 16),
+        ("top_class", C.c_int32),
+        ("top_ms", C.c_double),
+        ("top_bytes", C.c_double),
     ]
 
 

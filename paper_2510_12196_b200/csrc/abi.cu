@@ -98,7 +98,7 @@ void release_stream(cudaStream_t s) {
 // dominated small-graph partitioner calls.  Blocks are cached per
 // (stream, size class) for the life of the process and handed out again
 // only on the stream they were released on (stream order = happens-before).
-constexpr size_t kCacheMax = (size_t)64 << 20;  // larger buffers go to the pool
+constexpr size_t kCacheMax = (size_t)16 << 30;  // larger buffers go to the pool
 
 static size_t size_class(size_t b) {
   size_t c = 256;
@@ -298,8 +298,12 @@ void prof_end(void* token, cudaStream_t s, double extra_bytes) {
   }
 }
 
-void prof_collect(double* ms, double* bytes, long long* count) {
+void prof_collect(double* ms, double* bytes, long long* count, int* top_cls, double* top_ms,
+                  double* top_bytes) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
+  *top_cls = -1;
+  *top_ms = 0.0;
+  *top_bytes = 0.0;
   for (auto& r : g_recs) {
     cudaEventSynchronize(r.b);
     float t = 0.f;
@@ -308,6 +312,11 @@ void prof_collect(double* ms, double* bytes, long long* count) {
       ms[r.cls] += t;
       bytes[r.cls] += r.bytes;
       count[r.cls] += 1;
+      if (r.bytes > *top_bytes) {
+        *top_cls = r.cls;
+        *top_ms = t;
+        *top_bytes = r.bytes;
+      }
     }
     g_evpool.push_back(r.a);
     g_evpool.push_back(r.b);

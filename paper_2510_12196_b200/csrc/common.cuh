@@ -122,7 +122,9 @@ void prof_set(bool on);
 void prof_begin(int cls, double bytes, cudaStream_t s, void** token);
 void prof_end(void* token, cudaStream_t s, double extra_bytes);
 // accumulate totals per class (ms, bytes, launches); clears the records
-void prof_collect(double* ms, double* bytes, long long* count);
+// and the single scope with the most bytes
+void prof_collect(double* ms, double* bytes, long long* count, int* top_cls, double* top_ms,
+                  double* top_bytes);
 
 struct ProfScope {
   void* tok = nullptr;

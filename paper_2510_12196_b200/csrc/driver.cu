@@ -686,7 +686,12 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     stats->l_max = l_max;
     double pms[P_COUNT] = {0}, pby[P_COUNT] = {0};
     long long pct[P_COUNT] = {0};
-    prof_collect(pms, pby, pct);
+    int tcls = -1;
+    double tms = 0, tby = 0;
+    prof_collect(pms, pby, pct, &tcls, &tms, &tby);
+    stats->top_class = tcls;
+    stats->top_ms = tms;
+    stats->top_bytes = tby;
     for (int c = 0; c < 16; ++c) {
       stats->prof_ms[c] = c < P_COUNT ? pms[c] : 0.0;
       stats->prof_bytes[c] = c < P_COUNT ? pby[c] : 0.0;
@@ -728,39 +733,117 @@ void fill_sources(int n, const int* off, int* src, cudaStream_t s) {
   GIM_LAUNCH_CHECK();
 }
 
+// Host int64 CSR -> device int32 level (graph.py:17-39 arrays).  The
+// arrays are narrowed to int32 ON THE HOST by worker threads, each writing
+// into its own double-buffered pinned staging block and copying on its own
+// stream, so narrowing, PCIe transfer and the other workers overlap and
+// only half the bytes cross the bus.  The same pass validates what the
+// device path relies on (values fit int32, positive vertex weights, total
+// vertex / edge weight < 2^31).
+namespace {
+struct UpJob {
+  const int64_t* src;
+  int* dst;
+  long long cnt;
+  int kind;  // 0 offsets/targets, 1 edge weights, 2 vertex weights
+};
+struct UpAcc {
+  long long sum_ew = 0, sum_vw = 0;
+  bool bad_range = false, bad_vw = false;
+};
+}  // namespace
+
 static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, const int64_t* ew,
                          const int64_t* vw, OwnedGraph& G, cudaStream_t s) {
   GIM_CHECK(n >= 0 && n < INT32_MAX, GIM_E_OVERFLOW, "n must be < 2^31");
   long long m2 = off[n];
   GIM_CHECK(m2 >= 0 && m2 < INT32_MAX, GIM_E_OVERFLOW, "2m must be < 2^31");
-  long long tv = 0, te = 0;
-  for (long long v = 0; v < n; ++v) {
-    GIM_CHECK(vw[v] > 0, GIM_E_INVALID, "vertex weights must be positive");
-    tv += vw[v];
-  }
-  GIM_CHECK(tv < INT32_MAX, GIM_E_OVERFLOW, "total vertex weight must be < 2^31");
-  for (long long e = 0; e < m2; ++e) te += ew[e];
-  GIM_CHECK(te < INT32_MAX, GIM_E_OVERFLOW, "total edge weight must be < 2^31");
   G.n = (int)n;
   G.m2 = m2;
-  G.total_vw = tv;
   G.off = DBuf<int>((size_t)n + 1, s);
   G.tgt = DBuf<int>((size_t)std::max(m2, 1ll), s);
   G.w = DBuf<int>((size_t)std::max(m2, 1ll), s);
   G.vw = DBuf<int>((size_t)std::max(n, 1ll), s);
   G.src = DBuf<int>((size_t)std::max(m2, 1ll), s);
-  long long biggest = std::max(m2, n + 1);
-  DBuf<long long> stage((size_t)std::max(biggest, 1ll), s);
-  auto up = [&](const int64_t* h, long long cnt, int* d) {
-    if (cnt == 0) return;
-    GIM_CUDA(cudaMemcpyAsync(stage.get(), h, sizeof(long long) * cnt, cudaMemcpyHostToDevice, s));
-    k_narrow<<<grid_for(cnt, 256), 256, 0, s>>>(cnt, stage.get(), d);
-    count_launch();
+  // device buffers come from `s`'s stream order: the workers' streams wait
+  GIM_CUDA(sync_stream(s));
+  constexpr long long kChunk = 1ll << 21;  // elements per staging buffer
+  std::vector<UpJob> jobs;
+  auto add = [&](const int64_t* h, long long cnt, int* d, int kind) {
+    for (long long i = 0; i < cnt; i += kChunk)
+      jobs.push_back(UpJob{h + i, d + i, std::min(kChunk, cnt - i), kind});
   };
-  up(off, n + 1, G.off.get());
-  up(tgt, m2, G.tgt.get());
-  up(ew, m2, G.w.get());
-  up(vw, n, G.vw.get());
+  add(off, n + 1, G.off.get(), 0);
+  add(tgt, m2, G.tgt.get(), 0);
+  add(ew, m2, G.w.get(), 1);
+  add(vw, n, G.vw.get(), 2);
+  const int T = (int)std::max<size_t>(1, std::min<size_t>(jobs.size(),
+                                       std::max(2u, std::min(8u, std::thread::hardware_concurrency()))));
+  std::vector<UpAcc> acc((size_t)T);
+  std::vector<std::exception_ptr> errs((size_t)T);
+  std::atomic<size_t> next{0};
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  auto worker = [&](int t) {
+    cudaStream_t ws = nullptr;
+    try {
+      GIM_CUDA(cudaSetDevice(dev));
+      ws = acquire_stream();
+      int* stage = static_cast<int*>(pinned_scratch(sizeof(int) * 2 * kChunk));
+      cudaEvent_t done[2];
+      GIM_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+      GIM_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+      bool used[2] = {false, false};
+      UpAcc& a = acc[(size_t)t];
+      for (int slot = 0;; slot ^= 1) {
+        const size_t j = next.fetch_add(1);
+        if (j >= jobs.size()) break;
+        const UpJob& J = jobs[j];
+        int* buf = stage + (size_t)slot * kChunk;
+        if (used[slot]) GIM_CUDA(cudaEventSynchronize(done[slot]));
+        long long sum = 0;
+        bool bad = false, nonpos = false;
+        for (long long i = 0; i < J.cnt; ++i) {
+          const int64_t x = J.src[i];
+          bad |= x < INT32_MIN || x > INT32_MAX;
+          nonpos |= x <= 0;
+          sum += x;
+          buf[i] = (int)x;
+        }
+        a.bad_range |= bad;
+        if (J.kind == 1) a.sum_ew += sum;
+        if (J.kind == 2) { a.sum_vw += sum; a.bad_vw |= nonpos; }
+        GIM_CUDA(cudaMemcpyAsync(J.dst, buf, sizeof(int) * J.cnt, cudaMemcpyHostToDevice, ws));
+        GIM_CUDA(cudaEventRecord(done[slot], ws));
+        used[slot] = true;
+      }
+      GIM_CUDA(sync_stream(ws));
+      cudaEventDestroy(done[0]);
+      cudaEventDestroy(done[1]);
+    } catch (...) {
+      errs[(size_t)t] = std::current_exception();
+      if (ws) sync_stream(ws);
+    }
+    release_stream(ws);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  UpAcc tot;
+  for (auto& a : acc) {
+    tot.sum_ew += a.sum_ew;
+    tot.sum_vw += a.sum_vw;
+    tot.bad_range |= a.bad_range;
+    tot.bad_vw |= a.bad_vw;
+  }
+  GIM_CHECK(!tot.bad_range, GIM_E_OVERFLOW, "CSR values must fit int32");
+  GIM_CHECK(!tot.bad_vw, GIM_E_INVALID, "vertex weights must be positive");
+  GIM_CHECK(tot.sum_vw < INT32_MAX, GIM_E_OVERFLOW, "total vertex weight must be < 2^31");
+  GIM_CHECK(tot.sum_ew < INT32_MAX, GIM_E_OVERFLOW, "total edge weight must be < 2^31");
+  G.total_vw = tot.sum_vw;
   fill_sources((int)n, G.off.get(), G.src.get(), s);
   GIM_LAUNCH_CHECK();
 }
@@ -1059,14 +1142,28 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     DBuf<int> part((size_t)n, s);
     DBuf<long long> bw((size_t)tp.k, s);
     integrated_map_device(G.view(), G.total_vw, *t, eps, seed, P, part.get(), bw.get(), stats, s);
-    DBuf<long long> wide((size_t)n, s);
-    k_widen<<<grid_for(n, 256), 256, 0, s>>>((int)n, part.get(), wide.get());
-    count_launch();
-    GIM_CUDA(cudaMemcpyAsync(out_assignment, wide.get(), sizeof(long long) * n,
-                             cudaMemcpyDeviceToHost, s));
+    // int32 assignment -> pinned staging -> widened to int64 on the host by
+    // worker threads (half the PCIe bytes, no pageable staging copy)
+    int* h_part = static_cast<int*>(pinned_scratch(sizeof(int) * (size_t)n));
+    GIM_CUDA(cudaMemcpyAsync(h_part, part.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
     GIM_CUDA(cudaMemcpyAsync(out_block_weights, bw.get(), sizeof(long long) * tp.k,
                              cudaMemcpyDeviceToHost, s));
     GIM_CUDA(sync_stream(s));
+    {
+      const int T = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+      const long long per = (n + T - 1) / T;
+      auto widen = [&](int t) {
+        const long long a = std::min<long long>(n, t * per), b = std::min<long long>(n, a + per);
+        for (long long i = a; i < b; ++i) out_assignment[i] = h_part[i];
+      };
+      std::vector<std::thread> pool;
+      if (n >= (1ll << 20))
+        for (int t = 1; t < T; ++t) pool.emplace_back(widen, t);
+      else
+        for (int t = 1; t < T; ++t) widen(t);
+      widen(0);
+      for (auto& th : pool) th.join();
+    }
     if (stats) stats->kernel_launches = launches();
   });
 }

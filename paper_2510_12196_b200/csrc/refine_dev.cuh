@@ -45,39 +45,58 @@ struct VertexEval {
   int best_b;          // -1: no admissible adjacent block
 };
 
-// `dmax` = max degree over the warp's groups (warp-uniform loop bound).
+// Neighbours in the same block are merged first: __match_any_sync groups the
+// lanes of a vertex group by block, the first lane of each block (the
+// "leader") gets conn(v, b) by a redux over its peers, and the cost sweep
+// runs over the leaders only — the number of DISTINCT adjacent blocks
+// (typically 1-3) instead of the degree.  Non-leader lanes hold the same
+// block as their leader, so dropping them changes no (gain, block) maximum.
+// `dmax` (max degree over the warp's groups) is unused but kept for callers.
 // Interior vertices (every neighbour in the own block) are the common case
 // after the first iterations: a warp whose groups have no candidate lane
-// skips the whole evaluation, so the pass degenerates to one row sweep.
+// skips the whole evaluation.
 template <int VW>
 __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, int myw, int dmax,
                                                 const Topo& t, const long long* s_dbit,
                                                 const unsigned char* allowed, bool need_conn) {
+  (void)dmax;
   VertexEval r;
   r.cur = 0;
   r.conn_own = 0;
   r.best_gain = kGainNone;
   r.best_b = -1;
-  const bool cand = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
-  if (!__any_sync(0xffffffffu, cand)) return r;
-  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
-  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
-  long long wv = valid ? myw : 0;
-  long long cur = wv * cdist(s_dbit, ocode, mycode);
-  long long co = (need_conn && valid && myb == own) ? wv : 0;
+  const bool cand0 = valid && myb >= 0 && myb != own && (allowed == nullptr || allowed[myb]);
+  if (!__any_sync(0xffffffffu, cand0)) return r;
+  const int lane = (int)lane_id();
+  const unsigned gmask =
+      VW == 32 ? 0xffffffffu : (((1u << VW) - 1u) << (lane & ~(VW - 1)));
+  const int key = valid ? myb : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, key) & gmask;
+  const bool leader = valid && lane == __ffs(peers) - 1;
+  const int conn = (int)__reduce_add_sync(peers, valid ? (unsigned)myw : 0u);
+  const unsigned lm = __ballot_sync(0xffffffffu, leader) & gmask;
+  const int trips = __reduce_max_sync(0xffffffffu, (unsigned)__popc(lm));
+  const unsigned long long ocode = t.code[(own < 0 ? 0 : own)];
+  const unsigned long long mycode = myb >= 0 ? t.code[myb] : 0ull;
+  const long long cl = leader ? (long long)conn : 0;
+  long long cur = cl * cdist(s_dbit, ocode, mycode);
+  long long co = (need_conn && leader && myb == own) ? cl : 0;
   long long cost = 0;
-  const int lim = min(dmax, VW);
-#pragma unroll 4
-  for (int i = 0; i < lim; ++i) {
-    unsigned long long ci = __shfl_sync(0xffffffffu, mycode, i, VW);
-    long long wi = __shfl_sync(0xffffffffu, wv, i, VW);
-    cost += wi * cdist(s_dbit, mycode, ci);
+  unsigned rem = lm;
+  for (int i = 0; i < trips; ++i) {
+    const int src = rem ? __ffs(rem) - 1 : lane;
+    const bool use = rem != 0;
+    rem &= rem - 1;
+    const unsigned long long ci = __shfl_sync(0xffffffffu, mycode, src);
+    const int wi = __shfl_sync(0xffffffffu, conn, src);
+    if (use) cost += (long long)wi * cdist(s_dbit, mycode, ci);
   }
 #pragma unroll
   for (int o = VW / 2; o > 0; o >>= 1) {
     cur += __shfl_xor_sync(0xffffffffu, cur, o);
     if (need_conn) co += __shfl_xor_sync(0xffffffffu, co, o);
   }
+  const bool cand = cand0 && leader;
   long long g = cand ? cur - cost : kGainNone;
   int b = cand ? myb : -1;
 #pragma unroll
@@ -93,12 +112,106 @@ __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, in
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Per-vertex gain evaluation, thread-per-vertex path.  One thread walks the
+// row and merges neighbours by block into at most TPV_DISTINCT (block, conn)
+// pairs held in registers (unrolled, statically indexed); then
+// cur = sum_j conn_j D(own, b_j), cost(b_i) = sum_j conn_j D(b_i, b_j) and
+// the best admissible b_i by (gain desc, block asc) — exactly Eq. 1 over the
+// reference's slot table (refinement.py:168-198).  No shuffles: a warp
+// evaluates 32 vertices at once with independent instruction streams, which
+// is what the latency-bound refinement phases need.  A vertex with more
+// distinct adjacent blocks than TPV_DISTINCT reports `overflow` and is
+// handed to the warp-per-vertex table path.  `tb` >= 0 also returns the
+// cost of moving to tb (rebalance fallback target).
+
+constexpr int TPV_DISTINCT = 8;
+
+struct ThreadEval {
+  long long cur, conn_own, best_gain, cost_tb;
+  int best_b;
+  bool overflow;
+};
+
+__device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const int* tgt,
+                                                  const int* w, const int* part, const Topo& t,
+                                                  const long long* s_dbit,
+                                                  const unsigned char* allowed, int tb) {
+  ThreadEval r;
+  r.cur = 0;
+  r.conn_own = 0;
+  r.best_gain = kGainNone;
+  r.best_b = -1;
+  r.cost_tb = 0;
+  r.overflow = false;
+  int nb[TPV_DISTINCT];
+  long long cw[TPV_DISTINCT];
+#pragma unroll
+  for (int j = 0; j < TPV_DISTINCT; ++j) {
+    nb[j] = -1;
+    cw[j] = 0;
+  }
+  int cnt = 0;
+  for (int e = e0; e < e1; ++e) {
+    const int b = part[tgt[e]];
+    const long long ww = w[e];
+    bool found = false;
+#pragma unroll
+    for (int j = 0; j < TPV_DISTINCT; ++j)
+      if (nb[j] == b) {
+        cw[j] += ww;
+        found = true;
+      }
+    if (!found) {
+      if (cnt == TPV_DISTINCT) {
+        r.overflow = true;
+        return r;
+      }
+#pragma unroll
+      for (int j = 0; j < TPV_DISTINCT; ++j)
+        if (j == cnt) {
+          nb[j] = b;
+          cw[j] = ww;
+        }
+      ++cnt;
+    }
+  }
+  unsigned long long code[TPV_DISTINCT];
+#pragma unroll
+  for (int j = 0; j < TPV_DISTINCT; ++j) code[j] = j < cnt ? t.code[nb[j]] : 0ull;
+  const unsigned long long oc = t.code[own];
+  const unsigned long long tc = tb >= 0 ? t.code[tb] : 0ull;
+#pragma unroll
+  for (int j = 0; j < TPV_DISTINCT; ++j) {
+    if (j < cnt) {
+      r.cur += cw[j] * cdist(s_dbit, oc, code[j]);
+      if (nb[j] == own) r.conn_own = cw[j];
+      if (tb >= 0) r.cost_tb += cw[j] * cdist(s_dbit, tc, code[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TPV_DISTINCT; ++i) {
+    if (i < cnt && nb[i] != own && (allowed == nullptr || allowed[nb[i]])) {
+      long long cost = 0;
+#pragma unroll
+      for (int j = 0; j < TPV_DISTINCT; ++j)
+        if (j < cnt) cost += cw[j] * cdist(s_dbit, code[i], code[j]);
+      const long long g = r.cur - cost;
+      if (best_better(g, nb[i], r.best_gain, r.best_b)) {
+        r.best_gain = g;
+        r.best_b = nb[i];
+      }
+    }
+  }
+  return r;
+}
+
 // cur = sum_u w D(own, Pi u) alone (rebalance fallback when no candidate)
 template <int VW>
 __device__ __forceinline__ long long cur_regs(bool valid, int own, int myb, int myw,
                                               const Topo& t, const long long* s_dbit) {
-  const unsigned long long ocode = __ldg(t.code + (own < 0 ? 0 : own));
-  const unsigned long long mycode = myb >= 0 ? __ldg(t.code + myb) : 0ull;
+  const unsigned long long ocode = t.code[(own < 0 ? 0 : own)];
+  const unsigned long long mycode = myb >= 0 ? t.code[myb] : 0ull;
   long long cur = valid ? (long long)myw * cdist(s_dbit, ocode, mycode) : 0;
 #pragma unroll
   for (int o = VW / 2; o > 0; o >>= 1) cur += __shfl_xor_sync(0xffffffffu, cur, o);
@@ -109,8 +222,8 @@ __device__ __forceinline__ long long cur_regs(bool valid, int own, int myb, int 
 template <int VW>
 __device__ __forceinline__ long long cost_regs(bool valid, int myb, int myw, int tb,
                                                const Topo& t, const long long* s_dbit) {
-  unsigned long long tc = __ldg(t.code + (tb < 0 ? 0 : tb));
-  unsigned long long mc = myb >= 0 ? __ldg(t.code + myb) : 0ull;
+  unsigned long long tc = t.code[(tb < 0 ? 0 : tb)];
+  unsigned long long mc = myb >= 0 ? t.code[myb] : 0ull;
   long long c = valid ? (long long)myw * cdist(s_dbit, tc, mc) : 0;
 #pragma unroll
   for (int o = VW / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -158,20 +271,20 @@ __device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int
                                                  const Topo& t, const long long* s_dbit,
                                                  const unsigned char* allowed) {
   const int lane = lane_id();
-  const unsigned long long oc = __ldg(t.code + own);
+  const unsigned long long oc = t.code[own];
   long long cur = 0;
   for (int j = lane; j < s; j += 32)
-    cur += (long long)wt.lw[j] * cdist(s_dbit, oc, __ldg(t.code + wt.lb[j]));
+    cur += (long long)wt.lw[j] * cdist(s_dbit, oc, t.code[wt.lb[j]]);
   cur = warp_sum_ll(cur);
   long long g = kGainNone;
   int b = -1;
   for (int i = lane; i < s; i += 32) {
     int bi = wt.lb[i];
     if (bi == own || (allowed && !allowed[bi])) continue;
-    unsigned long long ci = __ldg(t.code + bi);
+    unsigned long long ci = t.code[bi];
     long long cost = 0;
     for (int j = 0; j < s; ++j)
-      cost += (long long)wt.lw[j] * cdist(s_dbit, ci, __ldg(t.code + wt.lb[j]));
+      cost += (long long)wt.lw[j] * cdist(s_dbit, ci, t.code[wt.lb[j]]);
     long long gi = cur - cost;
     if (best_better(gi, bi, g, b)) { g = gi; b = bi; }
   }
@@ -191,10 +304,10 @@ __device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int
 
 __device__ __forceinline__ long long cost_table(const WarpTable& wt, int s, int tb,
                                                 const Topo& t, const long long* s_dbit) {
-  const unsigned long long tc = __ldg(t.code + tb);
+  const unsigned long long tc = t.code[tb];
   long long c = 0;
   for (int j = lane_id(); j < s; j += 32)
-    c += (long long)wt.lw[j] * cdist(s_dbit, tc, __ldg(t.code + wt.lb[j]));
+    c += (long long)wt.lw[j] * cdist(s_dbit, tc, t.code[wt.lb[j]]);
   return warp_sum_ll(c);
 }
 

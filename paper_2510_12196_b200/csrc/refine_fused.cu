@@ -36,6 +36,7 @@
 // ("yield"); the host runs the sort-based strong pass and relaunches.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -50,7 +51,12 @@ namespace gim {
 
 constexpr int kFusedBlock = 256;
 constexpr int kFusedWarps = kFusedBlock / 32;
-constexpr int kMaxCluster = 16;  // non-portable cluster size (B200 allows 16)
+constexpr int kMaxCluster = 16;
+// vertex-centric first filter when a level has at most this many vertex
+// groups per warp (else edge-parallel boundary pass + lists)
+constexpr int kVcSteps = 8;
+// longest row evaluated thread-per-vertex (longer rows: warp table path)
+constexpr int kTpvMaxDeg = 64;  // non-portable cluster size (B200 allows 16)
 constexpr int kCtrStride = 8;  // per-iteration-parity counters
 enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ };
 
@@ -85,10 +91,18 @@ struct FusedArgs {
   long long* ctr;      // [2 * kCtrStride] per-parity counters, [16] = J at entry
   FusedState* st;
   int bar_mode;        // GridBarrier mode
+  int smem_base;       // k_refine_smem: bytes of the regular dynamic region
+  long long* ptime;    // [16] per-phase ns (trace mode) or null
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
   unsigned long long seed;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Ctl {
   long long J, best_j, best_maxw, maxw, pass_counter;
@@ -125,6 +139,39 @@ __device__ __forceinline__ void warp_append(bool pred, int val, int* list, long 
   if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
 }
 
+// Warp-private append queue in shared memory: appends cost a ballot and a
+// shared store; the warp reserves list space with ONE global atomic per 32+
+// entries (the list counters are single addresses every warp hits) and
+// copies the entries out.  Warp-synchronous, so loops need not be
+// CTA-uniform and no CTA barrier stalls the latency-bound sweeps.
+struct WarpQueue {
+  int* buf;   // [kQueueCap] in shared memory, private to the warp
+  int cnt;    // warp-uniform
+};
+constexpr int kQueueCap = 64;
+
+__device__ __forceinline__ void wq_flush(WarpQueue& q, int* list, long long* counter) {
+  __syncwarp();
+  if (q.cnt == 0) return;
+  const unsigned lane = lane_id();
+  long long base = 0;
+  if (lane == 0)
+    base = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(counter),
+                                (unsigned long long)q.cnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int i = lane; i < q.cnt; i += 32) list[base + i] = q.buf[i];
+  __syncwarp();
+  q.cnt = 0;
+}
+
+__device__ __forceinline__ void wq_push(WarpQueue& q, bool pred, int val, int* list,
+                                        long long* counter) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (pred) q.buf[q.cnt + __popc(m & ((1u << lane_id()) - 1u))] = val;
+  q.cnt += __popc(m);
+  if (q.cnt >= 32) wq_flush(q, list, counter);
+}
+
 // Barrier across the CTAs of one refinement: a one-CTA launch only needs
 // __syncthreads; small graphs run as ONE thread-block cluster (plain launch,
 // hardware cluster barrier with release/acquire semantics, so many
@@ -139,33 +186,39 @@ struct GridBarrier {
 };
 
 template <int VW>
-__global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
+__device__ __forceinline__ void refine_body(const FusedArgs& A) {
   const GridBarrier grid{A.bar_mode};
   extern __shared__ unsigned char dsm[];
   __shared__ long long s_dbit[64];
   __shared__ Ctl C;
   __shared__ int s_nelig;
+  __shared__ int qbuf[kFusedWarps * 2 * kQueueCap];
   const int k = A.k;
   const int NC = 31 * A.rho;
   const int n = A.n;
   const int G = gridDim.x;
-  // dynamic smem: warp tables | pstar[k] | run[k] | elist[k] | cstar[k] | ovl[k] | elig[k]
-  int* tables = reinterpret_cast<int*>(dsm);
-  long long* pstar = reinterpret_cast<long long*>(tables + (size_t)kFusedWarps * 3 * k);
+  // dynamic smem: pstar[k] | run[k] | code[k] | warp tables | elist[k] | cstar[k] |
+  // wrun[warps*k] | ovl[k] | elig[k]
+  long long* pstar = reinterpret_cast<long long*>(dsm);
   long long* run = pstar + k;
-  int* elist = reinterpret_cast<int*>(run + k);
+  unsigned long long* s_code = reinterpret_cast<unsigned long long*>(run + k);
+  int* tables = reinterpret_cast<int*>(s_code + k);
+  int* elist = tables + (size_t)kFusedWarps * 3 * k;
   int* cstar = elist + k;
-  unsigned char* ovl = reinterpret_cast<unsigned char*>(cstar + k);
+  int* wrun = cstar + k;
+  unsigned char* ovl = reinterpret_cast<unsigned char*>(wrun + (size_t)kFusedWarps * k);
   unsigned char* elig = ovl + k;
 
   load_dbit(s_dbit, A.t);
+  for (int b = threadIdx.x; b < k; b += blockDim.x) s_code[b] = A.t.code[b];
+  Topo T = A.t;  // digit codes from shared memory
+  T.code = s_code;
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long NW = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long GT = (long long)gridDim.x * blockDim.x;
-  const long long wt0 = gt - lane;  // first thread of this warp (warp-uniform loops)
   constexpr int GPW = 32 / VW;
   const int gi = lane / VW, li = lane % VW;
   WarpTable wt;
@@ -184,14 +237,22 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       A.rtgt[v] = -1;
       A.flags0[v] = 0;
       A.flags1[v] = 0;
-      A.bstamp[v] = 0;
+      if (A.bstamp) A.bstamp[v] = 0;
     }
     for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
   }
   if (first) {
     long long acc = 0;
-    for (long long e = gt; e < A.m2; e += GT)
-      acc += (long long)A.w[e] * dist(A.t, A.part[A.src[e]], A.part[A.tgt[e]]);
+    if (A.src) {
+      for (long long e = gt; e < A.m2; e += GT)
+        acc += (long long)A.w[e] * dist(A.t, A.part[A.src[e]], A.part[A.tgt[e]]);
+    } else {  // shared-memory mode: rows
+      for (long long v = gt; v < n; v += GT) {
+        const int pv = A.part[v];
+        for (int e = A.off[v]; e < A.off[v + 1]; ++e)
+          acc += (long long)A.w[e] * dist(A.t, pv, A.part[A.tgt[e]]);
+      }
+    }
     block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
     for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
     if (blockIdx.x == 0)
@@ -235,6 +296,18 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
     C.strong_yield = 0;
   }
   __syncthreads();
+  // optional per-phase wall-clock accounting (GIM_TRACE_REFINE): CTA 0,
+  // thread 0 adds %globaltimer deltas between barriers into A.ptime[phase]
+  unsigned long long t_last = 0;
+  if (A.ptime && blockIdx.x == 0 && threadIdx.x == 0) t_last = globaltimer_ns();
+#define PHASE_MARK(id)                                                   \
+  do {                                                                   \
+    if (A.ptime && blockIdx.x == 0 && threadIdx.x == 0) {                \
+      const unsigned long long t_now = globaltimer_ns();                 \
+      A.ptime[(id)] += (long long)(t_now - t_last);                      \
+      t_last = t_now;                                                    \
+    }                                                                    \
+  } while (0)
 
   while (C.i < A.i_max) {
     const bool balanced_now = (double)C.maxw <= A.l_max;
@@ -255,9 +328,16 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
     const bool use_locks = C.locks_nonempty != 0;
     const int stamp = C.stamp + 1;
     bool incomplete = false;
+    // thread-per-vertex first filters straight over the vertex range when
+    // the level is small; otherwise an edge-parallel boundary pass + a
+    // compact list first (more memory-level parallelism for large levels)
+    const bool vcent = A.src == nullptr || (long long)n <= (long long)kVcSteps * GT;
+    WarpQueue qa{qbuf + warp * 2 * kQueueCap, 0}, qb{qbuf + (warp * 2 + 1) * kQueueCap, 0};
     if (balanced_now) {
-      // ---- boundary stamps: edge-parallel, int4-vectorised over E_u
-      {
+      // ---- K9 first filter (refinement.py:201-244)
+      long long ns = n;  // items: vertices (vcent) or the boundary list
+      if (!vcent) {
+        // boundary stamps: edge-parallel, int4-vectorised over E_u
         const long long m4 = A.m2 & ~3ll;
         for (long long e = gt * 4; e < m4; e += GT * 4) {
           int4 s4 = *reinterpret_cast<const int4*>(A.src + e);
@@ -271,70 +351,74 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         }
         for (long long e = m4 + gt; e < A.m2; e += GT)
           if (A.part[A.src[e]] != A.part[A.tgt[e]]) A.bstamp[A.src[e]] = stamp;
-      }
-      grid.sync();
-      // ---- boundary list (unlocked), split by degree
-      for (long long b0 = wt0; b0 < n; b0 += GT) {
-        const long long v = b0 + lane;
-        bool bnd = false, heavy = false;
-        if (v < n && A.bstamp[v] == stamp && !(use_locks && lkf[v])) {
-          bnd = true;
-          heavy = A.off[v + 1] - A.off[v] > VW;
+        grid.sync();
+        PHASE_MARK(0);
+        // boundary list (unlocked)
+        for (long long b0 = gt - lane; b0 < n; b0 += GT) {
+          const long long v = b0 + lane;
+          const bool bnd = v < n && A.bstamp[v] == stamp && !(use_locks && lkf[v]);
+          wq_push(qa, bnd, (int)v, A.lsmall, cnt + C_SMALL);
         }
-        warp_append(bnd && !heavy, (int)v, A.lsmall, cnt + C_SMALL);
-        warp_append(bnd && heavy, (int)v, A.lheavy, cnt + C_HEAVY);
+        wq_flush(qa, A.lsmall, cnt + C_SMALL);
+        grid.sync();
+        PHASE_MARK(1);
+        ns = cnt[C_SMALL];
       }
-      grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
-      // ---- K9 first filter over the boundary list
-      const long long ns = cnt[C_SMALL], nh = cnt[C_HEAVY];
-      for (long long ib = gw * GPW; ib < ns; ib += NW * GPW) {
-        const long long idx = ib + gi;
-        const bool live = idx < ns;
-        const int v = live ? A.lsmall[idx] : 0;
-        int e0 = 0, d = 0, own = 0;
+      for (long long b0 = gt - lane; b0 < ns; b0 += GT) {
+        const long long idx = b0 + lane;
+        bool live = idx < ns;
+        int v = 0, own = 0, e0 = 0, e1 = 0;
         if (live) {
-          e0 = A.off[v];
-          d = A.off[v + 1] - e0;
+          v = vcent ? (int)idx : A.lsmall[idx];
+          if (vcent && use_locks && lkf[v]) live = false;
+        }
+        ThreadEval r{};
+        r.best_b = -1;
+        bool ovf = false;
+        if (live) {
           own = A.part[v];
+          e0 = A.off[v];
+          e1 = A.off[v + 1];
+          if (e1 - e0 > kTpvMaxDeg) {
+            ovf = true;
+          } else {
+            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, nullptr, -1);
+            ovf = r.overflow;
+          }
         }
-        const bool valid = live && li < d;
-        int myb = -1, myw = 0;
-        if (valid) {
-          myb = A.part[A.tgt[e0 + li]];
-          myw = A.w[e0 + li];
+        // rows too long / too many distinct blocks: the warp evaluates them
+        // one by one with the shared-memory block table
+        unsigned om = __ballot_sync(0xffffffffu, live && ovf);
+        while (om) {
+          const int l = __ffs(om) - 1;
+          om &= om - 1;
+          const int u = __shfl_sync(0xffffffffu, v, l);
+          const int ou = __shfl_sync(0xffffffffu, own, l);
+          const int sz = warp_build_table(wt, k, A.off[u], A.off[u + 1], A.tgt, A.w, A.part);
+          const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, nullptr);
+          if (lane == l) {
+            r.best_b = q.best_b;
+            r.best_gain = q.best_gain;
+            r.conn_own = q.conn_own;
+          }
         }
-        const int dmax = __reduce_max_sync(0xffffffffu, live ? d : 0);
-        VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, dmax, A.t, s_dbit, nullptr,
-                                     A.jet != 0);
         bool ok = false;
         if (live && r.best_b >= 0) {
           if (r.best_gain >= 0) ok = true;
           else if (A.jet) ok = (double)(-r.best_gain) < floor(A.jet_c * (double)r.conn_own);
         }
-        if (ok && li == 0) {
+        if (ok) {
           A.dest[v] = r.best_b;
           A.gkey[v] = r.best_gain;
         }
-        warp_append(ok && li == 0, v, A.lcand, cnt + C_CAND);
+        wq_push(qa, ok, v, A.lcand, cnt + C_CAND);
       }
-      for (long long hi = gw; hi < nh; hi += NW) {
-        const int v = A.lheavy[hi];
-        const int own = A.part[v];
-        int s = warp_build_table(wt, k, A.off[v], A.off[v + 1], A.tgt, A.w, A.part);
-        VertexEval r = eval_table(wt, s, own, A.t, s_dbit, nullptr);
-        bool ok = false;
-        if (r.best_b >= 0) {
-          if (r.best_gain >= 0) ok = true;
-          else if (A.jet) ok = (double)(-r.best_gain) < floor(A.jet_c * (double)r.conn_own);
-        }
-        if (ok && lane == 0) {
-          A.dest[v] = r.best_b;
-          A.gkey[v] = r.best_gain;
-        }
-        warp_append(ok && lane == 0, v, A.lcand, cnt + C_CAND);
-      }
+      wq_flush(qa, A.lcand, cnt + C_CAND);
       grid.sync();
+      PHASE_MARK(2);
+      // every CTA has read the previous iteration's counters by now (they
+      // were consumed before this iteration's first barrier)
+      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K10 second filter over the candidates
       const long long nc = cnt[C_CAND];
       for (long long ib = gw * GPW; ib < nc; ib += NW * GPW) {
@@ -344,14 +428,14 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         long long fut = 0;
         if (live) {
           const long long gv = A.gkey[v];
-          const unsigned long long oc = __ldg(A.t.code + A.part[v]);
-          const unsigned long long dc = __ldg(A.t.code + A.dest[v]);
+          const unsigned long long oc = T.code[A.part[v]];
+          const unsigned long long dc = T.code[A.dest[v]];
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
             int u = A.tgt[e];
             long long gu = A.gkey[u];
             bool earlier = gu > gv || (gu == gv && u < v);
             int pos = earlier ? A.dest[u] : A.part[u];
-            unsigned long long pc = __ldg(A.t.code + pos);
+            unsigned long long pc = T.code[pos];
             fut += (long long)A.w[e] * (cdist(s_dbit, oc, pc) - cdist(s_dbit, dc, pc));
           }
         }
@@ -359,9 +443,11 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
         const bool m = live && li == 0 && fut >= 0;
         if (m) tmf[v] = 1;
-        warp_append(m, v, lmov, cnt + C_MOV);
+        wq_push(qa, m, v, lmov, cnt + C_MOV);
       }
+      wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
+      PHASE_MARK(3);
     } else {
       // ---- K11 weak rebalance candidates (refinement.py:273-309)
       for (int b = threadIdx.x; b < k; b += blockDim.x) {
@@ -378,50 +464,62 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       __syncthreads();
       const int n_elig = s_nelig;
       incomplete = n_elig == 0;
-      for (long long b0 = wt0; b0 < n; b0 += GT) {  // vertices of overloaded blocks
-        const long long v = b0 + lane;
-        bool inb = false, heavy = false;
-        if (v < n && ovl[A.part[v]]) {
-          inb = true;
-          heavy = A.off[v + 1] - A.off[v] > VW;
+      long long ns = n;
+      if (!vcent) {  // vertices of overloaded blocks
+        for (long long b0 = gt - lane; b0 < n; b0 += GT) {
+          const long long v = b0 + lane;
+          const bool inb = v < n && ovl[A.part[v]];
+          wq_push(qa, inb, (int)v, A.lsmall, cnt + C_SMALL);
         }
-        warp_append(inb && !heavy, (int)v, A.lsmall, cnt + C_SMALL);
-        warp_append(inb && heavy, (int)v, A.lheavy, cnt + C_HEAVY);
+        wq_flush(qa, A.lsmall, cnt + C_SMALL);
+        grid.sync();
+        PHASE_MARK(4);
+        ns = cnt[C_SMALL];
       }
-      grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
-      const long long ns = cnt[C_SMALL], nh = cnt[C_HEAVY];
-      for (long long ib = gw * GPW; ib < ns; ib += NW * GPW) {
-        const long long idx = ib + gi;
-        const bool live = idx < ns;
-        const int v = live ? A.lsmall[idx] : 0;
-        int e0 = 0, d = 0, own = 0;
+      for (long long b0 = gt - lane; b0 < ns; b0 += GT) {
+        const long long idx = b0 + lane;
+        bool live = idx < ns;
+        int v = 0, own = 0;
         if (live) {
-          e0 = A.off[v];
-          d = A.off[v + 1] - e0;
+          v = vcent ? (int)idx : A.lsmall[idx];
           own = A.part[v];
+          live = ovl[own] != 0;
         }
-        const bool valid = live && li < d;
-        int myb = -1, myw = 0;
-        if (valid) {
-          myb = A.part[A.tgt[e0 + li]];
-          myw = A.w[e0 + li];
-        }
-        const int dmax = __reduce_max_sync(0xffffffffu, live ? d : 0);
-        VertexEval r = eval_regs<VW>(valid, live ? own : 0, myb, myw, dmax, A.t, s_dbit, elig,
-                                     false);
-        bool need = live && r.best_b < 0 && n_elig > 0;
-        unsigned any = __ballot_sync(0xffffffffu, need);
-        int tb = -1;
-        if (need) {
+        int tb = -1;  // random eligible target if no adjacent block qualifies
+        if (live && n_elig > 0) {
           unsigned long long h = hash2(A.seed, (unsigned long long)v,
                                        (unsigned long long)C.pass_counter);
           tb = elist[h % (unsigned long long)n_elig];
         }
-        long long cost = 0, cur = 0;
-        if (any) {
-          cost = cost_regs<VW>(valid && need, myb, myw, need ? tb : 0, A.t, s_dbit);
-          cur = cur_regs<VW>(valid && need, own, myb, myw, A.t, s_dbit);
+        ThreadEval r{};
+        r.best_b = -1;
+        bool ovf = false;
+        if (live) {
+          const int e0 = A.off[v], e1 = A.off[v + 1];
+          if (e1 - e0 > kTpvMaxDeg) {
+            ovf = true;
+          } else {
+            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, elig, tb);
+            ovf = r.overflow;
+          }
+        }
+        unsigned om = __ballot_sync(0xffffffffu, live && ovf);
+        while (om) {
+          const int l = __ffs(om) - 1;
+          om &= om - 1;
+          const int u = __shfl_sync(0xffffffffu, v, l);
+          const int ou = __shfl_sync(0xffffffffu, own, l);
+          const int tbl = __shfl_sync(0xffffffffu, tb, l);
+          const int sz = warp_build_table(wt, k, A.off[u], A.off[u + 1], A.tgt, A.w, A.part);
+          const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, elig);
+          long long ctb = 0;
+          if (q.best_b < 0 && tbl >= 0) ctb = cost_table(wt, sz, tbl, T, s_dbit);  // warp-uniform
+          if (lane == l) {
+            r.best_b = q.best_b;
+            r.best_gain = q.best_gain;
+            r.cur = q.cur;
+            r.cost_tb = ctb;
+          }
         }
         int target = -1;
         long long gain = 0;
@@ -429,12 +527,12 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           if (r.best_b >= 0) {
             target = r.best_b;
             gain = r.best_gain;
-          } else if (need) {
+          } else if (tb >= 0) {
             target = tb;
-            gain = cur - cost;
+            gain = r.cur - r.cost_tb;
           }
         }
-        const bool isc = li == 0 && target >= 0;
+        const bool isc = target >= 0;
         if (isc) {
           A.rtgt[v] = target;
           int cell = slot_for_gain(gain) * A.rho + v % A.rho;
@@ -442,63 +540,67 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
           atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
                     (unsigned long long)(long long)A.vw[v]);
         }
-        warp_append(isc, v, A.lcand, cnt + C_CAND);
+        wq_push(qa, isc, v, A.lcand, cnt + C_CAND);
       }
-      for (long long hi = gw; hi < nh; hi += NW) {
-        const int v = A.lheavy[hi];
-        const int own = A.part[v];
-        int s = warp_build_table(wt, k, A.off[v], A.off[v + 1], A.tgt, A.w, A.part);
-        VertexEval r = eval_table(wt, s, own, A.t, s_dbit, elig);
-        int target = -1;
-        long long gain = 0;
-        if (r.best_b >= 0) {
-          target = r.best_b;
-          gain = r.best_gain;
-        } else if (n_elig > 0) {
-          unsigned long long h = hash2(A.seed, (unsigned long long)v,
-                                       (unsigned long long)C.pass_counter);
-          target = elist[h % (unsigned long long)n_elig];
-          gain = r.cur - cost_table(wt, s, target, A.t, s_dbit);
-        }
-        const bool isc = lane == 0 && target >= 0;
-        if (isc) {
-          A.rtgt[v] = target;
-          int cell = slot_for_gain(gain) * A.rho + v % A.rho;
-          A.rcell[v] = (unsigned char)cell;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
-                    (unsigned long long)(long long)A.vw[v]);
-        }
-        warp_append(isc, v, A.lcand, cnt + C_CAND);
-      }
+      wq_flush(qa, A.lcand, cnt + C_CAND);
       // the lock set is cleared on every rebalance pass (refinement.py:425)
       for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;
       grid.sync();
+      PHASE_MARK(5);
+      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block (every
-      // CTA redundantly) and this CTA's per-block weight of c*-cell vertices
-      for (int b = threadIdx.x; b < k; b += blockDim.x) {
-        run[b] = 0;
-        if (!ovl[b]) { cstar[b] = NC; pstar[b] = 0; continue; }
+      // CTA redundantly; one warp per overloaded block, 32 cells per step with
+      // a shuffle prefix) and per-(warp, block) weights of c*-cell vertices
+      // over the warp's slice of this CTA's vertex range
+      for (int b = warp; b < k; b += kFusedWarps) {
+        if (!ovl[b]) {  // warp-uniform
+          if (lane == 0) { cstar[b] = NC; pstar[b] = 0; }
+          continue;
+        }
         const double excess = (double)A.bw[b] - A.l_max;
         long long P = 0;
-        int c = 0;
-        for (; c < NC; ++c) {
-          long long wc = A.W[(size_t)b * NC + c];
-          if ((double)(P + wc) > excess) break;
-          P += wc;
+        int c = NC;
+        for (int c0 = 0; c0 < NC; c0 += 32) {
+          const int cc = c0 + lane;
+          const long long x = cc < NC ? A.W[(size_t)b * NC + cc] : 0;
+          long long incl = x;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const unsigned over = __ballot_sync(0xffffffffu, cc < NC && (double)(P + incl) > excess);
+          if (over) {
+            const int l = __ffs(over) - 1;
+            c = c0 + l;
+            P += __shfl_sync(0xffffffffu, incl - x, l);
+            break;
+          }
+          P += __shfl_sync(0xffffffffu, incl, 31);
         }
-        cstar[b] = c;
-        pstar[b] = P;
+        if (lane == 0) { cstar[b] = c; pstar[b] = P; }
       }
+      for (int i = threadIdx.x; i < kFusedWarps * k; i += blockDim.x) wrun[i] = 0;
       __syncthreads();
-      for (int v = r0 + threadIdx.x; v < r1; v += blockDim.x) {
+      const int RW = (r1 - r0 + kFusedWarps - 1) / kFusedWarps;  // warp slice
+      const int w0 = min(r1, r0 + warp * RW), w1 = min(r1, w0 + RW);
+      for (int v = w0 + lane; v < w1; v += 32) {
         if (A.rtgt[v] < 0) continue;
         const int b = A.part[v];
-        if ((int)A.rcell[v] == cstar[b])
-          atomicAdd(reinterpret_cast<unsigned long long*>(&run[b]), (unsigned long long)(long long)A.vw[v]);
+        if ((int)A.rcell[v] == cstar[b]) atomicAdd(&wrun[warp * k + b], A.vw[v]);
       }
       __syncthreads();
-      for (int b = threadIdx.x; b < k; b += blockDim.x) A.S[(size_t)b * G + blockIdx.x] = run[b];
+      for (int b = threadIdx.x; b < k; b += blockDim.x) {  // CTA total; warp exclusive prefix
+        int acc = 0;
+        for (int w = 0; w < kFusedWarps; ++w) {
+          const int x = wrun[w * k + b];
+          wrun[w * k + b] = acc;
+          acc += x;
+        }
+        A.S[(size_t)b * G + blockIdx.x] = acc;
+      }
       grid.sync();
+      PHASE_MARK(6);
       // step B: exclusive scan of S over CTAs, one warp per block
       for (long long b = gw; b < k; b += NW) {
         long long carry = 0;
@@ -517,49 +619,49 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         }
       }
       grid.sync();
-      // step C: in-cell prefix in vertex order (warp 0 walks the CTA range),
-      // whole cells before c* everywhere else
+      PHASE_MARK(7);
+      // step C: in-cell prefix in vertex order — every warp walks its slice
+      // with __match_any_sync ranking, starting from (earlier CTAs) +
+      // (earlier warps of this CTA); whole cells before c* everywhere else
       for (int b = threadIdx.x; b < k; b += blockDim.x) run[b] = A.S[(size_t)b * G + blockIdx.x];
       __syncthreads();
-      if (warp == 0) {
-        for (int v0 = r0; v0 < r1; v0 += 32) {
-          const int v = v0 + lane;
-          bool partial = false;
-          int b = 0;
-          long long wv = 0;
-          if (v < r1 && A.rtgt[v] >= 0) {
-            b = A.part[v];
-            partial = (int)A.rcell[v] == cstar[b];
-            wv = A.vw[v];
-          }
-          const unsigned act = __ballot_sync(0xffffffffu, partial);
-          bool take = false;
-          if (partial) {
-            const unsigned peers = __match_any_sync(act, b);
-            const int leader = __ffs(peers) - 1;
-            long long before = 0, total = 0;
-            unsigned mm = peers;
-            while (mm) {
-              const int l = __ffs(mm) - 1;
-              mm &= mm - 1;
-              const long long x = __shfl_sync(peers, wv, l);
-              if (l < lane) before += x;
-              total += x;
-            }
-            const double excess = (double)A.bw[b] - A.l_max;
-            take = (double)(pstar[b] + run[b] + before) < excess;
-            __syncwarp(peers);
-            if (lane == leader) run[b] += total;
-          }
-          if (take) {
-            tmf[v] = 1;
-            A.dest[v] = A.rtgt[v];
-          }
-          warp_append(take, v, lmov, cnt + C_MOV);
+      for (int v0 = w0; v0 < w1; v0 += 32) {  // warp-uniform
+        const int v = v0 + lane;
+        bool partial = false;
+        int b = 0;
+        int wv = 0;
+        if (v < w1 && A.rtgt[v] >= 0) {
+          b = A.part[v];
+          partial = (int)A.rcell[v] == cstar[b];
+          wv = A.vw[v];
         }
+        const unsigned act = __ballot_sync(0xffffffffu, partial);
+        bool take = false;
+        if (partial) {
+          const unsigned peers = __match_any_sync(act, b);
+          const int leader = __ffs(peers) - 1;
+          long long before = 0, total = 0;
+          unsigned mm = peers;
+          while (mm) {
+            const int l = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const long long x = __shfl_sync(peers, (long long)wv, l);
+            if (l < (int)lane) before += x;
+            total += x;
+          }
+          const double excess = (double)A.bw[b] - A.l_max;
+          take = (double)(pstar[b] + run[b] + wrun[warp * k + b] + before) < excess;
+          __syncwarp(peers);
+          if ((int)lane == leader) wrun[warp * k + b] += (int)total;
+        }
+        if (take) {
+          tmf[v] = 1;
+          A.dest[v] = A.rtgt[v];
+        }
+        wq_push(qa, take, v, lmov, cnt + C_MOV);
       }
       const long long nc = cnt[C_CAND];
-      for (long long b0 = wt0; b0 < nc; b0 += GT) {
+      for (long long b0 = gt - lane; b0 < nc; b0 += GT) {
         const long long idx = b0 + lane;
         bool take = false;
         int v = 0;
@@ -571,9 +673,11 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
             A.dest[v] = A.rtgt[v];
           }
         }
-        warp_append(take, v, lmov, cnt + C_MOV);
+        wq_push(qa, take, v, lmov, cnt + C_MOV);
       }
+      wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
+      PHASE_MARK(8);
     }
     // ---- K13 apply moves over the movers: exact dJ + block weights
     {
@@ -584,14 +688,14 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
         if (idx < nm) {
           const int v = lmov[idx];
           const int ov = A.part[v], nv = A.dest[v];
-          const unsigned long long oc = __ldg(A.t.code + ov), nc = __ldg(A.t.code + nv);
+          const unsigned long long oc = T.code[ov], nc = T.code[nv];
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
             const int u = A.tgt[e];
             const bool um = tmf[u];
             const int ou = A.part[u];
             const int nu = um ? A.dest[u] : ou;
-            const long long dd = cdist(s_dbit, nc, __ldg(A.t.code + nu)) -
-                                 cdist(s_dbit, oc, __ldg(A.t.code + ou));
+            const long long dd = cdist(s_dbit, nc, T.code[nu]) -
+                                 cdist(s_dbit, oc, T.code[ou]);
             acc += (long long)A.w[e] * dd * (um ? 1 : 2);
           }
           if (li == 0 && ov != nv) {
@@ -605,6 +709,7 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
     }
     grid.sync();
+      PHASE_MARK(9);
     // ---- commit + restore the list invariants
     {
       const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
@@ -622,6 +727,7 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       }
     }
     grid.sync();
+      PHASE_MARK(10);
     // ---- Alg. 4 control (refinement.py:433-463), replicated per CTA
     const long long mx = block_max_bw(A.bw, k);
     if (threadIdx.x == 0) {
@@ -673,6 +779,7 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
       C.it++;
     }
     __syncthreads();
+    PHASE_MARK(11);
     if (C.brk) break;
     if (C.take) {
       for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
@@ -710,6 +817,95 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   }
 }
 
+template <int VW>
+__global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
+  refine_body<VW>(A);
+}
+
+// Shared-memory-resident refinement of a small graph: ONE CTA copies the
+// CSR, the mapping and every per-vertex work array into shared memory and
+// runs the same Alg. 4 loop on them (generic pointers), so every gather in
+// the latency-bound phases is a shared-memory access instead of an L2 round
+// trip.  Layout after the regular dynamic region (A.smem_base bytes):
+//   int64: gkey[n] bw[k] best_bw[k] W[k*NC] S[k] ctr[17]
+//   int32: off[n+1] tgt[m2] w[m2] vw[n] part[n] best[n] dest[n] rtgt[n]
+//          lheavy[n] lcand[n] lmov0[n] lmov1[n]
+//   uint8: flags0[n] flags1[n] rcell[n]
+template <int VW>
+__global__ void __launch_bounds__(kFusedBlock) k_refine_smem(FusedArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ FusedArgs SA;
+  const int n = A.n, k = A.k, NC = 31 * A.rho;
+  const long long m2 = A.m2;
+  long long* q = reinterpret_cast<long long*>(dsm + A.smem_base);
+  long long* gkey = q;
+  long long* bw = gkey + n;
+  long long* best_bw = bw + k;
+  long long* W = best_bw + k;
+  long long* S = W + (size_t)k * NC;
+  long long* ctr = S + k;
+  int* ip = reinterpret_cast<int*>(ctr + 17);
+  int* off = ip;
+  int* tgt = off + n + 1;
+  int* w = tgt + m2;
+  int* vw = w + m2;
+  int* part = vw + n;
+  int* best = part + n;
+  int* dest = best + n;
+  int* rtgt = dest + n;
+  int* lheavy = rtgt + n;
+  int* lcand = lheavy + n;
+  int* lmov0 = lcand + n;
+  int* lmov1 = lmov0 + n;
+  unsigned char* f0 = reinterpret_cast<unsigned char*>(lmov1 + n);
+  unsigned char* f1 = f0 + n;
+  unsigned char* rcell = f1 + n;
+  const bool first = !A.st->started;
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) off[i] = A.off[i];
+  for (long long e = threadIdx.x; e < m2; e += blockDim.x) {
+    tgt[e] = A.tgt[e];
+    w[e] = A.w[e];
+  }
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    vw[v] = A.vw[v];
+    part[v] = A.part[v];
+    if (!first) best[v] = A.best[v];
+  }
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {
+    bw[b] = A.bw[b];
+    if (!first) best_bw[b] = A.best_bw[b];
+  }
+  for (int i = threadIdx.x; i < 17; i += blockDim.x) ctr[i] = 0;
+  if (threadIdx.x == 0) {
+    SA = A;
+    SA.off = off; SA.tgt = tgt; SA.w = w; SA.vw = vw; SA.src = nullptr;
+    SA.part = part; SA.bw = bw; SA.best = best; SA.best_bw = best_bw;
+    SA.dest = dest; SA.gkey = gkey; SA.flags0 = f0; SA.flags1 = f1;
+    SA.rtgt = rtgt; SA.rcell = rcell; SA.bstamp = nullptr; SA.lsmall = nullptr;
+    SA.lheavy = lheavy; SA.lcand = lcand; SA.lmov0 = lmov0; SA.lmov1 = lmov1;
+    SA.W = W; SA.S = S; SA.ctr = ctr;
+    SA.bar_mode = 0;
+  }
+  __syncthreads();
+  refine_body<VW>(SA);
+  __syncthreads();
+  const bool yielded = A.st->status != 0;  // strong pass due: the host needs everything
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    A.part[v] = part[v];
+    if (yielded) A.best[v] = best[v];
+  }
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {
+    A.bw[b] = bw[b];
+    if (yielded) A.best_bw[b] = best_bw[b];
+  }
+}
+
+// shared-memory bytes of k_refine_smem beyond the regular dynamic region
+static size_t smem_resident_bytes(long long n, long long m2, int k, int NC) {
+  return 8 * ((size_t)n + 2 * (size_t)k + (size_t)k * NC + (size_t)k + 17) +
+         4 * ((size_t)n + 1 + 2 * (size_t)m2 + 11 * (size_t)n) + 3 * (size_t)n;
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -742,7 +938,60 @@ static int cluster_vertices_per_cta() {
   static const int v = [] {
     const char* e = std::getenv("GIM_CLUSTER_VPC");
     int x = e ? std::atoi(e) : 0;
-    return x > 0 ? x : 512;
+    return x > 0 ? x : 256;
+  }();
+  return v;
+}
+
+// graphs up to this many vertices (and fitting) refine shared-memory
+// resident in one CTA (GIM_SMEM_MAXN overrides; 0 disables)
+static long long smem_max_n() {
+  static const long long v = [] {
+    const char* e = std::getenv("GIM_SMEM_MAXN");
+    return e ? std::atoll(e) : 1000ll;
+  }();
+  return v;
+}
+
+// dynamic shared memory available to k_refine_smem<VW> (opt-in maximum
+// minus its static shared memory); sets the attribute once per device
+template <int VW>
+static size_t smem_dyn_limit_vw() {
+  static std::mutex mu;
+  static std::map<int, size_t> cache;
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int optin = 0;
+  GIM_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  GIM_CUDA(cudaFuncGetAttributes(&fa, k_refine_smem<VW>));
+  const size_t lim = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+  GIM_CUDA(cudaFuncSetAttribute(k_refine_smem<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)lim));
+  cache.emplace(dev, lim);
+  return lim;
+}
+
+struct VWDISPATCH {};
+template <class>
+static size_t smem_dyn_limit(int vw) {
+  switch (vw) {
+    case 4: return smem_dyn_limit_vw<4>();
+    case 8: return smem_dyn_limit_vw<8>();
+    case 16: return smem_dyn_limit_vw<16>();
+    default: return smem_dyn_limit_vw<32>();
+  }
+}
+
+// vertices per CTA of a cooperative-grid refinement (GIM_COOP_VPC overrides)
+static int coop_vpc() {
+  static const int v = [] {
+    const char* e = std::getenv("GIM_COOP_VPC");
+    int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : 128;
   }();
   return v;
 }
@@ -756,7 +1005,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   const DevGraph& g = L.g;
   const int k = t.k;
   const int NC = 31 * cfg.rho;
-  size_t smem = (size_t)kFusedWarps * 3 * k * sizeof(int) + (size_t)k * (8 + 8 + 4 + 4 + 1 + 1);
+  size_t smem = (size_t)kFusedWarps * 4 * k * sizeof(int) + (size_t)k * (8 + 8 + 8 + 4 + 4 + 1 + 1);
   smem = (smem + 15) & ~(size_t)15;
   int maxb = 0;
   switch (L.vw) {
@@ -770,14 +1019,19 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   // otherwise ~1K vertices per CTA, at most one full co-resident wave
   const int vpc = cluster_vertices_per_cta();
   int G, mode;
-  if (g.n <= (long long)vpc) {
+  const size_t extra = smem_resident_bytes(g.n, g.m2, k, NC);
+  if (g.n <= smem_max_n() && smem + extra <= smem_dyn_limit<VWDISPATCH>(L.vw)) {
+    G = 1;
+    mode = 3;
+  } else if (g.n <= (long long)vpc) {
     G = 1;
     mode = 0;
   } else if (g.n <= (long long)vpc * kMaxCluster) {
     G = (g.n + vpc - 1) / vpc;
     mode = 1;
   } else {
-    G = (int)std::min<long long>((long long)maxb, ((long long)g.n + 1023) / 1024);
+    G = (int)std::min<long long>((long long)maxb,
+                                 ((long long)g.n + coop_vpc() - 1) / coop_vpc());
     mode = 2;
   }
   if (fb.S_cap < (long long)G * k) {
@@ -818,7 +1072,9 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.S = fb.S.get();
   A.ctr = fb.ctr;
   A.st = fb.state;
-  A.bar_mode = mode;
+  A.bar_mode = mode == 3 ? 0 : mode;
+  A.smem_base = (int)smem;
+  A.ptime = nullptr;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
   A.phi = cfg.phi;
@@ -836,11 +1092,32 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     case 16: fn = (void*)k_refine_fused<16>; break;
     default: fn = (void*)k_refine_fused<32>; break;
   }
+  static const bool trace = std::getenv("GIM_TRACE_REFINE") != nullptr;
+  cudaEvent_t te[2];
+  DBuf<long long> ptime;
+  if (trace) {
+    ptime = DBuf<long long>(16, s);
+    GIM_CUDA(cudaMemsetAsync(ptime.get(), 0, 16 * sizeof(long long), s));
+    A.ptime = ptime.get();
+    GIM_CUDA(cudaEventCreate(&te[0]));
+    GIM_CUDA(cudaEventCreate(&te[1]));
+    GIM_CUDA(cudaEventRecord(te[0], s));
+  }
+  const long long it0 = fb.lp_seen + fb.weak_seen, lp0 = fb.lp_seen;
   {
     // one launch = many Alg. 4 iterations; per-iteration algorithmic bytes
     // are accounted by the host from the iteration count
     ProfScope prof(P_LP_EVAL, 0.0, s);
-    if (mode == 0) {
+    if (mode == 3) {
+      void* fs = nullptr;
+      switch (L.vw) {
+        case 4: fs = (void*)k_refine_smem<4>; break;
+        case 8: fs = (void*)k_refine_smem<8>; break;
+        case 16: fs = (void*)k_refine_smem<16>; break;
+        default: fs = (void*)k_refine_smem<32>; break;
+      }
+      GIM_CUDA(cudaLaunchKernel(fs, dim3(1), dim3(kFusedBlock), args, smem + extra, s));
+    } else if (mode == 0) {
       GIM_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kFusedBlock), args, smem, s));
     } else if (mode == 1) {
       cudaLaunchConfig_t lc{};
@@ -866,6 +1143,24 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
                  (12.0 * (double)g.m2 + 8.0 * (double)g.n);
     fb.lp_seen = fb.h_state->lp;
     fb.weak_seen = fb.h_state->weak;
+  }
+  if (trace) {
+    GIM_CUDA(cudaEventRecord(te[1], s));
+    GIM_CUDA(cudaEventSynchronize(te[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, te[0], te[1]);
+    const long long its = fb.lp_seen + fb.weak_seen - it0;
+    long long pt[16];
+    GIM_CUDA(cudaMemcpy(pt, ptime.get(), sizeof(pt), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "refine n=%d m2=%lld k=%d G=%d mode=%d iters=%lld lp=%lld ms=%.3f us/iter=%.1f |",
+                 g.n, g.m2, k, G, mode, its, fb.lp_seen - lp0, ms,
+                 its ? 1000.0 * ms / (double)its : 0.0);
+    static const char* nm[12] = {"stamp", "blist", "ff", "sf", "wlist", "wcand", "wA", "wB",
+                                 "wsel", "apply", "commit", "ctl"};
+    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.1f", nm[i], pt[i] / 1000.0);
+    std::fprintf(stderr, "\n");
+    cudaEventDestroy(te[0]);
+    cudaEventDestroy(te[1]);
   }
   return fb.h_state->status == 0;
 }

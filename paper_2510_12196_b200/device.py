@@ -323,7 +323,8 @@ PROF_CLASSES = ("jeval", "hem", "contract", "lp_eval", "lp_second", "apply", "re
 
 def stats_dict(st: _lib.GimImStats) -> dict:
     d = {f: getattr(st, f) for f, _ in _lib.GimImStats._fields_
-         if f not in ("level_n", "level_m2", "prof_ms", "prof_bytes", "prof_count")}
+         if f not in ("level_n", "level_m2", "prof_ms", "prof_bytes", "prof_count", "top_class",
+                     "top_ms", "top_bytes")}
     d["level_n"] = [st.level_n[i] for i in range(min(st.n_levels, 64))]
     d["level_m2"] = [st.level_m2[i] for i in range(min(st.n_levels, 64))]
     prof = {}
@@ -332,6 +333,8 @@ def stats_dict(st: _lib.GimImStats) -> dict:
             prof[name] = {"ms": st.prof_ms[i], "bytes": st.prof_bytes[i],
                           "count": st.prof_count[i]}
     d["profile"] = prof
+    d["top_launch"] = ({"class": PROF_CLASSES[st.top_class], "ms": st.top_ms,
+                        "bytes": st.top_bytes} if 0 <= st.top_class < len(PROF_CLASSES) else None)
     return d
 
 

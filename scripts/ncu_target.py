@@ -4,6 +4,10 @@
                 window (launch list / per-kernel share of a step)
   --mode lp   : warm-up map, then the level-0 LP / J / HEM / contraction
                 kernels on the final mapping inside the window (full sets)
+  --mode refine0 : warm-up map, then ONE device-resident Alg. 4 refinement
+                (k_refine_fused) of the finest level inside the window,
+                started from the final mapping with 2% of the vertices moved
+                to random blocks (LP + weak-rebalance work as on level 0)
 """
 import argparse
 import sys
@@ -20,7 +24,7 @@ H, DIST = (4, 8, 6), (1, 10, 100)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", choices=["step", "lp"], default="step")
+    ap.add_argument("--mode", choices=["step", "lp", "refine0"], default="step")
     ap.add_argument("--logn", type=int, default=20)
     args = ap.parse_args()
     g = gen_rgg(1 << args.logn, 0.55, 1)
@@ -31,6 +35,23 @@ def main():
     if args.mode == "step":
         prof.start()
         D.integrated_map_device(dg, H, DIST, 0.03, 1)
+        torch.cuda.synchronize()
+        prof.stop()
+    elif args.mode == "refine0":
+        k = 1
+        for x in H:
+            k *= x
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        idx = torch.randperm(dg.n, device="cuda", generator=gen)[: dg.n // 50]
+        a = a.clone()
+        a[idx] = torch.randint(0, k, (idx.numel(),), device="cuda", dtype=torch.int32,
+                               generator=gen)
+        bw2 = D.block_weights(dg, a, k)
+        l_max = 1.03 * dg.total_weight / k
+        torch.cuda.synchronize()
+        prof.start()
+        D.refine(dg, H, DIST, a, bw2, i_max=12, i_w_max=10, sigma_fraction=0.005, seed=3,
+                 l_max=l_max)
         torch.cuda.synchronize()
         prof.stop()
     else:

@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--no-fanout", action="store_true")
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--seeds", type=int, nargs="+", default=[0])
+    ap.add_argument("--no-host", action="store_true")
     args = ap.parse_args()
     D.set_fanout(not args.no_fanout)
     D.set_profiling(args.profile)
@@ -27,13 +29,17 @@ def main():
         g = gen_rgg(1 << logn, 0.55, 1)
         print(f"gen 2^{logn}: n={g.n} m={g.m} {time.time()-t0:.1f}s", flush=True)
         dg = D.DeviceGraph.from_host(g)
-        for r in range(args.reps):
-            torch.cuda.synchronize()
-            t0 = time.time()
-            a, bw, st = D.integrated_map_device(dg, h, d, 0.03, 0)
-            torch.cuda.synchronize()
-            wall = time.time() - t0
-            print(json.dumps({"logn": logn, "rep": r, "wall_s": wall, **st}), flush=True)
+        for seed in args.seeds:
+            for r in range(args.reps):
+                torch.cuda.synchronize()
+                t0 = time.time()
+                a, bw, st = D.integrated_map_device(dg, h, d, 0.03, seed)
+                torch.cuda.synchronize()
+                wall = time.time() - t0
+                print(json.dumps({"logn": logn, "seed": seed, "rep": r, "wall_s": wall, **st}),
+                      flush=True)
+        if args.no_host:
+            continue
         t0 = time.time()
         ah, bwh, st = D.integrated_map_host(g.offsets, g.edge_targets, g.edge_weights,
                                             g.vertex_weights, h, d, 0.03, 0)
