@@ -152,28 +152,44 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
     cw[j] = 0;
   }
   int cnt = 0;
-  for (int e = e0; e < e1; ++e) {
-    const int b = part[tgt[e]];
-    const long long ww = w[e];
-    bool found = false;
+  // rows in chunks of 4: the target / weight loads and then the block
+  // gathers of a chunk are independent, so they overlap
+  for (int e = e0; e < e1; e += 4) {
+    int tg[4], wg[4], pb[4];
 #pragma unroll
-    for (int j = 0; j < TPV_DISTINCT; ++j)
-      if (nb[j] == b) {
-        cw[j] += ww;
-        found = true;
+    for (int q = 0; q < 4; ++q)
+      if (e + q < e1) {
+        tg[q] = tgt[e + q];
+        wg[q] = w[e + q];
       }
-    if (!found) {
-      if (cnt == TPV_DISTINCT) {
-        r.overflow = true;
-        return r;
-      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (e + q < e1) pb[q] = part[tg[q]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (e + q >= e1) break;
+      const int b = pb[q];
+      const long long ww = wg[q];
+      bool found = false;
 #pragma unroll
       for (int j = 0; j < TPV_DISTINCT; ++j)
-        if (j == cnt) {
-          nb[j] = b;
-          cw[j] = ww;
+        if (nb[j] == b) {
+          cw[j] += ww;
+          found = true;
         }
-      ++cnt;
+      if (!found) {
+        if (cnt == TPV_DISTINCT) {
+          r.overflow = true;
+          return r;
+        }
+#pragma unroll
+        for (int j = 0; j < TPV_DISTINCT; ++j)
+          if (j == cnt) {
+            nb[j] = b;
+            cw[j] = ww;
+          }
+        ++cnt;
+      }
     }
   }
   unsigned long long code[TPV_DISTINCT];

@@ -191,7 +191,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   extern __shared__ unsigned char dsm[];
   __shared__ long long s_dbit[64];
   __shared__ Ctl C;
-  __shared__ int s_nelig;
+  __shared__ int s_nelig, s_novl;
+  __shared__ long long scan_tot[kFusedWarps];
   __shared__ int qbuf[kFusedWarps * 2 * kQueueCap];
   const int k = A.k;
   const int NC = 31 * A.rho;
@@ -205,7 +206,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   int* tables = reinterpret_cast<int*>(s_code + k);
   int* elist = tables + (size_t)kFusedWarps * 3 * k;
   int* cstar = elist + k;
-  int* wrun = cstar + k;
+  int* olist = cstar + k;
+  int* wrun = olist + k;
   unsigned char* ovl = reinterpret_cast<unsigned char*>(wrun + (size_t)kFusedWarps * k);
   unsigned char* elig = ovl + k;
 
@@ -455,11 +457,22 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         elig[b] = (double)A.bw[b] < A.sigma;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {  // ascending eligible list
-        int ne = 0;
-        for (int b = 0; b < k; ++b)
-          if (elig[b]) elist[ne++] = b;
-        s_nelig = ne;
+      if (warp == 0) {  // ascending eligible / overloaded lists (ballot compaction)
+        int ne = 0, no = 0;
+        for (int b0 = 0; b0 < k; b0 += 32) {
+          const int b = b0 + lane;
+          const bool e = b < k && elig[b], o = b < k && ovl[b];
+          const unsigned me = __ballot_sync(0xffffffffu, e), mo = __ballot_sync(0xffffffffu, o);
+          const unsigned lt = (1u << lane) - 1u;
+          if (e) elist[ne + __popc(me & lt)] = b;
+          if (o) olist[no + __popc(mo & lt)] = b;
+          ne += __popc(me);
+          no += __popc(mo);
+        }
+        if (lane == 0) {
+          s_nelig = ne;
+          s_novl = no;
+        }
       }
       __syncthreads();
       const int n_elig = s_nelig;
@@ -549,34 +562,46 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       PHASE_MARK(5);
       if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block (every
-      // CTA redundantly; one warp per overloaded block, 32 cells per step with
-      // a shuffle prefix) and per-(warp, block) weights of c*-cell vertices
-      // over the warp's slice of this CTA's vertex range
-      for (int b = warp; b < k; b += kFusedWarps) {
-        if (!ovl[b]) {  // warp-uniform
-          if (lane == 0) { cstar[b] = NC; pstar[b] = 0; }
-          continue;
-        }
+      // CTA redundantly; one warp per overloaded block, all cell chunks
+      // loaded before the shuffle prefix) and per-(warp, block) weights of
+      // c*-cell vertices over the warp's slice of this CTA's vertex range.
+      // Only overloaded blocks have a c* cell (cstar = NC elsewhere).
+      const int n_ovl = s_novl;
+      for (int b = threadIdx.x; b < k; b += blockDim.x) {
+        cstar[b] = NC;
+        pstar[b] = 0;
+      }
+      __syncthreads();
+      for (int i = warp; i < n_ovl; i += kFusedWarps) {
+        const int b = olist[i];
         const double excess = (double)A.bw[b] - A.l_max;
+        constexpr int kMaxChunks = 8;  // NC = 31 * rho <= 248
+        long long x[kMaxChunks];
+#pragma unroll
+        for (int h = 0; h < kMaxChunks; ++h) {
+          const int cc = h * 32 + lane;
+          x[h] = cc < NC ? A.W[(size_t)b * NC + cc] : 0;
+        }
         long long P = 0;
         int c = NC;
-        for (int c0 = 0; c0 < NC; c0 += 32) {
-          const int cc = c0 + lane;
-          const long long x = cc < NC ? A.W[(size_t)b * NC + cc] : 0;
-          long long incl = x;
+#pragma unroll
+        for (int h = 0; h < kMaxChunks; ++h) {
+          if (h * 32 >= NC || c < NC) break;  // warp-uniform
+          long long incl = x[h];
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const long long y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
           }
+          const int cc = h * 32 + lane;
           const unsigned over = __ballot_sync(0xffffffffu, cc < NC && (double)(P + incl) > excess);
           if (over) {
             const int l = __ffs(over) - 1;
-            c = c0 + l;
-            P += __shfl_sync(0xffffffffu, incl - x, l);
-            break;
+            c = h * 32 + l;
+            P += __shfl_sync(0xffffffffu, incl - x[h], l);
+          } else {
+            P += __shfl_sync(0xffffffffu, incl, 31);
           }
-          P += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (lane == 0) { cstar[b] = c; pstar[b] = P; }
       }
@@ -584,13 +609,16 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       __syncthreads();
       const int RW = (r1 - r0 + kFusedWarps - 1) / kFusedWarps;  // warp slice
       const int w0 = min(r1, r0 + warp * RW), w1 = min(r1, w0 + RW);
-      for (int v = w0 + lane; v < w1; v += 32) {
-        if (A.rtgt[v] < 0) continue;
-        const int b = A.part[v];
-        if ((int)A.rcell[v] == cstar[b]) atomicAdd(&wrun[warp * k + b], A.vw[v]);
+      if (n_ovl > 0) {
+        for (int v = w0 + lane; v < w1; v += 32) {
+          if (A.rtgt[v] < 0) continue;
+          const int b = A.part[v];
+          if ((int)A.rcell[v] == cstar[b]) atomicAdd(&wrun[warp * k + b], A.vw[v]);
+        }
       }
       __syncthreads();
-      for (int b = threadIdx.x; b < k; b += blockDim.x) {  // CTA total; warp exclusive prefix
+      for (int i = threadIdx.x; i < n_ovl; i += blockDim.x) {  // CTA total; warp prefix
+        const int b = olist[i];
         int acc = 0;
         for (int w = 0; w < kFusedWarps; ++w) {
           const int x = wrun[w * k + b];
@@ -601,29 +629,48 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       }
       grid.sync();
       PHASE_MARK(6);
-      // step B: exclusive scan of S over CTAs, one warp per block
-      for (long long b = gw; b < k; b += NW) {
-        long long carry = 0;
-        long long* row = A.S + (size_t)b * G;
-        for (int c0 = 0; c0 < G; c0 += 32) {
-          const int c = c0 + lane;
-          long long x = c < G ? row[c] : 0;
-          long long incl = x;
+      // step B: exclusive scan of S over CTAs for every overloaded block,
+      // one CTA per row (<= 3 entries per thread + a block-wide scan)
+      for (int i = blockIdx.x; i < n_ovl; i += G) {
+        long long* row = A.S + (size_t)olist[i] * G;
+        const int E = (G + kFusedBlock - 1) / kFusedBlock;  // <= 3
+        const int c0 = threadIdx.x * E;
+        long long v3[3] = {0, 0, 0};
+        long long tsum = 0;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+        for (int j = 0; j < 3; ++j)
+          if (j < E && c0 + j < G) {
+            v3[j] = row[c0 + j];
+            tsum += v3[j];
           }
-          if (c < G) row[c] = carry + incl - x;
-          carry += __shfl_sync(0xffffffffu, incl, 31);
+        long long incl = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
+        if (lane == 31) scan_tot[warp] = incl;
+        __syncthreads();
+        long long base = 0;
+        for (int w = 0; w < warp; ++w) base += scan_tot[w];
+        long long run_ex = base + incl - tsum;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j < E && c0 + j < G) {
+            row[c0 + j] = run_ex;
+            run_ex += v3[j];
+          }
+        __syncthreads();
       }
       grid.sync();
       PHASE_MARK(7);
       // step C: in-cell prefix in vertex order — every warp walks its slice
       // with __match_any_sync ranking, starting from (earlier CTAs) +
       // (earlier warps of this CTA); whole cells before c* everywhere else
-      for (int b = threadIdx.x; b < k; b += blockDim.x) run[b] = A.S[(size_t)b * G + blockIdx.x];
+      for (int i = threadIdx.x; i < n_ovl; i += blockDim.x) {
+        const int b = olist[i];
+        run[b] = A.S[(size_t)b * G + blockIdx.x];
+      }
       __syncthreads();
       for (int v0 = w0; v0 < w1; v0 += 32) {  // warp-uniform
         const int v = v0 + lane;
@@ -1005,7 +1052,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   const DevGraph& g = L.g;
   const int k = t.k;
   const int NC = 31 * cfg.rho;
-  size_t smem = (size_t)kFusedWarps * 4 * k * sizeof(int) + (size_t)k * (8 + 8 + 8 + 4 + 4 + 1 + 1);
+  size_t smem = (size_t)kFusedWarps * 4 * k * sizeof(int) + (size_t)k * (8 + 8 + 8 + 4 + 4 + 4 + 1 + 1);
   smem = (smem + 15) & ~(size_t)15;
   int maxb = 0;
   switch (L.vw) {
