@@ -92,6 +92,7 @@ struct FusedArgs {
   FusedState* st;
   int bar_mode;        // GridBarrier mode
   int smem_base;       // k_refine_smem: bytes of the regular dynamic region
+  int vc_steps;        // vertex-centric first filters up to vc_steps vertices per thread
   long long* ptime;    // [16] per-phase ns (trace mode) or null
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
@@ -333,7 +334,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     // thread-per-vertex first filters straight over the vertex range when
     // the level is small; otherwise an edge-parallel boundary pass + a
     // compact list first (more memory-level parallelism for large levels)
-    const bool vcent = A.src == nullptr || (long long)n <= (long long)kVcSteps * GT;
+    const bool vcent = A.src == nullptr || (long long)n <= (long long)A.vc_steps * GT;
     WarpQueue qa{qbuf + warp * 2 * kQueueCap, 0}, qb{qbuf + (warp * 2 + 1) * kQueueCap, 0};
     if (balanced_now) {
       // ---- K9 first filter (refinement.py:201-244)
@@ -609,11 +610,33 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       __syncthreads();
       const int RW = (r1 - r0 + kFusedWarps - 1) / kFusedWarps;  // warp slice
       const int w0 = min(r1, r0 + warp * RW), w1 = min(r1, w0 + RW);
+      // the c*-cell ("partial") candidates of the warp's slice, in vertex
+      // order, are compacted into lheavy[w0 ..) for the walk in step C
+      int n_part = 0;
       if (n_ovl > 0) {
-        for (int v = w0 + lane; v < w1; v += 32) {
-          if (A.rtgt[v] < 0) continue;
-          const int b = A.part[v];
-          if ((int)A.rcell[v] == cstar[b]) atomicAdd(&wrun[warp * k + b], A.vw[v]);
+        const unsigned lt = (1u << lane) - 1u;
+        for (int v0 = w0; v0 < w1; v0 += 64) {  // warp-uniform, two chunks in flight
+          const int va = v0 + lane, vb = v0 + 32 + lane;
+          const int ta = va < w1 ? A.rtgt[va] : -1;
+          const int tb2 = vb < w1 ? A.rtgt[vb] : -1;
+          bool pa = false, pb = false;
+          int ba = 0, bb = 0;
+          if (ta >= 0) {
+            ba = A.part[va];
+            pa = (int)A.rcell[va] == cstar[ba];
+          }
+          if (tb2 >= 0) {
+            bb = A.part[vb];
+            pb = (int)A.rcell[vb] == cstar[bb];
+          }
+          if (pa) atomicAdd(&wrun[warp * k + ba], A.vw[va]);
+          if (pb) atomicAdd(&wrun[warp * k + bb], A.vw[vb]);
+          const unsigned ma = __ballot_sync(0xffffffffu, pa);
+          if (pa) A.lheavy[w0 + n_part + __popc(ma & lt)] = va;
+          n_part += __popc(ma);
+          const unsigned mb = __ballot_sync(0xffffffffu, pb);
+          if (pb) A.lheavy[w0 + n_part + __popc(mb & lt)] = vb;
+          n_part += __popc(mb);
         }
       }
       __syncthreads();
@@ -672,14 +695,15 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         run[b] = A.S[(size_t)b * G + blockIdx.x];
       }
       __syncthreads();
-      for (int v0 = w0; v0 < w1; v0 += 32) {  // warp-uniform
-        const int v = v0 + lane;
+      for (int i0 = 0; i0 < n_part; i0 += 32) {  // warp-uniform, listed partials only
+        const bool live = i0 + lane < n_part;
+        const int v = live ? A.lheavy[w0 + i0 + lane] : 0;
         bool partial = false;
         int b = 0;
         int wv = 0;
-        if (v < w1 && A.rtgt[v] >= 0) {
+        if (live) {
           b = A.part[v];
-          partial = (int)A.rcell[v] == cstar[b];
+          partial = true;
           wv = A.vw[v];
         }
         const unsigned act = __ballot_sync(0xffffffffu, partial);
@@ -1033,6 +1057,17 @@ static size_t smem_dyn_limit(int vw) {
   }
 }
 
+// vertex-centric first filters while a level has at most this many
+// vertices per thread (GIM_VC_STEPS overrides)
+static int vc_steps() {
+  static const int v = [] {
+    const char* e = std::getenv("GIM_VC_STEPS");
+    int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : kVcSteps;
+  }();
+  return v;
+}
+
 // vertices per CTA of a cooperative-grid refinement (GIM_COOP_VPC overrides)
 static int coop_vpc() {
   static const int v = [] {
@@ -1121,6 +1156,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.st = fb.state;
   A.bar_mode = mode == 3 ? 0 : mode;
   A.smem_base = (int)smem;
+  A.vc_steps = vc_steps();
   A.ptime = nullptr;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
