@@ -125,7 +125,7 @@ __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, in
 // handed to the warp-per-vertex table path.  `tb` >= 0 also returns the
 // cost of moving to tb (rebalance fallback target).
 
-constexpr int TPV_DISTINCT = 8;
+constexpr int TPV_DISTINCT = 4;
 
 struct ThreadEval {
   long long cur, conn_own, best_gain, cost_tb;
@@ -193,25 +193,33 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
     }
   }
   unsigned long long code[TPV_DISTINCT];
-#pragma unroll
-  for (int j = 0; j < TPV_DISTINCT; ++j) code[j] = j < cnt ? t.code[nb[j]] : 0ull;
+  bool adm[TPV_DISTINCT];
+  bool any = false;
   const unsigned long long oc = t.code[own];
-  const unsigned long long tc = tb >= 0 ? t.code[tb] : 0ull;
 #pragma unroll
   for (int j = 0; j < TPV_DISTINCT; ++j) {
+    code[j] = j < cnt ? t.code[nb[j]] : oc;
+    adm[j] = j < cnt && nb[j] != own && (allowed == nullptr || allowed[nb[j]]);
+    any |= adm[j];
     if (j < cnt) {
       r.cur += cw[j] * cdist(s_dbit, oc, code[j]);
       if (nb[j] == own) r.conn_own = cw[j];
-      if (tb >= 0) r.cost_tb += cw[j] * cdist(s_dbit, tc, code[j]);
     }
   }
+  if (tb >= 0) {
+    const unsigned long long tc = t.code[tb];
+#pragma unroll
+    for (int j = 0; j < TPV_DISTINCT; ++j)
+      if (j < cnt) r.cost_tb += cw[j] * cdist(s_dbit, tc, code[j]);
+  }
+  if (!any) return r;  // interior vertex / nothing admissible: no candidate
 #pragma unroll
   for (int i = 0; i < TPV_DISTINCT; ++i) {
-    if (i < cnt && nb[i] != own && (allowed == nullptr || allowed[nb[i]])) {
+    if (adm[i]) {
       long long cost = 0;
 #pragma unroll
       for (int j = 0; j < TPV_DISTINCT; ++j)
-        if (j < cnt) cost += cw[j] * cdist(s_dbit, code[i], code[j]);
+        if (j < cnt && j != i) cost += cw[j] * cdist(s_dbit, code[i], code[j]);
       const long long g = r.cur - cost;
       if (best_better(g, nb[i], r.best_gain, r.best_b)) {
         r.best_gain = g;

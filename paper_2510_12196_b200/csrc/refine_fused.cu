@@ -231,6 +231,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   const int R = (n + G - 1) / G;  // contiguous vertex range of this CTA
   const int r0 = min(n, (int)blockIdx.x * R), r1 = min(n, r0 + R);
 
+  // thread-per-vertex first filters straight over the vertex range when the
+  // level is small; otherwise the filters run over compact lists built from
+  // ext[v] = #neighbours in another block (bstamp), which the move
+  // application keeps exact (more memory-level parallelism for big levels)
+  const bool vcent = A.src == nullptr || (long long)n <= (long long)A.vc_steps * GT;
+  int* const ext = vcent ? nullptr : A.bstamp;
+
   // ---- entry
   const bool first = !A.st->started;
   const bool reinit = first || A.st->reinit;
@@ -240,9 +247,16 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       A.rtgt[v] = -1;
       A.flags0[v] = 0;
       A.flags1[v] = 0;
-      if (A.bstamp) A.bstamp[v] = 0;
     }
     for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
+  }
+  if (ext) {  // boundary counts of the entry mapping, thread per vertex
+    for (long long v = gt; v < n; v += GT) {
+      const int pv = A.part[v];
+      int c = 0;
+      for (int e = A.off[v]; e < A.off[v + 1]; ++e) c += A.part[A.tgt[e]] != pv;
+      ext[v] = c;
+    }
   }
   if (first) {
     long long acc = 0;
@@ -334,32 +348,15 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     // thread-per-vertex first filters straight over the vertex range when
     // the level is small; otherwise an edge-parallel boundary pass + a
     // compact list first (more memory-level parallelism for large levels)
-    const bool vcent = A.src == nullptr || (long long)n <= (long long)A.vc_steps * GT;
     WarpQueue qa{qbuf + warp * 2 * kQueueCap, 0}, qb{qbuf + (warp * 2 + 1) * kQueueCap, 0};
     if (balanced_now) {
       // ---- K9 first filter (refinement.py:201-244)
       long long ns = n;  // items: vertices (vcent) or the boundary list
       if (!vcent) {
-        // boundary stamps: edge-parallel, int4-vectorised over E_u
-        const long long m4 = A.m2 & ~3ll;
-        for (long long e = gt * 4; e < m4; e += GT * 4) {
-          int4 s4 = *reinterpret_cast<const int4*>(A.src + e);
-          int4 t4 = *reinterpret_cast<const int4*>(A.tgt + e);
-          int ps0 = A.part[s4.x], ps1 = A.part[s4.y], ps2 = A.part[s4.z], ps3 = A.part[s4.w];
-          int pt0 = A.part[t4.x], pt1 = A.part[t4.y], pt2 = A.part[t4.z], pt3 = A.part[t4.w];
-          if (ps0 != pt0) A.bstamp[s4.x] = stamp;
-          if (ps1 != pt1) A.bstamp[s4.y] = stamp;
-          if (ps2 != pt2) A.bstamp[s4.z] = stamp;
-          if (ps3 != pt3) A.bstamp[s4.w] = stamp;
-        }
-        for (long long e = m4 + gt; e < A.m2; e += GT)
-          if (A.part[A.src[e]] != A.part[A.tgt[e]]) A.bstamp[A.src[e]] = stamp;
-        grid.sync();
-        PHASE_MARK(0);
-        // boundary list (unlocked)
+        // boundary list (unlocked): ext[v] > 0
         for (long long b0 = gt - lane; b0 < n; b0 += GT) {
           const long long v = b0 + lane;
-          const bool bnd = v < n && A.bstamp[v] == stamp && !(use_locks && lkf[v]);
+          const bool bnd = v < n && ext[v] > 0 && !(use_locks && lkf[v]);
           wq_push(qa, bnd, (int)v, A.lsmall, cnt + C_SMALL);
         }
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
@@ -760,6 +757,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           const int v = lmov[idx];
           const int ov = A.part[v], nv = A.dest[v];
           const unsigned long long oc = T.code[ov], nc = T.code[nv];
+          int dext = 0;
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
             const int u = A.tgt[e];
             const bool um = tmf[u];
@@ -768,7 +766,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             const long long dd = cdist(s_dbit, nc, T.code[nu]) -
                                  cdist(s_dbit, oc, T.code[ou]);
             acc += (long long)A.w[e] * dd * (um ? 1 : 2);
+            if (ext) {  // boundary counts: edge (v,u) before / after the moves
+              const int dx = (int)(nv != nu) - (int)(ov != ou);
+              dext += dx;
+              if (!um && dx) atomicAdd(&ext[u], dx);  // movers update their own
+            }
           }
+          if (ext && dext) atomicAdd(&ext[v], dext);
           if (li == 0 && ov != nv) {
             atomicAdd(reinterpret_cast<unsigned long long*>(&A.bw[ov]),
                       (unsigned long long)(-(long long)A.vw[v]));
