@@ -1,0 +1,38 @@
+"""Run the BASELINE configs 3 and 4 (R-MAT scale 22 -> H=4:8:8, 3D grid
+256^3 -> H=4:16:8) through integrated_map_device: time, balance, J."""
+import argparse
+import json
+import time
+
+import torch
+
+from paper_2510_12196_b200 import device as D
+from paper_2510_12196_b200.generators import gen_grid3d, gen_rmat
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--which", nargs="+", default=["rmat", "grid3d"])
+ap.add_argument("--rmat-scale", type=int, default=22)
+ap.add_argument("--grid", type=int, default=256)
+ap.add_argument("--reps", type=int, default=2)
+args = ap.parse_args()
+for w in args.which:
+    t0 = time.time()
+    if w == "rmat":
+        g = gen_rmat(args.rmat_scale)
+        h, d = (4, 8, 8), (1, 10, 100)
+    else:
+        g = gen_grid3d(args.grid, args.grid, args.grid)
+        h, d = (4, 16, 8), (1, 10, 100)
+    print(f"{w}: n={g.n} m={g.m} gen {time.time() - t0:.1f}s", flush=True)
+    dg = D.DeviceGraph.from_host(g)
+    for r in range(args.reps):
+        torch.cuda.synchronize()
+        t0 = time.time()
+        a, bw, st = D.integrated_map_device(dg, h, d, 0.03, r)
+        torch.cuda.synchronize()
+        print(json.dumps({"cfg": w, "rep": r, "wall_ms": (time.time() - t0) * 1e3,
+                          "J": st["final_j"], "maxw": st["max_block_weight"],
+                          "l_max": st["l_max"], "balanced": st["max_block_weight"] <= st["l_max"],
+                          "levels": st["n_levels"], "level_n": st["level_n"],
+                          **{k: round(st[k], 1) for k in ("ms_coarsen", "ms_initial",
+                                                          "ms_refine")}}), flush=True)
