@@ -294,14 +294,17 @@ def run_gpu(args) -> dict | None:
         distances = DIST
     for w in range(args.warmup):  # pinned staging, upload buffers, worker streams
         integrated_map(hg, Topo(), EPS, seed_of(10**6 + w))
-    e2e_ms = []
+    e2e_ms, e2e_parts = [], []
     barrier()
     for step in range(args.steps):
         flush.fill_((step + 7) & 0xff)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        m = integrated_map(hg, Topo(), EPS, seed_of(step))
+        est: dict = {}
+        m = integrated_map(hg, Topo(), EPS, seed_of(step), stats=est)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_parts.append([round(est["ms_upload"], 2), round(est["ms_total"], 2),
+                          round(est["ms_download"], 2)])
         assert m.max_block_weight() <= (1.0 + EPS) * g.total_weight / k
     barrier()
     e2e_total = maxed(sum(e2e_ms))
@@ -336,7 +339,8 @@ def run_gpu(args) -> dict | None:
         "step_phases_ms": {"coarsen/initial/refine": phases},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "seconds_per_map": e2e_total / args.steps / 1000.0,
-                "step_ms": [round(x, 3) for x in e2e_ms]},
+                "step_ms": [round(x, 3) for x in e2e_ms],
+                "upload/map/download_ms": e2e_parts},
         "quality": {"J": js, "J_geomean": float(np.exp(np.mean(np.log(js)))),
                     "balanced": bool(balanced),
                     "J_reference_seed0": REF_J_SEED0.get(args.logn)},

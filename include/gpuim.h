@@ -98,6 +98,9 @@ typedef struct gim_im_stats {
    * its class, device ms and bytes — the finest-level refinement launch */
   int32_t top_class;
   double top_ms, top_bytes;
+  /* host-array entry (gim_integrated_map) only: wall ms of the upload
+   * (host narrowing + H2D) and of the download (D2H + widening) */
+  double ms_upload, ms_download;
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */

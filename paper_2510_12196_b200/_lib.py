@@ -79,6 +79,8 @@ class GimImStats(C.Structure):
         ("top_class", C.c_int32),
         ("top_ms", C.c_double),
         ("top_bytes", C.c_double),
+        ("ms_upload", C.c_double),
+        ("ms_download", C.c_double),
     ]
 
 

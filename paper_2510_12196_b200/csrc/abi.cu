@@ -99,6 +99,7 @@ void release_stream(cudaStream_t s) {
 // (stream, size class) for the life of the process and handed out again
 // only on the stream they were released on (stream order = happens-before).
 constexpr size_t kCacheMax = (size_t)16 << 30;  // larger buffers go to the pool
+constexpr size_t kTrimClass = (size_t)16 << 20;  // "large" size classes
 
 static size_t size_class(size_t b) {
   size_t c = 256;
@@ -139,6 +140,17 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
       it->second.pop_back();
       g_cache_owned[p] = c;
       return p;
+    }
+  }
+  if (c >= kTrimClass) {
+    // a large class this stream has not cached: hand this stream's other
+    // large cached blocks back to the pool first, so the pool serves the
+    // request from memory it already holds instead of mapping new pages
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto& kv : g_cache_free) {
+      if (kv.first.s != s || kv.first.c < kTrimClass) continue;
+      for (void* q : kv.second) cudaFreeAsync(q, s);
+      kv.second.clear();
     }
   }
   void* p = raw_alloc(c, s);

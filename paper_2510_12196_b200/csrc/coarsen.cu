@@ -109,6 +109,106 @@ __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restri
   block_sum_atomic<BLOCK>(cnt, matched);
 }
 
+// Thread-per-vertex preference (rows up to kHemTpv slots): one thread walks
+// its row in chunks of 4 (the target / weight loads, then the eligibility
+// gathers of a chunk, are independent and overlap) — no shuffles, 32
+// vertices per warp in flight.  elig_c[u] = c_u for unmatched u, -1 for
+// matched u (one gather instead of partner[u] + vw[u]).  Longer rows are
+// evaluated in place by the whole warp (strided slots + shuffle argmax).
+constexpr int kHemTpv = 32;
+
+__global__ void k_hem_elig(int n, const int* __restrict__ partner, const int* __restrict__ vw,
+                           int* __restrict__ elig_c) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    elig_c[v] = partner[v] < 0 ? vw[v] : -1;
+}
+
+__global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restrict__ off,
+                                                      const int* __restrict__ tgt,
+                                                      const int* __restrict__ w,
+                                                      const int* __restrict__ elig_c,
+                                                      double l_max, unsigned long long seed,
+                                                      int* __restrict__ pref) {
+  const int lane = lane_id();
+  const long long T = (long long)gridDim.x * blockDim.x;
+  for (long long b0 = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; b0 < n; b0 += T) {
+    const int v = (int)(b0 + lane);
+    const bool inr = v < n;
+    const int cvv = inr ? elig_c[v] : -1;
+    const bool active = cvv >= 0;  // unmatched
+    int e0 = 0, e1 = 0;
+    if (active) {
+      e0 = off[v];
+      e1 = off[v + 1];
+    }
+    const bool longrow = active && e1 - e0 > kHemTpv;
+    HemCand best;
+    best.u = -1;
+    best.w = best.c = best.slot = 0;
+    best.h = 0;
+    if (active && !longrow) {
+      const long long cv = cvv;
+      for (int e = e0; e < e1; e += 4) {
+        int tg[4], wg[4], cg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e + q < e1) {
+            tg[q] = tgt[e + q];
+            wg[q] = w[e + q];
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e + q < e1) cg[q] = elig_c[tg[q]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (e + q >= e1) break;
+          const int cu = cg[q];
+          if (cu < 0 || (double)(cv + cu) > l_max) continue;
+          HemCand c;
+          c.w = wg[q];
+          c.c = cu;
+          c.slot = e + q;
+          c.u = tg[q];
+          c.h = hash2(seed, (unsigned long long)min(v, c.u), (unsigned long long)max(v, c.u));
+          if (hem_better(c, best)) best = c;
+        }
+      }
+    }
+    // long rows: the warp evaluates them one by one
+    unsigned lm = __ballot_sync(0xffffffffu, longrow);
+    while (lm) {
+      const int l = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int x = __shfl_sync(0xffffffffu, v, l);
+      const int xb = __shfl_sync(0xffffffffu, e0, l), xe = __shfl_sync(0xffffffffu, e1, l);
+      const long long cx = __shfl_sync(0xffffffffu, cvv, l);
+      HemCand bx;
+      bx.u = -1;
+      bx.w = bx.c = bx.slot = 0;
+      bx.h = 0;
+      for (int e = xb + lane; e < xe; e += 32) {
+        const int u = tgt[e];
+        const int cu = elig_c[u];
+        if (cu < 0 || (double)(cx + cu) > l_max) continue;
+        HemCand c;
+        c.w = w[e];
+        c.c = cu;
+        c.slot = e;
+        c.u = u;
+        c.h = hash2(seed, (unsigned long long)min(x, u), (unsigned long long)max(x, u));
+        if (hem_better(c, bx)) bx = c;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        HemCand y = hem_shfl(bx, o);
+        if (hem_better(y, bx)) bx = y;
+      }
+      if (lane == l) best = bx;
+    }
+    if (inr) pref[v] = active ? best.u : -1;
+  }
+}
+
 static int pick_vw(long long m2, int n) {
   double avg = n ? (double)m2 / n : 0.0;
   if (avg <= 3.0) return 4;
@@ -122,18 +222,13 @@ void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
   if (g.n == 0) return;
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
-  int vw = pick_vw(g.m2, g.n);
-  long long groups = (long long)g.n * vw;
-  int grid = grid_for(groups, B, kSMs * 16);
-  switch (vw) {
-    case 4: k_hem_pref<4><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
-    case 8: k_hem_pref<8><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
-    case 16: k_hem_pref<16><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
-    default: k_hem_pref<32><<<grid, B, 0, s>>>(g.n, g.off, g.tgt, g.w, g.vw, partner, l_max, seed, pref); break;
-  }
+  DBuf<int> elig((size_t)g.n, s);
+  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, elig.get());
+  k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, elig.get(),
+                                                           l_max, seed, pref);
   k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched);
   GIM_LAUNCH_CHECK();
-  count_launch(2);
+  count_launch(3);
 }
 
 // ---------------------------------------------------------------------------
@@ -624,6 +719,161 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int*
   }
 }
 
+// Thread-per-coarse-vertex contraction (rows of L <= kCtTpv staged entries):
+// the thread walks its <= 2 member rows in chunks of 4 (independent loads),
+// maps each target through M and insertion-sorts (key, weight) into its own
+// column of a shared-memory scratch (conflict-free [i][thread] layout),
+// summing parallel edges and dropping the self loop — the same sorted,
+// deduplicated row as the warp path.  Rows are written at upper-bound
+// offsets (scan of L) with their true degree, then compacted.  Longer rows
+// go through the warp-per-row shared-memory path into the same buffers.
+constexpr int kCtTpv = 32;
+constexpr int kCtBlock = 128;
+
+__global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __restrict__ mem,
+                                                      const int* __restrict__ rowlen,
+                                                      const int* __restrict__ ub,
+                                                      const int* __restrict__ off,
+                                                      const int* __restrict__ tgt,
+                                                      const int* __restrict__ w,
+                                                      const int* __restrict__ cmap,
+                                                      int* __restrict__ t_tgt,
+                                                      int* __restrict__ t_w,
+                                                      int* __restrict__ cdeg) {
+  __shared__ int sK[kCtTpv][kCtBlock], sW[kCtTpv][kCtBlock];
+  const int tid = threadIdx.x;
+  for (long long cc = (long long)blockIdx.x * kCtBlock + tid; cc < n_c;
+       cc += (long long)gridDim.x * kCtBlock) {
+    const int c = (int)cc;
+    if (rowlen[c] > kCtTpv) continue;  // warp path
+    const int v0 = mem[2 * c], v1 = mem[2 * c + 1];
+    int cnt = 0;
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const int vv = part ? v1 : v0;
+      if (vv < 0) break;
+      const int e1 = off[vv + 1];
+      for (int e = off[vv]; e < e1; e += 4) {
+        int tg[4], wg[4], kg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e + q < e1) {
+            tg[q] = tgt[e + q];
+            wg[q] = w[e + q];
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e + q < e1) kg[q] = cmap[tg[q]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (e + q >= e1) break;
+          const int key = kg[q];
+          if (key == c) continue;  // self loop
+          int pos = cnt;
+          while (pos > 0 && sK[pos - 1][tid] > key) --pos;
+          if (pos > 0 && sK[pos - 1][tid] == key) {
+            sW[pos - 1][tid] += wg[q];
+            continue;
+          }
+          for (int i = cnt; i > pos; --i) {
+            sK[i][tid] = sK[i - 1][tid];
+            sW[i][tid] = sW[i - 1][tid];
+          }
+          sK[pos][tid] = key;
+          sW[pos][tid] = wg[q];
+          ++cnt;
+        }
+      }
+    }
+    const int base = ub[c];
+    for (int i = 0; i < cnt; ++i) {
+      t_tgt[base + i] = sK[i][tid];
+      t_w[base + i] = sW[i][tid];
+    }
+    cdeg[c] = cnt;
+  }
+}
+
+// long rows (kCtTpv < L <= kRowCap): warp per row, shared-memory staging
+__global__ void __launch_bounds__(kRowWarps * 32) k_row_long(int n_c, const int* __restrict__ mem,
+                                                            const int* __restrict__ rowlen,
+                                                            const int* __restrict__ ub,
+                                                            const int* __restrict__ off,
+                                                            const int* __restrict__ tgt,
+                                                            const int* __restrict__ w,
+                                                            const int* __restrict__ cmap,
+                                                            int* __restrict__ t_tgt,
+                                                            int* __restrict__ t_w,
+                                                            int* __restrict__ cdeg) {
+  __shared__ int sK[kRowWarps][kRowCap], sW[kRowWarps][kRowCap];
+  __shared__ unsigned char sF[kRowWarps][kRowCap];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  int* K = sK[warp];
+  int* Wt = sW[warp];
+  unsigned char* F = sF[warp];
+  for (long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c0 < n_c;
+       c0 += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int c = (int)c0;
+    if (rowlen[c] <= kCtTpv) continue;  // warp-uniform
+    const int L = stage_row(c, mem, off, tgt, w, cmap, K, Wt);
+    int nf = 0;
+    for (int i = lane; i < L; i += 32) {
+      const int key = K[i];
+      bool first = key != INT_MAX;
+      for (int j = 0; j < i && first; ++j)
+        if (K[j] == key) first = false;
+      F[i] = first;
+      nf += first;
+    }
+    nf = warp_sum_i(nf);
+    __syncwarp();
+    const int base = ub[c];
+    for (int i = lane; i < L; i += 32) {
+      if (!F[i]) continue;
+      const int key = K[i];
+      long long sum = 0;
+      int rank = 0;
+      for (int j = 0; j < L; ++j) {
+        const int kj = K[j];
+        if (kj == key) sum += Wt[j];
+        rank += (F[j] && kj < key);
+      }
+      t_tgt[base + rank] = key;
+      t_w[base + rank] = (int)sum;
+    }
+    if (lane == 0) cdeg[c] = nf;
+    __syncwarp();
+  }
+}
+
+// compaction: row c moves from its upper-bound slot to its final offset
+__global__ void k_row_compact(int n_c, const int* __restrict__ ub, const int* __restrict__ c_off,
+                              const int* __restrict__ t_tgt, const int* __restrict__ t_w,
+                              int* __restrict__ c_tgt, int* __restrict__ c_w,
+                              int* __restrict__ c_src) {
+  const int lane = lane_id();
+  // warp per 32 rows: each row copied by lanes in turn (coalesced per row)
+  for (long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) - lane; r0 < n_c;
+       r0 += (long long)gridDim.x * blockDim.x) {
+    const int myc = (int)(r0 + lane);
+    int mb = 0, mo = 0, md = 0;
+    if (myc < n_c) {
+      mb = ub[myc];
+      mo = c_off[myc];
+      md = c_off[myc + 1] - mo;
+    }
+    for (int j = 0; j < 32; ++j) {
+      const int b = __shfl_sync(0xffffffffu, mb, j), o = __shfl_sync(0xffffffffu, mo, j),
+                d = __shfl_sync(0xffffffffu, md, j);
+      for (int i = lane; i < d; i += 32) {
+        c_tgt[o + i] = t_tgt[b + i];
+        c_w[o + i] = t_w[b + i];
+        c_src[o + i] = (int)r0 + j;
+      }
+    }
+  }
+}
+
 // contraction of a matching (partner[] given); falls back to the radix-sort
 // path when some coarse row exceeds kRowCap
 void contract_matching(const DevGraph& g, const int* cmap, const int* partner, int n_c,
@@ -632,18 +882,23 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
     contract(g, cmap, n_c, out, s);
     return;
   }
-  DBuf<int> mem((size_t)2 * n_c, s), rowlen((size_t)n_c, s);
-  DBuf<int> cdeg((size_t)n_c + 1, s), scal(2, s);  // [maxlen, m2c]
+  DBuf<int> mem((size_t)2 * n_c, s), rowlen((size_t)n_c + 1, s);
+  DBuf<int> cdeg((size_t)n_c + 1, s), ub((size_t)n_c + 1, s), scal(3, s);  // maxlen, m2c, ub total
   DBuf<int> cvw((size_t)n_c, s);
-  GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(int), s));
+  GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 3 * sizeof(int), s));
   GIM_CUDA(cudaMemsetAsync(cdeg.get() + n_c, 0, sizeof(int), s));
   k_members<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, partner, cmap, g.off, g.vw, mem.get(),
                                                rowlen.get(), cvw.get(), scal.get());
   count_launch();
   GIM_LAUNCH_CHECK();
-  int maxlen = 0;
-  GIM_CUDA(cudaMemcpyAsync(&maxlen, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  exclusive_scan<int>((long long)n_c, LoadAs<int, int>{rowlen.get()}, StoreTo<int>{ub.get()},
+                      scal.get() + 2, s);
+  int hs[3] = {0, 0, 0};
+  int* hp = static_cast<int*>(pinned_scratch(sizeof(hs)));
+  GIM_CUDA(cudaMemcpyAsync(hp, scal.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
   GIM_CUDA(sync_stream(s));
+  std::copy(hp, hp + 3, hs);
+  const int maxlen = hs[0], ubtot = hs[2];
   if (maxlen > kRowCap) {  // hub rows: radix-sort path for this level
     contract(g, cmap, n_c, out, s);
     return;
@@ -652,23 +907,31 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
   out.n = n_c;
   out.vw = std::move(cvw);
   out.off = DBuf<int>((size_t)n_c + 1, s);
-  const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
-  k_row_count<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), g.off, g.tgt, g.w, cmap,
-                                              cdeg.get());
+  DBuf<int> t_tgt((size_t)std::max(ubtot, 1), s), t_w((size_t)std::max(ubtot, 1), s);
+  k_row_tpv<<<grid_for(n_c, kCtBlock, kSMs * 16), kCtBlock, 0, s>>>(
+      n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
+      cdeg.get());
   count_launch();
+  if (maxlen > kCtTpv) {
+    const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
+    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(), g.off,
+                                               g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
+                                               cdeg.get());
+    count_launch();
+  }
   GIM_LAUNCH_CHECK();
   exclusive_scan<int>((long long)n_c + 1, LoadAs<int, int>{cdeg.get()},
                       StoreTo<int>{out.off.get()}, scal.get() + 1, s);
-  int m2c = 0;
-  GIM_CUDA(cudaMemcpyAsync(&m2c, out.off.get() + n_c, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(cudaMemcpyAsync(hp, out.off.get() + n_c, sizeof(int), cudaMemcpyDeviceToHost, s));
   GIM_CUDA(sync_stream(s));
+  const int m2c = hp[0];
   out.m2 = m2c;
   out.tgt = DBuf<int>((size_t)std::max(m2c, 1), s);
   out.w = DBuf<int>((size_t)std::max(m2c, 1), s);
   out.src = DBuf<int>((size_t)std::max(m2c, 1), s);
-  k_row_fill<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), g.off, g.tgt, g.w, cmap,
-                                             out.off.get(), out.tgt.get(), out.w.get(),
-                                             out.src.get());
+  k_row_compact<<<grid_for(n_c, 256, kSMs * 16), 256, 0, s>>>(
+      n_c, ub.get(), out.off.get(), t_tgt.get(), t_w.get(), out.tgt.get(), out.w.get(),
+      out.src.get());
   count_launch();
   GIM_LAUNCH_CHECK();
   prof.extra = 8.0 * m2c;

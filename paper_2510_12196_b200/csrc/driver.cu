@@ -7,6 +7,7 @@
 // operation order as the reference's Python float expressions, so control
 // decisions agree bit-for-bit; kernels only see the resulting doubles.
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <exception>
 #include <thread>
@@ -672,6 +673,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
       stats->level_n[i] = i < nl ? level_n[i] : 0;
       stats->level_m2[i] = i < nl ? level_m2[i] : 0;
     }
+    stats->ms_upload = stats->ms_download = 0.0;
     stats->ms_coarsen = a;
     stats->ms_initial = b;
     stats->ms_refine = c;
@@ -778,7 +780,7 @@ static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, co
   add(ew, m2, G.w.get(), 1);
   add(vw, n, G.vw.get(), 2);
   const int T = (int)std::max<size_t>(1, std::min<size_t>(jobs.size(),
-                                       std::max(2u, std::min(8u, std::thread::hardware_concurrency()))));
+                                       std::max(2u, std::min(16u, std::thread::hardware_concurrency()))));
   std::vector<UpAcc> acc((size_t)T);
   std::vector<std::exception_ptr> errs((size_t)T);
   std::atomic<size_t> next{0};
@@ -1137,11 +1139,16 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     cudaStream_t s = (cudaStream_t)stream;
     gim_im_params P = params ? *params : default_params();
     OwnedGraph G;
+    const auto t_up = std::chrono::steady_clock::now();
     upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
+    GIM_CUDA(sync_stream(s));
+    const double ms_up =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_up).count();
     Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
     DBuf<int> part((size_t)n, s);
     DBuf<long long> bw((size_t)tp.k, s);
     integrated_map_device(G.view(), G.total_vw, *t, eps, seed, P, part.get(), bw.get(), stats, s);
+    const auto t_down = std::chrono::steady_clock::now();
     // int32 assignment -> pinned staging -> widened to int64 on the host by
     // worker threads (half the PCIe bytes, no pageable staging copy)
     int* h_part = static_cast<int*>(pinned_scratch(sizeof(int) * (size_t)n));
@@ -1150,7 +1157,7 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
                              cudaMemcpyDeviceToHost, s));
     GIM_CUDA(sync_stream(s));
     {
-      const int T = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+      const int T = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
       const long long per = (n + T - 1) / T;
       auto widen = [&](int t) {
         const long long a = std::min<long long>(n, t * per), b = std::min<long long>(n, a + per);
@@ -1164,7 +1171,12 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
       widen(0);
       for (auto& th : pool) th.join();
     }
-    if (stats) stats->kernel_launches = launches();
+    if (stats) {
+      stats->kernel_launches = launches();
+      stats->ms_upload = ms_up;
+      stats->ms_download = std::chrono::duration<double, std::milli>(
+                               std::chrono::steady_clock::now() - t_down).count();
+    }
   });
 }
 
