@@ -229,6 +229,10 @@ void gim_set_fanout(int32_t on);
  * as per-phase launches with host control.  Results are identical. */
 void gim_set_fused(int32_t on);
 
+/* Partition the small leaf-parent subgraphs of the multisection as one batch
+ * (one launch per phase for all of them, default 1).  Results are identical. */
+void gim_set_batch(int32_t on);
+
 /* Contract level-stack matchings row-wise (default 1) or always with the
  * radix-sort path.  The coarse graphs are identical. */
 void gim_set_rowwise_contraction(int32_t on);

@@ -123,6 +123,7 @@ SIGNATURES: dict[str, list] = {
     "gim_set_profiling": [I32],
     "gim_set_fanout": [I32],
     "gim_set_fused": [I32],
+    "gim_set_batch": [I32],
     "gim_set_rowwise_contraction": [I32],
     "gim_launch_count": [],
     "gim_reset_launch_count": [],
@@ -131,7 +132,7 @@ SIGNATURES: dict[str, list] = {
 RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
             "gim_reset_launch_count": None, "gim_set_profiling": None,
             "gim_release_cached_memory": None,
-            "gim_set_fanout": None, "gim_set_fused": None,
+            "gim_set_fanout": None, "gim_set_fused": None, "gim_set_batch": None,
             "gim_set_rowwise_contraction": None}
 
 _lib = None

@@ -143,14 +143,18 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
     }
   }
   if (c >= kTrimClass) {
-    // a large class this stream has not cached: hand this stream's other
-    // large cached blocks back to the pool first, so the pool serves the
-    // request from memory it already holds instead of mapping new pages
+    // a large class this stream has none of: borrow a cached block one or two
+    // classes up before mapping new memory (level sizes vary a little from
+    // seed to seed and straddle class boundaries)
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    for (auto& kv : g_cache_free) {
-      if (kv.first.s != s || kv.first.c < kTrimClass) continue;
-      for (void* q : kv.second) cudaFreeAsync(q, s);
-      kv.second.clear();
+    for (size_t up = c << 1; up <= (c << 2); up <<= 1) {
+      auto it = g_cache_free.find(CacheKey{s, up});
+      if (it != g_cache_free.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        g_cache_owned[p] = up;
+        return p;
+      }
     }
   }
   void* p = raw_alloc(c, s);

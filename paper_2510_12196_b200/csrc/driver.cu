@@ -7,6 +7,8 @@
 // operation order as the reference's Python float expressions, so control
 // decisions agree bit-for-bit; kernels only see the resulting doubles.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <exception>
@@ -467,6 +469,197 @@ static void internal_partitioner(const DevGraph& g, long long total, int parts, 
 }
 
 // ---------------------------------------------------------------------------
+// batched internal partitioner for small subgraphs (batch.cu): same results
+// as internal_partitioner() per job, one launch per phase for all jobs
+
+struct BatchPartJob {
+  DevGraph g;
+  long long total;
+  double eps_local;
+  unsigned long long seed;
+  int* out_part;  // [g.n]
+};
+
+// batch-eligible: small enough that every level refines shared-memory resident
+static std::atomic<bool> g_batch{true};
+constexpr int kBatchMaxN = 1000;
+
+static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int parts, RunStats& st,
+                                       cudaStream_t s) {
+  std::vector<int> fast;  // jobs on the batched path
+  for (int j = 0; j < (int)jobs.size(); ++j) {
+    BatchPartJob& B = jobs[(size_t)j];
+    if (parts <= 1 || B.g.n <= parts) {  // trivial cases as internal_partitioner
+      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+      continue;
+    }
+    fast.push_back(j);
+  }
+  if (fast.empty()) return;
+  const int J = (int)fast.size();
+  Topo tf = get_flat_topo(parts);
+  std::vector<DevGraph> gs;
+  std::vector<double> lmax;
+  std::vector<unsigned long long> seeds;
+  for (int j : fast) {
+    const BatchPartJob& B = jobs[(size_t)j];
+    gs.push_back(B.g);
+    lmax.push_back((1.0 + B.eps_local) * (double)B.total / (double)parts);
+    seeds.push_back(B.seed);
+  }
+  std::vector<SmallStack> stacks;
+  DBuf<int> arena;
+  coarsen_small_batch(gs, lmax, seeds, std::max<long long>(64ll * parts, 2), stacks, arena, s);
+  // jobs the fast path cannot take: general path
+  std::vector<int> ok;
+  for (int i = 0; i < J; ++i) {
+    const SmallStack& S = stacks[(size_t)i];
+    bool fits = S.status == 0;
+    if (fits)
+      for (const DevGraph& g : S.levels)
+        fits = fits && refine_smem_fits(g.n, g.m2, parts, 2, refine_pick_vw(g.n, g.m2));
+    if (fits) {
+      ok.push_back(i);
+    } else {
+      BatchPartJob& B = jobs[(size_t)fast[(size_t)i]];
+      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+    }
+  }
+  if (ok.empty()) return;
+  static const bool debug = std::getenv("GIM_BATCH_DEBUG") != nullptr;
+  if (debug) {  // compare every fast-path level stack with the general one
+    for (int i : ok) {
+      const BatchPartJob& B = jobs[(size_t)fast[(size_t)i]];
+      const SmallStack& S = stacks[(size_t)i];
+      std::vector<Level> ref = build_level_stack(B.g, lmax[(size_t)i],
+                                                 std::max<long long>(64ll * parts, 2), B.seed, s);
+      GIM_CUDA(sync_stream(s));
+      std::fprintf(stderr, "[batch-debug] job %d n=%d levels fast=%d general=%d\n", i, B.g.n,
+                   S.nl, (int)ref.size());
+      for (int l = 0; l < std::min(S.nl, (int)ref.size()); ++l) {
+        const DevGraph& a = S.levels[(size_t)l];
+        const DevGraph& b = ref[(size_t)l].g;
+        auto fetch = [&](const int* p, long long cnt) {
+          std::vector<int> h((size_t)std::max(cnt, 0ll));
+          if (cnt > 0) GIM_CUDA(cudaMemcpy(h.data(), p, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+          return h;
+        };
+        bool same = a.n == b.n && a.m2 == b.m2 && fetch(a.off, a.n + 1) == fetch(b.off, b.n + 1) &&
+                    fetch(a.tgt, a.m2) == fetch(b.tgt, b.m2) && fetch(a.w, a.m2) == fetch(b.w, b.m2) &&
+                    fetch(a.vw, a.n) == fetch(b.vw, b.n);
+        if (l + 1 < S.nl && l + 1 < (int)ref.size())
+          same = same && fetch(S.cmap[(size_t)l], a.n) == fetch(ref[(size_t)l].cmap.get(), a.n);
+        std::fprintf(stderr, "[batch-debug]   level %d n=%d/%d m2=%lld/%lld %s\n", l, a.n, b.n,
+                     a.m2, b.m2, same ? "same" : "DIFFERENT");
+      }
+    }
+  }
+  st.partitioner_calls += (long long)ok.size();
+  const int K = (int)ok.size();
+  // per-job ping-pong partitions, block weights, refine scratch
+  int nmax = 0, lmaxn = 0;
+  for (int i : ok) {
+    nmax = std::max(nmax, gs[(size_t)i].n);
+    lmaxn = std::max(lmaxn, stacks[(size_t)i].nl);
+  }
+  DBuf<int> pa((size_t)K * nmax, s), pb((size_t)K * nmax, s), best((size_t)K * nmax, s);
+  DBuf<long long> bw((size_t)K * parts, s), best_bw((size_t)K * parts, s);
+  DBuf<FusedState> states((size_t)K, s);
+  std::vector<int*> cur((size_t)K), nxt((size_t)K);
+  for (int q = 0; q < K; ++q) {
+    cur[(size_t)q] = pa.get() + (size_t)q * nmax;
+    nxt[(size_t)q] = pb.get() + (size_t)q * nmax;
+  }
+  // initial partition of every coarsest graph (pipelines.py:206)
+  {
+    std::vector<DevGraph> coarsest;
+    std::vector<int*> outs;
+    for (int q = 0; q < K; ++q) {
+      const SmallStack& S = stacks[(size_t)ok[(size_t)q]];
+      coarsest.push_back(S.levels.back());
+      outs.push_back(cur[(size_t)q]);
+    }
+    ggg_batch(coarsest, parts, outs, s);
+  }
+  std::vector<char> failed((size_t)K, 0);
+  for (int t = 0; t < lmaxn; ++t) {
+    std::vector<BpJob> bp;
+    std::vector<SmemRefineJob> rj;
+    std::vector<int> who;
+    for (int q = 0; q < K; ++q) {
+      if (failed[(size_t)q]) continue;
+      const int i = ok[(size_t)q];
+      const SmallStack& S = stacks[(size_t)i];
+      const int li = S.nl - 1 - t;
+      if (li < 0) continue;
+      const DevGraph& g = S.levels[(size_t)li];
+      const bool project = t > 0;
+      if (project) std::swap(cur[(size_t)q], nxt[(size_t)q]);  // nxt = coarse part
+      long long* bwq = bw.get() + (size_t)q * parts;
+      bp.push_back(BpJob{g.n, parts, project ? S.cmap[(size_t)li] : nullptr,
+                         project ? nxt[(size_t)q] : nullptr, cur[(size_t)q], g.vw, bwq});
+      const BatchPartJob& B = jobs[(size_t)fast[(size_t)i]];
+      RefCfg cfg = config_for_level(li, S.nl, 0.999, 2, 1, 0.25, 0.065, 0.005, 10,
+                                    hash2(B.seed, 101, (unsigned long long)li));
+      SmemRefineJob R;
+      R.g = g;
+      R.vw = refine_pick_vw(g.n, g.m2);
+      R.part = cur[(size_t)q];
+      R.bw = bwq;
+      R.cfg.l_max = lmax[(size_t)i];
+      R.cfg.sigma = lmax[(size_t)i] * (1.0 - cfg.sigma_fraction);
+      R.cfg.phi = cfg.phi;
+      R.cfg.jet_c = cfg.jet_c;
+      R.cfg.jet = cfg.jet;
+      R.cfg.rho = cfg.rho;
+      R.cfg.i_max = cfg.i_max;
+      R.cfg.i_w_max = cfg.i_w_max;
+      R.cfg.seed = cfg.seed;
+      R.best = best.get() + (size_t)q * nmax;
+      R.best_bw = best_bw.get() + (size_t)q * parts;
+      rj.push_back(R);
+      who.push_back(q);
+    }
+    if (rj.empty()) continue;
+    bproj_bw_batch(bp, s);
+    std::vector<char> yielded;
+    refine_smem_batch(rj, tf, states.get(), yielded, s);
+    for (size_t r = 0; r < rj.size(); ++r) {
+      st.init_refine_iterations += rj[r].iters;
+      st.lp += rj[r].lp;
+      st.weak += rj[r].weak;
+      if (yielded[r]) failed[(size_t)who[r]] = 1;  // strong pass due: general path
+    }
+  }
+  if (debug) {  // final partitions vs the general path
+    GIM_CUDA(sync_stream(s));
+    for (int q = 0; q < K; ++q) {
+      if (failed[(size_t)q]) continue;
+      BatchPartJob& B = jobs[(size_t)fast[(size_t)ok[(size_t)q]]];
+      DBuf<int> ref((size_t)std::max(B.g.n, 1), s);
+      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, ref.get(), st, s);
+      GIM_CUDA(sync_stream(s));
+      std::vector<int> x((size_t)B.g.n), y((size_t)B.g.n);
+      GIM_CUDA(cudaMemcpy(x.data(), cur[(size_t)q], sizeof(int) * B.g.n, cudaMemcpyDeviceToHost));
+      GIM_CUDA(cudaMemcpy(y.data(), ref.get(), sizeof(int) * B.g.n, cudaMemcpyDeviceToHost));
+      int diff = 0;
+      for (int v = 0; v < B.g.n; ++v) diff += x[(size_t)v] != y[(size_t)v];
+      std::fprintf(stderr, "[batch-debug] job %d final partition: %d of %d differ\n", q, diff,
+                   B.g.n);
+    }
+  }
+  for (int q = 0; q < K; ++q) {
+    BatchPartJob& B = jobs[(size_t)fast[(size_t)ok[(size_t)q]]];
+    if (failed[(size_t)q]) {
+      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+      continue;
+    }
+    GIM_CUDA(cudaMemcpyAsync(B.out_part, cur[(size_t)q], sizeof(int) * (size_t)B.g.n,
+                             cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // hierarchical multisection (pipelines.py:49-110)
 
 struct MsCtx {
@@ -542,6 +735,38 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
   for (int j = 0; j < parts; ++j) {
     trans[j] = DBuf<int>((size_t)std::max(subs[j].n, 1), s);
     gather(subs[j].n, ids[j].get(), translation, trans[j].get(), s);
+  }
+  if (level - 1 == 1 && g_batch.load() && C.h[0] > 1) {
+    // the children split straight into leaves: partition all of them in one
+    // batch (one launch per phase) when they are small
+    bool small = true;
+    for (int j = 0; j < parts; ++j) small = small && subs[j].n <= kBatchMaxN;
+    if (small) {
+      std::vector<BatchPartJob> jobs;
+      std::vector<DBuf<int>> cparts((size_t)parts);
+      const int cp = (int)C.h[0];
+      for (int j = 0; j < parts; ++j) {
+        cparts[(size_t)j] = DBuf<int>((size_t)std::max(subs[j].n, 1), s);
+        if (subs[j].n == 0) continue;
+        const double eps_child =
+            adaptive_imbalance(C.eps, C.total, child_total[j], C.k, C.h[0], 1);
+        jobs.push_back(BatchPartJob{subs[j].view(), child_total[j], eps_child,
+                                    hash2(node_seed, (unsigned long long)level,
+                                          (unsigned long long)j),
+                                    cparts[(size_t)j].get()});
+      }
+      internal_partitioner_batch(jobs, cp, *C.st, s);
+      for (int j = 0; j < parts; ++j) {
+        if (subs[j].n == 0) continue;
+        ident.push_back(j);
+        ident.push_back(0);
+        const int base = calc_id(C.h, ident);
+        ident.pop_back();
+        ident.pop_back();
+        leaf_scatter(subs[j].n, trans[j].get(), cparts[(size_t)j].get(), base, C.assignment, s);
+      }
+      return;
+    }
   }
   const bool fan_out = level - 1 >= 1 && parts > 1 && C.threads;
   if (!fan_out) {
@@ -1190,4 +1415,5 @@ extern "C" void gim_reset_launch_count(void) { reset_launches(); }
 
 extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }
 extern "C" void gim_set_fused(int32_t on) { gim::g_fused.store(on != 0); }
+extern "C" void gim_set_batch(int32_t on) { gim::g_batch.store(on != 0); }
 extern "C" void gim_set_rowwise_contraction(int32_t on) { gim::g_rowwise.store(on != 0); }

@@ -4,6 +4,9 @@
 // Reference: pipelines.py (_multi_source_bfs :113-129, greedy_graph_growing
 // :132-188, hierarchical_multisection leaf :78-80), graph.py
 // (extract_subgraphs :357-389).
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "radix.cuh"
@@ -205,6 +208,47 @@ void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
   count_launch();
   GIM_LAUNCH_CHECK();
   GIM_CUDA(sync_stream(s));  // job struct lives on this stack frame
+}
+
+// all coarsest graphs of a batched partitioner step, one CTA per graph
+void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
+               cudaStream_t s) {
+  const int J = (int)gs.size();
+  if (J == 0) return;
+  ProfScope prof(P_GGG, 0.0, s);
+  size_t max_words = 0;
+  long long scratch_words = 0;
+  std::vector<size_t> words((size_t)J);
+  for (int j = 0; j < J; ++j) {
+    words[(size_t)j] = (size_t)2 * gs[(size_t)j].n + k + (size_t)k * gs[(size_t)j].n;
+    max_words = std::max(max_words, words[(size_t)j]);
+  }
+  const bool use_smem = max_words * sizeof(int) <= 160 * 1024;
+  if (!use_smem)
+    for (int j = 0; j < J; ++j) scratch_words += (long long)words[(size_t)j];
+  DBuf<int> scratch((size_t)std::max(scratch_words, 1ll), s);
+  DBuf<long long> bwork((size_t)k * J, s);
+  // pageable staging: the call returns once the bytes are staged, so the
+  // vector may die right after (pinned scratch could be overwritten early)
+  std::vector<GggJob> hj((size_t)J);
+  long long off = 0;
+  for (int j = 0; j < J; ++j) {
+    const DevGraph& g = gs[(size_t)j];
+    hj[(size_t)j] = GggJob{g.n, k, g.off, g.tgt, g.w, g.vw, parts[(size_t)j],
+                   use_smem ? nullptr : scratch.get() + off, bwork.get() + (size_t)k * j,
+                   use_smem ? 1 : 0};
+    if (!use_smem) off += (long long)words[(size_t)j];
+  }
+  DBuf<GggJob> dj((size_t)J, s);
+  GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggJob) * (size_t)J,
+                           cudaMemcpyHostToDevice, s));
+  const size_t smem = use_smem ? max_words * sizeof(int) : 0;
+  if (use_smem && smem > 48 * 1024)
+    GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  160 * 1024));
+  k_ggg<<<J, kGggBlock, smem, s>>>(dj.get(), J);
+  count_launch();
+  GIM_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------------------

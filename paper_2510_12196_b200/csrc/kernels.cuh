@@ -1,6 +1,8 @@
 // Internal (C++) interface between the kernel translation units and the
 // host driver.  Nothing here crosses the C ABI.
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace gim {
@@ -147,6 +149,44 @@ struct FusedBuffers {
 };
 
 bool fused_supported(int k, int rho);
+
+// batched small-graph partitioner pieces (batch.cu)
+struct SmallStack {
+  int status = 0;                 // 0: fast path applies; 1: general path
+  int nl = 0;
+  std::vector<DevGraph> levels;   // [0] = the input graph
+  std::vector<const int*> cmap;   // level l -> l + 1 (null on the coarsest)
+};
+void coarsen_small_batch(const std::vector<DevGraph>& gs, const std::vector<double>& l_max,
+                         const std::vector<unsigned long long>& seeds, long long threshold,
+                         std::vector<SmallStack>& out, DBuf<int>& arena, cudaStream_t s);
+struct BpJob {
+  int n, k;
+  const int* cmap;     // null: no projection (coarsest level)
+  const int* coarse;   // coarse part (projection source)
+  int* part;           // fine part (in when cmap is null, else out)
+  const int* vw;
+  long long* bw;
+};
+void bproj_bw_batch(const std::vector<BpJob>& jobs, cudaStream_t s);
+void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
+               cudaStream_t s);
+
+// batched shared-memory-resident refinement (refine_fused.cu)
+struct SmemRefineJob {
+  DevGraph g;
+  int vw = 8;
+  int* part = nullptr;
+  long long* bw = nullptr;
+  FusedCfg cfg{};
+  int* best = nullptr;          // [n] scratch
+  long long* best_bw = nullptr; // [k] scratch
+  long long iters = 0, lp = 0, weak = 0;  // out
+};
+bool refine_smem_fits(long long n, long long m2, int k, int rho, int vw);
+int refine_pick_vw(long long n, long long m2);
+void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedState* states,
+                       std::vector<char>& yielded, cudaStream_t s);
 bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long* bw,
                       const FusedCfg& cfg, FusedBuffers& fb, cudaStream_t s);
 

@@ -93,6 +93,7 @@ struct FusedArgs {
   int bar_mode;        // GridBarrier mode
   int smem_base;       // k_refine_smem: bytes of the regular dynamic region
   int vc_steps;        // vertex-centric first filters up to vc_steps vertices per thread
+  int solo;            // 1: this CTA is a whole refinement (batched launch)
   long long* ptime;    // [16] per-phase ns (trace mode) or null
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
@@ -198,7 +199,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   const int k = A.k;
   const int NC = 31 * A.rho;
   const int n = A.n;
-  const int G = gridDim.x;
+  // a batched shared-memory launch runs one independent refinement per CTA
+  const int G = A.solo ? 1 : (int)gridDim.x;
+  const int BX = A.solo ? 0 : (int)blockIdx.x;
   // dynamic smem: pstar[k] | run[k] | code[k] | warp tables | elist[k] | cstar[k] |
   // wrun[warps*k] | ovl[k] | elig[k]
   long long* pstar = reinterpret_cast<long long*>(dsm);
@@ -218,10 +221,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   T.code = s_code;
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long NW = ((long long)gridDim.x * blockDim.x) >> 5;
-  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long GT = (long long)gridDim.x * blockDim.x;
+  const long long gw = ((long long)BX * blockDim.x + threadIdx.x) >> 5;
+  const long long NW = ((long long)G * blockDim.x) >> 5;
+  const long long gt = (long long)BX * blockDim.x + threadIdx.x;
+  const long long GT = (long long)G * blockDim.x;
   constexpr int GPW = 32 / VW;
   const int gi = lane / VW, li = lane % VW;
   WarpTable wt;
@@ -229,7 +232,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   wt.lb = wt.tab + k;
   wt.lw = wt.lb + k;
   const int R = (n + G - 1) / G;  // contiguous vertex range of this CTA
-  const int r0 = min(n, (int)blockIdx.x * R), r1 = min(n, r0 + R);
+  const int r0 = min(n, BX * R), r1 = min(n, r0 + R);
 
   // thread-per-vertex first filters straight over the vertex range when the
   // level is small; otherwise the filters run over compact lists built from
@@ -272,7 +275,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     }
     block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
     for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
-    if (blockIdx.x == 0)
+    if (BX == 0)
       for (int b = threadIdx.x; b < k; b += blockDim.x) A.best_bw[b] = A.bw[b];
   }
   grid.sync();
@@ -316,10 +319,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   // optional per-phase wall-clock accounting (GIM_TRACE_REFINE): CTA 0,
   // thread 0 adds %globaltimer deltas between barriers into A.ptime[phase]
   unsigned long long t_last = 0;
-  if (A.ptime && blockIdx.x == 0 && threadIdx.x == 0) t_last = globaltimer_ns();
+  if (A.ptime && BX == 0 && threadIdx.x == 0) t_last = globaltimer_ns();
 #define PHASE_MARK(id)                                                   \
   do {                                                                   \
-    if (A.ptime && blockIdx.x == 0 && threadIdx.x == 0) {                \
+    if (A.ptime && BX == 0 && threadIdx.x == 0) {                \
       const unsigned long long t_now = globaltimer_ns();                 \
       A.ptime[(id)] += (long long)(t_now - t_last);                      \
       t_last = t_now;                                                    \
@@ -418,7 +421,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       PHASE_MARK(2);
       // every CTA has read the previous iteration's counters by now (they
       // were consumed before this iteration's first barrier)
-      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
+      if (BX == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K10 second filter over the candidates
       const long long nc = cnt[C_CAND];
       for (long long ib = gw * GPW; ib < nc; ib += NW * GPW) {
@@ -558,7 +561,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;
       grid.sync();
       PHASE_MARK(5);
-      if (blockIdx.x == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
+      if (BX == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block (every
       // CTA redundantly; one warp per overloaded block, all cell chunks
       // loaded before the shuffle prefix) and per-(warp, block) weights of
@@ -645,13 +648,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           wrun[w * k + b] = acc;
           acc += x;
         }
-        A.S[(size_t)b * G + blockIdx.x] = acc;
+        A.S[(size_t)b * G + BX] = acc;
       }
       grid.sync();
       PHASE_MARK(6);
       // step B: exclusive scan of S over CTAs for every overloaded block,
       // one CTA per row (<= 3 entries per thread + a block-wide scan)
-      for (int i = blockIdx.x; i < n_ovl; i += G) {
+      for (int i = BX; i < n_ovl; i += G) {
         long long* row = A.S + (size_t)olist[i] * G;
         const int E = (G + kFusedBlock - 1) / kFusedBlock;  // <= 3
         const int c0 = threadIdx.x * E;
@@ -689,7 +692,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       // (earlier warps of this CTA); whole cells before c* everywhere else
       for (int i = threadIdx.x; i < n_ovl; i += blockDim.x) {
         const int b = olist[i];
-        run[b] = A.S[(size_t)b * G + blockIdx.x];
+        run[b] = A.S[(size_t)b * G + BX];
       }
       __syncthreads();
       for (int i0 = 0; i0 < n_part; i0 += 32) {  // warp-uniform, listed partials only
@@ -858,13 +861,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     if (C.brk) break;
     if (C.take) {
       for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
-      if (blockIdx.x == 0)
+      if (BX == 0)
         for (int b = threadIdx.x; b < k; b += blockDim.x) A.best_bw[b] = A.bw[b];
     }
   }
   // ---- exit: persist the control state; on completion restore the best
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (BX == 0 && threadIdx.x == 0) {
     FusedState& S1 = *A.st;
     S1.started = 1;
     S1.reinit = 0;
@@ -887,7 +890,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   }
   if (!C.strong_yield) {
     for (long long v = gt; v < n; v += GT) A.part[v] = A.best[v];
-    if (blockIdx.x == 0)
+    if (BX == 0)
       for (int b = threadIdx.x; b < k; b += blockDim.x) A.bw[b] = A.best_bw[b];
   }
 }
@@ -907,7 +910,7 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
 //          lheavy[n] lcand[n] lmov0[n] lmov1[n]
 //   uint8: flags0[n] flags1[n] rcell[n]
 template <int VW>
-__global__ void __launch_bounds__(kFusedBlock) k_refine_smem(FusedArgs A) {
+__device__ __forceinline__ void refine_smem_run(const FusedArgs& A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ FusedArgs SA;
   const int n = A.n, k = A.k, NC = 31 * A.rho;
@@ -973,6 +976,17 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_smem(FusedArgs A) {
     A.bw[b] = bw[b];
     if (yielded) A.best_bw[b] = best_bw[b];
   }
+}
+
+template <int VW>
+__global__ void __launch_bounds__(kFusedBlock) k_refine_smem(FusedArgs A) {
+  refine_smem_run<VW>(A);
+}
+
+// one CTA per independent refinement (the batched multisection leaves)
+template <int VW>
+__global__ void __launch_bounds__(kFusedBlock) k_refine_smem_batch(const FusedArgs* args) {
+  refine_smem_run<VW>(args[blockIdx.x]);
 }
 
 // shared-memory bytes of k_refine_smem beyond the regular dynamic region
@@ -1161,6 +1175,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.bar_mode = mode == 3 ? 0 : mode;
   A.smem_base = (int)smem;
   A.vc_steps = vc_steps();
+  A.solo = 0;
   A.ptime = nullptr;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
@@ -1250,6 +1265,132 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     cudaEventDestroy(te[1]);
   }
   return fb.h_state->status == 0;
+}
+
+// ---------------------------------------------------------------------------
+// batched shared-memory-resident refinement (one CTA per job)
+
+size_t refine_smem_regular_bytes(int k) {
+  size_t smem = (size_t)kFusedWarps * 4 * k * sizeof(int) + (size_t)k * (8 + 8 + 8 + 4 + 4 + 4 + 1 + 1);
+  return (smem + 15) & ~(size_t)15;
+}
+
+bool refine_smem_fits(long long n, long long m2, int k, int rho, int vw) {
+  if (n > smem_max_n()) return false;
+  const size_t need = refine_smem_regular_bytes(k) + smem_resident_bytes(n, m2, k, 31 * rho);
+  return need <= smem_dyn_limit<VWDISPATCH>(vw);
+}
+
+int refine_pick_vw(long long n, long long m2) {
+  double avg = n ? (double)m2 / (double)n : 0.0;
+  return avg <= 3.0 ? 4 : avg <= 6.0 ? 8 : avg <= 12.0 ? 16 : 32;
+}
+
+void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedState* states,
+                       std::vector<char>& yielded, cudaStream_t s) {
+  const int J = (int)jobs.size();
+  yielded.assign((size_t)J, 0);
+  if (J == 0) return;
+  const int k = t.k;
+  const size_t base = refine_smem_regular_bytes(k);
+  GIM_CUDA(cudaMemsetAsync(states, 0, sizeof(FusedState) * (size_t)J, s));
+  std::vector<FusedArgs> host((size_t)J);
+  for (int j = 0; j < J; ++j) {
+    const SmemRefineJob& R = jobs[(size_t)j];
+    FusedArgs A{};
+    A.n = R.g.n;
+    A.m2 = R.g.m2;
+    A.off = R.g.off;
+    A.tgt = R.g.tgt;
+    A.w = R.g.w;
+    A.vw = R.g.vw;
+    A.src = nullptr;
+    A.t = t;
+    A.k = k;
+    A.part = R.part;
+    A.bw = R.bw;
+    A.best = R.best;
+    A.best_bw = R.best_bw;
+    A.st = states + j;
+    A.bar_mode = 0;
+    A.solo = 1;
+    A.smem_base = (int)base;
+    A.vc_steps = vc_steps();
+    A.ptime = nullptr;
+    A.l_max = R.cfg.l_max;
+    A.sigma = R.cfg.sigma;
+    A.phi = R.cfg.phi;
+    A.jet_c = R.cfg.jet_c;
+    A.jet = R.cfg.jet;
+    A.rho = R.cfg.rho;
+    A.i_max = R.cfg.i_max;
+    A.i_w_max = R.cfg.i_w_max;
+    A.seed = R.cfg.seed;
+    host[(size_t)j] = A;
+  }
+  // group by lane width (the VW template), one launch per group
+  DBuf<FusedArgs> dargs((size_t)J, s);
+  std::vector<FusedArgs> ordered;
+  std::vector<int> order;
+  int vws[4] = {4, 8, 16, 32};
+  std::vector<std::pair<int, std::pair<int, size_t>>> groups;  // vw, (first, count) + smem
+  std::vector<size_t> gsmem;
+  for (int vw : vws) {
+    const int first = (int)ordered.size();
+    size_t mx = 0;
+    for (int j = 0; j < J; ++j)
+      if (jobs[(size_t)j].vw == vw) {
+        ordered.push_back(host[(size_t)j]);
+        order.push_back(j);
+        mx = std::max(mx, base + smem_resident_bytes(jobs[(size_t)j].g.n, jobs[(size_t)j].g.m2, k,
+                                                     31 * jobs[(size_t)j].cfg.rho));
+      }
+    if ((int)ordered.size() > first) {
+      groups.push_back({vw, {first, (size_t)((int)ordered.size() - first)}});
+      gsmem.push_back(mx);
+    }
+  }
+  GIM_CUDA(cudaMemcpyAsync(dargs.get(), ordered.data(), sizeof(FusedArgs) * (size_t)J,
+                           cudaMemcpyHostToDevice, s));  // pageable: staged before return
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const int vw = groups[gi].first, first = groups[gi].second.first;
+    const int cnt = (int)groups[gi].second.second;
+    const FusedArgs* a = dargs.get() + first;
+    const size_t lim = smem_dyn_limit<VWDISPATCH>(vw);
+    GIM_CHECK(gsmem[gi] <= lim, GIM_E_INTERNAL, "batched refinement exceeds shared memory");
+    static std::once_flag once[4];
+    auto set_attr = [&](const void* fn, int slot) {
+      std::call_once(once[slot], [&] {
+        GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim));
+      });
+    };
+    switch (vw) {
+      case 4: set_attr((const void*)k_refine_smem_batch<4>, 0); break;
+      case 8: set_attr((const void*)k_refine_smem_batch<8>, 1); break;
+      case 16: set_attr((const void*)k_refine_smem_batch<16>, 2); break;
+      default: set_attr((const void*)k_refine_smem_batch<32>, 3); break;
+    }
+    switch (vw) {
+      case 4: k_refine_smem_batch<4><<<cnt, kFusedBlock, gsmem[gi], s>>>(a); break;
+      case 8: k_refine_smem_batch<8><<<cnt, kFusedBlock, gsmem[gi], s>>>(a); break;
+      case 16: k_refine_smem_batch<16><<<cnt, kFusedBlock, gsmem[gi], s>>>(a); break;
+      default: k_refine_smem_batch<32><<<cnt, kFusedBlock, gsmem[gi], s>>>(a); break;
+    }
+    count_launch();
+    GIM_LAUNCH_CHECK();
+  }
+  // read back the job states (status: strong pass due) in launch order
+  FusedState* hs = static_cast<FusedState*>(pinned_scratch(sizeof(FusedState) * (size_t)J));
+  GIM_CUDA(cudaMemcpyAsync(hs, states, sizeof(FusedState) * (size_t)J, cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(sync_stream(s));
+  for (int j = 0; j < J; ++j) {
+    // states are indexed by the original job (A.st = states + j)
+    yielded[(size_t)j] = hs[j].status != 0;
+    jobs[(size_t)j].iters = hs[j].iters;
+    jobs[(size_t)j].lp = hs[j].lp;
+    jobs[(size_t)j].weak = hs[j].weak;
+  }
+  (void)order;
 }
 
 }  // namespace gim

@@ -390,6 +390,11 @@ def set_fused(on: bool) -> None:
     _lib.load().gim_set_fused(1 if on else 0)
 
 
+def set_batch(on: bool) -> None:
+    """Batched partitioning of the multisection's small leaf-parent subgraphs."""
+    _lib.load().gim_set_batch(1 if on else 0)
+
+
 def set_rowwise_contraction(on: bool) -> None:
     """Row-wise contraction of matchings vs the radix-sort path."""
     _lib.load().gim_set_rowwise_contraction(1 if on else 0)
