@@ -96,15 +96,16 @@ __global__ void __launch_bounds__(kBcBlock) k_coarsen_small(BcJob* jobs) {
   const int* w = J.w;
   const int* vw = J.vw;
   int n = J.n;
+  long long m2 = J.m2;
   for (int lev = 0;; ++lev) {
     if ((long long)n < J.threshold) break;
     if (lev + 1 >= kBcMaxLevels) {
       if (threadIdx.x == 0) J.status = 1;
       break;
     }
-    // scratch of this level: partner, pref / elig, cmap (kept), mem, L/ub, cnt
-    const long long need = 7ll * n + 4 + 2ll * J.m2 * 2;  // rough upper bound incl. temp pairs
-    if (s_top + need + 4ll * n + 3ll * J.m2 > J.cap) {
+    // this level needs <= 4n (partner, elig, pref, cmap) + 5 n_c + 2 (mem, L,
+    // cnt, cvw) + 2 m2 (staged pairs) + 2 n_c + 1 + 2 m2 (the coarse level)
+    if (s_top + 11ll * n + 4ll * m2 + 8 > J.cap) {
       if (threadIdx.x == 0) J.status = 1;
       break;
     }
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kBcBlock) k_coarsen_small(BcJob* jobs) {
     int* tk = cvw + n_c;     // [ubtot] staged keys
     int* tw = tk + ubtot;    // [ubtot] staged weights
     long long after = (tw + ubtot) - A;
-    if (after + 3ll * n_c + 2ll * ubtot + 8 > J.cap) {
+    if (after + 2ll * n_c + 1 + 2ll * ubtot + 8 > J.cap) {
       if (threadIdx.x == 0) J.status = 1;
       break;
     }
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kBcBlock) k_coarsen_small(BcJob* jobs) {
     w = nw;
     vw = nvw;
     n = n_c;
+    m2 = m2c;
   }
   (void)s_stop;
 }

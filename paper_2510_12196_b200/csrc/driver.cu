@@ -122,9 +122,11 @@ static long long max_of(const std::vector<long long>& x) {
 
 // Alg. 4 with the persistent cooperative kernel (refine_fused.cu); the host
 // only performs the rare strong passes the kernel hands back.
+// `resume`: continue a refinement whose fused kernel (a batched launch) handed
+// back a strong pass; rb.best / rb.best_bw hold its best copy
 static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long long* bw_d,
                                const RefCfg& cfg, double l_max, RunStats& st, RefineBuffers& rb,
-                               cudaStream_t s) {
+                               cudaStream_t s, const FusedState* resume = nullptr) {
   const int n = L.g.n, k = t.k;
   FusedBuffers fb;
   fb.cand = rb.cand.get();
@@ -159,13 +161,19 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   fc.seed = cfg.seed;
   GIM_CUDA(cudaMemsetAsync(fb.state, 0, sizeof(FusedState), s));
   GIM_CUDA(cudaMemsetAsync(fb.ctr, 0, 17 * sizeof(long long), s));
+  bool skip_launch = false;
+  if (resume) {
+    hs = *resume;
+    skip_launch = true;
+  }
   long long strong = 0;
   bool host_finished = false;
   std::vector<long long> bw((size_t)k);
   std::vector<unsigned char> masks((size_t)k * 2);
   std::vector<int> el((size_t)k);
   for (;;) {
-    if (refine_fused_run(L, t, part, bw_d, fc, fb, s)) break;
+    if (!skip_launch && refine_fused_run(L, t, part, bw_d, fc, fb, s)) break;
+    skip_launch = false;
     // strong pass (refinement.py:350-386) + the same Alg. 4 bookkeeping
     GIM_CUDA(cudaMemcpyAsync(bw.data(), bw_d, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
     GIM_CUDA(sync_stream(s));
@@ -482,10 +490,48 @@ struct BatchPartJob {
 
 // batch-eligible: small enough that every level refines shared-memory resident
 static std::atomic<bool> g_batch{true};
-constexpr int kBatchMaxN = 1000;
+constexpr int kBatchMaxN = 16384;
+
+// jobs the batch hands back: general path, one host thread / stream each
+static void general_parallel(const std::vector<BatchPartJob*>& jobs, int parts, RunStats& st,
+                             cudaStream_t s) {
+  if (jobs.empty()) return;
+  if (jobs.size() == 1) {
+    BatchPartJob& B = *jobs[0];
+    internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+    return;
+  }
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  GIM_CUDA(sync_stream(s));
+  std::vector<std::thread> workers;
+  std::vector<std::exception_ptr> errs(jobs.size());
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    workers.emplace_back([&, j] {
+      cudaStream_t cs = nullptr;
+      try {
+        GIM_CUDA(cudaSetDevice(dev));
+        cs = acquire_stream();
+        BatchPartJob& B = *jobs[j];
+        DBuf<int> p((size_t)std::max(B.g.n, 1), cs);
+        internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, p.get(), st, cs);
+        GIM_CUDA(cudaMemcpyAsync(B.out_part, p.get(), sizeof(int) * B.g.n,
+                                 cudaMemcpyDeviceToDevice, cs));
+        GIM_CUDA(sync_stream(cs));
+      } catch (...) {
+        errs[j] = std::current_exception();
+      }
+      release_stream(cs);
+    });
+  }
+  for (auto& w : workers) w.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
 
 static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int parts, RunStats& st,
                                        cudaStream_t s) {
+  std::vector<BatchPartJob*> general;
   std::vector<int> fast;  // jobs on the batched path
   for (int j = 0; j < (int)jobs.size(); ++j) {
     BatchPartJob& B = jobs[(size_t)j];
@@ -514,18 +560,19 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
   std::vector<int> ok;
   for (int i = 0; i < J; ++i) {
     const SmallStack& S = stacks[(size_t)i];
-    bool fits = S.status == 0;
-    if (fits)
-      for (const DevGraph& g : S.levels)
-        fits = fits && refine_smem_fits(g.n, g.m2, parts, 2, refine_pick_vw(g.n, g.m2));
-    if (fits) {
+    if (S.status == 0) {
       ok.push_back(i);
     } else {
       BatchPartJob& B = jobs[(size_t)fast[(size_t)i]];
-      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+      if (std::getenv("GIM_BATCH_DEBUG"))
+        std::fprintf(stderr, "[batch-debug] job n=%d: level stack needs the general path\n", B.g.n);
+      general.push_back(&B);
     }
   }
-  if (ok.empty()) return;
+  if (ok.empty()) {
+    general_parallel(general, parts, st, s);
+    return;
+  }
   static const bool debug = std::getenv("GIM_BATCH_DEBUG") != nullptr;
   if (debug) {  // compare every fast-path level stack with the general one
     for (int i : ok) {
@@ -564,7 +611,7 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
   }
   DBuf<int> pa((size_t)K * nmax, s), pb((size_t)K * nmax, s), best((size_t)K * nmax, s);
   DBuf<long long> bw((size_t)K * parts, s), best_bw((size_t)K * parts, s);
-  DBuf<FusedState> states((size_t)K, s);
+  DBuf<FusedState> states((size_t)2 * K, s);
   std::vector<int*> cur((size_t)K), nxt((size_t)K);
   for (int q = 0; q < K; ++q) {
     cur[(size_t)q] = pa.get() + (size_t)q * nmax;
@@ -584,8 +631,8 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
   std::vector<char> failed((size_t)K, 0);
   for (int t = 0; t < lmaxn; ++t) {
     std::vector<BpJob> bp;
-    std::vector<SmemRefineJob> rj;
-    std::vector<int> who;
+    std::vector<SmemRefineJob> rj, rc;  // shared-memory resident / cluster
+    std::vector<int> who, whoc;
     for (int q = 0; q < K; ++q) {
       if (failed[(size_t)q]) continue;
       const int i = ok[(size_t)q];
@@ -617,18 +664,59 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
       R.cfg.seed = cfg.seed;
       R.best = best.get() + (size_t)q * nmax;
       R.best_bw = best_bw.get() + (size_t)q * parts;
-      rj.push_back(R);
-      who.push_back(q);
+      if (refine_smem_fits(g.n, g.m2, parts, R.cfg.rho, R.vw)) {
+        rj.push_back(R);
+        who.push_back(q);
+      } else {
+        rc.push_back(R);
+        whoc.push_back(q);
+      }
     }
-    if (rj.empty()) continue;
+    if (rj.empty() && rc.empty()) continue;
     bproj_bw_batch(bp, s);
     std::vector<char> yielded;
-    refine_smem_batch(rj, tf, states.get(), yielded, s);
-    for (size_t r = 0; r < rj.size(); ++r) {
-      st.init_refine_iterations += rj[r].iters;
-      st.lp += rj[r].lp;
-      st.weak += rj[r].weak;
-      if (yielded[r]) failed[(size_t)who[r]] = 1;  // strong pass due: general path
+    // a refinement that handed back a strong pass resumes on the general
+    // device loop (host strong pass, relaunches) exactly where it stopped
+    auto account = [&](std::vector<SmemRefineJob>& v, const std::vector<int>& w,
+                       FusedState* dstates) {
+      for (size_t r = 0; r < v.size(); ++r) {
+        if (!yielded[r]) {
+          st.init_refine_iterations += v[r].iters;
+          st.lp += v[r].lp;
+          st.weak += v[r].weak;
+          continue;
+        }
+        const int q = w[r];
+        const int i = ok[(size_t)q];
+        const SmallStack& S = stacks[(size_t)i];
+        const int li = S.nl - 1 - t;
+        const BatchPartJob& B = jobs[(size_t)fast[(size_t)i]];
+        RefCfg cfg = config_for_level(li, S.nl, 0.999, 2, 1, 0.25, 0.065, 0.005, 10,
+                                      hash2(B.seed, 101, (unsigned long long)li));
+        FusedState hs0;
+        GIM_CUDA(cudaMemcpyAsync(&hs0, dstates + r, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
+        RefineLevel L;
+        L.g = v[r].g;
+        prepare_level(L, parts, s);
+        RefineBuffers rb;
+        alloc_refine_buffers(rb, L.g.n, parts, s);
+        GIM_CUDA(cudaMemcpyAsync(rb.best.get(), v[r].best, sizeof(int) * (size_t)L.g.n,
+                                 cudaMemcpyDeviceToDevice, s));
+        GIM_CUDA(cudaMemcpyAsync(rb.best_bw.get(), v[r].best_bw, sizeof(long long) * parts,
+                                 cudaMemcpyDeviceToDevice, s));
+        GIM_CUDA(sync_stream(s));
+        if (std::getenv("GIM_BATCH_DEBUG"))
+          std::fprintf(stderr, "[batch-debug] job n=%d: strong pass, resumed\n", v[r].g.n);
+        refine_device_loop(L, tf, v[r].part, v[r].bw, cfg, v[r].cfg.l_max, st, rb, s, &hs0);
+      }
+    };
+    if (!rc.empty()) {
+      refine_cluster_batch(rc, tf, states.get() + K, yielded, s);
+      account(rc, whoc, states.get() + K);
+    }
+    if (!rj.empty()) {
+      refine_smem_batch(rj, tf, states.get(), yielded, s);
+      account(rj, who, states.get());
     }
   }
   if (debug) {  // final partitions vs the general path
@@ -651,12 +739,13 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
   for (int q = 0; q < K; ++q) {
     BatchPartJob& B = jobs[(size_t)fast[(size_t)ok[(size_t)q]]];
     if (failed[(size_t)q]) {
-      internal_partitioner(B.g, B.total, parts, B.eps_local, B.seed, B.out_part, st, s);
+      general.push_back(&B);
       continue;
     }
     GIM_CUDA(cudaMemcpyAsync(B.out_part, cur[(size_t)q], sizeof(int) * (size_t)B.g.n,
                              cudaMemcpyDeviceToDevice, s));
   }
+  general_parallel(general, parts, st, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -805,6 +894,123 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     if (e) std::rethrow_exception(e);
 }
 
+// Breadth-first multisection: all nodes of one tree level are partitioned
+// together — as one batch when they are small (internal_partitioner_batch),
+// else one host thread per node — then all their children are extracted.
+// Every node computes exactly what descend() computes for it; only the
+// order of independent work changes.
+struct MsNode {
+  OwnedGraph own;  // empty for the root
+  DevGraph g;
+  DBuf<int> trans_own;
+  const int* trans = nullptr;
+  long long total = 0;
+  std::vector<int> ident;
+  unsigned long long seed = 0;
+};
+
+static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, const int* ids,
+                             unsigned long long seed, cudaStream_t s) {
+  std::vector<MsNode> nodes(1);
+  nodes[0].g = root;
+  nodes[0].trans = ids;
+  nodes[0].total = total;
+  nodes[0].seed = seed;
+  for (int level = (int)C.h.size(); level >= 1; --level) {
+    const int parts = (int)C.h[level - 1];
+    long long k_sub = 1;
+    for (int i = 0; i < level; ++i) k_sub *= C.h[i];
+    const int N = (int)nodes.size();
+    std::vector<DBuf<int>> part((size_t)N);
+    for (int j = 0; j < N; ++j) part[(size_t)j] = DBuf<int>((size_t)std::max(nodes[(size_t)j].g.n, 1), s);
+    bool small = parts > 1;
+    for (const MsNode& nd : nodes) small = small && nd.g.n <= kBatchMaxN;
+    if (parts == 1) {
+      for (int j = 0; j < N; ++j)
+        GIM_CUDA(cudaMemsetAsync(part[(size_t)j].get(), 0, sizeof(int) * nodes[(size_t)j].g.n, s));
+    } else if (small) {
+      std::vector<BatchPartJob> jobs;
+      for (int j = 0; j < N; ++j) {
+        const MsNode& nd = nodes[(size_t)j];
+        jobs.push_back(BatchPartJob{nd.g, nd.total,
+                                    adaptive_imbalance(C.eps, C.total, nd.total, C.k, k_sub, level),
+                                    nd.seed, part[(size_t)j].get()});
+      }
+      internal_partitioner_batch(jobs, parts, *C.st, s);
+    } else if (N == 1 || !C.threads) {
+      for (int j = 0; j < N; ++j) {
+        const MsNode& nd = nodes[(size_t)j];
+        internal_partitioner(nd.g, nd.total, parts,
+                             adaptive_imbalance(C.eps, C.total, nd.total, C.k, k_sub, level),
+                             nd.seed, part[(size_t)j].get(), *C.st, s);
+      }
+    } else {  // large nodes: one host thread / stream each
+      GIM_CUDA(sync_stream(s));
+      std::vector<std::thread> workers;
+      std::vector<std::exception_ptr> errs((size_t)N);
+      for (int j = 0; j < N; ++j) {
+        workers.emplace_back([&, j] {
+          cudaStream_t cs = nullptr;
+          try {
+            GIM_CUDA(cudaSetDevice(C.device));
+            cs = acquire_stream();
+            const MsNode& nd = nodes[(size_t)j];
+            DBuf<int> p((size_t)std::max(nd.g.n, 1), cs);
+            internal_partitioner(nd.g, nd.total, parts,
+                                 adaptive_imbalance(C.eps, C.total, nd.total, C.k, k_sub, level),
+                                 nd.seed, p.get(), *C.st, cs);
+            GIM_CUDA(cudaMemcpyAsync(part[(size_t)j].get(), p.get(), sizeof(int) * nd.g.n,
+                                     cudaMemcpyDeviceToDevice, cs));
+            GIM_CUDA(sync_stream(cs));
+          } catch (...) {
+            errs[(size_t)j] = std::current_exception();
+          }
+          release_stream(cs);
+        });
+      }
+      for (auto& w : workers) w.join();
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    }
+    if (level == 1) {  // leaves (pipelines.py:78-80)
+      for (int j = 0; j < N; ++j) {
+        MsNode& nd = nodes[(size_t)j];
+        nd.ident.push_back(0);
+        const int base = calc_id(C.h, nd.ident);
+        leaf_scatter(nd.g.n, nd.trans, part[(size_t)j].get(), base, C.assignment, s);
+      }
+      return;
+    }
+    std::vector<MsNode> next;
+    for (int j = 0; j < N; ++j) {
+      MsNode& nd = nodes[(size_t)j];
+      DBuf<long long> bw((size_t)parts, s);
+      block_weights(nd.g.n, nd.g.vw, part[(size_t)j].get(), parts, bw.get(), s);
+      std::vector<long long> child_total((size_t)parts);
+      GIM_CUDA(cudaMemcpyAsync(child_total.data(), bw.get(), sizeof(long long) * parts,
+                               cudaMemcpyDeviceToHost, s));
+      std::vector<OwnedGraph> subs;
+      std::vector<DBuf<int>> sids;
+      extract_subgraphs(nd.g, part[(size_t)j].get(), parts, subs, sids, s);  // synchronizes s
+      for (int c = 0; c < parts; ++c) {
+        if (subs[(size_t)c].n == 0) continue;  // descend() returns at once for empty nodes
+        MsNode ch;
+        ch.own = std::move(subs[(size_t)c]);
+        ch.g = ch.own.view();
+        ch.trans_own = DBuf<int>((size_t)std::max(ch.g.n, 1), s);
+        gather(ch.g.n, sids[(size_t)c].get(), nd.trans, ch.trans_own.get(), s);
+        ch.trans = ch.trans_own.get();
+        ch.total = child_total[(size_t)c];
+        ch.ident = nd.ident;
+        ch.ident.push_back(c);
+        ch.seed = hash2(nd.seed, (unsigned long long)level, (unsigned long long)c);
+        next.push_back(std::move(ch));
+      }
+    }
+    nodes = std::move(next);
+  }
+}
+
 static void hierarchical_multisection(const DevGraph& g, long long total,
                                       const std::vector<long long>& h,
                                       const std::vector<long long>& d, double eps,
@@ -826,6 +1032,10 @@ static void hierarchical_multisection(const DevGraph& g, long long total,
   DBuf<int> ident_ids((size_t)g.n, s);
   k_iota<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, ident_ids.get());
   count_launch();
+  if (g_batch.load()) {
+    multisection_bfs(C, g, total, ident_ids.get(), seed, s);
+    return;
+  }
   std::vector<int> ident;
   descend(C, g, total, (int)h.size(), ident, ident_ids.get(), seed, s);
 }

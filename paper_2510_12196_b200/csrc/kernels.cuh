@@ -187,6 +187,8 @@ bool refine_smem_fits(long long n, long long m2, int k, int rho, int vw);
 int refine_pick_vw(long long n, long long m2);
 void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedState* states,
                        std::vector<char>& yielded, cudaStream_t s);
+void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedState* states,
+                          std::vector<char>& yielded, cudaStream_t s);
 bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long* bw,
                       const FusedCfg& cfg, FusedBuffers& fb, cudaStream_t s);
 

@@ -94,6 +94,7 @@ struct FusedArgs {
   int smem_base;       // k_refine_smem: bytes of the regular dynamic region
   int vc_steps;        // vertex-centric first filters up to vc_steps vertices per thread
   int solo;            // 1: this CTA is a whole refinement (batched launch)
+  int csize;           // >0: one cluster of csize CTAs per refinement (batched launch)
   long long* ptime;    // [16] per-phase ns (trace mode) or null
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
@@ -200,8 +201,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   const int NC = 31 * A.rho;
   const int n = A.n;
   // a batched shared-memory launch runs one independent refinement per CTA
-  const int G = A.solo ? 1 : (int)gridDim.x;
-  const int BX = A.solo ? 0 : (int)blockIdx.x;
+  // (or one thread-block cluster per refinement: csize CTAs each)
+  const int G = A.solo ? 1 : A.csize ? A.csize : (int)gridDim.x;
+  const int BX = A.solo ? 0 : A.csize ? (int)(blockIdx.x % A.csize) : (int)blockIdx.x;
   // dynamic smem: pstar[k] | run[k] | code[k] | warp tables | elist[k] | cstar[k] |
   // wrun[warps*k] | ovl[k] | elig[k]
   long long* pstar = reinterpret_cast<long long*>(dsm);
@@ -900,6 +902,13 @@ __global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
   refine_body<VW>(A);
 }
 
+// one thread-block cluster per independent refinement (batched launch)
+template <int VW>
+__global__ void __launch_bounds__(kFusedBlock) k_refine_cluster_batch(const FusedArgs* args,
+                                                                      int csize) {
+  refine_body<VW>(args[blockIdx.x / csize]);
+}
+
 // Shared-memory-resident refinement of a small graph: ONE CTA copies the
 // CSR, the mapping and every per-vertex work array into shared memory and
 // runs the same Alg. 4 loop on them (generic pointers), so every gather in
@@ -1176,6 +1185,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.smem_base = (int)smem;
   A.vc_steps = vc_steps();
   A.solo = 0;
+  A.csize = 0;
   A.ptime = nullptr;
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
@@ -1314,6 +1324,7 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
     A.st = states + j;
     A.bar_mode = 0;
     A.solo = 1;
+    A.csize = 0;
     A.smem_base = (int)base;
     A.vc_steps = vc_steps();
     A.ptime = nullptr;
@@ -1391,6 +1402,145 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
     jobs[(size_t)j].weak = hs[j].weak;
   }
   (void)order;
+}
+
+// batched cluster-mode refinement: one cluster per job, per-job scratch in
+// global memory (levels too large to be shared-memory resident)
+void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedState* states,
+                          std::vector<char>& yielded, cudaStream_t s) {
+  const int J = (int)jobs.size();
+  yielded.assign((size_t)J, 0);
+  if (J == 0) return;
+  const int k = t.k;
+  const size_t base = refine_smem_regular_bytes(k);
+  GIM_CUDA(cudaMemsetAsync(states, 0, sizeof(FusedState) * (size_t)J, s));
+  // scratch arena: per job 8 int arrays, gkey, 3 byte arrays, W, S, ctr
+  std::vector<size_t> off((size_t)J + 1, 0);
+  auto words = [&](const SmemRefineJob& R) {
+    const size_t n = (size_t)std::max(R.g.n, 1), NC = 31 * (size_t)R.cfg.rho;
+    return 8 * n + 2 * n + (3 * n + 7) / 4 + 2 * ((size_t)k * NC + (size_t)k * kMaxCluster + 17) + 8;
+  };
+  for (int j = 0; j < J; ++j) off[(size_t)j + 1] = off[(size_t)j] + ((words(jobs[(size_t)j]) + 3) & ~(size_t)3);
+  DBuf<int> arena(off[(size_t)J], s);
+  std::vector<FusedArgs> host((size_t)J);
+  for (int j = 0; j < J; ++j) {
+    const SmemRefineJob& R = jobs[(size_t)j];
+    const size_t n = (size_t)std::max(R.g.n, 1), NC = 31 * (size_t)R.cfg.rho;
+    int* a = arena.get() + off[(size_t)j];
+    FusedArgs A{};
+    A.n = R.g.n;
+    A.m2 = R.g.m2;
+    A.off = R.g.off;
+    A.tgt = R.g.tgt;
+    A.w = R.g.w;
+    A.vw = R.g.vw;
+    A.src = nullptr;
+    A.t = t;
+    A.k = k;
+    A.part = R.part;
+    A.bw = R.bw;
+    A.best = R.best;
+    A.best_bw = R.best_bw;
+    A.dest = a;
+    A.rtgt = a + n;
+    A.lsmall = a + 2 * n;
+    A.lheavy = a + 3 * n;
+    A.lcand = a + 4 * n;
+    A.lmov0 = a + 5 * n;
+    A.lmov1 = a + 6 * n;
+    A.bstamp = nullptr;
+    long long* q = reinterpret_cast<long long*>(a + 8 * n);  // 8-byte aligned (n ints * 8)
+    A.gkey = q;
+    A.W = q + n;
+    A.S = A.W + (size_t)k * NC;
+    A.ctr = A.S + (size_t)k * kMaxCluster;
+    unsigned char* b = reinterpret_cast<unsigned char*>(A.ctr + 17);
+    A.flags0 = b;
+    A.flags1 = b + n;
+    A.rcell = b + 2 * n;
+    A.st = states + j;
+    A.smem_base = (int)base;
+    A.vc_steps = vc_steps();
+    A.solo = 0;
+    A.ptime = nullptr;
+    A.l_max = R.cfg.l_max;
+    A.sigma = R.cfg.sigma;
+    A.phi = R.cfg.phi;
+    A.jet_c = R.cfg.jet_c;
+    A.jet = R.cfg.jet;
+    A.rho = R.cfg.rho;
+    A.i_max = R.cfg.i_max;
+    A.i_w_max = R.cfg.i_w_max;
+    A.seed = R.cfg.seed;
+    host[(size_t)j] = A;
+    GIM_CUDA(cudaMemsetAsync(A.ctr, 0, 17 * sizeof(long long), s));
+  }
+  const int vpc = cluster_vertices_per_cta();
+  DBuf<FusedArgs> dargs((size_t)J, s);
+  std::vector<FusedArgs> ordered;
+  struct Grp { int vw, first, cnt, cs; };
+  std::vector<Grp> groups;
+  for (int vw : {4, 8, 16, 32}) {
+    const int first = (int)ordered.size();
+    int cs = 1;
+    for (int j = 0; j < J; ++j)
+      if (jobs[(size_t)j].vw == vw) {
+        cs = std::max(cs, std::min(kMaxCluster, (jobs[(size_t)j].g.n + vpc - 1) / vpc));
+        ordered.push_back(host[(size_t)j]);
+      }
+    const int cnt = (int)ordered.size() - first;
+    if (cnt) {
+      for (int i = first; i < first + cnt; ++i) {
+        ordered[(size_t)i].csize = cs;
+        ordered[(size_t)i].bar_mode = cs > 1 ? 1 : 0;
+      }
+      groups.push_back({vw, first, cnt, cs});
+    }
+  }
+  GIM_CUDA(cudaMemcpyAsync(dargs.get(), ordered.data(), sizeof(FusedArgs) * (size_t)J,
+                           cudaMemcpyHostToDevice, s));  // pageable: staged before return
+  static std::once_flag once[4];
+  for (const Grp& g : groups) {
+    void* fn = nullptr;
+    int slot = 0;
+    switch (g.vw) {
+      case 4: fn = (void*)k_refine_cluster_batch<4>; slot = 0; break;
+      case 8: fn = (void*)k_refine_cluster_batch<8>; slot = 1; break;
+      case 16: fn = (void*)k_refine_cluster_batch<16>; slot = 2; break;
+      default: fn = (void*)k_refine_cluster_batch<32>; slot = 3; break;
+    }
+    std::call_once(once[slot], [&] {
+      GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)std::max<size_t>(base, 48 * 1024)));
+    });
+    const FusedArgs* a = dargs.get() + g.first;
+    int cs = g.cs;
+    void* args[] = {(void*)&a, (void*)&cs};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)(g.cnt * g.cs));
+    lc.blockDim = dim3(kFusedBlock);
+    lc.dynamicSmemBytes = base;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)g.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    GIM_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+    count_launch();
+  }
+  FusedState* hs = static_cast<FusedState*>(pinned_scratch(sizeof(FusedState) * (size_t)J));
+  GIM_CUDA(cudaMemcpyAsync(hs, states, sizeof(FusedState) * (size_t)J, cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(sync_stream(s));
+  for (int j = 0; j < J; ++j) {
+    yielded[(size_t)j] = hs[j].status != 0;
+    jobs[(size_t)j].iters = hs[j].iters;
+    jobs[(size_t)j].lp = hs[j].lp;
+    jobs[(size_t)j].weak = hs[j].weak;
+  }
 }
 
 }  // namespace gim
