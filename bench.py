@@ -207,6 +207,23 @@ def ncu_traffic(cls: str):
     return None
 
 
+def max_over_ranks(x: float, world: int, device) -> float:
+    """The job's time is the slowest rank's (replicas run concurrently)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(m: int, steps: int, world: int, max_total_ms: float) -> float:
+    """Whole-job edges/s: every rank maps the graph `steps` times (weak
+    scaling: per-GPU work fixed), the job ends with the slowest rank."""
+    return m * steps * world / (max_total_ms / 1000.0)
+
+
 def run_gpu(args) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -237,11 +254,7 @@ def run_gpu(args) -> dict | None:
         torch.cuda.synchronize()
 
     def maxed(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks(x, world, "cuda")
 
     # warm-up (also JIT-free: libgpuim is prebuilt)
     for w in range(args.warmup):
@@ -269,7 +282,7 @@ def run_gpu(args) -> dict | None:
             last = st
     barrier()
     total_ms = maxed(sum(step_ms))
-    value = g.m * args.steps * world / (total_ms / 1000.0)
+    value = job_throughput(g.m, args.steps, world, total_ms)
 
     # ---- kernel attribution: one extra map with per-scope CUDA events and
     # the multisection fan-out off, so scopes on concurrent streams do not
@@ -308,7 +321,7 @@ def run_gpu(args) -> dict | None:
         assert m.max_block_weight() <= (1.0 + EPS) * g.total_weight / k
     barrier()
     e2e_total = maxed(sum(e2e_ms))
-    e2e_value = g.m * args.steps * world / (e2e_total / 1000.0)
+    e2e_value = job_throughput(g.m, args.steps, world, e2e_total)
     # bytes that cross PCIe: the CSR narrowed to int32 on the host, the int32
     # assignment and the int64 block weights back
     h2d = 4 * (g.n + 1) + 4 * len(g.edge_targets) * 2 + 4 * g.n

@@ -287,3 +287,52 @@ def test_integrated_map_matches_oracle_rgg(D, mode):
     a, bw, l_max = O.integrated_map(g, t, 0.03, 0, coarsest_factor=16)
     assert np.array_equal(m.assignment, a)
     assert m.max_block_weight() <= l_max
+
+
+@pytest.mark.parametrize("logn", [13, 16])
+def test_batched_multisection_equals_recursive(D, logn):
+    """The breadth-first, batched multisection (one launch per phase for all
+    small tree nodes, strong passes resumed on the device loop) computes the
+    same assignment as the recursive per-node path."""
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << logn, 0.55, 1)
+    dg = D.DeviceGraph.from_host(g)
+    h, d = (4, 8, 6), (1, 10, 100)
+    try:
+        D.set_batch(False)
+        a = np_(D.hierarchical_multisection(dg, h, d, 0.03, 5))
+        D.set_batch(True)
+        b = np_(D.hierarchical_multisection(dg, h, d, 0.03, 5))
+    finally:
+        D.set_batch(True)
+    assert np.array_equal(a, b)
+
+
+def test_batched_integrated_map_equals_recursive(D):
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << 16, 0.55, 1)
+    dg = D.DeviceGraph.from_host(g)
+    h, d = (4, 8, 6), (1, 10, 100)
+    try:
+        D.set_batch(False)
+        a, bwa, sa = D.integrated_map_device(dg, h, d, 0.03, 2)
+        D.set_batch(True)
+        b, bwb, sb = D.integrated_map_device(dg, h, d, 0.03, 2)
+    finally:
+        D.set_batch(True)
+    assert np.array_equal(np_(a), np_(b))
+    assert np.array_equal(np_(bwa), np_(bwb))
+    assert sa["final_j"] == sb["final_j"]
+
+
+def test_rmat_small_matches_oracle(D):
+    """Skewed degrees: two-hop matching and hub rows (general-path fallbacks
+    of the batched partitioner, radix contraction) — identical to the oracle."""
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(11)
+    t = O.OTopology((2, 4, 2), (1, 10, 100))
+    m = integrated_map(g, t, 0.03, 1, coarsest_factor=16)
+    a, bw, l_max = O.integrated_map(g, t, 0.03, 1, coarsest_factor=16)
+    assert np.array_equal(m.assignment, a)
+    assert np.array_equal(m.block_weights, bw)
