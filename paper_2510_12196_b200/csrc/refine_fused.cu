@@ -4,14 +4,15 @@
 // J tracking and best-mapping bookkeeping — with grid-wide barriers between
 // phases and no host round trip per iteration.
 //
-// Work lists.  Every phase starts from a compact list instead of sweeping
-// all vertices with one warp each: an edge-parallel, vectorised sweep stamps
-// boundary vertices (some neighbour in another block — only they can have a
-// label-propagation candidate, refinement.py:187-190), a vertex sweep
-// compacts them, and the gain evaluation, second filter, move application
-// and commit then run over the boundary / candidate / mover lists.  Lists
-// are appended with warp-aggregated atomics (order is irrelevant: every
-// per-vertex result and every reduction is order-independent integer math).
+// Work lists.  Gains are evaluated thread-per-vertex (eval_thread): small
+// levels sweep every vertex directly; large levels first compact the
+// boundary vertices from ext[v] (#neighbours in another block, initialised
+// per launch and kept exact by the move application), so no per-iteration
+// boundary pass over the edges is needed.  The second filter, move
+// application and commit run over the candidate / mover lists.  Lists are
+// appended through warp-private shared-memory queues (one global atomic per
+// >= 32 entries; order is irrelevant: every per-vertex result and every
+// reduction is order-independent integer math).
 // Invariants kept between iterations: gkey = LLONG_MIN and rtgt = -1 for
 // every non-candidate; move flags are set only for the current movers and
 // the lock set (= previous LP movers), both listed, so resets touch only
