@@ -294,6 +294,128 @@ __global__ void __launch_bounds__(256) k_bproj_bw(const BpJob* jobs) {
   for (int b = threadIdx.x; b < J.k; b += blockDim.x) J.bw[b] = hist[b];
 }
 
+// ---- batched subgraph extraction (graph.py:357-389) for one tree level:
+// one CTA per node; children get local ids in vertex order, rows keep only
+// slots inside the part in CSR order, plus the children's global ids.
+// Child c of a node lives at the node's arena offset cbase[c]; every array
+// starts 16-byte aligned (the edge-parallel kernels load int4):
+// off[n_c + 1] | tgt[m2_c] | w[m2_c] | src[m2_c] | vw[n_c] | trans[n_c]
+
+__host__ __device__ __forceinline__ long long ex_r4(long long x) { return (x + 3) & ~3ll; }
+
+constexpr int kExBlock = 512;
+constexpr int kExMaxParts = 64;
+
+struct ExNode {
+  int n, parts;
+  const int* off;
+  const int* tgt;
+  const int* w;
+  const int* vw;
+  const int* part;
+  const int* trans;    // global ids of the node's vertices
+  int* arena;
+  long long cap;       // words
+  int* scratch;        // [2 n]: local ids, kept degrees / offsets
+  // out
+  int status;
+  int cn[kExMaxParts], cm2[kExMaxParts];
+  long long cbase[kExMaxParts];
+  long long ctotal[kExMaxParts];
+};
+
+__global__ void __launch_bounds__(kExBlock) k_extract_batch(ExNode* nodes) {
+  ExNode& X = nodes[blockIdx.x];
+  const int n = X.n, P = X.parts;
+  int* local = X.scratch;
+  int* kdeg = X.scratch + n;
+  __shared__ int s_cnt[kExMaxParts], s_m2[kExMaxParts];
+  __shared__ long long s_tot[kExMaxParts];
+  for (int c = threadIdx.x; c < P; c += kExBlock) {
+    s_cnt[c] = 0;
+    s_m2[c] = 0;
+    s_tot[c] = 0;
+  }
+  __syncthreads();
+  // per part: local ids (stable ranks) and kept-degree prefix sums, by CTA
+  // scans over the vertex range (parts are few)
+  for (int c = 0; c < P; ++c) {
+    int carry = 0, carry2 = 0;
+    long long tot = 0;
+    __shared__ int t1, t2;
+    for (int base = 0; base < n; base += kExBlock) {
+      const int v = base + threadIdx.x;
+      int in = 0, kd = 0;
+      if (v < n && X.part[v] == c) {
+        in = 1;
+        for (int e = X.off[v]; e < X.off[v + 1]; ++e) kd += X.part[X.tgt[e]] == c;
+        tot += X.vw[v];
+      }
+      const int ex = block_excl_scan<int, kExBlock>(in, &t1);
+      const int ex2 = block_excl_scan<int, kExBlock>(kd, &t2);
+      if (in) {
+        local[v] = carry + ex;
+        kdeg[v] = carry2 + ex2;  // row offset inside the child
+      }
+      carry += t1;
+      carry2 += t2;
+      __syncthreads();
+    }
+    tot = bc_sum(tot);
+    if (threadIdx.x == 0) {
+      s_cnt[c] = carry;
+      s_m2[c] = carry2;
+      s_tot[c] = tot;
+    }
+  }
+  __syncthreads();
+  // arena layout of the children
+  __shared__ long long s_base[kExMaxParts];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) {
+    long long at = 0;
+    s_bad = 0;
+    for (int c = 0; c < P; ++c) {
+      s_base[c] = at;
+      at += ex_r4(s_cnt[c] + 1ll) + 3 * ex_r4(s_m2[c]) + 2 * ex_r4(s_cnt[c]);
+    }
+    if (at > X.cap) s_bad = 1;
+    X.status = s_bad;
+    for (int c = 0; c < P; ++c) {
+      X.cn[c] = s_cnt[c];
+      X.cm2[c] = s_m2[c];
+      X.cbase[c] = s_base[c];
+      X.ctotal[c] = s_tot[c];
+    }
+  }
+  __syncthreads();
+  if (s_bad) return;
+  for (int v = threadIdx.x; v < n; v += kExBlock) {
+    const int c = X.part[v];
+    const int nc = s_cnt[c], mc = s_m2[c];
+    int* co = X.arena + s_base[c];
+    int* ct = co + ex_r4(nc + 1ll);
+    int* cw = ct + ex_r4(mc);
+    int* cs = cw + ex_r4(mc);
+    int* cv = cs + ex_r4(mc);
+    int* cg = cv + ex_r4(nc);
+    const int lv = local[v];
+    int o = kdeg[v];
+    co[lv] = o;
+    if (lv == nc - 1) co[nc] = mc;
+    cv[lv] = X.vw[v];
+    cg[lv] = X.trans[v];
+    for (int e = X.off[v]; e < X.off[v + 1]; ++e) {
+      const int u = X.tgt[e];
+      if (X.part[u] != c) continue;
+      ct[o] = local[u];
+      cw[o] = X.w[e];
+      cs[o] = lv;
+      ++o;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host wrappers
 
@@ -354,6 +476,71 @@ void coarsen_small_batch(const std::vector<DevGraph>& gs, const std::vector<doub
       }
       S.levels.push_back(d);
       S.cmap.push_back(l + 1 < b.nl ? A + L.cmap : nullptr);
+    }
+  }
+}
+
+void extract_batch(const std::vector<DevGraph>& gs, const std::vector<const int*>& parts_of,
+                   const std::vector<const int*>& trans, int parts, std::vector<ExChild>& out,
+                   DBuf<int>& arena, cudaStream_t s) {
+  const int N = (int)gs.size();
+  out.clear();
+  if (N == 0) return;
+  GIM_CHECK(parts <= kExMaxParts, GIM_E_UNSUPPORTED, "too many parts for batched extraction");
+  std::vector<long long> base((size_t)N + 1, 0), sbase((size_t)N + 1, 0);
+  for (int j = 0; j < N; ++j) {
+    const DevGraph& g = gs[(size_t)j];
+    base[(size_t)j + 1] =
+        base[(size_t)j] + ex_r4((g.n + 1ll) * 3 + 3 * g.m2 + 20ll * parts + 64);
+    sbase[(size_t)j + 1] = sbase[(size_t)j] + 2ll * g.n + 4;
+  }
+  arena = DBuf<int>((size_t)base[(size_t)N], s);
+  DBuf<int> scratch((size_t)sbase[(size_t)N], s);
+  std::vector<ExNode> hn((size_t)N);
+  for (int j = 0; j < N; ++j) {
+    const DevGraph& g = gs[(size_t)j];
+    ExNode x{};
+    x.n = g.n;
+    x.parts = parts;
+    x.off = g.off;
+    x.tgt = g.tgt;
+    x.w = g.w;
+    x.vw = g.vw;
+    x.part = parts_of[(size_t)j];
+    x.trans = trans[(size_t)j];
+    x.arena = arena.get() + base[(size_t)j];
+    x.cap = base[(size_t)j + 1] - base[(size_t)j];
+    x.scratch = scratch.get() + sbase[(size_t)j];
+    hn[(size_t)j] = x;
+  }
+  DBuf<ExNode> dn((size_t)N, s);
+  GIM_CUDA(cudaMemcpyAsync(dn.get(), hn.data(), sizeof(ExNode) * (size_t)N,
+                           cudaMemcpyHostToDevice, s));
+  k_extract_batch<<<N, kExBlock, 0, s>>>(dn.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  ExNode* hr = static_cast<ExNode*>(pinned_scratch(sizeof(ExNode) * (size_t)N));
+  GIM_CUDA(cudaMemcpyAsync(hr, dn.get(), sizeof(ExNode) * (size_t)N, cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(sync_stream(s));
+  for (int j = 0; j < N; ++j) {
+    const ExNode& x = hr[j];
+    GIM_CHECK(x.status == 0, GIM_E_INTERNAL, "batched extraction arena overflow");
+    for (int c = 0; c < parts; ++c) {
+      ExChild ch;
+      ch.node = j;
+      ch.part = c;
+      ch.total = x.ctotal[c];
+      int* co = arena.get() + base[(size_t)j] + x.cbase[c];
+      const int nc = x.cn[c], mc = x.cm2[c];
+      ch.g.n = nc;
+      ch.g.m2 = mc;
+      ch.g.off = co;
+      ch.g.tgt = co + ex_r4(nc + 1ll);
+      ch.g.w = ch.g.tgt + ex_r4(mc);
+      ch.g.src = ch.g.w + ex_r4(mc);
+      ch.g.vw = ch.g.src + ex_r4(mc);
+      ch.trans = ch.g.vw + ex_r4(nc);
+      out.push_back(ch);
     }
   }
 }

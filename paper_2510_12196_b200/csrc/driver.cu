@@ -912,6 +912,7 @@ struct MsNode {
 static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, const int* ids,
                              unsigned long long seed, cudaStream_t s) {
   std::vector<MsNode> nodes(1);
+  std::vector<DBuf<int>> arenas;  // batched extractions: children live here
   nodes[0].g = root;
   nodes[0].trans = ids;
   nodes[0].total = total;
@@ -982,6 +983,32 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
       return;
     }
     std::vector<MsNode> next;
+    if (parts <= 64) {  // all children of this tree level in one launch
+      std::vector<DevGraph> gs;
+      std::vector<const int*> pp, tr;
+      for (int j = 0; j < N; ++j) {
+        gs.push_back(nodes[(size_t)j].g);
+        pp.push_back(part[(size_t)j].get());
+        tr.push_back(nodes[(size_t)j].trans);
+      }
+      std::vector<ExChild> kids;
+      arenas.emplace_back();
+      extract_batch(gs, pp, tr, parts, kids, arenas.back(), s);
+      for (const ExChild& x : kids) {
+        if (x.g.n == 0) continue;  // descend() returns at once for empty nodes
+        const MsNode& nd = nodes[(size_t)x.node];
+        MsNode ch;
+        ch.g = x.g;
+        ch.trans = x.trans;
+        ch.total = x.total;
+        ch.ident = nd.ident;
+        ch.ident.push_back(x.part);
+        ch.seed = hash2(nd.seed, (unsigned long long)level, (unsigned long long)x.part);
+        next.push_back(std::move(ch));
+      }
+      nodes = std::move(next);
+      continue;
+    }
     for (int j = 0; j < N; ++j) {
       MsNode& nd = nodes[(size_t)j];
       DBuf<long long> bw((size_t)parts, s);

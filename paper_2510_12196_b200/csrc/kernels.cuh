@@ -169,6 +169,15 @@ struct BpJob {
   long long* bw;
 };
 void bproj_bw_batch(const std::vector<BpJob>& jobs, cudaStream_t s);
+struct ExChild {
+  int node = 0, part = 0;
+  long long total = 0;     // c(V) of the child
+  DevGraph g;              // views into the extraction arena
+  const int* trans = nullptr;  // global ids
+};
+void extract_batch(const std::vector<DevGraph>& gs, const std::vector<const int*>& parts_of,
+                   const std::vector<const int*>& trans, int parts, std::vector<ExChild>& out,
+                   DBuf<int>& arena, cudaStream_t s);
 void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
                cudaStream_t s);
 

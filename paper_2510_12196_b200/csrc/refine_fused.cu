@@ -52,6 +52,8 @@ namespace gim {
 
 constexpr int kFusedBlock = 256;
 constexpr int kFusedWarps = kFusedBlock / 32;
+// co-resident CTAs per SM the grid kernels are compiled for (register cap)
+constexpr int kFusedMinBlocks = 3;
 constexpr int kMaxCluster = 16;
 // vertex-centric first filter when a level has at most this many vertex
 // groups per warp (else edge-parallel boundary pass + lists)
@@ -899,13 +901,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
 }
 
 template <int VW>
-__global__ void __launch_bounds__(kFusedBlock) k_refine_fused(FusedArgs A) {
+__global__ void __launch_bounds__(kFusedBlock, kFusedMinBlocks) k_refine_fused(FusedArgs A) {
   refine_body<VW>(A);
 }
 
 // one thread-block cluster per independent refinement (batched launch)
 template <int VW>
-__global__ void __launch_bounds__(kFusedBlock) k_refine_cluster_batch(const FusedArgs* args,
+__global__ void __launch_bounds__(kFusedBlock, kFusedMinBlocks) k_refine_cluster_batch(const FusedArgs* args,
                                                                       int csize) {
   refine_body<VW>(args[blockIdx.x / csize]);
 }
