@@ -49,7 +49,7 @@ struct BcJob {
   int* arena;
   long long cap;  // words
   int nl;
-  int status;  // 0 ok, 1 needs the general path
+  int status;  // 0 ok, 1 level nl-1 needs two-hop matching, 2 out of room
   BcLevel lv[kBcMaxLevels];
 };
 
@@ -100,13 +100,13 @@ __global__ void __launch_bounds__(kBcBlock) k_coarsen_small(BcJob* jobs) {
   for (int lev = 0;; ++lev) {
     if ((long long)n < J.threshold) break;
     if (lev + 1 >= kBcMaxLevels) {
-      if (threadIdx.x == 0) J.status = 1;
+      if (threadIdx.x == 0) J.status = 2;
       break;
     }
     // this level needs <= 4n (partner, elig, pref, cmap) + 5 n_c + 2 (mem, L,
     // cnt, cvw) + 2 m2 (staged pairs) + 2 n_c + 1 + 2 m2 (the coarse level)
     if (s_top + 11ll * n + 4ll * m2 + 8 > J.cap) {
-      if (threadIdx.x == 0) J.status = 1;
+      if (threadIdx.x == 0) J.status = 2;
       break;
     }
     int* partner = A + s_top;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kBcBlock) k_coarsen_small(BcJob* jobs) {
     int* tw = tk + ubtot;    // [ubtot] staged weights
     long long after = (tw + ubtot) - A;
     if (after + 2ll * n_c + 1 + 2ll * ubtot + 8 > J.cap) {
-      if (threadIdx.x == 0) J.status = 1;
+      if (threadIdx.x == 0) J.status = 2;
       break;
     }
     for (int c = threadIdx.x; c < n_c; c += kBcBlock) {
@@ -458,7 +458,7 @@ void coarsen_small_batch(const std::vector<DevGraph>& gs, const std::vector<doub
     SmallStack& S = out[(size_t)j];
     S.status = b.status;
     S.nl = b.nl;
-    if (b.status) continue;
+    if (b.status == 2) continue;
     int* A = arena.get() + base[(size_t)j];
     for (int l = 0; l < b.nl; ++l) {
       const BcLevel& L = b.lv[l];

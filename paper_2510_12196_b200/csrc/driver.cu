@@ -22,6 +22,7 @@
 namespace gim {
 
 void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s);
+void fill_sources(int n, const int* off, int* src, cudaStream_t s);
 void extract_subgraphs(const DevGraph& g, const int* part, int parts,
                        std::vector<OwnedGraph>& subs, std::vector<DBuf<int>>& ids,
                        cudaStream_t s);
@@ -407,8 +408,11 @@ static long long match_graph(const DevGraph& g, double l_max, unsigned long long
   return m;
 }
 
+// `first`: index of g0 in the whole stack (a continuation of a stack whose
+// first levels were built elsewhere uses the same per-level seeds)
 static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, long long threshold,
-                                            unsigned long long seed, cudaStream_t s) {
+                                            unsigned long long seed, cudaStream_t s,
+                                            int first = 0) {
   std::vector<Level> levels;
   levels.emplace_back();
   levels.back().g = g0;
@@ -416,7 +420,8 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
     Level& cur = levels.back();
     if ((long long)cur.g.n < threshold) break;
     DBuf<int> partner((size_t)std::max(cur.g.n, 1), s);
-    unsigned long long lseed = splitmix64(seed ^ (unsigned long long)(levels.size() - 1));
+    unsigned long long lseed =
+        splitmix64(seed ^ (unsigned long long)(first + levels.size() - 1));
     match_graph(cur.g, l_max, lseed, partner.get(), s);
     DBuf<int> cmap((size_t)std::max(cur.g.n, 1), s);
     int n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
@@ -556,6 +561,33 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
   std::vector<SmallStack> stacks;
   DBuf<int> arena;
   coarsen_small_batch(gs, lmax, seeds, std::max<long long>(64ll * parts, 2), stacks, arena, s);
+  // a stack that stopped at a level needing two-hop matching continues on
+  // the general level-stack code from that level (same per-level seeds);
+  // the job then refines in the batch like the others
+  std::vector<std::vector<Level>> tails((size_t)J);
+  std::vector<DBuf<int>> tail_src((size_t)J);
+  for (int i = 0; i < J; ++i) {
+    SmallStack& S = stacks[(size_t)i];
+    if (S.status != 1) continue;
+    DevGraph top = S.levels.back();
+    if (!top.src) {  // arena levels carry no E_u
+      tail_src[(size_t)i] = DBuf<int>((size_t)std::max<long long>(top.m2, 1), s);
+      fill_sources(top.n, top.off, tail_src[(size_t)i].get(), s);
+      top.src = tail_src[(size_t)i].get();
+    }
+    tails[(size_t)i] = build_level_stack(top, lmax[(size_t)i],
+                                         std::max<long long>(64ll * parts, 2), seeds[(size_t)i],
+                                         s, S.nl - 1);
+    std::vector<Level>& T = tails[(size_t)i];
+    S.levels.back() = top;
+    S.cmap.back() = T.size() > 1 ? T[0].cmap.get() : nullptr;
+    for (size_t l = 1; l < T.size(); ++l) {
+      S.levels.push_back(T[l].g);
+      S.cmap.push_back(l + 1 < T.size() ? T[l].cmap.get() : nullptr);
+    }
+    S.nl = (int)S.levels.size();
+    S.status = 0;
+  }
   // jobs the fast path cannot take: general path
   std::vector<int> ok;
   for (int i = 0; i < J; ++i) {
@@ -983,7 +1015,9 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
       return;
     }
     std::vector<MsNode> next;
-    if (parts <= 64) {  // all children of this tree level in one launch
+    bool small_nodes = parts <= 64;
+    for (const MsNode& nd : nodes) small_nodes = small_nodes && nd.g.n <= kBatchMaxN;
+    if (small_nodes) {  // all children of this tree level in one launch (CTA per node)
       std::vector<DevGraph> gs;
       std::vector<const int*> pp, tr;
       for (int j = 0; j < N; ++j) {

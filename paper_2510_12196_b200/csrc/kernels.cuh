@@ -152,7 +152,7 @@ bool fused_supported(int k, int rho);
 
 // batched small-graph partitioner pieces (batch.cu)
 struct SmallStack {
-  int status = 0;                 // 0: fast path applies; 1: general path
+  int status = 0;                 // 0 done; 1 the top level needs two-hop (continue); 2 general path
   int nl = 0;
   std::vector<DevGraph> levels;   // [0] = the input graph
   std::vector<const int*> cmap;   // level l -> l + 1 (null on the coarsest)
