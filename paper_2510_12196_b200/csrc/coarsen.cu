@@ -12,6 +12,13 @@
 
 namespace gim {
 
+// device-side "round 2 only below 40 % matched" (coarsening.py:167-170):
+// `gate` is a snapshot of the matched count after round 1
+__device__ __forceinline__ bool hem_gated(const long long* gate, int n) {
+  return gate && (n ? (double)*gate / (double)n : 1.0) >= 0.40;
+}
+
+
 // ---------------------------------------------------------------------------
 // K3 heavy-edge preference: per unmatched v, argmax over eligible unmatched
 // neighbours u (c_v + c_u <= l_max) of (w^2/(c_v c_u), hash2(seed,min,max)),
@@ -70,7 +77,9 @@ __global__ void __launch_bounds__(256) k_hem_pref(int n, const int* __restrict__
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restrict__ pref,
                                                       int* __restrict__ partner,
-                                                      long long* __restrict__ matched) {
+                                                      long long* __restrict__ matched,
+                                                      const long long* gate = nullptr) {
+  if (hem_gated(gate, n)) return;
   long long cnt = 0;
   for (int v = blockIdx.x * BLOCK + threadIdx.x; v < n; v += gridDim.x * BLOCK) {
     int u = pref[v];
@@ -92,7 +101,8 @@ __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restri
 constexpr int kHemTpv = 32;
 
 __global__ void k_hem_elig(int n, const int* __restrict__ partner, const int* __restrict__ vw,
-                           int* __restrict__ elig_c) {
+                           int* __restrict__ elig_c, const long long* gate) {
+  if (hem_gated(gate, n)) return;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     elig_c[v] = partner[v] < 0 ? vw[v] : -1;
 }
@@ -102,7 +112,9 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
                                                       const int* __restrict__ w,
                                                       const int* __restrict__ elig_c,
                                                       double l_max, unsigned long long seed,
-                                                      int* __restrict__ pref) {
+                                                      int* __restrict__ pref,
+                                                      const long long* gate) {
+  if (hem_gated(gate, n)) return;
   const int lane = lane_id();
   const long long T = (long long)gridDim.x * blockDim.x;
   for (long long b0 = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; b0 < n; b0 += T) {
@@ -192,18 +204,21 @@ static int pick_vw(long long m2, int n) {
 }
 
 void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
-               unsigned long long seed, long long* matched, cudaStream_t s) {
+               unsigned long long seed, long long* matched, cudaStream_t s,
+               const long long* gate) {
   if (g.n == 0) return;
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
   DBuf<int> elig((size_t)g.n, s);
-  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, elig.get());
+  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, elig.get(), gate);
   k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, elig.get(),
-                                                           l_max, seed, pref);
-  k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched);
+                                                           l_max, seed, pref, gate);
+  k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched, gate);
   GIM_LAUNCH_CHECK();
   count_launch(3);
 }
+
+
 
 // ---------------------------------------------------------------------------
 // K5 two-hop matching (coarsening.py:98-161).  Leaves and twins form
@@ -923,6 +938,105 @@ void project(int n, const int* cmap, const int* pc, int* pf, cudaStream_t s) {
   k_project<<<grid_for(n, 256), 256, 0, s>>>(n, cmap, pc, pf);
   count_launch();
   GIM_LAUNCH_CHECK();
+}
+
+__global__ void k_copy_ll(const long long* src, long long* dst) { *dst = *src; }
+
+__global__ void k_pack4(const long long* a, const int* b, const int* c, const int* d,
+                        long long* out) {
+  out[0] = *a;
+  out[1] = *b;
+  out[2] = *c;
+  out[3] = d ? *d : -1;
+}
+
+// ---------------------------------------------------------------------------
+// One level of the stack with a single host round trip (the common case):
+// both matching rounds (round 2 gated on the device), the coarse ids and the
+// member table speculatively, then ONE read of (matched, n_c, max row).
+// The contraction then runs without waiting: arrays are sized by the upper
+// bound m2 and the true 2m_c stays on the device (*m2c_dev) until the
+// caller reads every level's at once.  Returns false (nothing allocated
+// for the coarse level) when the level needs the general path: < 40 %
+// matched (two-hop), or hub rows > kRowCap.
+bool coarsen_level_fast(const DevGraph& g_in, double l_max, unsigned long long lseed,
+                        int* partner, int* cmap, int* n_c_out, long long* matched_out,
+                        OwnedGraph& out, int* m2c_dev, bool* stalled, const int* g_m2_dev,
+                        long long* g_m2_out, cudaStream_t s) {
+  DevGraph g = g_in;
+  const int n = g.n;
+  *stalled = false;
+  GIM_CUDA(cudaMemsetAsync(partner, 0xff, sizeof(int) * (size_t)std::max(n, 1), s));
+  DBuf<int> pref((size_t)std::max(n, 1), s);
+  DBuf<long long> cnt(2, s);  // [matched, matched after round 1]
+  GIM_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(long long), s));
+  hem_round(g, partner, pref.get(), l_max, splitmix64(lseed ^ 1ull), cnt.get(), s, nullptr);
+  k_copy_ll<<<1, 1, 0, s>>>(cnt.get(), cnt.get() + 1);
+  hem_round(g, partner, pref.get(), l_max, splitmix64(lseed ^ 2ull), cnt.get(), s,
+            cnt.get() + 1);
+  // speculative coarse ids + members (valid unless two-hop changes partner)
+  DBuf<int> ids((size_t)std::max(n, 1), s), tot(1, s);
+  exclusive_scan<int>(n, IsRoot{partner}, StoreTo<int>{ids.get()}, tot.get(), s);
+  k_coarse_map<<<grid_for(n, 256), 256, 0, s>>>(n, partner, ids.get(), cmap);
+  DBuf<int> mem((size_t)2 * std::max(n, 1), s), rowlen((size_t)n + 1, s), cvw((size_t)std::max(n, 1), s);
+  DBuf<int> scal(3, s);  // maxlen, ubtot, m2c
+  GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 3 * sizeof(int), s));
+  k_members<<<grid_for(n, 256), 256, 0, s>>>(n, partner, cmap, g.off, g.vw, mem.get(),
+                                             rowlen.get(), cvw.get(), scal.get());
+  DBuf<long long> pack(4, s);
+  k_pack4<<<1, 1, 0, s>>>(cnt.get(), tot.get(), scal.get(), g_m2_dev, pack.get());
+  count_launch(5);
+  GIM_LAUNCH_CHECK();
+  long long* hp = static_cast<long long*>(pinned_scratch(4 * sizeof(long long)));
+  GIM_CUDA(cudaMemcpyAsync(hp, pack.get(), 4 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(sync_stream(s));
+  const long long matched = hp[0];
+  const int n_c = (int)hp[1], maxlen = (int)hp[2];
+  if (g_m2_dev) {  // this level's own 2m was still on the device
+    g.m2 = hp[3];
+    *g_m2_out = hp[3];
+  }
+  *matched_out = matched;
+  *n_c_out = n_c;
+  const double frac = n ? (double)matched / (double)n : 1.0;
+  if (frac < 0.40 || maxlen > kRowCap) return false;
+  if ((double)n_c * 1.02 > (double)n) {  // stall guard
+    *stalled = true;
+    return true;
+  }
+  ProfScope prof(P_CONTRACT, 12.0 * n + 12.0 * g.m2 + 8.0 * n_c, s);
+  const long long cap = std::max<long long>(g.m2, 1);
+  out.n = n_c;
+  out.vw = std::move(cvw);
+  out.off = DBuf<int>((size_t)n_c + 1, s);
+  out.tgt = DBuf<int>((size_t)cap, s);
+  out.w = DBuf<int>((size_t)cap, s);
+  out.src = DBuf<int>((size_t)cap, s);
+  DBuf<int> ub((size_t)n_c + 1, s), cdeg((size_t)n_c + 1, s);
+  DBuf<int> t_tgt((size_t)cap, s), t_w((size_t)cap, s);
+  GIM_CUDA(cudaMemsetAsync(cdeg.get() + n_c, 0, sizeof(int), s));
+  exclusive_scan<int>((long long)n_c, LoadAs<int, int>{rowlen.get()}, StoreTo<int>{ub.get()},
+                      scal.get() + 1, s);
+  k_row_tpv<<<grid_for(n_c, kCtBlock, kSMs * 16), kCtBlock, 0, s>>>(
+      n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
+      cdeg.get());
+  count_launch();
+  if (maxlen > kCtTpv) {
+    const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
+    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(), g.off,
+                                               g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
+                                               cdeg.get());
+    count_launch();
+  }
+  exclusive_scan<int>((long long)n_c + 1, LoadAs<int, int>{cdeg.get()},
+                      StoreTo<int>{out.off.get()}, m2c_dev, s);
+  k_row_compact<<<grid_for(n_c, 256, kSMs * 16), 256, 0, s>>>(
+      n_c, ub.get(), out.off.get(), t_tgt.get(), t_w.get(), out.tgt.get(), out.w.get(),
+      out.src.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  out.m2 = cap;  // upper bound until the next level's round trip reads *m2c_dev
+  return true;
 }
 
 }  // namespace gim

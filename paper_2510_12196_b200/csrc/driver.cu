@@ -416,17 +416,72 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
   std::vector<Level> levels;
   levels.emplace_back();
   levels.back().g = g0;
+  // 2m of levels built by the one-round-trip path, read back in one copy
+  constexpr int kMaxPending = 64;
+  DBuf<int> m2c(kMaxPending, s);
+  std::vector<int> pending;  // level indices
+  auto resolve = [&] {
+    if (pending.empty()) return;
+    int* h = static_cast<int*>(pinned_scratch(sizeof(int) * kMaxPending));
+    GIM_CUDA(cudaMemcpyAsync(h, m2c.get(), sizeof(int) * kMaxPending, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    for (size_t i = 0; i < pending.size(); ++i) {
+      Level& L = levels[(size_t)pending[i]];
+      L.own.m2 = h[i];
+      L.g.m2 = h[i];
+    }
+    pending.clear();
+  };
   for (;;) {
     Level& cur = levels.back();
     if ((long long)cur.g.n < threshold) break;
     DBuf<int> partner((size_t)std::max(cur.g.n, 1), s);
     unsigned long long lseed =
         splitmix64(seed ^ (unsigned long long)(first + levels.size() - 1));
-    match_graph(cur.g, l_max, lseed, partner.get(), s);
     DBuf<int> cmap((size_t)std::max(cur.g.n, 1), s);
-    int n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
-    if ((double)n_c * 1.02 > (double)cur.g.n) break;  // stall guard
+    int n_c = 0;
     Level next;
+    if (g_rowwise.load() && (int)pending.size() < kMaxPending) {
+      long long m = 0, true_m2 = -1;
+      bool stalled = false;
+      // the current level's 2m, if still on the device, rides on this round trip
+      const bool cur_pending = !pending.empty() && pending.back() == (int)levels.size() - 1;
+      const int* cur_m2_dev = cur_pending ? m2c.get() + (pending.size() - 1) : nullptr;
+      const bool ok = coarsen_level_fast(cur.g, l_max, lseed, partner.get(), cmap.get(), &n_c,
+                                         &m, next.own, m2c.get() + pending.size(), &stalled,
+                                         cur_m2_dev, &true_m2, s);
+      if (cur_pending) {
+        cur.own.m2 = true_m2;
+        cur.g.m2 = true_m2;
+      }
+      if (ok) {
+        if (stalled) break;
+        next.g = next.own.view();
+        cur.cmap = std::move(cmap);
+        cur.n_c = n_c;
+        pending.push_back((int)levels.size());
+        levels.push_back(std::move(next));
+        continue;
+      }
+      // this level needs the general code: two-hop matching / hub rows
+      resolve();
+      Level& c2 = levels.back();
+      DBuf<long long> md(1, s);
+      if ((c2.g.n ? (double)m / (double)c2.g.n : 1.0) < 0.40)
+        two_hop(c2.g, partner.get(), l_max, m, md.get(), s);
+      n_c = coarse_map(c2.g.n, partner.get(), cmap.get(), s);
+      if ((double)n_c * 1.02 > (double)c2.g.n) break;  // stall guard
+      contract_matching(c2.g, cmap.get(), partner.get(), n_c, next.own, s);
+      next.g = next.own.view();
+      c2.cmap = std::move(cmap);
+      c2.n_c = n_c;
+      levels.push_back(std::move(next));
+      continue;
+    }
+    resolve();
+    match_graph(cur.g, l_max, lseed, partner.get(), s);
+    n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
+    if ((double)n_c * 1.02 > (double)cur.g.n) break;  // stall guard
     if (g_rowwise.load())
       contract_matching(cur.g, cmap.get(), partner.get(), n_c, next.own, s);
     else
@@ -436,6 +491,7 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
     cur.n_c = n_c;
     levels.push_back(std::move(next));
   }
+  resolve();
   return levels;
 }
 

@@ -57,7 +57,8 @@ void block_weights(int n, const int* vw, const int* part, int k, long long* bw,
 
 // ---- coarsen.cu
 void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
-               unsigned long long seed, long long* matched, cudaStream_t s);
+               unsigned long long seed, long long* matched, cudaStream_t s,
+               const long long* gate = nullptr);
 long long two_hop(const DevGraph& g, int* partner, double l_max, long long matched_now,
                   long long* matched_d, cudaStream_t s);
 int coarse_map(int n, const int* partner, int* cmap, cudaStream_t s);
@@ -65,6 +66,10 @@ long long contract_into(const DevGraph& g, const int* cmap, int n_c, int* c_off,
                         int* c_w, int* c_vw, int* c_src, cudaStream_t s);
 void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cudaStream_t s);
 // contraction of a matching (<= 2 members per coarse vertex), row-wise
+bool coarsen_level_fast(const DevGraph& g, double l_max, unsigned long long lseed, int* partner,
+                        int* cmap, int* n_c_out, long long* matched_out, OwnedGraph& out,
+                        int* m2c_dev, bool* stalled, const int* g_m2_dev, long long* g_m2_out,
+                        cudaStream_t s);
 void contract_matching(const DevGraph& g, const int* cmap, const int* partner, int n_c,
                        OwnedGraph& out, cudaStream_t s);
 void project(int n, const int* cmap, const int* pc, int* pf, cudaStream_t s);
