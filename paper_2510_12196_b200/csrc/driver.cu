@@ -185,6 +185,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
       if (masks[k + b]) el[ne++] = b;
     }
     const bool incomplete = ne == 0;
+    if (L.heavy.get() == nullptr) prepare_level(L, k, s);  // host strong pass: heavy list
     GIM_CUDA(cudaMemcpyAsync(rb.masks.get(), masks.data(), (size_t)k * 2, cudaMemcpyHostToDevice, s));
     if (ne)
       GIM_CUDA(cudaMemcpyAsync(rb.elist.get(), el.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, s));
@@ -254,7 +255,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
 static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, const RefCfg& cfg,
                    double l_max, RunStats& st, RefineBuffers& rb, cudaStream_t s) {
   const int n = L.g.n, k = t.k;
-  if (L.heavy.get() == nullptr) prepare_level(L, k, s);
+  prepare_level_vw(L);
   alloc_refine_buffers(rb, n, k, s);
   const bool aligned = ((reinterpret_cast<uintptr_t>(L.g.src) |
                          reinterpret_cast<uintptr_t>(L.g.tgt)) & 15) == 0;
@@ -262,6 +263,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
     refine_device_loop(L, t, part, bw_d, cfg, l_max, st, rb, s);
     return;
   }
+  if (L.heavy.get() == nullptr) prepare_level(L, k, s);
   // host mirrors
   size_t pin_bytes = sizeof(long long) * ((size_t)k + 2) + (size_t)k * 2 + sizeof(int) * (size_t)k;
   char* pin = static_cast<char*>(g_pin.get(pin_bytes));

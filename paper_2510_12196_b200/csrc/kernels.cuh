@@ -108,6 +108,8 @@ struct RefineBuffers {
 };
 
 void prepare_level(RefineLevel& L, int k, cudaStream_t s);
+// lane width only (the fused loop needs no heavy list until a host strong pass)
+void prepare_level_vw(RefineLevel& L);
 void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s);
 void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigned char* locked,
              int jet, double jet_c, RefineBuffers& rb, cudaStream_t s);

@@ -386,10 +386,15 @@ struct HeavyOut {
   }
 };
 
-void prepare_level(RefineLevel& L, int k, cudaStream_t s) {
+void prepare_level_vw(RefineLevel& L) {
   const DevGraph& g = L.g;
   double avg = g.n ? (double)g.m2 / g.n : 0.0;
   L.vw = avg <= 3.0 ? 4 : avg <= 6.0 ? 8 : avg <= 12.0 ? 16 : 32;
+}
+
+void prepare_level(RefineLevel& L, int k, cudaStream_t s) {
+  const DevGraph& g = L.g;
+  prepare_level_vw(L);
   GIM_CHECK((long long)k * 12 * 4 <= 200 * 1024 || g.n == 0, GIM_E_UNSUPPORTED,
             "k too large for the shared-memory connectivity table (k <= 4266)");
   L.heavy = DBuf<int>((size_t)std::max(g.n, 1), s);
