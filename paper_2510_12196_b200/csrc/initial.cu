@@ -5,7 +5,6 @@
 // :132-188, hierarchical_multisection leaf :78-80), graph.py
 // (extract_subgraphs :357-389).
 #include <algorithm>
-#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -192,185 +191,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
 
-// Warp-per-graph greedy growing (same semantics as k_ggg): the coarsest
-// partitioner graphs hold a few hundred vertices, so one warp with no CTA
-// barriers runs the n sequential growth steps fastest.  BFS seeds use a
-// frontier queue; every selection is a warp argmax/argmin over shared
-// memory.  Layout: dist[n] part[n] q0[n] q1[n] conn[k*n] (ints), bw[k] (int64).
-__device__ __forceinline__ void warp_argmax(int& a, int& b) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int a2 = __shfl_xor_sync(0xffffffffu, a, o), b2 = __shfl_xor_sync(0xffffffffu, b, o);
-    if (a2 > a || (a2 == a && b2 < b)) { a = a2; b = b2; }
-  }
-}
-
-__device__ void warp_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
-                         int ns, int* q0, int* q1) {
-  __shared__ int s_nn;
-  const int lane = lane_id();
-  for (int v = lane; v < n; v += 32) dist[v] = -1;
-  __syncwarp();
-  // the distinct seeds form the first frontier
-  int nf = 0;
-  for (int b = 0; b < ns; b += 32) {
-    const int i = b + lane;
-    const int x = i < ns ? seeds[i] : -1;
-    bool first = x >= 0;
-    for (int j2 = 0; j2 < i && first; ++j2) first = seeds[j2] != x;
-    const unsigned m = __ballot_sync(0xffffffffu, first);
-    if (first) {
-      q0[nf + __popc(m & ((1u << lane) - 1u))] = x;
-      dist[x] = 0;
-    }
-    nf += __popc(m);
-  }
-  __syncwarp();
-  int* F = q0;
-  int* N = q1;
-  for (int d = 0; nf > 0; ++d) {
-    if (lane == 0) s_nn = 0;
-    __syncwarp();
-    for (int i = lane; i < nf; i += 32) {
-      const int v = F[i];
-      for (int e = off[v]; e < off[v + 1]; ++e) {
-        const int u = tgt[e];
-        if (dist[u] < 0 && atomicCAS(&dist[u], -1, d + 1) == -1) N[atomicAdd(&s_nn, 1)] = u;
-      }
-    }
-    __syncwarp();
-    nf = s_nn;
-    __syncwarp();
-    int* t = F;
-    F = N;
-    N = t;
-  }
-}
-
-// lowest unreached vertex if any, else the first vertex of maximum distance
-__device__ int warp_pick_seed(int n, const int* dist) {
-  const int lane = lane_id();
-  int unr = INT_MAX, bd = -1, bv = INT_MAX;
-  for (int v = lane; v < n; v += 32) {
-    const int d = dist[v];
-    if (d < 0) unr = min(unr, v);
-    else if (d > bd) { bd = d; bv = v; }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) unr = min(unr, __shfl_xor_sync(0xffffffffu, unr, o));
-  if (unr != INT_MAX) return unr;
-  warp_argmax(bd, bv);
-  return bv;
-}
-
-__global__ void __launch_bounds__(32) k_ggg_warp(const GggJob* jobs, int njobs) {
-  const int j = blockIdx.x;
-  if (j >= njobs) return;
-  const GggJob J = jobs[j];
-  const int n = J.n, k = J.k, lane = lane_id();
-  extern __shared__ int sm[];
-  int* dist = sm;
-  int* part = dist + n;
-  int* q0 = part + n;
-  int* q1 = q0 + n;
-  int* seeds = q1 + n;
-  int* conn = seeds + k;
-  long long* bw = reinterpret_cast<long long*>(conn + (size_t)k * n + ((k * n + k) & 1));
-  if (k == 1) {
-    for (int v = lane; v < n; v += 32) J.part[v] = 0;
-    return;
-  }
-  int zero = 0;
-  warp_bfs(n, J.off, J.tgt, dist, &zero, 1, q0, q1);
-  int sv = warp_pick_seed(n, dist);
-  if (lane == 0) seeds[0] = sv;
-  __syncwarp();
-  for (int ns = 1; ns < k; ++ns) {
-    warp_bfs(n, J.off, J.tgt, dist, seeds, ns, q0, q1);
-    sv = warp_pick_seed(n, dist);
-    if (lane == 0) seeds[ns] = sv;
-    __syncwarp();
-  }
-  for (int v = lane; v < n; v += 32) part[v] = -1;
-  for (int i = lane; i < k * n; i += 32) conn[i] = 0;
-  for (int b = lane; b < k; b += 32) bw[b] = 0;
-  __syncwarp();
-  auto claim = [&](int v, int b) {
-    if (lane == 0) {
-      part[v] = b;
-      bw[b] += J.vw[v];
-    }
-    __syncwarp();
-    for (int e = J.off[v] + lane; e < J.off[v + 1]; e += 32) {
-      const int u = J.tgt[e];
-      if (part[u] < 0) atomicAdd(&conn[b * n + u], J.w[e]);
-    }
-    __syncwarp();
-  };
-  for (int b = 0; b < k; ++b) claim(seeds[b], b);
-  int next_free = 0;
-  for (int assigned = k; assigned < n; ++assigned) {
-    long long bwv = LLONG_MAX;
-    int bb = INT_MAX;
-    for (int b = lane; b < k; b += 32) {
-      const long long x = bw[b];
-      if (x < bwv) { bwv = x; bb = b; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
-      const int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-      if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
-    }
-    const int* cb = conn + bb * n;
-    int bc = 0, bv = INT_MAX;
-    for (int u = lane; u < n; u += 32) {
-      const int c = cb[u];
-      if (c > bc && part[u] < 0) { bc = c; bv = u; }
-    }
-    warp_argmax(bc, bv);
-    int v = bv;
-    if (bc == 0) {  // frontier dried up: lowest unassigned vertex
-      for (;;) {
-        const int x = next_free + lane;
-        const unsigned m = __ballot_sync(0xffffffffu, x < n && part[x] < 0);
-        if (m) { v = next_free + __ffs(m) - 1; break; }
-        next_free += 32;
-      }
-      next_free = v;
-    }
-    claim(v, bb);
-  }
-  for (int v = lane; v < n; v += 32) J.part[v] = part[v];
-}
-
-static size_t ggg_warp_smem(int n, int k) {
-  return sizeof(int) * ((size_t)4 * n + k + (size_t)k * n + 1) + sizeof(long long) * k + 8;
-}
-
-constexpr size_t kGggWarpSmem = 96 * 1024;
-
-static void launch_ggg_warp(const GggJob* dj, int njobs, size_t smem, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    GIM_CUDA(cudaFuncSetAttribute(k_ggg_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kGggWarpSmem));
-  });
-  k_ggg_warp<<<njobs, 32, smem, s>>>(dj, njobs);
-  count_launch();
-  GIM_LAUNCH_CHECK();
-}
-
 void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
   ProfScope prof(P_GGG, 0.0, s);
-  if (ggg_warp_smem(g.n, k) <= kGggWarpSmem) {
-    std::vector<GggJob> hj(1);
-    hj[0] = GggJob{g.n, k, g.off, g.tgt, g.w, g.vw, part, nullptr, nullptr, 1};
-    DBuf<GggJob> dj(1, s);
-    GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggJob), cudaMemcpyHostToDevice, s));
-    launch_ggg_warp(dj.get(), 1, ggg_warp_smem(g.n, k), s);
-    return;
-  }
   const size_t words = (size_t)2 * g.n + k + (size_t)k * g.n;
   const size_t smem = words * sizeof(int);
   const bool use_smem = smem <= 160 * 1024;
@@ -400,20 +222,6 @@ void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& 
   for (int j = 0; j < J; ++j) {
     words[(size_t)j] = (size_t)2 * gs[(size_t)j].n + k + (size_t)k * gs[(size_t)j].n;
     max_words = std::max(max_words, words[(size_t)j]);
-  }
-  size_t wmax = 0;
-  for (int j = 0; j < J; ++j) wmax = std::max(wmax, ggg_warp_smem(gs[(size_t)j].n, k));
-  if (wmax <= kGggWarpSmem) {  // warp per graph
-    std::vector<GggJob> hw((size_t)J);
-    for (int j = 0; j < J; ++j) {
-      const DevGraph& g = gs[(size_t)j];
-      hw[(size_t)j] = GggJob{g.n, k, g.off, g.tgt, g.w, g.vw, parts[(size_t)j], nullptr, nullptr, 1};
-    }
-    DBuf<GggJob> dw((size_t)J, s);
-    GIM_CUDA(cudaMemcpyAsync(dw.get(), hw.data(), sizeof(GggJob) * (size_t)J,
-                             cudaMemcpyHostToDevice, s));
-    launch_ggg_warp(dw.get(), J, wmax, s);
-    return;
   }
   const bool use_smem = max_words * sizeof(int) <= 160 * 1024;
   if (!use_smem)
