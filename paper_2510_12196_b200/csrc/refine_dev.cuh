@@ -133,10 +133,14 @@ struct ThreadEval {
   bool overflow;
 };
 
+// `flatd` > 0: single-level topology (the internal partitioner's), D(x,y) =
+// flatd * [x != y], so cost(b) = flatd * (W - conn(b)) and
+// gain(b) = flatd * (conn(b) - conn(own)) — no distance lookups at all.
 __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const int* tgt,
                                                   const int* w, const int* part, const Topo& t,
                                                   const long long* s_dbit,
-                                                  const unsigned char* allowed, int tb) {
+                                                  const unsigned char* allowed, int tb,
+                                                  long long flatd = 0) {
   ThreadEval r;
   r.cur = 0;
   r.conn_own = 0;
@@ -191,6 +195,30 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
         ++cnt;
       }
     }
+  }
+  if (flatd > 0) {
+    long long W = 0, ctb = 0;
+#pragma unroll
+    for (int j = 0; j < TPV_DISTINCT; ++j) {
+      if (j < cnt) {
+        W += cw[j];
+        if (nb[j] == own) r.conn_own = cw[j];
+        if (nb[j] == tb) ctb = cw[j];
+      }
+    }
+    r.cur = flatd * (W - r.conn_own);
+    if (tb >= 0) r.cost_tb = flatd * (W - ctb);
+#pragma unroll
+    for (int i = 0; i < TPV_DISTINCT; ++i) {
+      if (i < cnt && nb[i] != own && (allowed == nullptr || allowed[nb[i]])) {
+        const long long g = flatd * (cw[i] - r.conn_own);
+        if (best_better(g, nb[i], r.best_gain, r.best_b)) {
+          r.best_gain = g;
+          r.best_b = nb[i];
+        }
+      }
+    }
+    return r;
   }
   unsigned long long code[TPV_DISTINCT];
   bool adm[TPV_DISTINCT];

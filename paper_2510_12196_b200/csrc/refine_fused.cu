@@ -224,6 +224,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   for (int b = threadIdx.x; b < k; b += blockDim.x) s_code[b] = A.t.code[b];
   Topo T = A.t;  // digit codes from shared memory
   T.code = s_code;
+  __syncthreads();
+  const long long flatd = A.t.L == 1 ? s_dbit[0] : 0;  // single-level topology
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const long long gw = ((long long)BX * blockDim.x + threadIdx.x) >> 5;
@@ -390,7 +392,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           if (e1 - e0 > kTpvMaxDeg) {
             ovf = true;
           } else {
-            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, nullptr, -1);
+            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, nullptr, -1, flatd);
             ovf = r.overflow;
           }
         }
@@ -518,7 +520,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           if (e1 - e0 > kTpvMaxDeg) {
             ovf = true;
           } else {
-            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, elig, tb);
+            r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, elig, tb, flatd);
             ovf = r.overflow;
           }
         }
