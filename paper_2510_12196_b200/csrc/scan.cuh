@@ -114,12 +114,37 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_down(long long n, In in, Ou
   }
 }
 
+// small inputs: one CTA walks the range in 1024-element chunks (one launch
+// instead of three — the coarse levels are launch-latency bound)
+constexpr long long kScanSmall = 8192;
+
+template <class T, class In, class Out>
+__global__ void __launch_bounds__(1024) k_scan_small(long long n, In in, Out out, T* total) {
+  __shared__ T tot;
+  T carry = 0;
+  for (long long b = 0; b < n; b += 1024) {
+    const long long i = b + threadIdx.x;
+    const T v = i < n ? in(i) : T(0);
+    const T ex = block_excl_scan<T, 1024>(v, &tot);
+    if (i < n) out(i, carry + ex);
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
 // exclusive scan of in(0..n-1); total (device pointer, may be null) gets the sum
 template <class T, class In, class Out>
 void exclusive_scan(long long n, In in, Out out, T* total, cudaStream_t s) {
   long long tiles = (n + kScanTile - 1) / kScanTile;
   if (tiles == 0) {
     if (total) GIM_CUDA(cudaMemsetAsync(total, 0, sizeof(T), s));
+    return;
+  }
+  if (n <= kScanSmall) {
+    k_scan_small<T, In, Out><<<1, 1024, 0, s>>>(n, in, out, total);
+    GIM_LAUNCH_CHECK();
+    count_launch(1);
     return;
   }
   DBuf<T> sums((size_t)tiles, s);
