@@ -132,7 +132,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   FusedBuffers fb;
   fb.cand = rb.cand.get();
   fb.tm0 = rb.to_move.get();
-  fb.tm1 = rb.locks.get();
+  fb.tm1 = fb.tm0 + rb.cap_n;  // contiguous with tm0: the fused loop keeps uint16 move stamps in both
   fb.rcell = rb.rcell.get();
   fb.dest = rb.dest.get();
   fb.rtgt = rb.dest2.get();

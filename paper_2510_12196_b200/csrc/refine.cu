@@ -493,7 +493,7 @@ void alloc_refine_buffers(RefineBuffers& rb, int n, int k, cudaStream_t s) {
   rb.cap_k = k;
   size_t nn = (size_t)std::max(n, 1);
   rb.cand = DBuf<unsigned char>(nn, s);
-  rb.to_move = DBuf<unsigned char>(nn, s);
+  rb.to_move = DBuf<unsigned char>(2 * nn, s);  // 2 bytes per vertex: fused-loop move stamps
   rb.locks = DBuf<unsigned char>(nn, s);
   rb.dest = DBuf<int>(nn, s);
   rb.dest2 = DBuf<int>(nn, s);

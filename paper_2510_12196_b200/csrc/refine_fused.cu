@@ -114,6 +114,7 @@ struct Ctl {
   long long J, best_j, best_maxw, maxw, pass_counter;
   long long iters, lp, weak;
   int i, i_w, best_balanced, locks_nonempty, lp_par, prev_n, it, stamp;
+  int lock_stamp;  // move stamp of the locked set (previous LP movers), 0: none
   int brk, take, strong_yield;
 };
 
@@ -255,8 +256,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     for (long long v = gt; v < n; v += GT) {
       A.gkey[v] = kGainNone;
       A.rtgt[v] = -1;
-      A.flags0[v] = 0;
-      A.flags1[v] = 0;
+      reinterpret_cast<unsigned short*>(A.flags0)[v] = 0;  // move stamp
     }
     for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
   }
@@ -318,6 +318,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   }
   if (threadIdx.x == 0) {
     C.it = 0;
+    C.lock_stamp = 0;  // every launch starts without locks (after a rebalance pass)
     C.iters = C.lp = C.weak = 0;
     C.brk = 0;
     C.strong_yield = 0;
@@ -336,9 +337,26 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     }                                                                    \
   } while (0)
 
+  // Move stamps (uint16 over the two flag bytes of a vertex): a vertex moves
+  // in iteration `it` iff mstamp == stamp_of(it); the locked set is the
+  // previous LP pass's movers (stamp C.lock_stamp), so nothing is ever
+  // cleared.  The old part of a mover lives in opart, so the move
+  // application can commit in place while others read it.
+  unsigned short* const mstamp = reinterpret_cast<unsigned short*>(A.flags0);
+  int* const opart = A.lmov1;
   while (C.i < A.i_max) {
     const bool balanced_now = (double)C.maxw <= A.l_max;
-    const bool entry_locks_empty = !C.locks_nonempty;
+    if (C.it > 0 && C.it % 65534 == 0) {  // stamp wrap: keep only the locks
+      const unsigned short ls = (unsigned short)C.lock_stamp;
+      for (long long v = gt; v < n; v += GT)
+        mstamp[v] = (ls && mstamp[v] == ls) ? 1 : 0;
+      grid.sync();
+      if (threadIdx.x == 0 && ls) C.lock_stamp = 1;
+      __syncthreads();
+    }
+    const unsigned short cur_stamp = (unsigned short)(2 + C.it % 65534);
+    const unsigned short lock_stamp = (unsigned short)C.lock_stamp;
+    const bool entry_locks_empty = lock_stamp == 0;
     if (!balanced_now && !(C.i_w < A.i_w_max)) {  // strong pass: hand back to the host
       if (threadIdx.x == 0) C.strong_yield = 1;
       __syncthreads();
@@ -347,12 +365,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     const int q = C.it & 1;
     long long* cnt = A.ctr + q * kCtrStride;          // this iteration (zeroed beforehand)
     long long* cnt_next = A.ctr + (q ^ 1) * kCtrStride;
-    unsigned char* tmf = C.lp_par ? A.flags1 : A.flags0;   // to_move flags
-    unsigned char* lkf = C.lp_par ? A.flags0 : A.flags1;   // lock flags (= previous movers)
-    int* lmov = C.lp_par ? A.lmov1 : A.lmov0;
-    const int* lprev = C.lp_par ? A.lmov0 : A.lmov1;
-    const int prev_n = C.prev_n;
-    const bool use_locks = C.locks_nonempty != 0;
+    int* lmov = A.lmov0;
+    const bool use_locks = lock_stamp != 0;
     const int stamp = C.stamp + 1;
     bool incomplete = false;
     // thread-per-vertex first filters straight over the vertex range when
@@ -366,7 +380,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         // boundary list (unlocked): ext[v] > 0
         for (long long b0 = gt - lane; b0 < n; b0 += GT) {
           const long long v = b0 + lane;
-          const bool bnd = v < n && ext[v] > 0 && !(use_locks && lkf[v]);
+          const bool bnd = v < n && ext[v] > 0 && !(use_locks && mstamp[v] == lock_stamp);
           wq_push(qa, bnd, (int)v, A.lsmall, cnt + C_SMALL);
         }
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
@@ -380,7 +394,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         int v = 0, own = 0, e0 = 0, e1 = 0;
         if (live) {
           v = vcent ? (int)idx : A.lsmall[idx];
-          if (vcent && use_locks && lkf[v]) live = false;
+          if (vcent && use_locks && mstamp[v] == lock_stamp) live = false;
         }
         ThreadEval r{};
         r.best_b = -1;
@@ -452,7 +466,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
         const bool m = live && li == 0 && fut >= 0;
-        if (m) tmf[v] = 1;
+        if (m) {
+          mstamp[v] = cur_stamp;
+          opart[v] = A.part[v];
+        }
         wq_push(qa, m, v, lmov, cnt + C_MOV);
       }
       wq_flush(qa, lmov, cnt + C_MOV);
@@ -564,8 +581,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         wq_push(qa, isc, v, A.lcand, cnt + C_CAND);
       }
       wq_flush(qa, A.lcand, cnt + C_CAND);
-      // the lock set is cleared on every rebalance pass (refinement.py:425)
-      for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;
+      // the lock set is cleared on every rebalance pass (refinement.py:425):
+      // lock_stamp becomes 0 at the end of this iteration
       grid.sync();
       PHASE_MARK(5);
       if (BX == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
@@ -733,7 +750,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           if ((int)lane == leader) wrun[warp * k + b] += (int)total;
         }
         if (take) {
-          tmf[v] = 1;
+          mstamp[v] = cur_stamp;
+          opart[v] = A.part[v];
           A.dest[v] = A.rtgt[v];
         }
         wq_push(qa, take, v, lmov, cnt + C_MOV);
@@ -747,7 +765,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           v = A.lcand[idx];
           take = (int)A.rcell[v] < cstar[A.part[v]];
           if (take) {
-            tmf[v] = 1;
+            mstamp[v] = cur_stamp;
+            opart[v] = A.part[v];
             A.dest[v] = A.rtgt[v];
           }
         }
@@ -757,23 +776,25 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       grid.sync();
       PHASE_MARK(8);
     }
-    // ---- K13 apply moves over the movers: exact dJ + block weights
+    // ---- K13 apply + commit over the movers: exact dJ, block weights, ext
+    // counts, part[v] = dest[v] in place (a mover's neighbours read its old
+    // block from opart), then restore the list invariants
     {
-      const long long nm = cnt[C_MOV];
+      const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
       long long acc = 0;
       for (long long ib = gw * GPW; ib < nm; ib += NW * GPW) {
         const long long idx = ib + gi;
         if (idx < nm) {
           const int v = lmov[idx];
-          const int ov = A.part[v], nv = A.dest[v];
-          const unsigned long long oc = T.code[ov], nc = T.code[nv];
+          const int ov = opart[v], nv = A.dest[v];
+          const unsigned long long oc = T.code[ov], nc2 = T.code[nv];
           int dext = 0;
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
             const int u = A.tgt[e];
-            const bool um = tmf[u];
-            const int ou = A.part[u];
+            const bool um = mstamp[u] == cur_stamp;
+            const int ou = um ? opart[u] : A.part[u];
             const int nu = um ? A.dest[u] : ou;
-            const long long dd = cdist(s_dbit, nc, T.code[nu]) -
+            const long long dd = cdist(s_dbit, nc2, T.code[nu]) -
                                  cdist(s_dbit, oc, T.code[ou]);
             acc += (long long)A.w[e] * dd * (um ? 1 : 2);
             if (ext) {  // boundary counts: edge (v,u) before / after the moves
@@ -783,36 +804,27 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             }
           }
           if (ext && dext) atomicAdd(&ext[v], dext);
-          if (li == 0 && ov != nv) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&A.bw[ov]),
-                      (unsigned long long)(-(long long)A.vw[v]));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&A.bw[nv]),
-                      (unsigned long long)(long long)A.vw[v]);
+          if (li == 0) {
+            A.part[v] = nv;
+            if (ov != nv) {
+              atomicAdd(reinterpret_cast<unsigned long long*>(&A.bw[ov]),
+                        (unsigned long long)(-(long long)A.vw[v]));
+              atomicAdd(reinterpret_cast<unsigned long long*>(&A.bw[nv]),
+                        (unsigned long long)(long long)A.vw[v]);
+            }
           }
         }
       }
       block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
-    }
-    grid.sync();
-      PHASE_MARK(9);
-    // ---- commit + restore the list invariants
-    {
-      const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
-      for (long long i = gt; i < nm; i += GT) {
-        const int v = lmov[i];
-        A.part[v] = A.dest[v];
-        if (!balanced_now) tmf[v] = 0;  // no locks after a rebalance pass
-      }
       if (balanced_now) {
         for (long long i = gt; i < nc; i += GT) A.gkey[A.lcand[i]] = kGainNone;
-        for (long long i = gt; i < prev_n; i += GT) lkf[lprev[i]] = 0;  // old locks
       } else {
         for (long long i = gt; i < nc; i += GT) A.rtgt[A.lcand[i]] = -1;
         for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
       }
     }
     grid.sync();
-      PHASE_MARK(10);
+    PHASE_MARK(9);
     // ---- Alg. 4 control (refinement.py:433-463), replicated per CTA
     const long long mx = block_max_bw(A.bw, k);
     if (threadIdx.x == 0) {
@@ -828,15 +840,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         C.i_w++;
         C.pass_counter++;
       }
-      // the move flags of this pass become the next locks (LP) or are gone
-      if (balanced_now) {
-        C.locks_nonempty = mv > 0;
-        C.lp_par ^= 1;
-        C.prev_n = (int)mv;
-      } else {
-        C.locks_nonempty = 0;
-        C.prev_n = 0;
-      }
+      // this pass's movers become the next locks (LP) or there are none
+      C.lock_stamp = (balanced_now && mv > 0) ? cur_stamp : 0;
+      C.locks_nonempty = C.lock_stamp != 0;
+      C.prev_n = 0;
       if (mv == 0 && ((balanced_now && entry_locks_empty) || (!balanced_now && incomplete))) {
         C.brk = 1;
       } else {
