@@ -1323,7 +1323,7 @@ static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, co
   G.src = DBuf<int>((size_t)std::max(m2, 1ll), s);
   // device buffers come from `s`'s stream order: the workers' streams wait
   GIM_CUDA(sync_stream(s));
-  constexpr long long kChunk = 1ll << 21;  // elements per staging buffer
+  constexpr long long kChunk = 1ll << 19;  // elements per staging buffer
   std::vector<UpJob> jobs;
   auto add = [&](const int64_t* h, long long cnt, int* d, int kind) {
     for (long long i = 0; i < cnt; i += kChunk)
