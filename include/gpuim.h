@@ -193,6 +193,16 @@ int gim_internal_partitioner(const gim_graph* g, int32_t k, double eps_local, ui
 int gim_hierarchical_multisection(const gim_graph* g, const gim_topology* t, double eps,
                                   uint64_t seed, int32_t* assignment, void* stream);
 
+/* GPU-HM as a standalone algorithm on HOST int64 CSR arrays (the reference
+ * Graph's own arrays): hierarchical_multisection of the whole graph with the
+ * built-in partitioner (pipelines.py:49-110).  out_assignment int64[n],
+ * out_block_weights int64[k] are host buffers. */
+int gim_hierarchical_multisection_host(int64_t n, const int64_t* offsets, const int64_t* targets,
+                                       const int64_t* edge_weights,
+                                       const int64_t* vertex_weights, const gim_topology* t,
+                                       double eps, uint64_t seed, int64_t* out_assignment,
+                                       int64_t* out_block_weights, void* stream);
+
 /* ---- the drop-in ------------------------------------------------------- */
 /* Default keyword arguments of integrated_map. */
 int gim_default_params(gim_im_params* out);

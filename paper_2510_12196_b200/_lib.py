@@ -116,6 +116,7 @@ SIGNATURES: dict[str, list] = {
     "gim_greedy_graph_growing": [GP, I32, P, P],
     "gim_internal_partitioner": [GP, I32, DBL, U64, P, P],
     "gim_hierarchical_multisection": [GP, TP, DBL, U64, P, P],
+    "gim_hierarchical_multisection_host": [I64, P, P, P, P, TP, DBL, U64, P, P, P],
     "gim_default_params": [PARP],
     "gim_integrated_map_device": [GP, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_integrated_map": [I64, P, P, P, P, TP, DBL, U64, PARP, P, P, PSTP, P],

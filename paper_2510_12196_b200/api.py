@@ -97,23 +97,54 @@ def integrated_map(g, t, eps: float, seed: int = 0, *, coarsest_factor: int = 12
     return m
 
 
+def hierarchical_multisection(g, t, eps: float, partitioner=None, seed: int = 0,
+                              trace: list | None = None):
+    """GPU-HM: recursive multisection along the machine hierarchy
+    (pipelines.py:49-110) of the whole graph on the B200, with the built-in
+    multilevel partitioner.  Same signature and return type as the
+    reference; `ValueError` on an empty graph.  The reference's plugin seam
+    (a Python `partitioner` callable) and `trace` records run the user's
+    Python code per tree node and are not part of the GPU path: they raise
+    NotImplementedError (use the reference package for them)."""
+    from . import device as D
+
+    n = len(g.offsets) - 1
+    if n == 0:
+        raise ValueError("cannot map an empty graph")
+    if partitioner is not None or trace is not None:
+        raise NotImplementedError(
+            "custom partitioners / trace records are not supported on the GPU path")
+    a, bw = D.hierarchical_multisection_host(g.offsets, g.edge_targets, g.edge_weights,
+                                             g.vertex_weights, tuple(t.hierarchy),
+                                             tuple(t.distances), eps, seed)
+    return _mapping_type()(a, bw)
+
+
 _INSTALL_SITES = ("promap.pipelines", "promap.estimators", "promap.cli", "promap.bench", "promap")
+_NAMES = ("integrated_map", "hierarchical_multisection")
 
 
 def install() -> list[str]:
-    """Rebind `integrated_map` in every reference module that imported it
-    (pipelines, estimators.py:17, cli.py:33, bench.py:25, __init__.py:43), so
-    the reference's estimator, CLI and bench run on the GPU path unchanged.
-    Returns the patched module names."""
+    """Rebind `integrated_map` and `hierarchical_multisection` in every
+    reference module that imported them (pipelines, estimators.py:17,
+    cli.py:33, bench.py:25, __init__.py:42-43), so the reference's estimators
+    (IntegratedMapper, MultisectionMapper), CLI (`--algo im|hm`) and bench run
+    on the GPU path unchanged.  Returns the patched module names."""
     import importlib
 
+    ours = {"integrated_map": integrated_map,
+            "hierarchical_multisection": hierarchical_multisection}
     patched = []
     for name in _INSTALL_SITES:
         mod = importlib.import_module(name)
-        if hasattr(mod, "integrated_map"):
-            if not hasattr(mod, "_cpu_integrated_map"):
-                mod._cpu_integrated_map = mod.integrated_map
-            mod.integrated_map = integrated_map
+        hit = False
+        for fn in _NAMES:
+            if hasattr(mod, fn):
+                if not hasattr(mod, f"_cpu_{fn}"):
+                    setattr(mod, f"_cpu_{fn}", getattr(mod, fn))
+                setattr(mod, fn, ours[fn])
+                hit = True
+        if hit:
             patched.append(name)
     return patched
 
@@ -124,5 +155,6 @@ def uninstall() -> None:
 
     for name in _INSTALL_SITES:
         mod = sys.modules.get(name) or importlib.import_module(name)
-        if hasattr(mod, "_cpu_integrated_map"):
-            mod.integrated_map = mod._cpu_integrated_map
+        for fn in _NAMES:
+            if hasattr(mod, f"_cpu_{fn}"):
+                setattr(mod, fn, getattr(mod, f"_cpu_{fn}"))

@@ -1665,6 +1665,40 @@ extern "C" int gim_hierarchical_multisection(const gim_graph* g, const gim_topol
   });
 }
 
+// GPU-HM on host arrays (pipelines.py:49-110 as a standalone algorithm):
+// upload as gim_integrated_map, multisection of the whole graph, int64 out
+extern "C" int gim_hierarchical_multisection_host(int64_t n, const int64_t* offsets,
+                                                  const int64_t* targets,
+                                                  const int64_t* edge_weights,
+                                                  const int64_t* vertex_weights,
+                                                  const gim_topology* t, double eps,
+                                                  uint64_t seed, int64_t* out_assignment,
+                                                  int64_t* out_block_weights, void* stream) {
+  return guard([&] {
+    GIM_CHECK(t && offsets && out_assignment && out_block_weights, GIM_E_INVALID,
+              "null argument");
+    GIM_CHECK(n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+    cudaStream_t s = (cudaStream_t)stream;
+    OwnedGraph G;
+    upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
+    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
+    std::vector<long long> d(t->distances, t->distances + t->levels);
+    DBuf<int> part((size_t)n, s);
+    DBuf<long long> bw((size_t)tp.k, s);
+    RunStats st;
+    reset_launches();
+    hierarchical_multisection(G.view(), G.total_vw, h, d, eps, seed, part.get(), st, s);
+    block_weights((int)n, G.vw.get(), part.get(), tp.k, bw.get(), s);
+    int* h_part = static_cast<int*>(pinned_scratch(sizeof(int) * (size_t)n));
+    GIM_CUDA(cudaMemcpyAsync(h_part, part.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(out_block_weights, bw.get(), sizeof(long long) * tp.k,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    for (long long i = 0; i < n; ++i) out_assignment[i] = h_part[i];
+  });
+}
+
 extern "C" int gim_integrated_map_device(const gim_graph* g, const gim_topology* t, double eps,
                                          uint64_t seed, const gim_im_params* params,
                                          int32_t* out_assignment, int64_t* out_block_weights,

@@ -380,6 +380,24 @@ def integrated_map_host(offsets, targets, eweights, vweights, hierarchy, distanc
     return a, bw, stats_dict(st)
 
 
+def hierarchical_multisection_host(offsets, targets, eweights, vweights, hierarchy, distances,
+                                   eps: float, seed: int = 0):
+    """GPU-HM on HOST int64 arrays -> (assignment int64 np, block weights int64 np)."""
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    tgt = np.ascontiguousarray(targets, dtype=np.int64)
+    ew = np.ascontiguousarray(eweights, dtype=np.int64)
+    vw = np.ascontiguousarray(vweights, dtype=np.int64)
+    n = len(off) - 1
+    k = int(np.prod(hierarchy))
+    a = np.empty(max(n, 0), dtype=np.int64)
+    bw = np.empty(k, dtype=np.int64)
+    t = topology_struct(hierarchy, distances)
+    ptr = lambda x: x.ctypes.data if x.size else None  # noqa: E731
+    _lib.call("gim_hierarchical_multisection_host", int(n), ptr(off), ptr(tgt), ptr(ew), ptr(vw),
+              C.byref(t), float(eps), int(seed) & (2**64 - 1), ptr(a), ptr(bw), stream_ptr())
+    return a, bw
+
+
 def set_fanout(on: bool) -> None:
     """Sibling multisection subtrees on concurrent host threads/streams."""
     _lib.load().gim_set_fanout(1 if on else 0)

@@ -55,6 +55,12 @@ def test_dropin_signature_matches_reference():
         assert sig.parameters[k].kind == inspect.Parameter.KEYWORD_ONLY
 
 
+def test_gpu_hm_signature_matches_reference():
+    from paper_2510_12196_b200 import hierarchical_multisection
+    names = list(inspect.signature(hierarchical_multisection).parameters)
+    assert names == ["g", "t", "eps", "partitioner", "seed", "trace"]
+
+
 def test_dropin_rejects_like_reference():
     from paper_2510_12196_b200 import integrated_map
     from paper_2510_12196_b200.generators import HostGraph, gen_grid
@@ -87,8 +93,10 @@ patched = P.install()
 assert set(patched) == {{'promap.pipelines','promap.estimators','promap.cli','promap.bench','promap'}}, patched
 for m in (promap, promap.pipelines, promap.estimators, promap.cli, promap.bench):
     assert m.integrated_map is P.integrated_map
+    assert m.hierarchical_multisection is P.hierarchical_multisection
 P.uninstall()
 assert promap.pipelines.integrated_map is not P.integrated_map
+assert promap.pipelines.hierarchical_multisection is not P.hierarchical_multisection
 print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)

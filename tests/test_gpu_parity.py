@@ -336,3 +336,26 @@ def test_rmat_small_matches_oracle(D):
     a, bw, l_max = O.integrated_map(g, t, 0.03, 1, coarsest_factor=16)
     assert np.array_equal(m.assignment, a)
     assert np.array_equal(m.block_weights, bw)
+
+
+def test_gpu_hm_host_api_golden(D, golden):
+    """GPU-HM through the drop-in (host int64 arrays in, Mapping out) equals
+    the reference's hierarchical_multisection on its golden cases."""
+    from paper_2510_12196_b200 import hierarchical_multisection
+    for c in golden("multisection"):
+        g, t = c.graph(), c.topology()
+        m = hierarchical_multisection(g, t, c.scalar("eps"), seed=int(c["seed"]))
+        assert np.array_equal(m.assignment, c["assignment"].astype(np.int64))
+        assert np.array_equal(m.block_weights,
+                              O.block_weights(g.vertex_weights, c["assignment"], t.k))
+
+
+def test_gpu_hm_matches_oracle_rgg(D):
+    from paper_2510_12196_b200 import hierarchical_multisection
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << 13, 0.55, 1)
+    t = O.OTopology((4, 8, 2), (1, 10, 100))
+    m = hierarchical_multisection(g, t, 0.03, seed=4)
+    assert np.array_equal(m.assignment, O.hierarchical_multisection(g, t, 0.03, seed=4))
+    with pytest.raises(NotImplementedError):
+        hierarchical_multisection(g, t, 0.03, partitioner=lambda *a: None)
