@@ -38,6 +38,8 @@ extern "C" {
 #define GIM_E_OVERFLOW 4    /* value does not fit the int32 device layout   */
 #define GIM_E_INTERNAL 5    /* unexpected internal failure                 */
 #define GIM_E_EMPTY 6       /* empty graph (reference raises ValueError)     */
+#define GIM_E_FORMAT 7      /* malformed METIS file (MetisFormatError)       */
+#define GIM_E_IO 8          /* file cannot be opened / read                  */
 
 #define GIM_MAX_LEVELS 8
 
@@ -246,6 +248,16 @@ void gim_set_batch(int32_t on);
 /* Contract level-stack matchings row-wise (default 1) or always with the
  * radix-sort path.  The coarse graphs are identical. */
 void gim_set_rowwise_contraction(int32_t on);
+
+/* ---- METIS input (graph.py:170-294, load_metis) -------------------------
+ * gim_metis_load parses and validates a METIS ascii file with the reference's
+ * rules and messages ("line N: ...", GIM_E_FORMAT) into a host CSR held by
+ * *handle and reports n and 2m; gim_metis_fetch copies it into caller int64
+ * arrays (offsets[n+1], targets[2m], edge weights[2m], vertex weights[n],
+ * sources[2m]; any may be null) and frees the handle. */
+int gim_metis_load(const char* path, void** handle, int64_t* n, int64_t* m2);
+int gim_metis_fetch(void* handle, int64_t* offsets, int64_t* targets, int64_t* eweights,
+                    int64_t* vweights, int64_t* sources);
 
 /* kernels launched by this host thread since the last reset (evidence). */
 int64_t gim_launch_count(void);

@@ -5,9 +5,12 @@ Drop-in for the reference's `promap.pipelines.integrated_map`
 `Mapping` result, computed by hand-written sm_100a kernels in libgpuim.so
 (see include/gpuim.h and DESIGN.md).  `hierarchical_multisection` is GPU-HM,
 the reference's multisection algorithm (pipelines.py:49-110) on the same
-kernels.  `install()` rebinds both entry points in every reference module
-that imported them.
+kernels.  `load_metis` is a native (C++) drop-in for promap.graph.load_metis.
+`install()` rebinds these entry points in every reference module that
+imported them.
 """
 from .api import Mapping, hierarchical_multisection, install, integrated_map, uninstall
+from .metis import MetisFormatError, load_metis
 
-__all__ = ["integrated_map", "hierarchical_multisection", "install", "uninstall", "Mapping"]
+__all__ = ["integrated_map", "hierarchical_multisection", "load_metis", "MetisFormatError",
+           "install", "uninstall", "Mapping"]

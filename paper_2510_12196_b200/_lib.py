@@ -19,6 +19,8 @@ GIM_E_UNSUPPORTED = 3
 GIM_E_OVERFLOW = 4
 GIM_E_INTERNAL = 5
 GIM_E_EMPTY = 6
+GIM_E_FORMAT = 7
+GIM_E_IO = 8
 
 
 class GimGraph(C.Structure):
@@ -129,6 +131,9 @@ SIGNATURES: dict[str, list] = {
     "gim_launch_count": [],
     "gim_reset_launch_count": [],
     "gim_release_cached_memory": [],
+    "gim_metis_load": [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                       C.POINTER(C.c_int64)],
+    "gim_metis_fetch": [C.c_void_p, P, P, P, P, P],
 }
 RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
             "gim_reset_launch_count": None, "gim_set_profiling": None,

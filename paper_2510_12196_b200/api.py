@@ -120,20 +120,25 @@ def hierarchical_multisection(g, t, eps: float, partitioner=None, seed: int = 0,
     return _mapping_type()(a, bw)
 
 
-_INSTALL_SITES = ("promap.pipelines", "promap.estimators", "promap.cli", "promap.bench", "promap")
-_NAMES = ("integrated_map", "hierarchical_multisection")
+_INSTALL_SITES = ("promap.pipelines", "promap.estimators", "promap.cli", "promap.bench", "promap",
+                  "promap.graph")
+_NAMES = ("integrated_map", "hierarchical_multisection", "load_metis")
 
 
 def install() -> list[str]:
-    """Rebind `integrated_map` and `hierarchical_multisection` in every
-    reference module that imported them (pipelines, estimators.py:17,
-    cli.py:33, bench.py:25, __init__.py:42-43), so the reference's estimators
-    (IntegratedMapper, MultisectionMapper), CLI (`--algo im|hm`) and bench run
-    on the GPU path unchanged.  Returns the patched module names."""
+    """Rebind `integrated_map`, `hierarchical_multisection` and
+    `load_metis` in every reference module that imported them (pipelines,
+    graph, estimators.py:17, cli.py:31-33, bench.py:23-25, __init__.py), so
+    the reference's estimators (IntegratedMapper, MultisectionMapper), CLI
+    (`--algo im|hm`, METIS input) and bench run on the native path
+    unchanged.  Returns the patched module names."""
     import importlib
 
+    from .metis import load_metis
+
     ours = {"integrated_map": integrated_map,
-            "hierarchical_multisection": hierarchical_multisection}
+            "hierarchical_multisection": hierarchical_multisection,
+            "load_metis": load_metis}
     patched = []
     for name in _INSTALL_SITES:
         mod = importlib.import_module(name)

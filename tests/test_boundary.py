@@ -87,10 +87,12 @@ def test_install_rebinds_every_import_site():
     code = f"""
 import sys
 sys.path.insert(0, {str(REF)!r}); sys.path.insert(0, {str(ROOT)!r})
-import promap, promap.pipelines, promap.estimators, promap.cli, promap.bench
+import promap, promap.pipelines, promap.estimators, promap.cli, promap.bench, promap.graph
 import paper_2510_12196_b200 as P
 patched = P.install()
-assert set(patched) == {{'promap.pipelines','promap.estimators','promap.cli','promap.bench','promap'}}, patched
+assert set(patched) == {{'promap.pipelines','promap.estimators','promap.cli','promap.bench','promap','promap.graph'}}, patched
+for m in (promap.graph, promap.cli, promap.bench):
+    assert m.load_metis is P.load_metis
 for m in (promap, promap.pipelines, promap.estimators, promap.cli, promap.bench):
     assert m.integrated_map is P.integrated_map
     assert m.hierarchical_multisection is P.hierarchical_multisection
