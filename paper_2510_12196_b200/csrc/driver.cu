@@ -141,6 +141,7 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   fb.best_bw = rb.best_bw.get();
   fb.ctr = rb.fctr.get();
   fb.bstamp = rb.bstamp.get();
+  fb.wdeg = rb.rvals2.get();  // free during the fused loop (host strong passes only)
   const size_t nn = (size_t)rb.cap_n;
   fb.lsmall = rb.lists.get();
   fb.lheavy = fb.lsmall + nn;

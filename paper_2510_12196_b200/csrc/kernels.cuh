@@ -145,7 +145,7 @@ struct FusedBuffers {
   unsigned char *cand = nullptr, *tm0 = nullptr, *tm1 = nullptr, *rcell = nullptr;
   int *dest = nullptr, *rtgt = nullptr, *best = nullptr;
   long long *gkey = nullptr, *best_bw = nullptr, *ctr = nullptr;
-  int *bstamp = nullptr, *lsmall = nullptr, *lheavy = nullptr, *lcand = nullptr;
+  int *bstamp = nullptr, *wdeg = nullptr, *lsmall = nullptr, *lheavy = nullptr, *lcand = nullptr;
   int *lmov0 = nullptr, *lmov1 = nullptr;
   long long lp_seen = 0, weak_seen = 0;
   // owned

@@ -83,7 +83,8 @@ struct FusedArgs {
   unsigned char* flags1;
   int* rtgt;
   unsigned char* rcell;
-  int* bstamp;         // boundary stamp per vertex
+  int* bstamp;         // ext: boundary counts per vertex (large levels)
+  int* wdeg;           // weighted degree per vertex (with ext), else null
   int* lsmall;         // work lists
   int* lheavy;
   int* lcand;
@@ -260,12 +261,16 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     }
     for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
   }
-  if (ext) {  // boundary counts of the entry mapping, thread per vertex
+  if (ext) {  // boundary counts of the entry mapping + weighted degrees
     for (long long v = gt; v < n; v += GT) {
       const int pv = A.part[v];
-      int c = 0;
-      for (int e = A.off[v]; e < A.off[v + 1]; ++e) c += A.part[A.tgt[e]] != pv;
+      int c = 0, wd = 0;
+      for (int e = A.off[v]; e < A.off[v + 1]; ++e) {
+        c += A.part[A.tgt[e]] != pv;
+        wd += A.w[e];
+      }
       ext[v] = c;
+      A.wdeg[v] = wd;
     }
   }
   if (first) {
@@ -532,7 +537,12 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         ThreadEval r{};
         r.best_b = -1;
         bool ovf = false;
-        if (live) {
+        if (live && ext && ext[v] == 0) {
+          // interior vertex (every neighbour in its own block): no adjacent
+          // candidate, cur = 0, cost(tb) = wdeg * D(tb, own) — no row walk
+          if (tb >= 0)
+            r.cost_tb = (long long)A.wdeg[v] * cdist(s_dbit, T.code[tb], T.code[own]);
+        } else if (live) {
           const int e0 = A.off[v], e1 = A.off[v + 1];
           if (e1 - e0 > kTpvMaxDeg) {
             ovf = true;
@@ -1184,6 +1194,7 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.rtgt = fb.rtgt;
   A.rcell = fb.rcell;
   A.bstamp = fb.bstamp;
+  A.wdeg = fb.wdeg;
   A.lsmall = fb.lsmall;
   A.lheavy = fb.lheavy;
   A.lcand = fb.lcand;
