@@ -382,11 +382,21 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       // ---- K9 first filter (refinement.py:201-244)
       long long ns = n;  // items: vertices (vcent) or the boundary list
       if (!vcent) {
-        // boundary list (unlocked): ext[v] > 0
-        for (long long b0 = gt - lane; b0 < n; b0 += GT) {
-          const long long v = b0 + lane;
-          const bool bnd = v < n && ext[v] > 0 && !(use_locks && mstamp[v] == lock_stamp);
-          wq_push(qa, bnd, (int)v, A.lsmall, cnt + C_SMALL);
+        // boundary list (unlocked): ext[v] > 0; four vertices per thread
+        // per step with their loads issued together
+        for (long long b0 = (gt - lane) * 4; b0 < n; b0 += GT * 4) {
+          bool bnd[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            bnd[q] = v < n && ext[v] > 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            if (bnd[q] && use_locks && mstamp[v] == lock_stamp) bnd[q] = false;
+            wq_push(qa, bnd[q], (int)v, A.lsmall, cnt + C_SMALL);
+          }
         }
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
         grid.sync();
@@ -509,10 +519,18 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       incomplete = n_elig == 0;
       long long ns = n;
       if (!vcent) {  // vertices of overloaded blocks
-        for (long long b0 = gt - lane; b0 < n; b0 += GT) {
-          const long long v = b0 + lane;
-          const bool inb = v < n && ovl[A.part[v]];
-          wq_push(qa, inb, (int)v, A.lsmall, cnt + C_SMALL);
+        for (long long b0 = (gt - lane) * 4; b0 < n; b0 += GT * 4) {
+          int pv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            pv[q] = v < n ? A.part[v] : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            wq_push(qa, pv[q] >= 0 && ovl[pv[q]], (int)v, A.lsmall, cnt + C_SMALL);
+          }
         }
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
         grid.sync();
@@ -649,28 +667,29 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       int n_part = 0;
       if (n_ovl > 0) {
         const unsigned lt = (1u << lane) - 1u;
-        for (int v0 = w0; v0 < w1; v0 += 64) {  // warp-uniform, two chunks in flight
-          const int va = v0 + lane, vb = v0 + 32 + lane;
-          const int ta = va < w1 ? A.rtgt[va] : -1;
-          const int tb2 = vb < w1 ? A.rtgt[vb] : -1;
-          bool pa = false, pb = false;
-          int ba = 0, bb = 0;
-          if (ta >= 0) {
-            ba = A.part[va];
-            pa = (int)A.rcell[va] == cstar[ba];
+        for (int v0 = w0; v0 < w1; v0 += 128) {  // warp-uniform, four chunks in flight
+          int tq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int vq = v0 + q * 32 + lane;
+            tq[q] = vq < w1 ? A.rtgt[vq] : -1;
           }
-          if (tb2 >= 0) {
-            bb = A.part[vb];
-            pb = (int)A.rcell[vb] == cstar[bb];
+          int bq[4];
+          bool pq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int vq = v0 + q * 32 + lane;
+            bq[q] = tq[q] >= 0 ? A.part[vq] : 0;
+            pq[q] = tq[q] >= 0 && (int)A.rcell[vq] == cstar[bq[q]];
           }
-          if (pa) atomicAdd(&wrun[warp * k + ba], A.vw[va]);
-          if (pb) atomicAdd(&wrun[warp * k + bb], A.vw[vb]);
-          const unsigned ma = __ballot_sync(0xffffffffu, pa);
-          if (pa) A.lheavy[w0 + n_part + __popc(ma & lt)] = va;
-          n_part += __popc(ma);
-          const unsigned mb = __ballot_sync(0xffffffffu, pb);
-          if (pb) A.lheavy[w0 + n_part + __popc(mb & lt)] = vb;
-          n_part += __popc(mb);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int vq = v0 + q * 32 + lane;
+            if (pq[q]) atomicAdd(&wrun[warp * k + bq[q]], A.vw[vq]);
+            const unsigned mq = __ballot_sync(0xffffffffu, pq[q]);
+            if (pq[q]) A.lheavy[w0 + n_part + __popc(mq & lt)] = vq;
+            n_part += __popc(mq);
+          }
         }
       }
       __syncthreads();
