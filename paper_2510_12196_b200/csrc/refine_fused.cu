@@ -57,7 +57,7 @@ constexpr int kFusedMinBlocks = 3;
 constexpr int kMaxCluster = 16;
 // vertex-centric first filter when a level has at most this many vertex
 // groups per warp (else edge-parallel boundary pass + lists)
-constexpr int kVcSteps = 8;
+constexpr int kVcSteps = 2;
 // longest row evaluated thread-per-vertex (longer rows: warp table path)
 constexpr int kTpvMaxDeg = 64;  // non-portable cluster size (B200 allows 16)
 constexpr int kCtrStride = 8;  // per-iteration-parity counters
