@@ -718,6 +718,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int*
 // go through the warp-per-row shared-memory path into the same buffers.
 constexpr int kCtTpv = 32;
 constexpr int kCtBlock = 128;
+// slots per row chunk (8 ints = one 32-byte sector of targets / weights)
+constexpr int kCtChunk = 8;
 
 __global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __restrict__ mem,
                                                       const int* __restrict__ rowlen,
@@ -742,19 +744,19 @@ __global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __rest
       const int vv = part ? v1 : v0;
       if (vv < 0) break;
       const int e1 = off[vv + 1];
-      for (int e = off[vv]; e < e1; e += 4) {
-        int tg[4], wg[4], kg[4];
+      for (int e = off[vv]; e < e1; e += kCtChunk) {
+        int tg[kCtChunk], wg[kCtChunk], kg[kCtChunk];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kCtChunk; ++q)
           if (e + q < e1) {
             tg[q] = tgt[e + q];
             wg[q] = w[e + q];
           }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kCtChunk; ++q)
           if (e + q < e1) kg[q] = cmap[tg[q]];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kCtChunk; ++q) {
           if (e + q >= e1) break;
           const int key = kg[q];
           if (key == c) continue;  // self loop
