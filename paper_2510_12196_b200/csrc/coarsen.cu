@@ -100,19 +100,33 @@ __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restri
 // evaluated in place by the whole warp (strided slots + shuffle argmax).
 constexpr int kHemTpv = 32;
 
+// per-vertex round data, one 16-byte gather per candidate: c_u (-1 when u
+// is matched) and S_u = splitmix64(seed ^ splitmix64(u)), the first two
+// stages of hash2(seed, a, b) = splitmix64(S_a ^ b) for a = min(v, u)
+struct __align__(16) HemV {
+  unsigned long long s;
+  int c;
+  int pad;
+};
+
 __global__ void k_hem_elig(int n, const int* __restrict__ partner, const int* __restrict__ vw,
-                           int* __restrict__ elig_c, const long long* gate) {
+                           unsigned long long seed, HemV* __restrict__ ev,
+                           const long long* gate) {
   if (hem_gated(gate, n)) return;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    elig_c[v] = partner[v] < 0 ? vw[v] : -1;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    HemV x;
+    x.s = splitmix64(seed ^ splitmix64((unsigned long long)v));
+    x.c = partner[v] < 0 ? vw[v] : -1;
+    x.pad = 0;
+    ev[v] = x;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restrict__ off,
                                                       const int* __restrict__ tgt,
                                                       const int* __restrict__ w,
-                                                      const int* __restrict__ elig_c,
-                                                      double l_max, unsigned long long seed,
-                                                      int* __restrict__ pref,
+                                                      const HemV* __restrict__ ev,
+                                                      double l_max, int* __restrict__ pref,
                                                       const long long* gate) {
   if (hem_gated(gate, n)) return;
   const int lane = lane_id();
@@ -120,7 +134,11 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
   for (long long b0 = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; b0 < n; b0 += T) {
     const int v = (int)(b0 + lane);
     const bool inr = v < n;
-    const int cvv = inr ? elig_c[v] : -1;
+    HemV me;
+    me.s = 0;
+    me.c = -1;
+    if (inr) me = ev[v];
+    const int cvv = me.c;
     const bool active = cvv >= 0;  // unmatched
     int e0 = 0, e1 = 0;
     if (active) {
@@ -135,7 +153,8 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
     if (active && !longrow) {
       const long long cv = cvv;
       for (int e = e0; e < e1; e += 4) {
-        int tg[4], wg[4], cg[4];
+        int tg[4], wg[4];
+        HemV cg[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (e + q < e1) {
@@ -144,18 +163,19 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
           }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (e + q < e1) cg[q] = elig_c[tg[q]];
+          if (e + q < e1) cg[q] = ev[tg[q]];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (e + q >= e1) break;
-          const int cu = cg[q];
+          const int cu = cg[q].c;
           if (cu < 0 || (double)(cv + cu) > l_max) continue;
           HemCand c;
           c.w = wg[q];
           c.c = cu;
           c.slot = e + q;
           c.u = tg[q];
-          c.h = hash2(seed, (unsigned long long)min(v, c.u), (unsigned long long)max(v, c.u));
+          c.h = v < c.u ? splitmix64(me.s ^ (unsigned long long)c.u)
+                        : splitmix64(cg[q].s ^ (unsigned long long)v);  // = hash2(seed, min, max)
           if (hem_better(c, best)) best = c;
         }
       }
@@ -168,20 +188,23 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
       const int x = __shfl_sync(0xffffffffu, v, l);
       const int xb = __shfl_sync(0xffffffffu, e0, l), xe = __shfl_sync(0xffffffffu, e1, l);
       const long long cx = __shfl_sync(0xffffffffu, cvv, l);
+      const unsigned long long sx = __shfl_sync(0xffffffffu, me.s, l);
       HemCand bx;
       bx.u = -1;
       bx.w = bx.c = bx.slot = 0;
       bx.h = 0;
       for (int e = xb + lane; e < xe; e += 32) {
         const int u = tgt[e];
-        const int cu = elig_c[u];
+        const HemV hu = ev[u];
+        const int cu = hu.c;
         if (cu < 0 || (double)(cx + cu) > l_max) continue;
         HemCand c;
         c.w = w[e];
         c.c = cu;
         c.slot = e;
         c.u = u;
-        c.h = hash2(seed, (unsigned long long)min(x, u), (unsigned long long)max(x, u));
+        c.h = x < u ? splitmix64(sx ^ (unsigned long long)u)
+                    : splitmix64(hu.s ^ (unsigned long long)x);  // = hash2(seed, min, max)
         if (hem_better(c, bx)) bx = c;
       }
 #pragma unroll
@@ -209,10 +232,10 @@ void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
   if (g.n == 0) return;
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
-  DBuf<int> elig((size_t)g.n, s);
-  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, elig.get(), gate);
-  k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, elig.get(),
-                                                           l_max, seed, pref, gate);
+  DBuf<HemV> ev((size_t)g.n, s);
+  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, seed, ev.get(), gate);
+  k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, ev.get(),
+                                                           l_max, pref, gate);
   k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched, gate);
   GIM_LAUNCH_CHECK();
   count_launch(3);
