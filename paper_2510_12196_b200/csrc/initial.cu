@@ -28,6 +28,7 @@ namespace gim {
 // the global scratch); every selection is a CTA-wide argmax/argmin.
 
 constexpr int kGggBlock = 256;
+constexpr int kGggMaxK = 64;  // block weights in shared memory up to this k
 constexpr int kGggWarps = kGggBlock / 32;
 
 struct GggJob {
@@ -131,62 +132,61 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
     if (threadIdx.x == 0) seeds[ns] = sv;
     __syncthreads();
   }
-  // growth (pipelines.py:155-188)
+  // growth (pipelines.py:155-188), two barriers per step: (A) every thread
+  // finds the lightest block and its share of the argmax, (B) every thread
+  // merges the warp results, falls back to the lowest unassigned vertex
+  // when the frontier is dry, and applies the claim's row update
+  __shared__ long long s_bw[kGggMaxK];
+  long long* bw = k <= kGggMaxK ? s_bw : J.bwork;
   for (int v = threadIdx.x; v < n; v += blockDim.x) part[v] = -1;
   for (long long i = threadIdx.x; i < (long long)k * n; i += blockDim.x) conn[i] = 0;
-  for (int b = threadIdx.x; b < k; b += blockDim.x) J.bwork[b] = 0;
-  if (threadIdx.x == 0) s_next = 0;
+  for (int b = threadIdx.x; b < k; b += blockDim.x) bw[b] = 0;
   __syncthreads();
-  auto claim = [&](int v, int b) {
+  auto claim_rows = [&](int v, int b) {  // all threads; part[v] / bw by thread 0
     if (threadIdx.x == 0) {
       part[v] = b;
-      J.bwork[b] += J.vw[v];
+      bw[b] += J.vw[v];
     }
-    __syncthreads();
     for (int e = J.off[v] + threadIdx.x; e < J.off[v + 1]; e += blockDim.x) {
-      int u = J.tgt[e];
-      if (part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per thread
+      const int u = J.tgt[e];
+      if (u != v && part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per thread
     }
-    __syncthreads();
   };
-  for (int b = 0; b < k; ++b) claim(seeds[b], b);
-  for (int assigned = k; assigned < n; ++assigned) {
-    if (threadIdx.x < 32) {  // lightest block, lowest id on ties
-      long long bwv = LLONG_MAX;
-      int bb = INT_MAX;
-      for (int b = threadIdx.x; b < k; b += 32) {
-        long long x = J.bwork[b];
-        if (x < bwv) { bwv = x; bb = b; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
-        int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-        if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
-      }
-      if (threadIdx.x == 0) s_b = bb;
-    }
+  for (int b = 0; b < k; ++b) {
+    claim_rows(seeds[b], b);
     __syncthreads();
-    const int bb = s_b;
+  }
+  int next_free = 0;  // identical in every thread
+  for (int assigned = k; assigned < n; ++assigned) {
+    long long bwv = LLONG_MAX;
+    int bb = 0;
+    for (int b = 0; b < k; ++b) {  // lightest block, lowest id on ties
+      const long long x = bw[b];
+      if (x < bwv) { bwv = x; bb = b; }
+    }
     const int* cb = conn + (long long)bb * n;
     int bc = 0, bv = INT_MAX;
     for (int u = threadIdx.x; u < n; u += blockDim.x) {
-      int c = cb[u];
+      const int c = cb[u];
       if (c > bc && part[u] < 0) { bc = c; bv = u; }
     }
-    cta_argmax(bc, bv, sa, sb);
-    if (threadIdx.x == 0) {
-      int v = bv;
-      if (bc == 0) {  // frontier dried up: lowest unassigned vertex
-        int f = s_next;
-        while (part[f] >= 0) ++f;
-        s_next = f;
-        v = f;
-      }
-      s_v = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int a2 = __shfl_xor_sync(0xffffffffu, bc, o), b2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      if (a2 > bc || (a2 == bc && b2 < bv)) { bc = a2; bv = b2; }
     }
+    if (lane_id() == 0) { sa[threadIdx.x >> 5] = bc; sb[threadIdx.x >> 5] = bv; }
     __syncthreads();
-    claim(s_v, bb);
+    int ga = sa[0], gv = sb[0];
+    for (int i = 1; i < kGggWarps; ++i)
+      if (sa[i] > ga || (sa[i] == ga && sb[i] < gv)) { ga = sa[i]; gv = sb[i]; }
+    if (ga == 0) {  // frontier dried up: lowest unassigned vertex (CTA-uniform)
+      while (part[next_free] >= 0) ++next_free;
+      gv = next_free;
+      __syncthreads();  // every thread has scanned part[] before the claim writes it
+    }
+    claim_rows(gv, bb);
+    __syncthreads();
   }
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
