@@ -5,6 +5,7 @@
 // :132-188, hierarchical_multisection leaf :78-80), graph.py
 // (extract_subgraphs :357-389).
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -42,6 +43,8 @@ struct GggJob {
   int* scratch;     // global fallback: dist[n] + part[n] + seeds[k] + conn[k*n]
   long long* bwork; // [k]
   int use_smem;
+  int m2;
+  int stage;        // 1: the graph itself is copied into shared memory too
 };
 
 // CTA-wide lexicographic max of (a, -b): larger a wins, ties -> smaller b
@@ -119,15 +122,38 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
     for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
     return;
   }
+  // small graphs: CSR staged in shared memory (every growth step walks a row
+  // and reads a vertex weight on its critical path)
+  const int* g_off = J.off;
+  const int* g_tgt = J.tgt;
+  const int* g_w = J.w;
+  const int* g_vw = J.vw;
+  if (J.stage) {
+    int* so = conn + (size_t)k * n;
+    int* st = so + n + 1;
+    int* sw = st + J.m2;
+    int* sv = sw + J.m2;
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) so[i] = J.off[i];
+    for (int i = threadIdx.x; i < J.m2; i += blockDim.x) {
+      st[i] = J.tgt[i];
+      sw[i] = J.w[i];
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sv[i] = J.vw[i];
+    __syncthreads();
+    g_off = so;
+    g_tgt = st;
+    g_w = sw;
+    g_vw = sv;
+  }
   // seeds (pipelines.py:143-153)
   if (threadIdx.x == 0) s_v = 0;
   __syncthreads();
-  cta_bfs(n, J.off, J.tgt, dist, &s_v, 1);
+  cta_bfs(n, g_off, g_tgt, dist, &s_v, 1);
   int sv = cta_pick_seed(n, dist, sa, sb);
   if (threadIdx.x == 0) seeds[0] = sv;
   __syncthreads();
   for (int ns = 1; ns < k; ++ns) {
-    cta_bfs(n, J.off, J.tgt, dist, seeds, ns);
+    cta_bfs(n, g_off, g_tgt, dist, seeds, ns);
     sv = cta_pick_seed(n, dist, sa, sb);
     if (threadIdx.x == 0) seeds[ns] = sv;
     __syncthreads();
@@ -145,11 +171,11 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   auto claim_rows = [&](int v, int b) {  // all threads; part[v] / bw by thread 0
     if (threadIdx.x == 0) {
       part[v] = b;
-      bw[b] += J.vw[v];
+      bw[b] += g_vw[v];
     }
-    for (int e = J.off[v] + threadIdx.x; e < J.off[v + 1]; e += blockDim.x) {
-      const int u = J.tgt[e];
-      if (u != v && part[u] < 0) conn[(long long)b * n + u] += J.w[e];  // distinct u per thread
+    for (int e = g_off[v] + threadIdx.x; e < g_off[v + 1]; e += blockDim.x) {
+      const int u = g_tgt[e];
+      if (u != v && part[u] < 0) conn[(long long)b * n + u] += g_w[e];  // distinct u per thread
     }
   };
   for (int b = 0; b < k; ++b) {
@@ -191,39 +217,25 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
 
-void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
-  ProfScope prof(P_GGG, 0.0, s);
-  const size_t words = (size_t)2 * g.n + k + (size_t)k * g.n;
-  const size_t smem = words * sizeof(int);
-  const bool use_smem = smem <= 160 * 1024;
-  DBuf<int> scratch(use_smem ? 1 : words, s);
-  DBuf<long long> bwork((size_t)k, s);
-  GggJob job{g.n, k, g.off, g.tgt, g.w, g.vw, part, scratch.get(), bwork.get(), use_smem ? 1 : 0};
-  DBuf<GggJob> dj(1, s);
-  GIM_CUDA(cudaMemcpyAsync(dj.get(), &job, sizeof(GggJob), cudaMemcpyHostToDevice, s));
-  if (use_smem && smem > 48 * 1024)
-    GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  160 * 1024));
-  k_ggg<<<1, kGggBlock, use_smem ? smem : 0, s>>>(dj.get(), 1);
-  count_launch();
-  GIM_LAUNCH_CHECK();
-  GIM_CUDA(sync_stream(s));  // job struct lives on this stack frame
-}
-
-// all coarsest graphs of a batched partitioner step, one CTA per graph
-void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
-               cudaStream_t s) {
+// one CTA per graph; working set (and, when it fits, the graph) in shared
+// memory, else a global scratch
+static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
+                       cudaStream_t s) {
   const int J = (int)gs.size();
   if (J == 0) return;
   ProfScope prof(P_GGG, 0.0, s);
-  size_t max_words = 0;
-  long long scratch_words = 0;
+  constexpr size_t kMax = 160 * 1024;
+  size_t max_words = 0, max_staged = 0;
   std::vector<size_t> words((size_t)J);
   for (int j = 0; j < J; ++j) {
-    words[(size_t)j] = (size_t)2 * gs[(size_t)j].n + k + (size_t)k * gs[(size_t)j].n;
+    const DevGraph& g = gs[(size_t)j];
+    words[(size_t)j] = (size_t)2 * g.n + k + (size_t)k * g.n;
     max_words = std::max(max_words, words[(size_t)j]);
+    max_staged = std::max(max_staged, words[(size_t)j] + (size_t)g.n + 1 + 2 * (size_t)g.m2 + g.n);
   }
-  const bool use_smem = max_words * sizeof(int) <= 160 * 1024;
+  const bool use_smem = max_words * sizeof(int) <= kMax;
+  const bool stage = max_staged * sizeof(int) <= kMax;
+  long long scratch_words = 0;
   if (!use_smem)
     for (int j = 0; j < J; ++j) scratch_words += (long long)words[(size_t)j];
   DBuf<int> scratch((size_t)std::max(scratch_words, 1ll), s);
@@ -235,20 +247,33 @@ void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& 
   for (int j = 0; j < J; ++j) {
     const DevGraph& g = gs[(size_t)j];
     hj[(size_t)j] = GggJob{g.n, k, g.off, g.tgt, g.w, g.vw, parts[(size_t)j],
-                   use_smem ? nullptr : scratch.get() + off, bwork.get() + (size_t)k * j,
-                   use_smem ? 1 : 0};
+                           use_smem ? nullptr : scratch.get() + off,
+                           bwork.get() + (size_t)k * j, use_smem ? 1 : 0, (int)g.m2,
+                           stage ? 1 : 0};
     if (!use_smem) off += (long long)words[(size_t)j];
   }
   DBuf<GggJob> dj((size_t)J, s);
   GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggJob) * (size_t)J,
                            cudaMemcpyHostToDevice, s));
-  const size_t smem = use_smem ? max_words * sizeof(int) : 0;
-  if (use_smem && smem > 48 * 1024)
+  const size_t smem = !use_smem ? 0 : (stage ? max_staged : max_words) * sizeof(int);
+  static std::once_flag once;
+  std::call_once(once, [] {
     GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  160 * 1024));
+                                  (int)(160 * 1024)));
+  });
   k_ggg<<<J, kGggBlock, smem, s>>>(dj.get(), J);
   count_launch();
   GIM_LAUNCH_CHECK();
+}
+
+void greedy_graph_growing(const DevGraph& g, int k, int* part, cudaStream_t s) {
+  launch_ggg(std::vector<DevGraph>{g}, k, std::vector<int*>{part}, s);
+}
+
+// all coarsest graphs of a batched partitioner step, one CTA per graph
+void ggg_batch(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
+               cudaStream_t s) {
+  launch_ggg(gs, k, parts, s);
 }
 
 // ---------------------------------------------------------------------------
