@@ -5,6 +5,7 @@
 // :132-188, hierarchical_multisection leaf :78-80), graph.py
 // (extract_subgraphs :357-389).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -217,8 +218,304 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
 
+// ---------------------------------------------------------------------------
+// K15' greedy graph growing for graphs too large for shared memory (the
+// stalled coarsest graphs of R-MAT inputs: 10^5..10^6 vertices, many of them
+// isolated).  The CTA-wide argmax over all n vertices per claimed vertex
+// above is O(n^2); here every block's frontier is indexed by a two-level max
+// structure — cmax[b][c] >= max conn[b][u] over the unassigned u of chunk c
+// (kGgCh vertices), smax[b][s] >= max cmax[b][c] over superchunk s (kGgSc
+// chunks) — kept as UPPER bounds: a claim only raises them (atomicMax), and
+// an assigned vertex is dropped lazily: a query that finds no unassigned
+// vertex attaining a bound recomputes that chunk/superchunk and retries.
+// The query walks smax -> cmax -> conn taking the lowest index attaining the
+// maximum at each level, which is exactly the heap pop of pipelines.py:
+// maximum connectivity, ties to the lowest vertex id.
+//
+// One warp drives the growth loop (lightest block, query, claim, row update
+// for rows up to kGgWarpRow slots) with no CTA barrier; longer rows (hubs)
+// are handed to the whole CTA.  Isolated vertices claimed by the fallback
+// cost one step of the warp.
+
+constexpr int kGgCh = 256;
+constexpr int kGgSc = 256;
+constexpr int kGgWarpRow = 512;
+
+__device__ __forceinline__ int warp_max_int(int v) {
+  return (int)__reduce_max_sync(0xffffffffu, (unsigned)v);  // v >= 0
+}
+
+struct GggLargeJob {
+  int n;
+  int k;
+  const int* off;
+  const int* tgt;
+  const int* w;
+  const int* vw;
+  int* part;        // out [n], also the working assignment
+  int* dist;        // [n]
+  int* seeds;       // [k]
+  int* conn;        // [k][n], zeroed by the host
+  int* cmax;        // [k][nch], zeroed by the host
+  int* gsmax;       // [k][nsc] (when not in shared memory), zeroed by the host
+  long long* bwork; // [k]
+  int smax_smem;
+};
+
+__device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b, int nch,
+                                              int nsc, int* smax, int t0, int stride) {
+  const int n = J.n;
+  int* cb = J.conn + (size_t)b * n;
+  int* mb = J.cmax + (size_t)b * nch;
+  int* sb = smax + (size_t)b * nsc;
+  const int e1 = __ldg(J.off + v + 1);
+  for (int e = __ldg(J.off + v) + t0; e < e1; e += stride) {
+    const int u = __ldg(J.tgt + e);
+    if (u == v || __ldcg(J.part + u) >= 0) continue;
+    const int c = __ldcg(cb + u) + __ldg(J.w + e);  // distinct u per row
+    __stcg(cb + u, c);
+    atomicMax(mb + u / kGgCh, c);
+    atomicMax(sb + u / (kGgCh * kGgSc), c);
+  }
+}
+
+__global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs) {
+  const GggLargeJob J = jobs[blockIdx.x];
+  const int n = J.n, k = J.k;
+  extern __shared__ int sm[];
+  __shared__ int sa[kGggWarps], sb[kGggWarps];
+  __shared__ int s_cmd, s_v, s_b, s_zero;
+  __shared__ long long s_bw[kGggMaxK];
+  const int nch = (n + kGgCh - 1) / kGgCh, nsc = (nch + kGgSc - 1) / kGgSc;
+  int* smax = J.smax_smem ? sm : J.gsmax;
+  long long* bw = k <= kGggMaxK ? s_bw : J.bwork;
+  if (k == 1) {
+    for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
+    return;
+  }
+  if (J.smax_smem)
+    for (int i = threadIdx.x; i < k * nsc; i += blockDim.x) smax[i] = 0;
+  // seeds (pipelines.py:143-153)
+  if (threadIdx.x == 0) s_zero = 0;
+  __syncthreads();
+  cta_bfs(n, J.off, J.tgt, J.dist, &s_zero, 1);
+  int sv = cta_pick_seed(n, J.dist, sa, sb);
+  if (threadIdx.x == 0) J.seeds[0] = sv;
+  __syncthreads();
+  for (int ns = 1; ns < k; ++ns) {
+    cta_bfs(n, J.off, J.tgt, J.dist, J.seeds, ns);
+    sv = cta_pick_seed(n, J.dist, sa, sb);
+    if (threadIdx.x == 0) J.seeds[ns] = sv;
+    __syncthreads();
+  }
+  for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = -1;
+  for (int b = threadIdx.x; b < k; b += blockDim.x) bw[b] = 0;
+  __syncthreads();
+  for (int b = 0; b < k; ++b) {  // claim the seeds in block order
+    const int s = J.seeds[b];
+    if (threadIdx.x == 0) {
+      J.part[s] = b;
+      bw[b] += J.vw[s];
+    }
+    __syncthreads();
+    gg_row_update(J, s, b, nch, nsc, smax, threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  int assigned = k, next_free = 0;  // warp 0's loop state (uniform in the warp)
+  for (;;) {
+    if (warp == 0) {
+      int cmd = 2;
+      while (assigned < n) {
+        // lightest block, lowest id on ties
+        long long bwv = LLONG_MAX;
+        int bb = INT_MAX;
+        for (int b = lane; b < k; b += 32) {
+          const long long x = bw[b];
+          if (x < bwv) { bwv = x; bb = b; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
+          const int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+          if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
+        }
+        int* cb = J.conn + (size_t)bb * n;
+        int* mb = J.cmax + (size_t)bb * nch;
+        int* sbm = smax + (size_t)bb * nsc;
+        int v = -1;
+        for (;;) {  // query with lazy repair of stale bounds
+          int top = 0, ts = INT_MAX;
+          for (int i = lane; i < nsc; i += 32) {
+            const int x = J.smax_smem ? sbm[i] : __ldcg(sbm + i);
+            if (x > top) { top = x; ts = i; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const int x2 = __shfl_xor_sync(0xffffffffu, top, o);
+            const int s2 = __shfl_xor_sync(0xffffffffu, ts, o);
+            if (x2 > top || (x2 == top && s2 < ts)) { top = x2; ts = s2; }
+          }
+          if (top == 0) break;  // every frontier bound is empty
+          // lowest chunk of superchunk ts whose bound equals top
+          const int c0 = ts * kGgSc;
+          int cm[kGgSc / 32];
+#pragma unroll
+          for (int j = 0; j < kGgSc / 32; ++j) {
+            const int c = c0 + j * 32 + lane;
+            cm[j] = c < nch ? __ldcg(mb + c) : 0;
+          }
+          int ch = -1, smx = 0;
+#pragma unroll
+          for (int j = 0; j < kGgSc / 32; ++j) {
+            const unsigned m = __ballot_sync(0xffffffffu, cm[j] == top);
+            if (ch < 0 && m) ch = c0 + j * 32 + __ffs(m) - 1;
+            smx = max(smx, cm[j]);
+          }
+          if (ch < 0) {  // stale superchunk bound: tighten it and retry
+            smx = warp_max_int(smx);
+            if (lane == 0) {
+              if (J.smax_smem) sbm[ts] = smx;
+              else __stcg(sbm + ts, smx);
+            }
+            __syncwarp();
+            continue;
+          }
+          // lowest unassigned vertex of chunk ch with conn == top
+          const int u0 = ch * kGgCh;
+          int cv[kGgCh / 32];
+#pragma unroll
+          for (int j = 0; j < kGgCh / 32; ++j) {
+            const int u = u0 + j * 32 + lane;
+            cv[j] = u < n ? __ldcg(cb + u) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < kGgCh / 32; ++j) {
+            const int u = u0 + j * 32 + lane;
+            if (cv[j] > 0 && __ldcg(J.part + u) >= 0) cv[j] = 0;
+          }
+          int cmx = 0;
+#pragma unroll
+          for (int j = 0; j < kGgCh / 32; ++j) {
+            const unsigned m = __ballot_sync(0xffffffffu, cv[j] == top);
+            if (v < 0 && m) v = u0 + j * 32 + __ffs(m) - 1;
+            cmx = max(cmx, cv[j]);
+          }
+          if (v >= 0) break;
+          // stale chunk bound: tighten chunk and superchunk, retry
+          cmx = warp_max_int(cmx);
+          const int lj = (ch - c0) >> 5, ll = (ch - c0) & 31;
+#pragma unroll
+          for (int j = 0; j < kGgSc / 32; ++j)
+            if (j == lj && lane == ll) cm[j] = cmx;
+          int s2 = 0;
+#pragma unroll
+          for (int j = 0; j < kGgSc / 32; ++j) s2 = max(s2, cm[j]);
+          s2 = warp_max_int(s2);
+          if (lane == 0) {
+            __stcg(mb + ch, cmx);
+            if (J.smax_smem) sbm[ts] = s2;
+            else __stcg(sbm + ts, s2);
+          }
+          __syncwarp();
+        }
+        if (v < 0) {  // frontier dried up: lowest unassigned vertex
+          for (;;) {
+            const int u = next_free + lane;
+            const bool fr = u < n && __ldcg(J.part + u) < 0;
+            const unsigned m = __ballot_sync(0xffffffffu, fr);
+            if (m) {
+              v = next_free + __ffs(m) - 1;
+              next_free = v;
+              break;
+            }
+            next_free += 32;
+          }
+        }
+        if (lane == 0) {
+          __stcg(J.part + v, bb);
+          bw[bb] += __ldg(J.vw + v);
+        }
+        ++assigned;
+        __syncwarp();
+        const int deg = __ldg(J.off + v + 1) - __ldg(J.off + v);
+        if (deg > kGgWarpRow) {  // hub row: the whole CTA updates it
+          if (lane == 0) {
+            s_v = v;
+            s_b = bb;
+          }
+          cmd = 1;
+          break;
+        }
+        gg_row_update(J, v, bb, nch, nsc, smax, lane, 32);
+        __syncwarp();
+      }
+      if (lane == 0) s_cmd = cmd;
+    }
+    __syncthreads();
+    const int cmd = s_cmd;
+    if (cmd == 2) break;
+    gg_row_update(J, s_v, s_b, nch, nsc, smax, threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
+}
+
+static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
+                             const std::vector<int*>& parts, cudaStream_t s) {
+  const int J = (int)gs.size();
+  size_t total = 0, max_smax = 0;
+  std::vector<size_t> words((size_t)J);
+  for (int j = 0; j < J; ++j) {
+    const size_t n = (size_t)gs[(size_t)j].n;
+    const size_t nch = (n + kGgCh - 1) / kGgCh, nsc = (nch + kGgSc - 1) / kGgSc;
+    words[(size_t)j] = n + k + (size_t)k * n + (size_t)k * nch + (size_t)k * nsc;
+    total += words[(size_t)j];
+    max_smax = std::max(max_smax, (size_t)k * nsc);
+  }
+  constexpr size_t kMaxSmax = 96 * 1024;
+  const bool smax_smem = max_smax * sizeof(int) <= kMaxSmax;
+  DBuf<int> scratch(std::max<size_t>(total, 1), s);
+  GIM_CUDA(cudaMemsetAsync(scratch.get(), 0, sizeof(int) * total, s));
+  DBuf<long long> bwork((size_t)k * J, s);
+  std::vector<GggLargeJob> hj((size_t)J);
+  size_t off = 0;
+  for (int j = 0; j < J; ++j) {
+    const DevGraph& g = gs[(size_t)j];
+    const size_t n = (size_t)g.n;
+    const size_t nch = (n + kGgCh - 1) / kGgCh;
+    int* base = scratch.get() + off;
+    GggLargeJob& q = hj[(size_t)j];
+    q.n = g.n;
+    q.k = k;
+    q.off = g.off;
+    q.tgt = g.tgt;
+    q.w = g.w;
+    q.vw = g.vw;
+    q.part = parts[(size_t)j];
+    q.dist = base;
+    q.seeds = base + n;
+    q.conn = q.seeds + k;
+    q.cmax = q.conn + (size_t)k * n;
+    q.gsmax = q.cmax + (size_t)k * nch;
+    q.bwork = bwork.get() + (size_t)k * j;
+    q.smax_smem = smax_smem ? 1 : 0;
+    off += words[(size_t)j];
+  }
+  DBuf<GggLargeJob> dj((size_t)J, s);
+  GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggLargeJob) * (size_t)J,
+                           cudaMemcpyHostToDevice, s));
+  static std::once_flag once;
+  std::call_once(once, [] {
+    GIM_CUDA(cudaFuncSetAttribute(k_ggg_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kMaxSmax));
+  });
+  k_ggg_large<<<J, kGggBlock, smax_smem ? max_smax * sizeof(int) : 0, s>>>(dj.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
 // one CTA per graph; working set (and, when it fits, the graph) in shared
-// memory, else a global scratch
+// memory, else a global scratch (large graphs: k_ggg_large)
 static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector<int*>& parts,
                        cudaStream_t s) {
   const int J = (int)gs.size();
@@ -235,6 +532,12 @@ static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector
   }
   const bool use_smem = max_words * sizeof(int) <= kMax;
   const bool stage = max_staged * sizeof(int) <= kMax;
+  const char* fl = getenv("GIM_GGG_LARGE");  // tests: force the large-graph kernel
+  const bool force_large = fl && atoi(fl) != 0;
+  if ((!use_smem || force_large) && k <= kGggMaxK) {
+    launch_ggg_large(gs, k, parts, s);
+    return;
+  }
   long long scratch_words = 0;
   if (!use_smem)
     for (int j = 0; j < J; ++j) scratch_words += (long long)words[(size_t)j];

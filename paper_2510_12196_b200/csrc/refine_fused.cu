@@ -261,31 +261,40 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     }
     for (long long i = gt; i < (long long)k * NC; i += GT) A.W[i] = 0;
   }
-  if (ext) {  // boundary counts of the entry mapping + weighted degrees
+  if (ext || first) {
+    // one row sweep: boundary counts of the entry mapping + weighted degrees
+    // (large levels) and, on the first launch, J of the entry mapping
+    // (mapping.py:76-91), four slots' loads in flight per step
+    long long acc = 0;
     for (long long v = gt; v < n; v += GT) {
       const int pv = A.part[v];
+      const unsigned long long pc = T.code[pv];
+      const int e0 = A.off[v], e1 = A.off[v + 1];
       int c = 0, wd = 0;
-      for (int e = A.off[v]; e < A.off[v + 1]; ++e) {
-        c += A.part[A.tgt[e]] != pv;
-        wd += A.w[e];
+      for (int e = e0; e < e1; e += 4) {
+        int tg[4], wg[4], pb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          tg[q] = e + q < e1 ? A.tgt[e + q] : -1;
+          wg[q] = e + q < e1 ? A.w[e + q] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pb[q] = tg[q] >= 0 ? A.part[tg[q]] : pv;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          c += pb[q] != pv;
+          wd += wg[q];
+          if (first && pb[q] != pv) acc += (long long)wg[q] * cdist(s_dbit, pc, T.code[pb[q]]);
+        }
       }
-      ext[v] = c;
-      A.wdeg[v] = wd;
+      if (ext) {
+        ext[v] = c;
+        A.wdeg[v] = wd;
+      }
     }
+    if (first) block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
   }
   if (first) {
-    long long acc = 0;
-    if (A.src) {
-      for (long long e = gt; e < A.m2; e += GT)
-        acc += (long long)A.w[e] * dist(A.t, A.part[A.src[e]], A.part[A.tgt[e]]);
-    } else {  // shared-memory mode: rows
-      for (long long v = gt; v < n; v += GT) {
-        const int pv = A.part[v];
-        for (int e = A.off[v]; e < A.off[v + 1]; ++e)
-          acc += (long long)A.w[e] * dist(A.t, pv, A.part[A.tgt[e]]);
-      }
-    }
-    block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
     for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
     if (BX == 0)
       for (int b = threadIdx.x; b < k; b += blockDim.x) A.best_bw[b] = A.bw[b];
@@ -599,13 +608,24 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           }
         }
         const bool isc = target >= 0;
+        int wkey = -1;
+        unsigned vwv = 0;
         if (isc) {
           A.rtgt[v] = target;
-          int cell = slot_for_gain(gain) * A.rho + v % A.rho;
+          const int cell = slot_for_gain(gain) * A.rho + v % A.rho;
           A.rcell[v] = (unsigned char)cell;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)own * NC + cell]),
-                    (unsigned long long)(long long)A.vw[v]);
+          wkey = own * NC + cell;
+          vwv = (unsigned)A.vw[v];
         }
+        // warp-aggregated W update: list neighbours mostly share (block,
+        // cell), so one 64-bit atomic per distinct key instead of per vertex
+        // (the 16-bit split keeps the 32-bit reductions exact)
+        const unsigned peers = __match_any_sync(0xffffffffu, wkey);
+        const unsigned wlo = __reduce_add_sync(peers, vwv & 0xffffu);
+        const unsigned whi = __reduce_add_sync(peers, vwv >> 16);
+        if (isc && lane == __ffs(peers) - 1)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[wkey]),
+                    (unsigned long long)wlo + ((unsigned long long)whi << 16));
         wq_push(qa, isc, v, A.lcand, cnt + C_CAND);
       }
       wq_flush(qa, A.lcand, cnt + C_CAND);

@@ -14,7 +14,9 @@ ap.add_argument("--which", nargs="+", default=["rmat", "grid3d"])
 ap.add_argument("--rmat-scale", type=int, default=22)
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--profile", action="store_true", help="serialised per-class device times")
 args = ap.parse_args()
+D.set_profiling(args.profile)
 for w in args.which:
     t0 = time.time()
     if w == "rmat":
@@ -35,4 +37,6 @@ for w in args.which:
                           "l_max": st["l_max"], "balanced": st["max_block_weight"] <= st["l_max"],
                           "levels": st["n_levels"], "level_n": st["level_n"],
                           **{k: round(st[k], 1) for k in ("ms_coarsen", "ms_initial",
-                                                          "ms_refine")}}), flush=True)
+                                                          "ms_refine")},
+                          "profile": {k: round(v["ms"], 1) for k, v in st.get("profile", {}).items()},
+                          "top_launch": st.get("top_launch")}), flush=True)

@@ -359,3 +359,40 @@ def test_gpu_hm_matches_oracle_rgg(D):
     assert np.array_equal(m.assignment, O.hierarchical_multisection(g, t, 0.03, seed=4))
     with pytest.raises(NotImplementedError):
         hierarchical_multisection(g, t, 0.03, partitioner=lambda *a: None)
+
+
+def test_ggg_large_kernel_forced_golden(D, golden, monkeypatch):
+    """The large-graph greedy growing (two-level frontier maxima, lazy
+    repair, warp-driven claims) forced on every call: golden growing,
+    partitioner and multisection cases and a skewed R-MAT map stay exact."""
+    monkeypatch.setenv("GIM_GGG_LARGE", "1")
+    for c in golden("ggg"):
+        g = c.graph()
+        k = int(c["k"])
+        if g.n <= k:
+            continue
+        part = D.greedy_graph_growing(dev_graph(D, c), k)
+        assert np.array_equal(np_(part), c["part"])
+    for c in golden("partitioner"):
+        part = D.internal_partitioner(dev_graph(D, c), int(c["k"]), c.scalar("eps"),
+                                      int(c["seed"]))
+        assert np.array_equal(np_(part), c["part"])
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(11)
+    t = O.OTopology((2, 4, 2), (1, 10, 100))
+    m = integrated_map(g, t, 0.03, 1, coarsest_factor=16)
+    a, bw, _ = O.integrated_map(g, t, 0.03, 1, coarsest_factor=16)
+    assert np.array_equal(m.assignment, a)
+
+
+@pytest.mark.parametrize("scale,k", [(13, 4), (14, 8)])
+def test_ggg_large_graph_matches_oracle(D, scale, k):
+    """Graphs too large for the shared-memory growing kernel (R-MAT: hubs
+    handed to the whole CTA, isolated vertices claimed by the fallback)."""
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(scale)
+    og = O.as_ograph(g)
+    dg = D.DeviceGraph.from_host(g)
+    part = D.greedy_graph_growing(dg, k)
+    assert np.array_equal(np_(part), O.greedy_graph_growing(og, k))
