@@ -4,6 +4,10 @@
 // Reference: coarsening.py (match rounds :63-95, two-hop :98-161,
 // match_graph :164-173, coarse ids :176-188, contract :191-249, project
 // :269-277, build_level_stack :280-295).
+#include <cooperative_groups.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "radix.cuh"
@@ -11,6 +15,8 @@
 #include "coarsen_dev.cuh"
 
 namespace gim {
+
+namespace cg = cooperative_groups;
 
 // device-side "round 2 only below 40 % matched" (coarsening.py:167-170):
 // `gate` is a snapshot of the matched count after round 1
@@ -373,6 +379,135 @@ __global__ void k_relatives(int n, const int* __restrict__ off, const int* __res
   *progressed = prog;
 }
 
+// relatives in parallel, with the sequential result.  Matchmaker mm only
+// reads and writes the partner state of its currently unmatched neighbours,
+// so two matchmakers interact only through a shared unmatched neighbour.
+// Rounds: every live matchmaker (degree <= 8, >= 2 unmatched neighbours)
+// stamps its unmatched neighbours with atomicMin((round tag) | mm); a
+// matchmaker is ready when it owns all of them — no earlier pending
+// matchmaker can change its group, and the ready ones touch disjoint
+// vertex sets — and runs its pair-up; the rest retry next round.  The
+// lowest pending matchmaker is always ready.  A matchmaker seeing fewer
+// than two unmatched neighbours is dropped: the set only shrinks, so at its
+// sequential turn it would pair nothing either.  The tag decreases per
+// round, so stale stamps never need clearing (owner >= key <=> not claimed
+// by an earlier matchmaker this round).  One cooperative launch, two grid
+// barriers per round; state written by other CTAs is read through L2.
+__device__ __forceinline__ int rel_unmatched(const int* off, const int* tgt, const int* partner,
+                                             int mm, int* grp) {
+  int len = 0;
+  for (int e = off[mm]; e < off[mm + 1]; ++e) {
+    const int u = tgt[e];
+    if (__ldcg(partner + u) < 0) {
+      if (grp) {
+        int p = len;
+        while (p > 0 && grp[p - 1] > u) { grp[p] = grp[p - 1]; --p; }  // insertion sort
+        grp[p] = u;
+      }
+      ++len;
+    }
+  }
+  return len;
+}
+
+__global__ void __launch_bounds__(256) k_relatives_par(int n, const int* __restrict__ off,
+                                                       const int* __restrict__ tgt, int* partner,
+                                                       const int* __restrict__ vw, double l_max,
+                                                       long long* matched, int* progressed,
+                                                       int* la, int* lb,
+                                                       unsigned long long* owner, int* ctr) {
+  cg::grid_group grid = cg::this_grid();
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long GT = (long long)gridDim.x * blockDim.x;
+  for (long long v = gt; v < n; v += GT) {
+    const int d = off[v + 1] - off[v];
+    if (d < 2 || d > 8) continue;
+    if (rel_unmatched(off, tgt, partner, (int)v, nullptr) >= 2) la[atomicAdd(&ctr[0], 1)] = (int)v;
+  }
+  grid.sync();
+  long long local = 0;
+  int* cur = la;
+  int* nxt = lb;
+  for (int r = 0;; ++r) {
+    const int cnt = __ldcg(ctr + (r & 1));
+    if (cnt == 0) break;
+    const unsigned long long tag = (unsigned long long)(0x7fffffff - r) << 32;
+    for (long long i = gt; i < cnt; i += GT) {
+      const int mm = cur[i];
+      if (rel_unmatched(off, tgt, partner, mm, nullptr) < 2) {
+        cur[i] = -1;
+        continue;
+      }
+      for (int e = off[mm]; e < off[mm + 1]; ++e) {
+        const int u = tgt[e];
+        if (__ldcg(partner + u) < 0) atomicMin(owner + u, tag | (unsigned)mm);
+      }
+    }
+    if (gt == 0) ctr[(r + 1) & 1] = 0;  // last read in the previous round
+    grid.sync();
+    for (long long i = gt; i < cnt; i += GT) {
+      const int mm = cur[i];
+      if (mm < 0) continue;
+      const unsigned long long key = tag | (unsigned)mm;
+      bool ready = true;
+      for (int e = off[mm]; e < off[mm + 1]; ++e) ready &= __ldcg(owner + tgt[e]) >= key;
+      if (!ready) {
+        nxt[atomicAdd(&ctr[(r + 1) & 1], 1)] = mm;
+        continue;
+      }
+      int grp[8];
+      const int len = rel_unmatched(off, tgt, partner, mm, grp);
+      int i2 = 0;
+      while (i2 + 1 < len) {  // _pair_up (coarsening.py:98-110)
+        const int a = grp[i2], b = grp[i2 + 1];
+        if (__ldcg(partner + a) >= 0) { ++i2; continue; }
+        if (__ldcg(partner + b) >= 0 || (double)((long long)vw[a] + vw[b]) > l_max) { ++i2; continue; }
+        __stcg(partner + a, b);
+        __stcg(partner + b, a);
+        local += 2;
+        i2 += 2;
+      }
+    }
+    grid.sync();
+    int* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  local = warp_sum_ll(local);
+  if (lane_id() == 0 && local) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(matched), (unsigned long long)local);
+    atomicExch(progressed, 1);
+  }
+}
+
+static void relatives_parallel(const DevGraph& g, int* partner, double l_max, long long* matched_d,
+                               int* progressed, cudaStream_t s) {
+  static int occ = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relatives_par, 256, 0));
+  });
+  const int G = std::max(1, std::min(kSMs * std::max(occ, 1), (int)((g.n + 255) / 256)));
+  DBuf<int> la((size_t)std::max(g.n, 1), s), lb((size_t)std::max(g.n, 1), s), ctr(2, s);
+  DBuf<unsigned long long> owner((size_t)std::max(g.n, 1), s);
+  GIM_CUDA(cudaMemsetAsync(ctr.get(), 0, 2 * sizeof(int), s));
+  GIM_CUDA(cudaMemsetAsync(owner.get(), 0xff, sizeof(unsigned long long) * (size_t)g.n, s));
+  GIM_CUDA(cudaMemsetAsync(progressed, 0, sizeof(int), s));
+  int n = g.n;
+  const int* off = g.off;
+  const int* tgt = g.tgt;
+  const int* vwp = g.vw;
+  int* pa = la.get();
+  int* pb = lb.get();
+  unsigned long long* ow = owner.get();
+  int* ct = ctr.get();
+  void* args[] = {&n, &off, &tgt, &partner, &vwp, &l_max, &matched_d, &progressed,
+                  &pa, &pb, &ow, &ct};
+  GIM_CUDA(cudaLaunchCooperativeKernel((const void*)k_relatives_par, dim3(G), dim3(256), args, 0, s));
+  count_launch();
+  GIM_LAUNCH_CHECK();
+}
+
 // sort-and-pair one two-hop phase; returns after the pairing kernel
 static void two_hop_phase(const DevGraph& g, int* partner, double l_max, long long* matched,
                           bool twins, int* collision, cudaStream_t s) {
@@ -406,6 +541,12 @@ static void two_hop_phase(const DevGraph& g, int* partner, double l_max, long lo
   GIM_LAUNCH_CHECK();
 }
 
+// GIM_RELATIVES_SEQ=1: the single-thread sequential relatives (tests)
+static bool relatives_seq() {
+  const char* e = getenv("GIM_RELATIVES_SEQ");
+  return e && atoi(e) != 0;
+}
+
 // returns the matched count after two-hop (coarsening.py:113-161)
 long long two_hop(const DevGraph& g, int* partner, double l_max, long long matched_now,
                   long long* matched_d, cudaStream_t s) {
@@ -434,10 +575,14 @@ long long two_hop(const DevGraph& g, int* partner, double l_max, long long match
     GIM_CHECK(coll == 0, GIM_E_INTERNAL, "two-hop twin hash collision (non-identical "
                                          "neighbourhoods share a 64-bit key)");
     if (frac(m) >= target) return m;
-    k_relatives<<<1, 1, 0, s>>>(g.n, g.off, g.tgt, partner, g.vw, l_max, matched_d,
-                                flags.get() + 1);
-    count_launch();
-    GIM_LAUNCH_CHECK();
+    if (relatives_seq()) {
+      k_relatives<<<1, 1, 0, s>>>(g.n, g.off, g.tgt, partner, g.vw, l_max, matched_d,
+                                  flags.get() + 1);
+      count_launch();
+      GIM_LAUNCH_CHECK();
+    } else {
+      relatives_parallel(g, partner, l_max, matched_d, flags.get() + 1, s);
+    }
     m = read();
     int prog = 0;
     GIM_CUDA(cudaMemcpy(&prog, flags.get() + 1, sizeof(int), cudaMemcpyDeviceToHost));

@@ -396,3 +396,18 @@ def test_ggg_large_graph_matches_oracle(D, scale, k):
     dg = D.DeviceGraph.from_host(g)
     part = D.greedy_graph_growing(dg, k)
     assert np.array_equal(np_(part), O.greedy_graph_growing(og, k))
+
+
+def test_relatives_parallel_equals_sequential(D, monkeypatch):
+    """Two-hop relatives by rounds of disjoint ready matchmakers equal the
+    single-thread sequential sweep (coarsening.py:148-158) on R-MAT, where
+    relatives fire on most levels: identical level stacks and mappings."""
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(15)
+    t = O.OTopology((4, 8, 8), (1, 10, 100))
+    m_par = integrated_map(g, t, 0.03, 2)
+    monkeypatch.setenv("GIM_RELATIVES_SEQ", "1")
+    m_seq = integrated_map(g, t, 0.03, 2)
+    assert np.array_equal(m_par.assignment, m_seq.assignment)
+    assert np.array_equal(m_par.block_weights, m_seq.block_weights)
