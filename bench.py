@@ -195,13 +195,14 @@ def peaks() -> tuple[float, str]:
     return 6650.0, "fallback"
 
 
-def ncu_traffic(cls: str):
-    """dram bytes per launch of the dominant kernel class from the committed
-    ncu --set full capture (profiles/ncu_traffic.json), if any."""
+def ncu_traffic(cls: str, logn: int):
+    """DRAM bytes per launch of the dominant kernel class (average over the
+    class's launches in one map, and the largest launch) from the committed
+    ncu capture (profiles/ncu_traffic.json, scripts/ncu_traffic.py), if any."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get(cls)
+            return json.loads(p.read_text()).get(cls, {}).get(f"rgg{logn}")
         except Exception:  # noqa: BLE001
             return None
     return None
@@ -338,6 +339,7 @@ def run_gpu(args) -> dict | None:
     per_launch_ms = p["ms"] / max(p["count"], 1)
     achieved = (p["bytes"] / 1e9) / (p["ms"] / 1e3) if p["ms"] > 0 else 0.0
     peak, peak_kind = peaks()
+    tr = ncu_traffic(name, args.logn)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -361,7 +363,8 @@ def run_gpu(args) -> dict | None:
         "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES.get(name, name),
                      "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(name),
+                     "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                     "traffic_source": tr,
                      "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "launches": p["count"],
                      "note": "all launches of the class in one serialised map (fan-out off); "
@@ -370,7 +373,8 @@ def run_gpu(args) -> dict | None:
                          "kernel": KERNEL_NAMES.get(top["class"], top["class"]),
                          "ms": top["ms"], "bytes": top["bytes"],
                          "achieved": top["bytes"] / 1e9 / (top["ms"] / 1e3) if top["ms"] else 0.0,
-                         "frac": (top["bytes"] / 1e9 / (top["ms"] / 1e3) / peak) if top["ms"] else 0.0}},
+                         "frac": (top["bytes"] / 1e9 / (top["ms"] / 1e3) / peak) if top["ms"] else 0.0,
+                         "traffic": (tr or {}).get("largest_launch_dram_bytes")}},
         "profile_ms_serialised_map": {k2: v["ms"] for k2, v in prof.items()},
         "phases_ms_last_step": {"coarsen": last["ms_coarsen"], "initial": last["ms_initial"],
                                 "refine": last["ms_refine"], "total": last["ms_total"]},
