@@ -323,10 +323,12 @@ def run_gpu(args) -> dict | None:
     barrier()
     e2e_total = maxed(sum(e2e_ms))
     e2e_value = job_throughput(g.m, args.steps, world, e2e_total)
-    # bytes that cross PCIe: the CSR narrowed to int32 on the host, the int32
-    # assignment and the int64 block weights back
-    h2d = 4 * (g.n + 1) + 4 * len(g.edge_targets) * 2 + 4 * g.n
-    d2h = 4 * g.n + 8 * k
+    # bytes that cross PCIe, as counted by the library: the CSR narrowed to
+    # int32 on the host (weight chunks holding one value — unit weights — are
+    # filled on the device, not copied), the int32 assignment and the int64
+    # block weights back
+    h2d = int(est["bytes_h2d"])
+    d2h = int(est["bytes_d2h"])
 
     if rank != 0:
         return None

@@ -103,6 +103,9 @@ typedef struct gim_im_stats {
   /* host-array entry (gim_integrated_map) only: wall ms of the upload
    * (host narrowing + H2D) and of the download (D2H + widening) */
   double ms_upload, ms_download;
+  /* host-array entry only: bytes copied host -> device (int32 CSR; weight
+   * chunks holding one value are filled on the device instead) and back */
+  int64_t bytes_h2d, bytes_d2h;
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */

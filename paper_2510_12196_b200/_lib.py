@@ -83,6 +83,8 @@ class GimImStats(C.Structure):
         ("top_bytes", C.c_double),
         ("ms_upload", C.c_double),
         ("ms_download", C.c_double),
+        ("bytes_h2d", C.c_int64),
+        ("bytes_d2h", C.c_int64),
     ]
 
 

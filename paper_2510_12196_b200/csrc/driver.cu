@@ -1229,6 +1229,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
       stats->level_m2[i] = i < nl ? level_m2[i] : 0;
     }
     stats->ms_upload = stats->ms_download = 0.0;
+    stats->bytes_h2d = stats->bytes_d2h = 0;
     stats->ms_coarsen = a;
     stats->ms_initial = b;
     stats->ms_refine = c;
@@ -1305,13 +1306,22 @@ struct UpJob {
   int kind;  // 0 offsets/targets, 1 edge weights, 2 vertex weights
 };
 struct UpAcc {
-  long long sum_ew = 0, sum_vw = 0;
+  long long sum_ew = 0, sum_vw = 0, h2d = 0;
   bool bad_range = false, bad_vw = false;
 };
 }  // namespace
 
-static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, const int64_t* ew,
-                         const int64_t* vw, OwnedGraph& G, cudaStream_t s) {
+__global__ void k_fill_i32(long long n, int v, int* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+// returns the bytes copied host -> device.  Weight chunks holding one value
+// (unit-weight graphs: every chunk) are not copied: the device fills them.
+static long long upload_graph(long long n, const int64_t* off, const int64_t* tgt,
+                              const int64_t* ew, const int64_t* vw, OwnedGraph& G,
+                              cudaStream_t s) {
   GIM_CHECK(n >= 0 && n < INT32_MAX, GIM_E_OVERFLOW, "n must be < 2^31");
   long long m2 = off[n];
   GIM_CHECK(m2 >= 0 && m2 < INT32_MAX, GIM_E_OVERFLOW, "2m must be < 2^31");
@@ -1359,20 +1369,39 @@ static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, co
         int* buf = stage + (size_t)slot * kChunk;
         if (used[slot]) GIM_CUDA(cudaEventSynchronize(done[slot]));
         long long sum = 0;
-        bool bad = false, nonpos = false;
-        for (long long i = 0; i < J.cnt; ++i) {
-          const int64_t x = J.src[i];
-          bad |= x < INT32_MIN || x > INT32_MAX;
-          nonpos |= x <= 0;
-          sum += x;
-          buf[i] = (int)x;
+        bool bad = false, nonpos = false, same = J.kind != 0;
+        if (same) {  // weights: validate, and look for a constant chunk first
+          const int64_t x0 = J.src[0];
+          for (long long i = 0; i < J.cnt; ++i) {
+            const int64_t x = J.src[i];
+            bad |= x < INT32_MIN || x > INT32_MAX;
+            nonpos |= x <= 0;
+            sum += x;
+            same &= x == x0;
+          }
+          if (same && !bad) {
+            k_fill_i32<<<grid_for(J.cnt, 256), 256, 0, ws>>>(J.cnt, (int)x0, J.dst);
+            count_launch();
+            GIM_LAUNCH_CHECK();
+          } else {
+            for (long long i = 0; i < J.cnt; ++i) buf[i] = (int)J.src[i];
+          }
+        } else {
+          for (long long i = 0; i < J.cnt; ++i) {
+            const int64_t x = J.src[i];
+            bad |= x < INT32_MIN || x > INT32_MAX;
+            buf[i] = (int)x;
+          }
         }
         a.bad_range |= bad;
         if (J.kind == 1) a.sum_ew += sum;
         if (J.kind == 2) { a.sum_vw += sum; a.bad_vw |= nonpos; }
-        GIM_CUDA(cudaMemcpyAsync(J.dst, buf, sizeof(int) * J.cnt, cudaMemcpyHostToDevice, ws));
-        GIM_CUDA(cudaEventRecord(done[slot], ws));
-        used[slot] = true;
+        if (!(same && !bad)) {
+          GIM_CUDA(cudaMemcpyAsync(J.dst, buf, sizeof(int) * J.cnt, cudaMemcpyHostToDevice, ws));
+          GIM_CUDA(cudaEventRecord(done[slot], ws));
+          used[slot] = true;
+          a.h2d += (long long)sizeof(int) * J.cnt;
+        }
       }
       GIM_CUDA(sync_stream(ws));
       cudaEventDestroy(done[0]);
@@ -1395,6 +1424,7 @@ static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, co
     tot.sum_vw += a.sum_vw;
     tot.bad_range |= a.bad_range;
     tot.bad_vw |= a.bad_vw;
+    tot.h2d += a.h2d;
   }
   GIM_CHECK(!tot.bad_range, GIM_E_OVERFLOW, "CSR values must fit int32");
   GIM_CHECK(!tot.bad_vw, GIM_E_INVALID, "vertex weights must be positive");
@@ -1403,6 +1433,7 @@ static void upload_graph(long long n, const int64_t* off, const int64_t* tgt, co
   G.total_vw = tot.sum_vw;
   fill_sources((int)n, G.off.get(), G.src.get(), s);
   GIM_LAUNCH_CHECK();
+  return tot.h2d;
 }
 
 __global__ void k_widen(int n, const int* __restrict__ in, long long* __restrict__ out) {
@@ -1729,7 +1760,7 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     gim_im_params P = params ? *params : default_params();
     OwnedGraph G;
     const auto t_up = std::chrono::steady_clock::now();
-    upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
+    const long long h2d = upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
     GIM_CUDA(sync_stream(s));
     const double ms_up =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_up).count();
@@ -1763,6 +1794,8 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     if (stats) {
       stats->kernel_launches = launches();
       stats->ms_upload = ms_up;
+      stats->bytes_h2d = h2d;
+      stats->bytes_d2h = (long long)sizeof(int) * n + (long long)sizeof(long long) * tp.k;
       stats->ms_download = std::chrono::duration<double, std::milli>(
                                std::chrono::steady_clock::now() - t_down).count();
     }

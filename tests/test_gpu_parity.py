@@ -411,3 +411,31 @@ def test_relatives_parallel_equals_sequential(D, monkeypatch):
     m_seq = integrated_map(g, t, 0.03, 2)
     assert np.array_equal(m_par.assignment, m_seq.assignment)
     assert np.array_equal(m_par.block_weights, m_seq.block_weights)
+
+
+def test_host_upload_constant_weight_chunks(D):
+    """The host entry fills constant weight chunks on the device instead of
+    copying them: mappings equal the device-array path for unit vertex
+    weights + varied edge weights and for constant non-unit edge weights +
+    varied vertex weights, and bytes_h2d counts exactly what was copied."""
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200.generators import HostGraph, gen_rgg
+    g = gen_rgg(1 << 16, 0.55, 1)
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets))
+    lo, hi = np.minimum(src, g.edge_targets), np.maximum(src, g.edge_targets)
+    varied_ew = 1 + (lo * 7 + hi * 13) % 5           # symmetric
+    varied_vw = 1 + np.arange(g.n) % 3
+    h, d = (4, 8, 6), (1, 10, 100)
+    t = O.OTopology(h, d)
+    cases = [(varied_ew, np.ones(g.n, np.int64), 4 * (g.n + 1) + 8 * len(g.edge_targets)),
+             (np.full(len(g.edge_targets), 7), varied_vw,
+              4 * (g.n + 1) + 4 * len(g.edge_targets) + 4 * g.n)]
+    for ew, vw, want_h2d in cases:
+        hg = HostGraph(g.offsets, g.edge_targets, ew, vw)
+        st: dict = {}
+        m = integrated_map(hg, t, 0.03, 1, stats=st)
+        a, bw, _ = D.integrated_map_device(D.DeviceGraph.from_host(hg), h, d, 0.03, 1)
+        assert np.array_equal(m.assignment, np_(a))
+        assert np.array_equal(m.block_weights, np_(bw))
+        assert st["bytes_h2d"] == want_h2d
+        assert st["bytes_d2h"] == 4 * g.n + 8 * 192
