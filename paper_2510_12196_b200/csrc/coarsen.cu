@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restri
 // matched u (one gather instead of partner[u] + vw[u]).  Longer rows are
 // evaluated in place by the whole warp (strided slots + shuffle argmax).
 constexpr int kHemTpv = 32;
+constexpr int kHemHuge = 1024;
 
 // per-vertex round data, one 16-byte gather per candidate: c_u (-1 when u
 // is matched) and S_u = splitmix64(seed ^ splitmix64(u)), the first two
@@ -117,7 +118,8 @@ struct __align__(16) HemV {
 
 __global__ void k_hem_elig(int n, const int* __restrict__ partner, const int* __restrict__ vw,
                            unsigned long long seed, HemV* __restrict__ ev,
-                           const long long* gate) {
+                           const long long* gate, int* huge_cnt) {
+  if (huge_cnt && blockIdx.x == 0 && threadIdx.x == 0) *huge_cnt = 0;
   if (hem_gated(gate, n)) return;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     HemV x;
@@ -133,7 +135,9 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
                                                       const int* __restrict__ w,
                                                       const HemV* __restrict__ ev,
                                                       double l_max, int* __restrict__ pref,
-                                                      const long long* gate) {
+                                                      const long long* gate,
+                                                      int* __restrict__ huge,
+                                                      int* __restrict__ huge_cnt) {
   if (hem_gated(gate, n)) return;
   const int lane = lane_id();
   const long long T = (long long)gridDim.x * blockDim.x;
@@ -151,7 +155,10 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
       e0 = off[v];
       e1 = off[v + 1];
     }
-    const bool longrow = active && e1 - e0 > kHemTpv;
+    // hub rows: one CTA each in k_hem_pref_huge
+    const bool hugerow = active && e1 - e0 > kHemHuge;
+    if (hugerow) huge[atomicAdd(huge_cnt, 1)] = v;
+    const bool longrow = active && e1 - e0 > kHemTpv && !hugerow;
     HemCand best;
     best.u = -1;
     best.w = best.c = best.slot = 0;
@@ -220,7 +227,59 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
       }
       if (lane == l) best = bx;
     }
-    if (inr) pref[v] = active ? best.u : -1;
+    if (inr && !hugerow) pref[v] = active ? best.u : -1;
+  }
+}
+
+// hub rows (> kHemHuge slots, R-MAT): one CTA per row, strided slots, warp
+// shuffle argmax then across the CTA's warps
+__global__ void __launch_bounds__(256) k_hem_pref_huge(const int* __restrict__ off,
+                                                       const int* __restrict__ tgt,
+                                                       const int* __restrict__ w,
+                                                       const HemV* __restrict__ ev, double l_max,
+                                                       int* __restrict__ pref,
+                                                       const long long* gate, int n,
+                                                       const int* __restrict__ huge,
+                                                       const int* __restrict__ huge_cnt) {
+  if (hem_gated(gate, n)) return;
+  __shared__ HemCand sb[8];
+  const int cnt = *huge_cnt;
+  for (int h = blockIdx.x; h < cnt; h += gridDim.x) {
+    const int x = huge[h];
+    const HemV me = ev[x];
+    const long long cx = me.c;
+    HemCand bx;
+    bx.u = -1;
+    bx.w = bx.c = bx.slot = 0;
+    bx.h = 0;
+    for (int e = off[x] + threadIdx.x; e < off[x + 1]; e += blockDim.x) {
+      const int u = tgt[e];
+      const HemV hu = ev[u];
+      const int cu = hu.c;
+      if (cu < 0 || (double)(cx + cu) > l_max) continue;
+      HemCand c;
+      c.w = w[e];
+      c.c = cu;
+      c.slot = e;
+      c.u = u;
+      c.h = x < u ? splitmix64(me.s ^ (unsigned long long)u)
+                  : splitmix64(hu.s ^ (unsigned long long)x);  // = hash2(seed, min, max)
+      if (hem_better(c, bx)) bx = c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      HemCand y = hem_shfl(bx, o);
+      if (hem_better(y, bx)) bx = y;
+    }
+    if (lane_id() == 0) sb[threadIdx.x >> 5] = bx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      HemCand b = sb[0];
+      for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+        if (hem_better(sb[i], b)) b = sb[i];
+      pref[x] = b.u;
+    }
+    __syncthreads();
   }
 }
 
@@ -239,9 +298,18 @@ void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
   DBuf<HemV> ev((size_t)g.n, s);
-  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, seed, ev.get(), gate);
+  const bool hubs = g.m2 > (long long)kHemHuge;  // a row can exceed kHemHuge
+  DBuf<int> huge(hubs ? (size_t)g.n + 1 : 1, s);
+  int* hcnt = hubs ? huge.get() + g.n : nullptr;
+  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, seed, ev.get(), gate,
+                                                      hcnt);
   k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, ev.get(),
-                                                           l_max, pref, gate);
+                                                           l_max, pref, gate, huge.get(), hcnt);
+  if (hubs) {
+    k_hem_pref_huge<<<kSMs, B, 0, s>>>(g.off, g.tgt, g.w, ev.get(), l_max, pref, gate, g.n,
+                                            huge.get(), hcnt);
+    count_launch();
+  }
   k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched, gate);
   GIM_LAUNCH_CHECK();
   count_launch(3);

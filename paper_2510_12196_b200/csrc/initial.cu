@@ -4,6 +4,8 @@
 // Reference: pipelines.py (_multi_source_bfs :113-129, greedy_graph_growing
 // :132-188, hierarchical_multisection leaf :78-80), graph.py
 // (extract_subgraphs :357-389).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -15,6 +17,8 @@
 #include "scan.cuh"
 
 namespace gim {
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------
 // K15 greedy graph growing, one CTA per subgraph (the coarsest partitioner
@@ -228,18 +232,20 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
 // chunks) — kept as UPPER bounds: a claim only raises them (atomicMax), and
 // an assigned vertex is dropped lazily: a query that finds no unassigned
 // vertex attaining a bound recomputes that chunk/superchunk and retries.
+// A claimed vertex's conn entries are set to INT_MIN in every block, so the
+// query and the row update need no separate assignment lookup.
 // The query walks smax -> cmax -> conn taking the lowest index attaining the
 // maximum at each level, which is exactly the heap pop of pipelines.py:
 // maximum connectivity, ties to the lowest vertex id.
 //
 // One warp drives the growth loop (lightest block, query, claim, row update
-// for rows up to kGgWarpRow slots) with no CTA barrier; longer rows (hubs)
+// for rows up to kGgWarpRow slots) with no CTA barrier; longer rows
 // are handed to the whole CTA.  Isolated vertices claimed by the fallback
 // cost one step of the warp.
 
 constexpr int kGgCh = 256;
 constexpr int kGgSc = 256;
-constexpr int kGgWarpRow = 512;
+constexpr int kGgWarpRow = 128;
 
 __device__ __forceinline__ int warp_max_int(int v) {
   return (int)__reduce_max_sync(0xffffffffu, (unsigned)v);  // v >= 0
@@ -269,13 +275,25 @@ __device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b
   int* mb = J.cmax + (size_t)b * nch;
   int* sb = smax + (size_t)b * nsc;
   const int e1 = __ldg(J.off + v + 1);
-  for (int e = __ldg(J.off + v) + t0; e < e1; e += stride) {
-    const int u = __ldg(J.tgt + e);
-    if (u == v || __ldcg(J.part + u) >= 0) continue;
-    const int c = __ldcg(cb + u) + __ldg(J.w + e);  // distinct u per row
-    __stcg(cb + u, c);
-    atomicMax(mb + u / kGgCh, c);
-    atomicMax(sb + u / (kGgCh * kGgSc), c);
+  // four slots per thread per step with their loads issued together
+  for (int e = __ldg(J.off + v) + t0; e < e1; e += 4 * stride) {
+    int u[4], wq[4], c0[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int eq = e + q * stride;
+      u[q] = eq < e1 ? __ldg(J.tgt + eq) : v;
+      wq[q] = eq < e1 ? __ldg(J.w + eq) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c0[q] = u[q] != v ? __ldcg(cb + u[q]) : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (c0[q] < 0) continue;  // conn < 0: assigned (or padding / self)
+      const int c = c0[q] + wq[q];  // distinct u per row
+      __stcg(cb + u[q], c);
+      atomicMax(mb + u[q] / kGgCh, c);
+      atomicMax(sb + u[q] / (kGgCh * kGgSc), c);
+    }
   }
 }
 
@@ -284,7 +302,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   const int n = J.n, k = J.k;
   extern __shared__ int sm[];
   __shared__ int sa[kGggWarps], sb[kGggWarps];
-  __shared__ int s_cmd, s_v, s_b, s_zero;
+  __shared__ int s_cmd, s_v, s_b;
   __shared__ long long s_bw[kGggMaxK];
   const int nch = (n + kGgCh - 1) / kGgCh, nsc = (nch + kGgSc - 1) / kGgSc;
   int* smax = J.smax_smem ? sm : J.gsmax;
@@ -295,19 +313,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   }
   if (J.smax_smem)
     for (int i = threadIdx.x; i < k * nsc; i += blockDim.x) smax[i] = 0;
-  // seeds (pipelines.py:143-153)
-  if (threadIdx.x == 0) s_zero = 0;
-  __syncthreads();
-  cta_bfs(n, J.off, J.tgt, J.dist, &s_zero, 1);
-  int sv = cta_pick_seed(n, J.dist, sa, sb);
-  if (threadIdx.x == 0) J.seeds[0] = sv;
-  __syncthreads();
-  for (int ns = 1; ns < k; ++ns) {
-    cta_bfs(n, J.off, J.tgt, J.dist, J.seeds, ns);
-    sv = cta_pick_seed(n, J.dist, sa, sb);
-    if (threadIdx.x == 0) J.seeds[ns] = sv;
-    __syncthreads();
-  }
+  // seeds: k_ggg_seeds (grid-wide BFS) ran before this launch
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = -1;
   for (int b = threadIdx.x; b < k; b += blockDim.x) bw[b] = 0;
   __syncthreads();
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
       J.part[s] = b;
       bw[b] += J.vw[s];
     }
+    for (int b2 = threadIdx.x; b2 < k; b2 += blockDim.x) J.conn[(size_t)b2 * n + s] = INT_MIN;
     __syncthreads();
     gg_row_update(J, s, b, nch, nsc, smax, threadIdx.x, blockDim.x);
     __syncthreads();
@@ -389,11 +396,6 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             const int u = u0 + j * 32 + lane;
             cv[j] = u < n ? __ldcg(cb + u) : 0;
           }
-#pragma unroll
-          for (int j = 0; j < kGgCh / 32; ++j) {
-            const int u = u0 + j * 32 + lane;
-            if (cv[j] > 0 && __ldcg(J.part + u) >= 0) cv[j] = 0;
-          }
           int cmx = 0;
 #pragma unroll
           for (int j = 0; j < kGgCh / 32; ++j) {
@@ -401,7 +403,29 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             if (v < 0 && m) v = u0 + j * 32 + __ffs(m) - 1;
             cmx = max(cmx, cv[j]);
           }
-          if (v >= 0) break;
+          if (v >= 0) {
+            // eager removal of v from bb's bounds (no memory round: the
+            // chunk and superchunk values are in registers), so the next
+            // query of bb needs no repair for it
+            const int vj = (v - u0) >> 5, vl = (v - u0) & 31;
+            int c2 = 0;
+#pragma unroll
+            for (int j = 0; j < kGgCh / 32; ++j)
+              c2 = max(c2, (j == vj && lane == vl) ? 0 : cv[j]);
+            c2 = warp_max_int(c2);
+            const int lj = (ch - c0) >> 5, ll = (ch - c0) & 31;
+            int s2 = 0;
+#pragma unroll
+            for (int j = 0; j < kGgSc / 32; ++j)
+              s2 = max(s2, (j == lj && lane == ll) ? c2 : cm[j]);
+            s2 = warp_max_int(s2);
+            if (lane == 0) {
+              __stcg(mb + ch, c2);
+              if (J.smax_smem) sbm[ts] = s2;
+              else __stcg(sbm + ts, s2);
+            }
+            break;
+          }
           // stale chunk bound: tighten chunk and superchunk, retry
           cmx = warp_max_int(cmx);
           const int lj = (ch - c0) >> 5, ll = (ch - c0) & 31;
@@ -422,7 +446,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         if (v < 0) {  // frontier dried up: lowest unassigned vertex
           for (;;) {
             const int u = next_free + lane;
-            const bool fr = u < n && __ldcg(J.part + u) < 0;
+            const bool fr = u < n && __ldcg(J.conn + u) >= 0;  // block 0's row marks assigned
             const unsigned m = __ballot_sync(0xffffffffu, fr);
             if (m) {
               v = next_free + __ffs(m) - 1;
@@ -432,13 +456,15 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             next_free += 32;
           }
         }
+        const int vwv = __ldg(J.vw + v);
+        const int deg = __ldg(J.off + v + 1) - __ldg(J.off + v);
         if (lane == 0) {
-          __stcg(J.part + v, bb);
-          bw[bb] += __ldg(J.vw + v);
+          J.part[v] = bb;
+          bw[bb] += vwv;
         }
+        for (int b2 = lane; b2 < k; b2 += 32) __stcg(J.conn + (size_t)b2 * n + v, INT_MIN);
         ++assigned;
         __syncwarp();
-        const int deg = __ldg(J.off + v + 1) - __ldg(J.off + v);
         if (deg > kGgWarpRow) {  // hub row: the whole CTA updates it
           if (lane == 0) {
             s_v = v;
@@ -458,6 +484,144 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     gg_row_update(J, s_v, s_b, nch, nsc, smax, threadIdx.x, blockDim.x);
     __syncthreads();
   }
+}
+
+// Farthest-first seeds of a large graph (pipelines.py:113-153) on the whole
+// GPU: one cooperative launch runs the k multi-source BFS passes
+// (level-synchronous frontier queues; first visit claimed by atomicCAS on
+// dist, so distances are exact whatever the order; rows longer than 32 slots
+// are expanded by a warp in a second pass) and after each the pick — lowest
+// unreached vertex, else the first vertex of maximum distance — as grid-wide
+// atomicMin / atomicMax on packed keys.
+struct GgSeedArgs {
+  int n, k;
+  const int* off;
+  const int* tgt;
+  int* dist;
+  int* qa;
+  int* qb;
+  int* heavy;
+  int* ctr;                  // [0..1] queue counts, [2..3] heavy counts
+  unsigned long long* keys;  // [0] lowest unreached, [1] (dist << 32 | ~v) max
+  int* seeds;
+};
+
+__device__ __forceinline__ void gg_append(int* list, int* cnt, bool pred, int val) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return;
+  int base = 0;
+  if (lane_id() == __ffs(m) - 1) base = atomicAdd(cnt, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (pred) list[base + __popc(m & ((1u << lane_id()) - 1u))] = val;
+}
+
+__global__ void __launch_bounds__(256) k_ggg_seeds(GgSeedArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long GT = (long long)gridDim.x * blockDim.x;
+  const int lane = lane_id();
+  const long long gw = gt >> 5, NW = GT >> 5;
+  const int n = A.n;
+  for (int ns = 0; ns < A.k; ++ns) {
+    for (long long v = gt; v < n; v += GT) A.dist[v] = -1;
+    if (gt == 0) {
+      A.ctr[1] = A.ctr[2] = A.ctr[3] = 0;
+      A.keys[0] = ~0ull;
+      A.keys[1] = 0ull;
+    }
+    grid.sync();
+    if (gt == 0) {
+      const int ns0 = ns == 0 ? 1 : ns;
+      for (int i = 0; i < ns0; ++i) {
+        const int sv = ns == 0 ? 0 : A.seeds[i];
+        A.dist[sv] = 0;
+        A.qa[i] = sv;
+      }
+      A.ctr[0] = ns0;
+    }
+    grid.sync();
+    for (int d = 0;; ++d) {
+      const int cnt = __ldcg(A.ctr + (d & 1));
+      if (cnt == 0) break;
+      const int* cur = (d & 1) ? A.qb : A.qa;
+      int* nxt = (d & 1) ? A.qa : A.qb;
+      int* ncnt = A.ctr + ((d + 1) & 1);
+      int* hcnt = A.ctr + 2 + (d & 1);
+      for (long long b0 = gt - lane; b0 < cnt; b0 += GT) {  // warp-uniform loop
+        const long long i = b0 + lane;
+        int v = -1, e0 = 0, e1 = 0;
+        if (i < cnt) {
+          v = cur[i];
+          e0 = A.off[v];
+          e1 = A.off[v + 1];
+        }
+        const bool heavy = v >= 0 && e1 - e0 > 32;
+        gg_append(A.heavy, hcnt, heavy, v);
+        if (heavy) e1 = e0;
+        for (int e = e0;; ++e) {  // thread per vertex, warp-converged appends
+          const bool live = e < e1;
+          if (!__any_sync(0xffffffffu, live)) break;
+          bool fresh = false;
+          int u = 0;
+          if (live) {
+            u = A.tgt[e];
+            fresh = __ldcg(A.dist + u) < 0 && atomicCAS(A.dist + u, -1, d + 1) == -1;
+          }
+          gg_append(nxt, ncnt, fresh, u);
+        }
+      }
+      grid.sync();
+      // every thread has read this level's count: the count slot two levels
+      // on can be reset (it is next written in level d + 1 ... d + 2)
+      if (gt == 0) A.ctr[2 + ((d + 1) & 1)] = 0;
+      const int hc = __ldcg(hcnt);
+      for (long long h = gw; h < hc; h += NW) {
+        const int v = A.heavy[h];
+        const int e1 = A.off[v + 1];
+        for (int eb = A.off[v]; eb < e1; eb += 32) {
+          const int e = eb + lane;
+          bool fresh = false;
+          int u = 0;
+          if (e < e1) {
+            u = A.tgt[e];
+            fresh = __ldcg(A.dist + u) < 0 && atomicCAS(A.dist + u, -1, d + 1) == -1;
+          }
+          gg_append(nxt, ncnt, fresh, u);
+        }
+      }
+      if (gt == 0) A.ctr[d & 1] = 0;  // read by all before the barrier above
+      grid.sync();
+    }
+    for (long long v = gt; v < n; v += GT) {
+      const int dv = __ldcg(A.dist + v);
+      if (dv < 0) atomicMin(A.keys, (unsigned long long)v);
+      else atomicMax(A.keys + 1, ((unsigned long long)dv << 32) | (0xffffffffull - (unsigned)v));
+    }
+    grid.sync();
+    if (gt == 0) {
+      const unsigned long long ku = __ldcg(A.keys), kf = __ldcg(A.keys + 1);
+      A.seeds[ns] = ku != ~0ull ? (int)ku : (int)(0xffffffffull - (kf & 0xffffffffull));
+    }
+    grid.sync();
+  }
+}
+
+static void ggg_seeds(const DevGraph& g, int k, int* dist, int* seeds, cudaStream_t s) {
+  static int occ = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ggg_seeds, 256, 0));
+  });
+  const int G = std::max(1, std::min(kSMs * std::max(occ, 1), (int)((g.n + 255) / 256)));
+  const size_t n = (size_t)std::max(g.n, 1);
+  DBuf<int> q(3 * n + 4, s);
+  DBuf<unsigned long long> keys(2, s);
+  GgSeedArgs A{g.n, k, g.off, g.tgt, dist, q.get(), q.get() + n, q.get() + 2 * n,
+               q.get() + 3 * n, keys.get(), seeds};
+  void* args[] = {&A};
+  GIM_CUDA(cudaLaunchCooperativeKernel((const void*)k_ggg_seeds, dim3(G), dim3(256), args, 0, s));
+  count_launch();
+  GIM_LAUNCH_CHECK();
 }
 
 static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
@@ -501,6 +665,8 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     q.smax_smem = smax_smem ? 1 : 0;
     off += words[(size_t)j];
   }
+  for (int j = 0; j < J; ++j)
+    if (k > 1) ggg_seeds(gs[(size_t)j], k, hj[(size_t)j].dist, hj[(size_t)j].seeds, s);
   DBuf<GggLargeJob> dj((size_t)J, s);
   GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggLargeJob) * (size_t)J,
                            cudaMemcpyHostToDevice, s));

@@ -439,3 +439,25 @@ def test_host_upload_constant_weight_chunks(D):
         assert np.array_equal(m.block_weights, np_(bw))
         assert st["bytes_h2d"] == want_h2d
         assert st["bytes_d2h"] == 4 * g.n + 8 * 192
+
+
+def test_hem_hub_rows_match_oracle(D):
+    """Rows longer than 1024 slots (R-MAT hubs) are rated by one CTA each:
+    two HEM rounds equal the oracle's (coarsening.py:63-95), with vertex
+    weights that make some hub candidates ineligible."""
+    from paper_2510_12196_b200.generators import HostGraph, gen_rmat
+    g0 = gen_rmat(14)
+    assert np.diff(g0.offsets).max() > 1024
+    vw = 1 + np.arange(g0.n) % 4
+    g = HostGraph(g0.offsets, g0.edge_targets, g0.edge_weights, vw)
+    og = O.as_ograph(g)
+    dg = D.DeviceGraph.from_host(g)
+    l_max = 6.0
+    partner = torch.full((dg.n,), -1, dtype=torch.int32, device="cuda")
+    op = np.full(g.n, -1, np.int64)
+    m = 0
+    for seed in (11, 12):
+        pref, m = D.hem_round(dg, partner, l_max, seed, m)
+        op, opref = O.hem_round(og, op, l_max, seed)
+        assert np.array_equal(np_(pref), opref)
+        assert np.array_equal(np_(partner), op)
