@@ -127,6 +127,11 @@ __device__ __forceinline__ VertexEval eval_regs(bool valid, int own, int myb, in
 
 constexpr int TPV_DISTINCT = 4;
 
+#ifndef GIM_EVAL_CHUNK
+#define GIM_EVAL_CHUNK 4
+#endif
+constexpr int kEvalChunk = GIM_EVAL_CHUNK;  // row slots per load batch
+
 struct ThreadEval {
   long long cur, conn_own, best_gain, cost_tb;
   int best_b;
@@ -156,21 +161,21 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
     cw[j] = 0;
   }
   int cnt = 0;
-  // rows in chunks of 4: the target / weight loads and then the block
-  // gathers of a chunk are independent, so they overlap
-  for (int e = e0; e < e1; e += 4) {
-    int tg[4], wg[4], pb[4];
+  // rows in chunks of kEvalChunk: the target / weight loads and then the
+  // block gathers of a chunk are independent, so they overlap
+  for (int e = e0; e < e1; e += kEvalChunk) {
+    int tg[kEvalChunk], wg[kEvalChunk], pb[kEvalChunk];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < kEvalChunk; ++q)
       if (e + q < e1) {
         tg[q] = tgt[e + q];
         wg[q] = w[e + q];
       }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < kEvalChunk; ++q)
       if (e + q < e1) pb[q] = part[tg[q]];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kEvalChunk; ++q) {
       if (e + q >= e1) break;
       const int b = pb[q];
       const long long ww = wg[q];

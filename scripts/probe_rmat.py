@@ -14,6 +14,7 @@ from paper_2510_12196_b200.generators import gen_rmat
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=17)
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--trace", default="", help="chrome trace output path")
 args = ap.parse_args()
 g = gen_rmat(args.scale)
 dg = D.DeviceGraph.from_host(g)
@@ -23,6 +24,8 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     a, bw, st = D.integrated_map_device(dg, h, d, 0.03, 0)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+if args.trace:
+    prof.export_chrome_trace(args.trace)
 by = defaultdict(lambda: [0, 0.0, 0.0])
 for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA:
