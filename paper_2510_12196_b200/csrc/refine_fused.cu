@@ -61,7 +61,7 @@ constexpr int kVcSteps = 2;
 // longest row evaluated thread-per-vertex (longer rows: warp table path)
 constexpr int kTpvMaxDeg = 64;  // non-portable cluster size (B200 allows 16)
 constexpr int kCtrStride = 8;  // per-iteration-parity counters
-enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ };
+enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ, C_HUB, C_BIG };
 
 struct FusedArgs {
   int n;
@@ -100,6 +100,12 @@ struct FusedArgs {
   int solo;            // 1: this CTA is a whole refinement (batched launch)
   int csize;           // >0: one cluster of csize CTAs per refinement (batched launch)
   long long* ptime;    // [16] per-phase ns (trace mode) or null
+  int* hconn;          // [kHubBatch][k] conn tables of the hubs being evaluated (zeroed), or null
+  int* lhub;           // medium rows (kTpvMaxDeg, hub_deg] listed by the current pass
+  int* lbig;           // hub rows (> hub_deg) listed by the current pass
+  int hub_deg;         // rows longer than this are hubs (cooperative grids with hconn only)
+  int list_deg;        // rows longer than this are listed for the grid (<= hub_deg)
+  int hub_phases;      // bit 0: first filter, bit 1: rebalance candidates
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
   unsigned long long seed;
@@ -192,6 +198,179 @@ struct GridBarrier {
     else cg::this_grid().sync();
   }
 };
+
+// Hub rows (R-MAT: 10^4-10^5 slots) would serialise a whole pass on the one
+// warp that owns the vertex.  A pass lists its hubs instead; then every warp
+// of the grid takes kHubSeg-slot segments of the listed hubs and adds each
+// segment's conn(hub, b) into the hub's table (warp-aggregated by block),
+// and after a barrier one warp per hub evaluates it from that table exactly
+// like the in-warp table path.
+constexpr int kHubSeg = 1024;
+constexpr int kHubBatch = 256;  // hubs per accumulate/evaluate round
+// rows longer than this are listed for the grid (shorter ones beyond
+// kTpvMaxDeg stay with the owner warp: no extra barrier for a few of them);
+// GIM_LIST_DEG overrides
+constexpr int kListDeg = 256;
+
+__device__ __forceinline__ void hub_accumulate(const FusedArgs& A, const int* list, long long c0,
+                                               long long c1, long long gw, long long NW) {
+  // (hub, segment) work items: per-CTA exclusive scan of the hubs' segment
+  // counts, then grid-strided items located by binary search
+  __shared__ int s_pre[kHubBatch + 1];
+  __shared__ int s_wsum[kFusedWarps];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int nhc = (int)(c1 - c0);
+  int segs = 0;
+  if ((int)threadIdx.x < nhc) {
+    const int v = list[c0 + threadIdx.x];
+    segs = (A.off[v + 1] - A.off[v] + kHubSeg - 1) / kHubSeg;
+  }
+  int incl = segs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += s_wsum[w];
+  if ((int)threadIdx.x <= nhc) s_pre[threadIdx.x] = base + incl - segs;  // [nhc] = total
+  if (threadIdx.x == 0 && nhc == kHubBatch) {
+    int tot = 0;
+    for (int w = 0; w < kFusedWarps; ++w) tot += s_wsum[w];
+    s_pre[kHubBatch] = tot;
+  }
+  __syncthreads();
+  const int total = s_pre[nhc];
+  for (long long j = gw; j < total; j += NW) {
+    int lo = 0, hi = nhc - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= j) lo = mid;
+      else hi = mid - 1;
+    }
+    const int v = list[c0 + lo];
+    int* row = A.hconn + (size_t)lo * A.k;
+    const int e1 = A.off[v + 1];
+    const int sb = A.off[v] + (int)(j - s_pre[lo]) * kHubSeg, se = min(e1, sb + kHubSeg);
+    for (int eb = sb; eb < se; eb += 32) {
+      const int e = eb + lane;
+      const int b = e < se ? A.part[A.tgt[e]] : -1;
+      const int wv = e < se ? A.w[e] : 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int sum = (int)__reduce_add_sync(peers, (unsigned)wv);
+      if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(row + b, sum);
+    }
+  }
+  __syncthreads();  // s_pre / s_wsum reused by the next round
+}
+
+// warp table of a hub from its accumulated conn row (then zeroed for reuse)
+__device__ __forceinline__ int hub_table(const WarpTable& wt, int k, int* row) {
+  const int lane = lane_id();
+  int sz = 0;
+  for (int base = 0; base < k; base += 32) {
+    const int i = base + lane;
+    const int x = i < k ? __ldcg(row + i) : 0;
+    if (i < k) {
+      wt.tab[i] = x;
+      row[i] = 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, x != 0);
+    if (x != 0) {
+      const int pos = sz + __popc(m & ((1u << lane) - 1u));
+      wt.lb[pos] = i;
+      wt.lw[pos] = x;
+    }
+    sz += __popc(m);
+  }
+  __syncwarp();
+  return sz;
+}
+
+// one listed row, its conn table in wt: the first-filter decision (WEAK
+// false, refinement.py:201-244) or the rebalance candidate (WEAK true,
+// refinement.py:273-309), written exactly as the in-pass evaluation does
+template <bool WEAK>
+__device__ __forceinline__ void hub_eval_one(const FusedArgs& A, int u, int sz, const WarpTable& wt,
+                                             int k, const Topo& T, const long long* s_dbit,
+                                             long long* cnt, const unsigned char* elig,
+                                             const int* elist, int n_elig,
+                                             long long pass_counter, int NC) {
+  const int lane = lane_id();
+  const int ou = A.part[u];
+  if (!WEAK) {
+    const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, nullptr);
+    bool ok = false;
+    if (q.best_b >= 0) {
+      if (q.best_gain >= 0) ok = true;
+      else if (A.jet) ok = (double)(-q.best_gain) < floor(A.jet_c * (double)q.conn_own);
+    }
+    if (ok && lane == 0) {
+      A.dest[u] = q.best_b;
+      A.gkey[u] = q.best_gain;
+    }
+    warp_append(ok && lane == 0, u, A.lcand, cnt + C_CAND);
+  } else {
+    int tb = -1;
+    if (n_elig > 0) {
+      const unsigned long long h = hash2(A.seed, (unsigned long long)u,
+                                         (unsigned long long)pass_counter);
+      tb = elist[h % (unsigned long long)n_elig];
+    }
+    const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, elig);
+    long long ctb = 0;
+    if (q.best_b < 0 && tb >= 0) ctb = cost_table(wt, sz, tb, T, s_dbit);
+    int target = -1;
+    long long gain = 0;
+    if (q.best_b >= 0) {
+      target = q.best_b;
+      gain = q.best_gain;
+    } else if (tb >= 0) {
+      target = tb;
+      gain = q.cur - ctb;
+    }
+    if (target >= 0 && lane == 0) {
+      A.rtgt[u] = target;
+      const int cell = slot_for_gain(gain) * A.rho + u % A.rho;
+      A.rcell[u] = (unsigned char)cell;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)ou * NC + cell]),
+                (unsigned long long)(long long)A.vw[u]);
+    }
+    warp_append(target >= 0 && lane == 0, u, A.lcand, cnt + C_CAND);
+  }
+}
+
+// the rows a pass listed instead of evaluating: medium rows one warp each
+// (any warp of the grid, not the owner warp), hub rows by segments
+template <bool WEAK>
+__device__ __forceinline__ void hub_phase(const FusedArgs& A, const GridBarrier& grid,
+                                          long long* cnt, long long gw, long long NW,
+                                          const WarpTable& wt, int k, const Topo& T,
+                                          const long long* s_dbit, const unsigned char* elig,
+                                          const int* elist, int n_elig, long long pass_counter,
+                                          int NC) {
+  const long long nm = cnt[C_HUB], nb = cnt[C_BIG];
+  if (nm == 0 && nb == 0) return;
+  for (long long i = gw; i < nm; i += NW) {
+    const int u = A.lhub[i];
+    const int sz = warp_build_table(wt, k, A.off[u], A.off[u + 1], A.tgt, A.w, A.part);
+    hub_eval_one<WEAK>(A, u, sz, wt, k, T, s_dbit, cnt, elig, elist, n_elig, pass_counter, NC);
+  }
+  for (long long c0 = 0; c0 < nb; c0 += kHubBatch) {
+    const long long c1 = min(nb, c0 + (long long)kHubBatch);
+    hub_accumulate(A, A.lbig, c0, c1, gw, NW);
+    grid.sync();
+    for (long long i = c0 + gw; i < c1; i += NW) {
+      const int u = A.lbig[i];
+      const int sz = hub_table(wt, k, A.hconn + (size_t)(i - c0) * k);
+      hub_eval_one<WEAK>(A, u, sz, wt, k, T, s_dbit, cnt, elig, elist, n_elig, pass_counter, NC);
+    }
+    grid.sync();
+  }
+  if (nb == 0) grid.sync();
+}
 
 template <int VW>
 __device__ __forceinline__ void refine_body(const FusedArgs& A) {
@@ -423,17 +602,24 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         ThreadEval r{};
         r.best_b = -1;
         bool ovf = false;
+        bool hub = false, big = false;
         if (live) {
           own = A.part[v];
           e0 = A.off[v];
           e1 = A.off[v + 1];
-          if (e1 - e0 > kTpvMaxDeg) {
+          if (A.hconn && (A.hub_phases & 1) && e1 - e0 > A.list_deg) {
+            // evaluated by the grid after this pass
+            if (e1 - e0 > A.hub_deg) big = true;
+            else hub = true;
+          } else if (e1 - e0 > kTpvMaxDeg) {
             ovf = true;
           } else {
             r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, nullptr, -1, flatd);
             ovf = r.overflow;
           }
         }
+        wq_push(qb, hub, v, A.lhub, cnt + C_HUB);
+        warp_append(big, v, A.lbig, cnt + C_BIG);
         // rows too long / too many distinct blocks: the warp evaluates them
         // one by one with the shared-memory block table
         unsigned om = __ballot_sync(0xffffffffu, live && ovf);
@@ -462,7 +648,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         wq_push(qa, ok, v, A.lcand, cnt + C_CAND);
       }
       wq_flush(qa, A.lcand, cnt + C_CAND);
+      wq_flush(qb, A.lhub, cnt + C_HUB);
       grid.sync();
+      if (A.hconn && (A.hub_phases & 1))  // rows listed by this first filter
+        hub_phase<false>(A, grid, cnt, gw, NW, wt, k, T, s_dbit, nullptr, nullptr, 0, 0, NC);
       PHASE_MARK(2);
       // every CTA has read the previous iteration's counters by now (they
       // were consumed before this iteration's first barrier)
@@ -563,7 +752,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         }
         ThreadEval r{};
         r.best_b = -1;
-        bool ovf = false;
+        bool ovf = false, hub = false, big = false;
         if (live && ext && ext[v] == 0) {
           // interior vertex (every neighbour in its own block): no adjacent
           // candidate, cur = 0, cost(tb) = wdeg * D(tb, own) — no row walk
@@ -571,13 +760,19 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             r.cost_tb = (long long)A.wdeg[v] * cdist(s_dbit, T.code[tb], T.code[own]);
         } else if (live) {
           const int e0 = A.off[v], e1 = A.off[v + 1];
-          if (e1 - e0 > kTpvMaxDeg) {
+          if (A.hconn && (A.hub_phases & 2) && e1 - e0 > A.list_deg) {
+            // evaluated by the grid after this pass
+            if (e1 - e0 > A.hub_deg) big = true;
+            else hub = true;
+          } else if (e1 - e0 > kTpvMaxDeg) {
             ovf = true;
           } else {
             r = eval_thread(e0, e1, own, A.tgt, A.w, A.part, T, s_dbit, elig, tb, flatd);
             ovf = r.overflow;
           }
         }
+        wq_push(qb, hub, v, A.lhub, cnt + C_HUB);
+        warp_append(big, v, A.lbig, cnt + C_BIG);
         unsigned om = __ballot_sync(0xffffffffu, live && ovf);
         while (om) {
           const int l = __ffs(om) - 1;
@@ -598,7 +793,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         }
         int target = -1;
         long long gain = 0;
-        if (live) {
+        if (live && !hub && !big) {  // listed rows: decided by the grid below
           if (r.best_b >= 0) {
             target = r.best_b;
             gain = r.best_gain;
@@ -629,9 +824,13 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         wq_push(qa, isc, v, A.lcand, cnt + C_CAND);
       }
       wq_flush(qa, A.lcand, cnt + C_CAND);
+      wq_flush(qb, A.lhub, cnt + C_HUB);
       // the lock set is cleared on every rebalance pass (refinement.py:425):
       // lock_stamp becomes 0 at the end of this iteration
       grid.sync();
+      if (A.hconn && (A.hub_phases & 2))  // rows listed by this candidate pass
+        hub_phase<true>(A, grid, cnt, gw, NW, wt, k, T, s_dbit, elig, elist, s_nelig,
+                        C.pass_counter, NC);
       PHASE_MARK(5);
       if (BX == 0 && threadIdx.x < kCtrStride) cnt_next[threadIdx.x] = 0;
       // ---- K12 weak selection, step A: c*, P_{c*} per overloaded block (every
@@ -1166,6 +1365,20 @@ static int coop_vpc() {
   return v;
 }
 
+// rows longer than this are evaluated grid-wide (GIM_HUB_DEG overrides; 0 = off)
+static int hub_deg() {
+  const char* e = std::getenv("GIM_HUB_DEG");
+  return e ? std::atoi(e) : 2048;
+}
+static int list_deg() {
+  const char* e = std::getenv("GIM_LIST_DEG");
+  return e ? std::max(std::atoi(e), 1) : kListDeg;
+}
+static int hub_phases() {
+  const char* e = std::getenv("GIM_HUB_PHASES");
+  return e ? std::atoi(e) : 3;
+}
+
 bool fused_supported(int k, int rho) { return k <= 1024 && rho >= 1 && rho <= 8; }
 
 // runs Alg. 4 iterations on the device until the loop ends (returns true) or a
@@ -1249,6 +1462,24 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.solo = 0;
   A.csize = 0;
   A.ptime = nullptr;
+  // hub rows: grid-wide evaluation (cooperative grids only)
+  DBuf<int> hconn;
+  A.hconn = nullptr;
+  A.lhub = nullptr;
+  A.lbig = nullptr;
+  A.hub_deg = 0;
+  A.list_deg = 0;
+  A.hub_phases = 0;
+  if (mode == 2 && hub_deg() > 0 && g.m2 > hub_deg()) {
+    hconn = DBuf<int>((size_t)kHubBatch * k, s);
+    GIM_CUDA(cudaMemsetAsync(hconn.get(), 0, sizeof(int) * (size_t)kHubBatch * k, s));
+    A.hconn = hconn.get();
+    A.lhub = fb.lheavy;
+    A.lbig = fb.lmov1;
+    A.hub_deg = hub_deg();
+    A.list_deg = std::min(hub_deg(), list_deg());
+    A.hub_phases = hub_phases();
+  }
   A.l_max = cfg.l_max;
   A.sigma = cfg.sigma;
   A.phi = cfg.phi;
@@ -1390,6 +1621,12 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
     A.smem_base = (int)base;
     A.vc_steps = vc_steps();
     A.ptime = nullptr;
+    A.hconn = nullptr;
+    A.lhub = nullptr;
+    A.lbig = nullptr;
+    A.hub_deg = 0;
+    A.list_deg = 0;
+    A.hub_phases = 0;
     A.l_max = R.cfg.l_max;
     A.sigma = R.cfg.sigma;
     A.phi = R.cfg.phi;
@@ -1525,6 +1762,12 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
     A.vc_steps = vc_steps();
     A.solo = 0;
     A.ptime = nullptr;
+    A.hconn = nullptr;
+    A.lhub = nullptr;
+    A.lbig = nullptr;
+    A.hub_deg = 0;
+    A.list_deg = 0;
+    A.hub_phases = 0;
     A.l_max = R.cfg.l_max;
     A.sigma = R.cfg.sigma;
     A.phi = R.cfg.phi;
