@@ -23,6 +23,7 @@ oracle port, oracle/promap_np.py) on this box's host cores instead.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import math
 import os
@@ -129,13 +130,17 @@ def cpu_baseline_single() -> dict:
 # clocks during the timed region
 
 class Clocks:
-    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    QUERY = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.window = None  # (t0, t1) wall-clock seconds of the timed region
+
+    def mark(self, t0: float, t1: float) -> None:
+        self.window = (t0, t1)
 
     def __enter__(self):
         try:
@@ -158,18 +163,32 @@ class Clocks:
                 self.out = ""
 
     def summary(self) -> dict:
+        out = self._summary(self.window)
+        if not out["samples"] and self.window is not None:  # region shorter than the cadence
+            out = self._summary(None)
+            out["note"] = "no sample inside the timed region; all samples (warm-up included)"
+        return out
+
+    def _summary(self, window) -> dict:
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (self.out or "").splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
+            if len(f) < 7:
                 continue
+            if window is not None:  # samples taken inside the timed region only
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if not window[0] <= ts <= window[1]:
+                    continue
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
+                sm.append(float(f[1]))
+                mx = float(f[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, f[2:6]):
+            for nm, val in zip(names, f[3:7]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         loaded = [x for x in sm if x > 0.5 * (mx or 1)] or sm
@@ -257,6 +276,10 @@ def run_gpu(args) -> dict | None:
     def maxed(x: float) -> float:
         return max_over_ranks(x, world, "cuda")
 
+    # the clock sampler starts before the warm-up, so its own start-up (NVML
+    # initialisation takes the driver for a while) is not inside the timed
+    # steps; only samples taken inside the timed region are summarised
+    clk = Clocks(local).__enter__()
     # warm-up (also JIT-free: libgpuim is prebuilt)
     for w in range(args.warmup):
         D.integrated_map_device(dg, H, DIST, EPS, seed_of(10**6 + w))
@@ -266,7 +289,8 @@ def run_gpu(args) -> dict | None:
     # each whole map, nothing else recorded inside the timed steps)
     step_ms, js, balanced, launches, phases = [], [], True, 0, []
     barrier()
-    with Clocks(local) as clk:
+    t_region0 = time.time()
+    if True:
         for step in range(args.steps):
             flush.fill_(step & 0xff)  # L2 flush, outside the events
             a_ev = torch.cuda.Event(enable_timing=True)
@@ -282,6 +306,9 @@ def run_gpu(args) -> dict | None:
             phases.append([round(st[f], 2) for f in ("ms_coarsen", "ms_initial", "ms_refine")])
             last = st
     barrier()
+    clk.mark(t_region0, time.time())
+    time.sleep(0.25)  # let the sampler flush its last line
+    clk.__exit__(None, None, None)
     total_ms = maxed(sum(step_ms))
     value = job_throughput(g.m, args.steps, world, total_ms)
 

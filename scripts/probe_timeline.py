@@ -14,15 +14,17 @@ H, DIST = (4, 8, 6), (1, 10, 100)
 ap = argparse.ArgumentParser()
 ap.add_argument("--logn", type=int, default=22)
 ap.add_argument("--out", default="gpurun_out/timeline.json")
+ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--warm-seeds", type=int, default=2)
 args = ap.parse_args()
 g = gen_rgg(1 << args.logn, 0.55, 1)
 dg = D.DeviceGraph.from_host(g)
-for s in range(2):
+for s in range(args.warm_seeds):
     D.integrated_map_device(dg, H, DIST, 0.03, s)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     t0 = time.perf_counter()
-    a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, 0)
+    a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, args.seed)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
 prof.export_chrome_trace(args.out)
