@@ -298,7 +298,9 @@ void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
   DBuf<HemV> ev((size_t)g.n, s);
-  const bool hubs = g.m2 > (long long)kHemHuge;  // a row can exceed kHemHuge
+  // a row can exceed kHemHuge (row-length bound known for uploaded and
+  // matching-contracted levels; otherwise only the total bounds it)
+  const bool hubs = g.maxdeg >= 0 ? g.maxdeg > kHemHuge : g.m2 > (long long)kHemHuge;
   DBuf<int> huge(hubs ? (size_t)g.n + 1 : 1, s);
   int* hcnt = hubs ? huge.get() + g.n : nullptr;
   k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, seed, ev.get(), gate,
@@ -801,6 +803,7 @@ void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cuda
   DBuf<int> t((size_t)std::max<long long>(g.m2, 1), s), w((size_t)std::max<long long>(g.m2, 1), s),
       sr((size_t)std::max<long long>(g.m2, 1), s);
   out.n = n_c;
+  out.maxdeg = -1;  // unknown (radix path)
   out.off = DBuf<int>((size_t)n_c + 1, s);
   out.vw = DBuf<int>((size_t)std::max(n_c, 1), s);
   long long m2c = contract_into(g, cmap, n_c, out.off.get(), t.get(), w.get(), out.vw.get(),
@@ -1132,6 +1135,7 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
   }
   ProfScope prof(P_CONTRACT, 12.0 * g.n + 12.0 * g.m2 + 8.0 * n_c, s);
   out.n = n_c;
+  out.maxdeg = maxlen;  // rows of the merged members: an upper bound
   out.vw = std::move(cvw);
   out.off = DBuf<int>((size_t)n_c + 1, s);
   DBuf<int> t_tgt((size_t)std::max(ubtot, 1), s), t_w((size_t)std::max(ubtot, 1), s);
@@ -1245,6 +1249,7 @@ bool coarsen_level_fast(const DevGraph& g_in, double l_max, unsigned long long l
   ProfScope prof(P_CONTRACT, 12.0 * n + 12.0 * g.m2 + 8.0 * n_c, s);
   const long long cap = std::max<long long>(g.m2, 1);
   out.n = n_c;
+  out.maxdeg = maxlen;  // rows of the merged members: an upper bound
   out.vw = std::move(cvw);
   out.off = DBuf<int>((size_t)n_c + 1, s);
   out.tgt = DBuf<int>((size_t)cap, s);

@@ -1303,10 +1303,10 @@ struct UpJob {
   const int64_t* src;
   int* dst;
   long long cnt;
-  int kind;  // 0 offsets/targets, 1 edge weights, 2 vertex weights
+  int kind;  // 0 targets, 1 edge weights, 2 vertex weights, 3 offsets
 };
 struct UpAcc {
-  long long sum_ew = 0, sum_vw = 0, h2d = 0;
+  long long sum_ew = 0, sum_vw = 0, h2d = 0, maxdeg = 0;
   bool bad_range = false, bad_vw = false;
 };
 }  // namespace
@@ -1340,7 +1340,7 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
     for (long long i = 0; i < cnt; i += kChunk)
       jobs.push_back(UpJob{h + i, d + i, std::min(kChunk, cnt - i), kind});
   };
-  add(off, n + 1, G.off.get(), 0);
+  add(off, n + 1, G.off.get(), 3);
   add(tgt, m2, G.tgt.get(), 0);
   add(ew, m2, G.w.get(), 1);
   add(vw, n, G.vw.get(), 2);
@@ -1369,7 +1369,7 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
         int* buf = stage + (size_t)slot * kChunk;
         if (used[slot]) GIM_CUDA(cudaEventSynchronize(done[slot]));
         long long sum = 0;
-        bool bad = false, nonpos = false, same = J.kind != 0;
+        bool bad = false, nonpos = false, same = J.kind == 1 || J.kind == 2;
         if (same) {  // weights: validate, and look for a constant chunk first
           const int64_t x0 = J.src[0];
           for (long long i = 0; i < J.cnt; ++i) {
@@ -1392,6 +1392,9 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
             bad |= x < INT32_MIN || x > INT32_MAX;
             buf[i] = (int)x;
           }
+          if (J.kind == 3)  // row lengths inside the chunk (boundaries: below)
+            for (long long i = 1; i < J.cnt; ++i)
+              a.maxdeg = std::max<long long>(a.maxdeg, J.src[i] - J.src[i - 1]);
         }
         a.bad_range |= bad;
         if (J.kind == 1) a.sum_ew += sum;
@@ -1425,7 +1428,11 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
     tot.bad_range |= a.bad_range;
     tot.bad_vw |= a.bad_vw;
     tot.h2d += a.h2d;
+    tot.maxdeg = std::max(tot.maxdeg, a.maxdeg);
   }
+  for (long long b = kChunk; b <= n; b += kChunk)  // rows across chunk boundaries
+    tot.maxdeg = std::max<long long>(tot.maxdeg, off[b] - off[b - 1]);
+  G.maxdeg = (int)std::min<long long>(tot.maxdeg, INT32_MAX);
   GIM_CHECK(!tot.bad_range, GIM_E_OVERFLOW, "CSR values must fit int32");
   GIM_CHECK(!tot.bad_vw, GIM_E_INVALID, "vertex weights must be positive");
   GIM_CHECK(tot.sum_vw < INT32_MAX, GIM_E_OVERFLOW, "total vertex weight must be < 2^31");

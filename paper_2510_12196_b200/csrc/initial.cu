@@ -908,6 +908,7 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
     int e0 = hoff[v0], e1 = hoff[v1];
     OwnedGraph& sg = subs[j];
     sg.n = nj;
+    sg.maxdeg = -1;
     sg.m2 = e1 - e0;
     sg.off = DBuf<int>((size_t)nj + 1, s);
     sg.tgt = DBuf<int>((size_t)std::max(e1 - e0, 1), s);

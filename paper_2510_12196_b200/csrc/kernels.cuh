@@ -16,6 +16,7 @@ struct DevGraph {
   const int* w = nullptr;
   const int* vw = nullptr;
   const int* src = nullptr;
+  int maxdeg = -1;  // an upper bound of the longest row, -1 = unknown
 };
 
 inline DevGraph view(const gim_graph& g) {
@@ -35,6 +36,7 @@ struct OwnedGraph {
   int n = 0;
   long long m2 = 0;
   long long total_vw = 0;  // exact c(V)
+  int maxdeg = -1;         // an upper bound of the longest row, -1 = unknown
   DBuf<int> off, tgt, w, vw, src;
   DevGraph view() const {
     DevGraph d;
@@ -45,6 +47,7 @@ struct OwnedGraph {
     d.w = w.get();
     d.vw = vw.get();
     d.src = src.get();
+    d.maxdeg = maxdeg;
     return d;
   }
 };
