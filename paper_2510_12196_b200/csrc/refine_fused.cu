@@ -1470,14 +1470,15 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.hub_deg = 0;
   A.list_deg = 0;
   A.hub_phases = 0;
-  if (mode == 2 && hub_deg() > 0 && g.m2 > hub_deg()) {
+  const int ldeg = std::min(hub_deg(), list_deg());
+  if (mode == 2 && hub_deg() > 0 && (g.maxdeg < 0 ? g.m2 > ldeg : g.maxdeg > ldeg)) {
     hconn = DBuf<int>((size_t)kHubBatch * k, s);
     GIM_CUDA(cudaMemsetAsync(hconn.get(), 0, sizeof(int) * (size_t)kHubBatch * k, s));
     A.hconn = hconn.get();
     A.lhub = fb.lheavy;
     A.lbig = fb.lmov1;
     A.hub_deg = hub_deg();
-    A.list_deg = std::min(hub_deg(), list_deg());
+    A.list_deg = ldeg;
     A.hub_phases = hub_phases();
   }
   A.l_max = cfg.l_max;
