@@ -280,17 +280,17 @@ def run_gpu(args) -> dict | None:
     # initialisation takes the driver for a while) is not inside the timed
     # steps; only samples taken inside the timed region are summarised
     clk = Clocks(local).__enter__()
-    # warm-up (also JIT-free: libgpuim is prebuilt)
-    for w in range(args.warmup):
-        D.integrated_map_device(dg, H, DIST, EPS, seed_of(10**6 + w))
-    torch.cuda.synchronize()
+    try:
+        # warm-up (also JIT-free: libgpuim is prebuilt)
+        for w in range(args.warmup):
+            D.integrated_map_device(dg, H, DIST, EPS, seed_of(10**6 + w))
+        torch.cuda.synchronize()
 
-    # ---- device-resident timed region (no profiling: plain events around
-    # each whole map, nothing else recorded inside the timed steps)
-    step_ms, js, balanced, launches, phases = [], [], True, 0, []
-    barrier()
-    t_region0 = time.time()
-    if True:
+        # ---- device-resident timed region (no profiling: plain events
+        # around each whole map, nothing else recorded inside the timed steps)
+        step_ms, js, balanced, launches, phases = [], [], True, 0, []
+        barrier()
+        t_region0 = time.time()
         for step in range(args.steps):
             flush.fill_(step & 0xff)  # L2 flush, outside the events
             a_ev = torch.cuda.Event(enable_timing=True)
@@ -305,10 +305,11 @@ def run_gpu(args) -> dict | None:
             launches += st["kernel_launches"]
             phases.append([round(st[f], 2) for f in ("ms_coarsen", "ms_initial", "ms_refine")])
             last = st
-    barrier()
-    clk.mark(t_region0, time.time())
-    time.sleep(0.25)  # let the sampler flush its last line
-    clk.__exit__(None, None, None)
+        barrier()
+        clk.mark(t_region0, time.time())
+        time.sleep(0.25)  # let the sampler flush its last line
+    finally:
+        clk.__exit__(None, None, None)
     total_ms = maxed(sum(step_ms))
     value = job_throughput(g.m, args.steps, world, total_ms)
 
