@@ -54,3 +54,21 @@ def golden():
             cache[name] = load_golden(name)
         return cache[name]
     return get
+
+
+def csr_digest(g) -> np.ndarray:
+    """Order-sensitive uint64 digests of (offsets, targets, weights, vweights);
+    the same function scripts/make_golden_scale.py stored with each fixture."""
+    out = []
+    for a in (g.offsets, g.edge_targets, g.edge_weights, g.vertex_weights):
+        a = np.asarray(a, dtype=np.uint64)
+        mult = (np.arange(len(a), dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+                + np.uint64(1))
+        with np.errstate(over="ignore"):
+            out.append(np.uint64(np.sum(a * mult, dtype=np.uint64)))
+    return np.asarray(out, dtype=np.uint64)
+
+
+def load_npz(name: str) -> dict:
+    z = np.load(GOLDEN / f"{name}.npz")
+    return {k: z[k] for k in z.files}
