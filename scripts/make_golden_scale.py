@@ -91,9 +91,9 @@ def im_case(name, g, h, d, eps, seeds, recipe):
     np.savez_compressed(OUT / f"scale_{name}.npz", **bag)
 
 
-def rgg(logn, seeds):
+def rgg(logn, seeds, name=None):
     g = gen_rgg(1 << logn, 0.55, 1)
-    im_case(f"rgg{logn}", g, (4, 8, 6), (1, 10, 100), 0.03, seeds,
+    im_case(name or f"rgg{logn}", g, (4, 8, 6), (1, 10, 100), 0.03, seeds,
             f"gen_rgg(2^{logn}, 0.55, seed=1)")
 
 
@@ -265,8 +265,14 @@ def kat():
 
 CASES = {"kat": kat, "rgg16": lambda: rgg(16, [0, 1, 2]), "rgg18": lambda: rgg(18, [0]),
          "rgg20": lambda: rgg(20, [0]), "rgg22": lambda: rgg(22, [0]),
-         "rgg20s1": lambda: rgg(20, [1]), "grid3d52": grid3d52, "rmat14": rmat14,
+         "grid3d52": grid3d52, "rmat14": rmat14,
          "relatives": relatives, "envelope": envelope}
+
+# one seed per process (rgg 2^20 ~ 9 min, 2^22 ~ 45 min of one core each)
+for _s in range(1, 5):
+    CASES[f"rgg20s{_s}"] = (lambda s: lambda: rgg(20, [s], f"rgg20s{s}"))(_s)
+for _s in range(0, 3):
+    CASES[f"rgg22s{_s}"] = (lambda s: lambda: rgg(22, [s], f"rgg22s{s}"))(_s)
 
 if __name__ == "__main__":
     for c in sys.argv[1:]:

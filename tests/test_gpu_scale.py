@@ -47,8 +47,8 @@ def build_graph(recipe: str):
     raise KeyError(recipe)
 
 
-SCALE_CASES = [c for c in ("rgg16", "rgg18", "grid3d52", "rmat14", "rgg20", "rgg20s1", "rgg22")
-               if (GOLDEN / f"scale_{c}.npz").exists()]
+SCALE_CASES = sorted(p.stem[len("scale_"):] for p in GOLDEN.glob("scale_*.npz")
+                     if p.stem[len("scale_"):].startswith(("rgg", "grid3d", "rmat")))
 
 
 @pytest.mark.parametrize("case", SCALE_CASES)
