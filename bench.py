@@ -1,11 +1,12 @@
 """Benchmark: GPU-IM end-to-end mapping throughput on B200 (BASELINE.json).
 
-Workload (BASELINE.json configs[1]): random geometric
-graph, n = 2^20, radius 0.55*sqrt(ln n / n), graph seed 1 (m = 6,896,118,
-generator identical to the reference's gen_rgg), mapped to H = 4:8:6
-(k = 192), D = 1:10:100, eps = 0.03.  One "step" = one complete
-integrated_map (coarsening, initial multisection, refinement of every level)
-with a fresh mapping seed.
+Workload (BASELINE.json north star and configs[4]'s instance; configs[1]'s
+mapping H/D/eps): random geometric graph, n = 2^22, radius 0.55*sqrt(ln n / n),
+graph seed 1 (m = 30,369,333, generator identical to the reference's
+gen_rgg), mapped to H = 4:8:6 (k = 192), D = 1:10:100, eps = 0.03
+(`--logn 20` gives configs[1] itself, m = 6,896,118).  One "step" = one
+complete integrated_map (coarsening, initial multisection, refinement of
+every level) with a fresh mapping seed.
 
   value  = undirected edges mapped per second, graph resident in HBM,
            CUDA events on the mapping stream, L2 flushed between steps
@@ -14,8 +15,11 @@ with a fresh mapping seed.
            arrays: H2D, mapping, D2H of the Mapping, per step
 
 Multi-GPU (torchrun): independent replicas (refinement does not shard, see
-DESIGN.md §6); every rank maps the graph with its own seeds, the timing is
-the max over ranks and value = all edges mapped / that time.
+DESIGN.md §8); every rank maps the graph with its own seeds, the timing is
+the max over ranks and value = all edges mapped / that time.  The ranks
+share only a gloo (CPU) group for the barrier and the max — no NCCL.  The
+line also carries config 5 ("replicas": 64 seeds split over the ranks,
+`concurrency` maps per GPU on separate streams, replicas.py).
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port, oracle/promap_np.py) on this box's host cores instead.
@@ -46,8 +50,21 @@ EPS = 0.03
 RADIUS = 0.55
 GRAPH_SEED = 1
 # J of the reference package (promap) on this exact workload, mapping seed 0,
-# measured in the build container: the quality yardstick
+# measured in the build container (scripts/make_golden_scale.py):
+# the quality yardstick; the full reference mappings are the goldens below
 REF_J_SEED0 = {20: 2893838}
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def reference_mapping(logn: int, seed: int):
+    """The reference package's own mapping of this workload (assignment, J)
+    if a golden made by scripts/make_golden_scale.py exists, else None."""
+    for name in (f"scale_rgg{logn}s{seed}", f"scale_rgg{logn}" if seed == 0 else None):
+        if name and (GOLDEN / f"{name}.npz").exists():
+            z = np.load(GOLDEN / f"{name}.npz")
+            if f"{seed}/assignment" in z.files:
+                return z[f"{seed}/assignment"].astype(np.int64), int(z[f"{seed}/j"])
+    return None
 
 
 def workload(logn: int) -> dict:
@@ -82,11 +99,114 @@ def cpu_sample_logn(budget_s: float) -> int:
     return best
 
 
+# ---- same-config CPU leg: the oracle's level-0 kernels and measured phases on
+# the FULL bench graph (forked workers share the graph copy-on-write)
+
+_FULL = {}
+
+
+def _full_stack_and_initial(_):
+    from oracle import promap_np as O
+    g, t, l_max = _FULL["g"], _FULL["t"], _FULL["l_max"]
+    k = t.k
+    t0 = time.perf_counter()
+    p = O.match_graph(g, l_max, O.splitmix64(0 ^ 0))
+    t_match = time.perf_counter() - t0
+    cm, n_c = O.coarse_map_from_matching(p)
+    t0 = time.perf_counter()
+    c = O.contract(g, cm, n_c)
+    t_contract = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    stack = O.build_level_stack(g, l_max, 128 * k, 0)
+    t_stack = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.hierarchical_multisection(stack[-1].graph, t, EPS, seed=O.hash2(0, 7, 7))
+    t_initial = time.perf_counter() - t0
+    return {"match_level0_s": t_match, "contract_level0_s": t_contract,
+            "level0_m2_coarse": int(len(c.edge_targets)), "level_stack_s": t_stack,
+            "initial_multisection_s": t_initial,
+            "level_n": [int(lv.graph.n) for lv in stack],
+            "level_m2": [int(len(lv.graph.edge_targets)) for lv in stack]}
+
+
+def _full_lp(_):
+    from oracle import promap_np as O
+    g, t, a = _FULL["g"], _FULL["t"], _FULL["a"]
+    cfg = O.config_for_level(0, 2)
+    t0 = time.perf_counter()
+    O.label_propagation_pass(g, t, a, np.zeros(g.n, dtype=bool), cfg)
+    return {"lp_pass_level0_s": time.perf_counter() - t0}
+
+
+def _full_j(_):
+    from oracle import promap_np as O
+    g, t, a = _FULL["g"], _FULL["t"], _FULL["a"]
+    t0 = time.perf_counter()
+    j = O.total_cost(g, t, a)
+    return {"total_cost_s": time.perf_counter() - t0, "J_of_fixed_partition": int(j)}
+
+
+def same_config_cpu(logn: int) -> dict:
+    """SURVEY §8(d) CPU reference on the bench graph itself (1 core per
+    kernel, run side by side): measured — level-0 match_graph, contract of
+    that matching, the whole level stack, the initial multisection on its
+    coarsest graph, one level-0 LP pass and J on a fixed partition (the
+    reference's own seed-0 mapping when its golden is present); extrapolated
+    — the refinement, as iterations per level (the GPU run's, identical to
+    the reference's: the mappings are bit-exact) x the level-0 LP + J time
+    scaled by each level's n + 2m."""
+    import multiprocessing as mp
+    from oracle import promap_np as O
+    from paper_2510_12196_b200.generators import gen_rgg
+    t0 = time.perf_counter()
+    g = gen_rgg(1 << logn, RADIUS, GRAPH_SEED)
+    t_gen = time.perf_counter() - t0
+    t = O.OTopology(H, DIST)
+    ref = reference_mapping(logn, 0)
+    if ref is not None:
+        a, part_src = ref[0], "the reference package's seed-0 mapping (golden)"
+    else:
+        a = (np.arange(g.n, dtype=np.int64) * t.k // g.n)
+        part_src = "contiguous vertex blocks"
+    _FULL.update(g=O.as_ograph(g), t=t, l_max=(1.0 + EPS) * g.total_weight / t.k, a=a)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(3) as pool:
+        rs = [pool.apply_async(f, (None,)) for f in (_full_stack_and_initial, _full_lp, _full_j)]
+        out = {}
+        for r in rs:
+            out.update(r.get())
+    wall = time.perf_counter() - t0
+    _FULL.clear()
+    prof = ROOT / "profiles" / f"workload_rgg{logn}.json"
+    iters = json.loads(prof.read_text())["level_iters"] if prof.exists() else None
+    n0, m0 = out["level_n"][0], out["level_m2"][0]
+    per_level = out["lp_pass_level0_s"] + out["total_cost_s"]
+    refine_s = None
+    if iters is not None and len(iters) == len(out["level_n"]):
+        refine_s = sum(it * per_level * (n + m2) / (n0 + m0)
+                       for it, n, m2 in zip(iters, out["level_n"], out["level_m2"]))
+    e2e = None if refine_s is None else \
+        out["level_stack_s"] + out["initial_multisection_s"] + refine_s
+    return {"graph": f"rgg n=2^{logn} (the bench graph), m = {g.m}", "generation_s": t_gen,
+            "cores": 1, "kernels_side_by_side": 3, "leg_wall_s": wall,
+            "fixed_partition": part_src, **out,
+            "refine_iterations_per_level": iters,
+            "refine_extrapolated_s": refine_s,
+            "e2e_seconds_per_map": e2e,
+            "e2e_edges_per_s_1core": None if e2e is None else g.m / e2e,
+            "note": "coarsening (level stack) and initial mapping measured on this graph; "
+                    "refinement EXTRAPOLATED (iterations per level x level-0 LP pass + J "
+                    "time scaled by n+2m); oracle = numpy port of the reference, 1 core"}
+
+
 def run_reference(args) -> dict:
     """The reference algorithm on the host cores: one oracle integrated_map
-    per core per step (distinct seeds), aggregate edges/s."""
+    per core per step on a bounded sample graph of the same recipe (distinct
+    seeds), aggregate edges/s; plus the same-config leg above."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
+    same = same_config_cpu(args.logn) if args.same_config else None
     logn = cpu_sample_logn(180.0 / max(args.steps + args.warmup, 1))
     ctx = mp.get_context("spawn")
     times, js, ok = [], [], True
@@ -105,7 +225,7 @@ def run_reference(args) -> dict:
     value = m * cores * len(times) / total
     sample = (f"oracle integrated_map on rgg n=2^{logn} (same recipe/H/D/eps), one map per "
               f"core per step, {cores} processes in parallel")
-    return {
+    out = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / len(times), "higher_is_better": True,
@@ -116,6 +236,16 @@ def run_reference(args) -> dict:
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "quality": {"J_geomean": float(np.exp(np.mean(np.log(js)))), "balanced": bool(ok)},
     }
+    if same is not None:
+        same["value_same_config_extrapolated"] = None if same["e2e_edges_per_s_1core"] is None \
+            else same["e2e_edges_per_s_1core"] * cores
+        same["sample_bias"] = (None if same["value_same_config_extrapolated"] is None else
+                               value / same["value_same_config_extrapolated"])
+        same["note2"] = ("value_same_config_extrapolated = cores x the 1-core same-config rate "
+                         "(perfect-scaling upper bound, SURVEY 8(d) cfg 5 rule); sample_bias = "
+                         "the line's sampled value / that figure")
+        out["same_config"] = same
+    return out
 
 
 def cpu_baseline_single() -> dict:
@@ -227,8 +357,9 @@ def ncu_traffic(cls: str, logn: int):
     return None
 
 
-def max_over_ranks(x: float, world: int, device) -> float:
-    """The job's time is the slowest rank's (replicas run concurrently)."""
+def max_over_ranks(x: float, world: int, device="cpu") -> float:
+    """The job's time is the slowest rank's (replicas run concurrently);
+    reduced over the gloo (CPU) group — the replicas use no NCCL."""
     if world == 1:
         return x
     import torch
@@ -236,6 +367,16 @@ def max_over_ranks(x: float, world: int, device) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_lists(x: list, world: int) -> list:
+    """All ranks' lists concatenated (gloo object gather), rank order."""
+    if world == 1:
+        return list(x)
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, list(x))
+    return [y for part in out for y in part]
 
 
 def job_throughput(m: int, steps: int, world: int, max_total_ms: float) -> float:
@@ -252,8 +393,8 @@ def run_gpu(args) -> dict | None:
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1:  # barrier + max over ranks only: a CPU group, no NCCL
+        dist.init_process_group("gloo")
 
     from paper_2510_12196_b200 import device as D
     from paper_2510_12196_b200 import integrated_map
@@ -274,7 +415,7 @@ def run_gpu(args) -> dict | None:
         torch.cuda.synchronize()
 
     def maxed(x: float) -> float:
-        return max_over_ranks(x, world, "cuda")
+        return max_over_ranks(x, world)
 
     # the clock sampler starts before the warm-up, so its own start-up (NVML
     # initialisation takes the driver for a while) is not inside the timed
@@ -315,16 +456,49 @@ def run_gpu(args) -> dict | None:
 
     # ---- kernel attribution: one extra map with per-scope CUDA events and
     # the multisection fan-out off, so scopes on concurrent streams do not
-    # inflate each other (outside the timed region)
-    D.set_profiling(True)
-    D.set_fanout(False)
+    # inflate each other (outside the timed region; per-call run flags)
     flush.fill_(1)
-    _, _, pst = D.integrated_map_device(dg, H, DIST, EPS, seed_of(0))
+    _, _, pst = D.integrated_map_device(dg, H, DIST, EPS, seed_of(0),
+                                        run_flags=D.run_flags(fanout=False, profile=True))
     torch.cuda.synchronize()
-    D.set_fanout(True)
-    D.set_profiling(False)
     prof = pst["profile"]
     top = pst["top_launch"]
+
+    # ---- parity at the bench config: seed 0 against the reference package's
+    # own mapping of this graph (golden made by running the reference)
+    ref = reference_mapping(args.logn, 0) if rank == 0 else None
+    parity = None
+    if rank == 0:
+        a0, _, st0 = D.integrated_map_device(dg, H, DIST, EPS, 0)
+        j_ref = ref[1] if ref is not None else REF_J_SEED0.get(args.logn)
+        parity = {"seed": 0, "J": st0["final_j"], "J_reference": j_ref,
+                  "assignment_identical": None if ref is None else
+                  bool(np.array_equal(a0.cpu().numpy().astype(np.int64), ref[0]))}
+        if j_ref is not None:
+            assert st0["final_j"] == j_ref, f"J(seed 0) {st0['final_j']} != reference {j_ref}"
+        if ref is not None:
+            assert parity["assignment_identical"], "seed-0 mapping differs from the reference's"
+
+    # ---- config 5 (BASELINE configs[4]): 64 seeds split over the ranks,
+    # `concurrency` maps per GPU on separate streams (replicas.py); wall
+    # clock between barriers, max over ranks
+    from paper_2510_12196_b200.replicas import DeviceRunner, split_jobs
+    c5 = {}
+    if args.replica_jobs > 0:
+        mine = split_jobs(list(range(args.replica_jobs)), world)[rank]
+        for conc in sorted({1, args.concurrency}):
+            runner = DeviceRunner(dg, conc)
+            runner.warm()
+            barrier()
+            r5 = runner.run(mine)
+            barrier()
+            wall = maxed(r5["t_end"] - r5["t_start"])
+            js5 = gather_lists([j["J"] for j in r5["jobs"]], world)
+            ok5 = all(gather_lists([j["balanced"] for j in r5["jobs"]], world))
+            c5[f"concurrency{conc}"] = {
+                "maps": len(js5), "wall_s": wall, "edges_per_s": len(js5) * g.m / wall,
+                "ms_per_map_wall": 1000.0 * wall * world / max(len(js5), 1),
+                "J_geomean": float(np.exp(np.mean(np.log(js5)))), "balanced": ok5}
 
     # ---- end to end through the public API: the reference Graph's own
     # (pageable) int64 numpy arrays in, a Mapping with int64 arrays out; wall
@@ -362,7 +536,9 @@ def run_gpu(args) -> dict | None:
         return None
 
     # roofline of the dominant kernel class (largest device time in the
-    # serialised attribution map): its algorithmic bytes / its event time
+    # serialised attribution map): SURVEY §8(d) algorithmic bytes of its
+    # launches — from the device counters each launch returns
+    # — over their summed event time
     dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     name, p = dom
     per_launch_bytes = p["bytes"] / max(p["count"], 1)
@@ -370,6 +546,18 @@ def run_gpu(args) -> dict | None:
     achieved = (p["bytes"] / 1e9) / (p["ms"] / 1e3) if p["ms"] > 0 else 0.0
     peak, peak_kind = peaks()
     tr = ncu_traffic(name, args.logn)
+    # per IM level: size, Alg. 4 iterations, device time, barriers, §8(d) bytes
+    levels = [{"level": i, "n": pst["level_n"][i], "m2": pst["level_m2"][i],
+               "iterations": pst["level_iters"][i],
+               "ms": round(pst["level_refine_ms"][i], 4),
+               "us_per_iteration": round(1000.0 * pst["level_refine_ms"][i] /
+                                         max(pst["level_iters"][i], 1), 2),
+               "barriers_per_iteration": round(pst["level_barriers"][i] /
+                                               max(pst["level_iters"][i], 1), 2),
+               "bytes_s8d": pst["level_bytes"][i],
+               "GBps_s8d": round(pst["level_bytes"][i] / 1e6 /
+                                 max(pst["level_refine_ms"][i], 1e-9), 1)}
+              for i in range(pst["n_levels"])]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -398,7 +586,10 @@ def run_gpu(args) -> dict | None:
                      "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "launches": p["count"],
                      "note": "all launches of the class in one serialised map (fan-out off); "
-                             "bytes = iterations x (12 B per directed slot + 8 B per vertex)",
+                             "bytes = SURVEY 8(d) formulas over device counters: LP 8*S + "
+                             "17n + 25*cand_slots, rebalance 8*S_over + 24*n_over + "
+                             "16*k*31*rho, apply 24*mover_slots, entry sweeps 8n + 12*2m",
+                     "counters": pst["acct"],
                      "largest_launch": None if top is None else {
                          "kernel": KERNEL_NAMES.get(top["class"], top["class"]),
                          "ms": top["ms"], "bytes": top["bytes"],
@@ -406,6 +597,10 @@ def run_gpu(args) -> dict | None:
                          "frac": (top["bytes"] / 1e9 / (top["ms"] / 1e3) / peak) if top["ms"] else 0.0,
                          "traffic": (tr or {}).get("largest_launch_dram_bytes")}},
         "profile_ms_serialised_map": {k2: v["ms"] for k2, v in prof.items()},
+        "refine_levels": levels,
+        "parity": parity,
+        "replicas": {"config": f"{args.replica_jobs} mapping seeds of this graph split over "
+                               f"{world} GPU(s), one process per GPU, no NCCL", **c5},
         "phases_ms_last_step": {"coarsen": last["ms_coarsen"], "initial": last["ms_initial"],
                                 "refine": last["ms_refine"], "total": last["ms_total"]},
         "clocks": clk.summary(),
@@ -421,8 +616,14 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--logn", type=int, default=20)
+    ap.add_argument("--logn", type=int, default=22)
+    ap.add_argument("--replica-jobs", type=int, default=64,
+                    help="config 5: seeds mapped by the replica runner (0: skip)")
+    ap.add_argument("--concurrency", type=int, default=3,
+                    help="config 5: concurrent maps per GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--same-config", type=int, default=1,
+                    help="reference arm: also time the oracle on the full bench graph (1/0)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

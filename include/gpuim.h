@@ -72,7 +72,38 @@ typedef struct gim_im_params {
   double sigma_coarse;     /* 0.065 */
   double sigma_fine;       /* 0.005 */
   int32_t iw_max_finest;   /* 10    */
+  /* mode flags of THIS call (GIM_RUN_* bits), or GIM_RUN_DEFAULT = the
+   * process defaults set by gim_set_* when the call starts.  Every mode
+   * gives identical results; they exist for A/B measurement and tests. */
+  int32_t run_flags;
 } gim_im_params;
+
+#define GIM_RUN_DEFAULT (-1)
+#define GIM_RUN_FUSED 1    /* Alg. 4 as one persistent kernel per level     */
+#define GIM_RUN_ROWWISE 2  /* row-wise contraction (else radix sort)        */
+#define GIM_RUN_BATCH 4    /* batched multisection leaf-parent partitioning */
+#define GIM_RUN_FANOUT 8   /* sibling subtrees on host threads / streams    */
+#define GIM_RUN_PROFILE 16 /* per-class CUDA-event profiling (prof_* stats) */
+
+/* Refinement counters (gim_im_stats.acct), summed over the IM levels'
+ * refinement launches; SURVEY §8(d) algorithmic bytes are computed from
+ * them. */
+#define GIM_ACCT_SCAN 0       /* vertices swept by list-building passes     */
+#define GIM_ACCT_BND 1        /* boundary vertices found (locked included)  */
+#define GIM_ACCT_EVAL_V 2     /* vertices evaluated by the LP first filter  */
+#define GIM_ACCT_EVAL_SLOTS 3 /* their row slots                            */
+#define GIM_ACCT_EVAL_S 4     /* their distinct adjacent blocks (S)         */
+#define GIM_ACCT_CAND_V 5     /* second-filter candidates                   */
+#define GIM_ACCT_CAND_SLOTS 6 /* their row slots                            */
+#define GIM_ACCT_MOV_V 7      /* movers applied                             */
+#define GIM_ACCT_MOV_SLOTS 8  /* their row slots                            */
+#define GIM_ACCT_OVL_V 9      /* rebalance: vertices of overloaded blocks   */
+#define GIM_ACCT_OVL_SLOTS 10 /* rebalance: row slots walked                */
+#define GIM_ACCT_OVL_S 11     /* rebalance: distinct adjacent blocks        */
+#define GIM_ACCT_LP_IT 12     /* LP iterations                              */
+#define GIM_ACCT_WEAK_IT 13   /* weak-rebalance iterations                  */
+#define GIM_ACCT_BARRIERS 14  /* grid / cluster / CTA barriers (CTA 0)      */
+#define GIM_ACCT_SWEEPS 15    /* entry sweeps over the whole CSR            */
 
 /* Counters of one integrated_map run (for roofline accounting). */
 typedef struct gim_im_stats {
@@ -106,6 +137,15 @@ typedef struct gim_im_stats {
   /* host-array entry only: bytes copied host -> device (int32 CSR; weight
    * chunks holding one value are filled on the device instead) and back */
   int64_t bytes_h2d, bytes_d2h;
+  /* refinement of each IM level (finest first): Alg. 4 iterations, device
+   * ms (events around the level's refinement), SURVEY §8(d) algorithmic
+   * bytes from the device counters, barriers executed */
+  int64_t level_iters[64];
+  double level_refine_ms[64];
+  double level_bytes[64];
+  int64_t level_barriers[64];
+  /* GIM_ACCT_* counters summed over the IM levels */
+  int64_t acct[16];
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -233,6 +273,8 @@ int gim_integrated_map(int64_t n, const int64_t* offsets, const int64_t* targets
 /* edge_sources from offsets (graph.py:32-36). */
 int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream);
 
+/* Process defaults of the GIM_RUN_* modes, read by calls that start later
+ * with run_flags = GIM_RUN_DEFAULT (calls in flight keep theirs). */
 /* Per-kernel-class CUDA-event timing for integrated_map stats. */
 void gim_set_profiling(int32_t on);
 
@@ -262,12 +304,15 @@ int gim_metis_load(const char* path, void** handle, int64_t* n, int64_t* m2);
 int gim_metis_fetch(void* handle, int64_t* offsets, int64_t* targets, int64_t* eweights,
                     int64_t* vweights, int64_t* sources);
 
-/* kernels launched by this host thread since the last reset (evidence). */
+/* kernels launched by kernel-level calls (outside integrated_map /
+ * multisection calls, which count their own in gim_im_stats) since the last
+ * reset (evidence). */
 int64_t gim_launch_count(void);
 void gim_reset_launch_count(void);
 
-/* Device scratch is cached per (stream, size class) across calls; this
- * returns every cached block to the CUDA stream-ordered pool. */
+/* Device scratch is cached per (device, stream, size class) across calls;
+ * this returns every cached block to the CUDA stream-ordered pools and trims
+ * them (synchronizes the devices that held cached blocks). */
 void gim_release_cached_memory(void);
 
 #ifdef __cplusplus

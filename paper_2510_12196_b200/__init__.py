@@ -9,8 +9,9 @@ kernels.  `load_metis` is a native (C++) drop-in for promap.graph.load_metis.
 `install()` rebinds these entry points in every reference module that
 imported them.
 """
-from .api import Mapping, hierarchical_multisection, install, integrated_map, uninstall
+from .api import (Mapping, empty_cache, hierarchical_multisection, install, integrated_map,
+                  uninstall)
 from .metis import MetisFormatError, load_metis
 
 __all__ = ["integrated_map", "hierarchical_multisection", "load_metis", "MetisFormatError",
-           "install", "uninstall", "Mapping"]
+           "install", "uninstall", "Mapping", "empty_cache"]

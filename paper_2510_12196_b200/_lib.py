@@ -53,7 +53,15 @@ class GimImParams(C.Structure):
         ("sigma_coarse", C.c_double),
         ("sigma_fine", C.c_double),
         ("iw_max_finest", C.c_int32),
+        ("run_flags", C.c_int32),
     ]
+
+
+RUN_DEFAULT = -1
+RUN_FUSED, RUN_ROWWISE, RUN_BATCH, RUN_FANOUT, RUN_PROFILE = 1, 2, 4, 8, 16
+ACCT_NAMES = ("scan", "bnd", "eval_v", "eval_slots", "eval_S", "cand_v", "cand_slots",
+              "mov_v", "mov_slots", "ovl_v", "ovl_slots", "ovl_S", "lp_it", "weak_it",
+              "barriers", "sweeps")
 
 
 class GimImStats(C.Structure):
@@ -85,6 +93,11 @@ class GimImStats(C.Structure):
         ("ms_download", C.c_double),
         ("bytes_h2d", C.c_int64),
         ("bytes_d2h", C.c_int64),
+        ("level_iters", C.c_int64 * 64),
+        ("level_refine_ms", C.c_double * 64),
+        ("level_bytes", C.c_double * 64),
+        ("level_barriers", C.c_int64 * 64),
+        ("acct", C.c_int64 * 16),
     ]
 
 

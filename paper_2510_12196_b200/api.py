@@ -120,6 +120,15 @@ def hierarchical_multisection(g, t, eps: float, partitioner=None, seed: int = 0,
     return _mapping_type()(a, bw)
 
 
+def empty_cache() -> None:
+    """Release the device scratch libgpuim caches across calls (per device,
+    stream and size class) back to the CUDA pools, e.g. before handing the
+    GPU memory to other torch code."""
+    from . import device as D
+
+    D.release_cached_memory()
+
+
 _INSTALL_SITES = ("promap.pipelines", "promap.estimators", "promap.cli", "promap.bench", "promap",
                   "promap.graph")
 _NAMES = ("integrated_map", "hierarchical_multisection", "load_metis")

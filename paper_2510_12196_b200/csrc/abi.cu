@@ -45,7 +45,7 @@ struct PinnedLease {
 thread_local PinnedLease g_pin_lease;
 
 std::mutex g_stream_mu;
-std::vector<cudaStream_t> g_stream_free;
+std::map<int, std::vector<cudaStream_t>> g_stream_free;  // per device
 }  // namespace
 
 void* pinned_scratch(size_t bytes) {
@@ -72,11 +72,14 @@ void* pinned_scratch(size_t bytes) {
 }
 
 cudaStream_t acquire_stream() {
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
   {
     std::lock_guard<std::mutex> lk(g_stream_mu);
-    if (!g_stream_free.empty()) {
-      cudaStream_t s = g_stream_free.back();
-      g_stream_free.pop_back();
+    auto& fl = g_stream_free[dev];
+    if (!fl.empty()) {
+      cudaStream_t s = fl.back();
+      fl.pop_back();
       return s;
     }
   }
@@ -87,8 +90,10 @@ cudaStream_t acquire_stream() {
 
 void release_stream(cudaStream_t s) {
   if (!s) return;
+  int dev = 0;
+  cudaGetDevice(&dev);  // a worker releases on the device it acquired on
   std::lock_guard<std::mutex> lk(g_stream_mu);
-  g_stream_free.push_back(s);
+  g_stream_free[dev].push_back(s);
 }
 
 // ---- stream-keyed caching allocator in front of the cudaMallocAsync pool.
@@ -108,14 +113,30 @@ static size_t size_class(size_t b) {
 }
 
 namespace {
+// keyed by device too: the legacy / per-thread default stream handles are
+// the same value on every device
 struct CacheKey {
+  int dev;
   cudaStream_t s;
   size_t c;
-  bool operator<(const CacheKey& o) const { return s != o.s ? s < o.s : c < o.c; }
+  bool operator<(const CacheKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    return s != o.s ? s < o.s : c < o.c;
+  }
+};
+struct Owned {
+  int dev;
+  size_t c;
 };
 std::mutex g_cache_mu;
 std::map<CacheKey, std::vector<void*>> g_cache_free;
-std::unordered_map<void*, size_t> g_cache_owned;
+std::unordered_map<void*, Owned> g_cache_owned;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
 }  // namespace
 
 static void* raw_alloc(size_t bytes, cudaStream_t s) {
@@ -132,13 +153,14 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
   configure_pool_once();
   if (bytes > kCacheMax) return raw_alloc(bytes, s);
   const size_t c = size_class(bytes);
+  const int dev = current_device();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache_free.find(CacheKey{s, c});
+    auto it = g_cache_free.find(CacheKey{dev, s, c});
     if (it != g_cache_free.end() && !it->second.empty()) {
       void* p = it->second.back();
       it->second.pop_back();
-      g_cache_owned[p] = c;
+      g_cache_owned[p] = Owned{dev, c};
       return p;
     }
   }
@@ -148,18 +170,18 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
     // seed to seed and straddle class boundaries)
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (size_t up = c << 1; up <= (c << 2); up <<= 1) {
-      auto it = g_cache_free.find(CacheKey{s, up});
+      auto it = g_cache_free.find(CacheKey{dev, s, up});
       if (it != g_cache_free.end() && !it->second.empty()) {
         void* p = it->second.back();
         it->second.pop_back();
-        g_cache_owned[p] = up;
+        g_cache_owned[p] = Owned{dev, up};
         return p;
       }
     }
   }
   void* p = raw_alloc(c, s);
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  g_cache_owned[p] = c;
+  g_cache_owned[p] = Owned{dev, c};
   return p;
 }
 
@@ -169,7 +191,7 @@ void dfree(void* p, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache_owned.find(p);
     if (it != g_cache_owned.end()) {
-      g_cache_free[CacheKey{s, it->second}].push_back(p);
+      g_cache_free[CacheKey{it->second.dev, s, it->second.c}].push_back(p);
       g_cache_owned.erase(it);
       return;
     }
@@ -177,12 +199,26 @@ void dfree(void* p, cudaStream_t s) {
   cudaFreeAsync(p, s);  // never throws from a destructor
 }
 
-// returns every cached block to the pool (stream-ordered on its stream)
+// returns every cached block to its device's pool (stream-ordered on the
+// stream that released it), then trims the pools
 void release_cached_memory() {
+  int cur = 0;
+  cudaGetDevice(&cur);
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto& kv : g_cache_free)
+  std::map<int, bool> devs;
+  for (auto& kv : g_cache_free) {
+    cudaSetDevice(kv.first.dev);
     for (void* p : kv.second) cudaFreeAsync(p, kv.first.s);
+    devs[kv.first.dev] = true;
+  }
   g_cache_free.clear();
+  for (auto& d : devs) {
+    cudaSetDevice(d.first);
+    cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d.first) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
+  cudaSetDevice(cur);
 }
 
 static std::mutex g_topo_mu;
@@ -203,6 +239,9 @@ Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances) {
     key.push_back(hierarchy[i]);
     key.push_back(distances[i]);
   }
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  key.push_back(-1 - dev);  // device tables: one copy per device
   std::lock_guard<std::mutex> lk(g_topo_mu);
   auto it = g_topo_cache.find(key);
   if (it != g_topo_cache.end()) return it->second;
@@ -265,62 +304,104 @@ static void configure_pool_once() {
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
-// process-wide (the multisection drives sibling subtrees from worker
-// threads; their launches belong to the same integrated_map call)
-static std::atomic<long long> g_launches{0};
-void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
-long long launches() { return g_launches.load(); }
-void reset_launches() { g_launches.store(0); }
+// ---- run contexts (common.cuh)
+static std::mutex g_flags_mu;
+static RunFlags g_default_flags;
+static RunCtx g_process_ctx;  // kernel-level calls outside integrated_map
+static thread_local RunCtx* t_ctx = nullptr;
 
-// ---- profiling registry (per host thread)
-struct ProfRec {
-  int cls;
-  double bytes;
-  cudaEvent_t a, b;
-};
-static std::atomic<bool> g_prof{false};
-static std::mutex g_prof_mu;
-static std::vector<ProfRec> g_recs;
-static std::vector<cudaEvent_t> g_evpool;
+RunCtx& ctx() { return t_ctx ? *t_ctx : g_process_ctx; }
 
-static cudaEvent_t ev_get() {  // caller holds g_prof_mu
-  if (!g_evpool.empty()) {
-    cudaEvent_t e = g_evpool.back();
-    g_evpool.pop_back();
-    return e;
+RunFlags default_flags() {
+  std::lock_guard<std::mutex> lk(g_flags_mu);
+  return g_default_flags;
+}
+
+void set_default_flags(const RunFlags& f) {
+  std::lock_guard<std::mutex> lk(g_flags_mu);
+  g_default_flags = f;
+  g_process_ctx.f = f;
+}
+
+CtxScope::CtxScope(RunCtx* c) : prev(t_ctx) { t_ctx = c; }
+CtxScope::~CtxScope() { t_ctx = prev; }
+
+void count_launch(long long n) { ctx().launches.fetch_add(n, std::memory_order_relaxed); }
+long long launches() { return ctx().launches.load(); }
+void reset_launches() { ctx().launches.store(0); }
+
+int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  GIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = sms;
+  return sms;
+}
+
+// ---- profiling records (per run context); CUDA events are pooled per device
+static std::mutex g_ev_mu;
+static std::map<int, std::vector<cudaEvent_t>> g_evpool;
+
+static cudaEvent_t ev_get() {
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    auto& pool = g_evpool[dev];
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
   }
   cudaEvent_t e;
   GIM_CUDA(cudaEventCreate(&e));
   return e;
 }
 
-bool prof_on() { return g_prof; }
-void prof_set(bool on) { g_prof = on; }
+static void ev_put(cudaEvent_t a, cudaEvent_t b) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_evpool[dev].push_back(a);
+  g_evpool[dev].push_back(b);
+}
+
+bool prof_on() { return ctx().f.prof; }
 
 void prof_begin(int cls, double bytes, cudaStream_t s, void** token) {
-  std::lock_guard<std::mutex> lk(g_prof_mu);
+  RunCtx& c = ctx();
   ProfRec r{cls, bytes, ev_get(), ev_get()};
   GIM_CUDA(cudaEventRecord(r.a, s));
-  g_recs.push_back(r);
-  *token = reinterpret_cast<void*>(g_recs.size());  // 1-based index
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.recs.push_back(r);
+  *token = reinterpret_cast<void*>(c.recs.size());  // 1-based index
 }
 
 void prof_end(void* token, cudaStream_t s, double extra_bytes) {
-  std::lock_guard<std::mutex> lk(g_prof_mu);
+  RunCtx& c = ctx();
+  std::lock_guard<std::mutex> lk(c.mu);
   size_t i = reinterpret_cast<size_t>(token) - 1;
-  if (i < g_recs.size()) {
-    g_recs[i].bytes += extra_bytes;
-    cudaEventRecord(g_recs[i].b, s);
+  if (i < c.recs.size()) {
+    c.recs[i].bytes += extra_bytes;
+    cudaEventRecord(c.recs[i].b, s);
   }
 }
 
 void prof_collect(double* ms, double* bytes, long long* count, int* top_cls, double* top_ms,
                   double* top_bytes) {
-  std::lock_guard<std::mutex> lk(g_prof_mu);
+  RunCtx& c = ctx();
+  std::lock_guard<std::mutex> lk(c.mu);
   *top_cls = -1;
   *top_ms = 0.0;
   *top_bytes = 0.0;
-  for (auto& r : g_recs) {
+  for (auto& r : c.recs) {
     cudaEventSynchronize(r.b);
     float t = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
@@ -334,15 +415,18 @@ void prof_collect(double* ms, double* bytes, long long* count, int* top_cls, dou
         *top_bytes = r.bytes;
       }
     }
-    g_evpool.push_back(r.a);
-    g_evpool.push_back(r.b);
+    ev_put(r.a, r.b);
   }
-  g_recs.clear();
+  c.recs.clear();
 }
 
 }  // namespace gim
 
-extern "C" void gim_set_profiling(int32_t on) { gim::prof_set(on != 0); }
+extern "C" void gim_set_profiling(int32_t on) {
+  gim::RunFlags f = gim::default_flags();
+  f.prof = on != 0;
+  gim::set_default_flags(f);
+}
 
 extern "C" int gim_version(void) {
   gim::configure_pool_once();

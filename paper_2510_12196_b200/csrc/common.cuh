@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -100,15 +102,84 @@ __host__ __device__ __forceinline__ uint64_t hash2(uint64_t seed, uint64_t a, ui
 }
 
 // ---------------------------------------------------------------------------
-// launch accounting (per host thread; reset by the driver)
+// per-call run context.  Everything one integrated_map / multisection call
+// accumulates or switches on — the kernel-launch count, the profiling
+// records, the refinement byte counters and the mode flags — lives in a
+// RunCtx owned by that call and installed on the calling thread (CtxScope);
+// the worker threads the call spawns install the same context.  Concurrent
+// calls on different host threads (several maps per GPU on separate
+// streams) therefore neither see nor reset each other's counters, and the
+// process-wide gim_set_* defaults only affect calls that start afterwards.
+// Kernel-level C-ABI calls outside such a call use the process context.
 
+// Refinement counters (device-side, summed per k_refine_* launch) from which
+// the algorithmic bytes of SURVEY §8(d) are computed
+enum Acct {
+  A_SCAN = 0,    // vertices swept by list-building passes (ext / overload test)
+  A_BND,         // boundary vertices found by those passes (locked included)
+  A_EVAL_V,      // vertices whose gains were evaluated (LP first filter)
+  A_EVAL_SLOTS,  // their row slots
+  A_EVAL_S,      // their distinct adjacent blocks (conn-table entries, S)
+  A_CAND_V,      // second-filter candidates
+  A_CAND_SLOTS,  // their row slots
+  A_MOV_V,       // movers applied
+  A_MOV_SLOTS,   // their row slots
+  A_OVL_V,       // rebalance: vertices of overloaded blocks considered
+  A_OVL_SLOTS,   // rebalance: row slots walked (non-interior candidates)
+  A_OVL_S,       // rebalance: distinct adjacent blocks of those
+  A_LP_IT,       // LP iterations
+  A_WEAK_IT,     // weak-rebalance iterations
+  A_BARRIERS,    // grid/cluster/CTA barriers executed (CTA 0)
+  A_SWEEPS,      // entry sweeps over the whole CSR (J of the entry mapping / ext)
+  A_COUNT
+};
+
+struct ProfRec {
+  int cls;
+  double bytes;
+  cudaEvent_t a, b;
+};
+
+struct RunFlags {
+  bool fused = true;    // Alg. 4 as one persistent kernel per level
+  bool rowwise = true;  // row-wise contraction (else radix sort)
+  bool batch = true;    // batched multisection leaf-parent partitioning
+  bool fanout = true;   // sibling subtrees on host threads / streams
+  bool prof = false;    // per-class CUDA-event profiling
+};
+
+struct RunCtx {
+  RunFlags f;
+  std::atomic<long long> launches{0};
+  std::mutex mu;  // guards recs
+  std::vector<ProfRec> recs;
+  std::atomic<long long> acct[A_COUNT];
+  RunCtx() { reset_acct(); }
+  void reset_acct() {
+    for (auto& a : acct) a.store(0);
+  }
+};
+
+RunCtx& ctx();             // the calling thread's current context
+RunFlags default_flags();  // process defaults (gim_set_*)
+void set_default_flags(const RunFlags& f);
+
+struct CtxScope {
+  RunCtx* prev;
+  explicit CtxScope(RunCtx* c);
+  ~CtxScope();
+  CtxScope(const CtxScope&) = delete;
+  CtxScope& operator=(const CtxScope&) = delete;
+};
+
+// launch accounting (current context)
 void count_launch(long long n = 1);
 long long launches();
 void reset_launches();
 
 // ---------------------------------------------------------------------------
 // kernel-class profiling with CUDA events on the launching stream (off by
-// default; bench.py turns it on for the timed region).  Each scope records
+// default; bench.py turns it on for one attribution map).  Each scope records
 // a start/stop event pair plus the algorithmic bytes of what it launched;
 // prof_collect() resolves the pairs once at the end (no per-scope syncs).
 
@@ -118,7 +189,6 @@ enum ProfClass {
 };
 
 bool prof_on();
-void prof_set(bool on);
 void prof_begin(int cls, double bytes, cudaStream_t s, void** token);
 void prof_end(void* token, cudaStream_t s, double extra_bytes);
 // accumulate totals per class (ms, bytes, launches); clears the records
@@ -141,7 +211,10 @@ struct ProfScope {
 // ---------------------------------------------------------------------------
 // launch geometry
 
-constexpr int kSMs = 148;
+constexpr int kSMs = 148;  // B200; grid-size heuristics only
+// SMs of the current device (cached per ordinal): cooperative grids must not
+// exceed what is co-resident on the actual part (MIG slices, reduced SKUs)
+int device_sms();
 
 inline int grid_for(long long work, int block, int max_blocks = kSMs * 16) {
   long long g = (work + block - 1) / block;

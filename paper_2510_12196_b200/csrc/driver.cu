@@ -6,6 +6,7 @@
 // fractions, Eq. 2) is evaluated on the host in IEEE double with the same
 // operation order as the reference's Python float expressions, so control
 // decisions agree bit-for-bit; kernels only see the resulting doubles.
+#include <array>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -110,10 +111,9 @@ static RefCfg config_for_level(int level, int n_levels, double phi, int rho, int
 // Alg. 4 (refinement.py:389-464).  `part`/`bw` are consumed and replaced by
 // the best mapping seen.
 
-// device-resident loop on/off (gim_set_fused; default on); both give identical results
-static std::atomic<bool> g_fused{true};
-// row-wise contraction of matchings (else the radix-sort path); identical graphs
-static std::atomic<bool> g_rowwise{true};
+// mode flags (RunFlags, per call): fused = device-resident loop (else per-phase
+// launches), rowwise = row-wise contraction of matchings (else radix sort),
+// batch / fanout = multisection scheduling; results are identical either way
 
 static long long max_of(const std::vector<long long>& x) {
   long long m = 0;
@@ -249,6 +249,8 @@ static void refine_device_loop(RefineLevel& L, const Topo& t, int* part, long lo
   st.lp += hs.lp;
   st.weak += hs.weak;
   st.strong += strong;
+  if (!st.in_initial)  // IM-level refinement counters (SURVEY §8(d) accounting)
+    for (int i = 0; i < A_COUNT; ++i) ctx().acct[i].fetch_add(hs.acct[i]);
   if (st.in_initial) st.init_refine_iterations += hs.iters;
   else st.refine_iterations += hs.iters;
 }
@@ -260,7 +262,7 @@ static void refine(RefineLevel& L, const Topo& t, int* part, long long* bw_d, co
   alloc_refine_buffers(rb, n, k, s);
   const bool aligned = ((reinterpret_cast<uintptr_t>(L.g.src) |
                          reinterpret_cast<uintptr_t>(L.g.tgt)) & 15) == 0;
-  if (g_fused.load() && fused_supported(k, cfg.rho) && n > 0 && aligned) {
+  if (ctx().f.fused && fused_supported(k, cfg.rho) && n > 0 && aligned) {
     refine_device_loop(L, t, part, bw_d, cfg, l_max, st, rb, s);
     return;
   }
@@ -444,7 +446,7 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
     DBuf<int> cmap((size_t)std::max(cur.g.n, 1), s);
     int n_c = 0;
     Level next;
-    if (g_rowwise.load() && (int)pending.size() < kMaxPending) {
+    if (ctx().f.rowwise && (int)pending.size() < kMaxPending) {
       long long m = 0, true_m2 = -1;
       bool stalled = false;
       // the current level's 2m, if still on the device, rides on this round trip
@@ -485,7 +487,7 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
     match_graph(cur.g, l_max, lseed, partner.get(), s);
     n_c = coarse_map(cur.g.n, partner.get(), cmap.get(), s);
     if ((double)n_c * 1.02 > (double)cur.g.n) break;  // stall guard
-    if (g_rowwise.load())
+    if (ctx().f.rowwise)
       contract_matching(cur.g, cmap.get(), partner.get(), n_c, next.own, s);
     else
       contract(cur.g, cmap.get(), n_c, next.own, s);
@@ -553,7 +555,6 @@ struct BatchPartJob {
 };
 
 // batch-eligible: small enough that every level refines shared-memory resident
-static std::atomic<bool> g_batch{true};
 constexpr int kBatchMaxN = 16384;
 
 // jobs the batch hands back: general path, one host thread / stream each
@@ -570,8 +571,10 @@ static void general_parallel(const std::vector<BatchPartJob*>& jobs, int parts, 
   GIM_CUDA(sync_stream(s));
   std::vector<std::thread> workers;
   std::vector<std::exception_ptr> errs(jobs.size());
+  RunCtx* const pc = &ctx();
   for (size_t j = 0; j < jobs.size(); ++j) {
-    workers.emplace_back([&, j] {
+    workers.emplace_back([&, j, pc] {
+      CtxScope scope(pc);
       cudaStream_t cs = nullptr;
       try {
         GIM_CUDA(cudaSetDevice(dev));
@@ -853,8 +856,6 @@ struct MsCtx {
   int device;
 };
 
-// sibling-subtree fan-out over host threads (gim_set_fanout; default on)
-static std::atomic<bool> g_fanout{true};
 
 static double adaptive_imbalance(double eps, long long total, long long sub, long long k,
                                  long long k_sub, int depth) {
@@ -916,7 +917,7 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     trans[j] = DBuf<int>((size_t)std::max(subs[j].n, 1), s);
     gather(subs[j].n, ids[j].get(), translation, trans[j].get(), s);
   }
-  if (level - 1 == 1 && g_batch.load() && C.h[0] > 1) {
+  if (level - 1 == 1 && ctx().f.batch && C.h[0] > 1) {
     // the children split straight into leaves: partition all of them in one
     // batch (one launch per phase) when they are small
     bool small = true;
@@ -961,8 +962,10 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
   GIM_CUDA(sync_stream(s));  // children read subs/trans from other streams
   std::vector<std::thread> workers;
   std::vector<std::exception_ptr> errs((size_t)parts);
+  RunCtx* const pc = &ctx();
   for (int j = 0; j < parts; ++j) {
-    workers.emplace_back([&, j] {
+    workers.emplace_back([&, j, pc] {
+      CtxScope scope(pc);
       cudaStream_t cs = nullptr;
       try {
         GIM_CUDA(cudaSetDevice(C.device));
@@ -1040,8 +1043,10 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
       GIM_CUDA(sync_stream(s));
       std::vector<std::thread> workers;
       std::vector<std::exception_ptr> errs((size_t)N);
+      RunCtx* const pc = &ctx();
       for (int j = 0; j < N; ++j) {
-        workers.emplace_back([&, j] {
+        workers.emplace_back([&, j, pc] {
+          CtxScope scope(pc);
           cudaStream_t cs = nullptr;
           try {
             GIM_CUDA(cudaSetDevice(C.device));
@@ -1146,13 +1151,13 @@ static void hierarchical_multisection(const DevGraph& g, long long total,
   C.eps = eps;
   C.assignment = assignment;
   C.st = &st;
-  C.threads = g_fanout;
+  C.threads = ctx().f.fanout;
   GIM_CUDA(cudaGetDevice(&C.device));
   GIM_CUDA(cudaMemsetAsync(assignment, 0, sizeof(int) * g.n, s));
   DBuf<int> ident_ids((size_t)g.n, s);
   k_iota<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, ident_ids.get());
   count_launch();
-  if (g_batch.load()) {
+  if (ctx().f.batch) {
     multisection_bfs(C, g, total, ident_ids.get(), seed, s);
     return;
   }
@@ -1199,6 +1204,13 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   GIM_CUDA(cudaEventRecord(ev[2], s));
   RefineBuffers rb;
   alloc_refine_buffers(rb, g0.n, (int)k, s);  // sized for level 0, reused by every level
+  // per-level refinement accounting: events around each level's refine and
+  // the device counters it added (SURVEY §8(d) bytes)
+  std::vector<cudaEvent_t> lev((size_t)2 * nl);
+  for (auto& e : lev) GIM_CUDA(cudaEventCreate(&e));
+  std::vector<std::array<long long, A_COUNT>> lacct((size_t)nl);
+  std::vector<long long> liters((size_t)nl);
+  ctx().reset_acct();
   for (int li = nl - 1; li >= 0; --li) {
     Level& L = levels[li];
     if (li < nl - 1) {
@@ -1212,7 +1224,14 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
                                   P.sigma_coarse, P.sigma_fine, P.iw_max_finest,
                                   hash2(seed, 211, (unsigned long long)li));
     L.rl.g = L.g;
+    long long a0[A_COUNT];
+    for (int i = 0; i < A_COUNT; ++i) a0[i] = ctx().acct[i].load();
+    const long long it0 = st.refine_iterations.load();
+    GIM_CUDA(cudaEventRecord(lev[(size_t)2 * li], s));
     refine(L.rl, t, cur.get(), out_bw, cfg, l_max, st, rb, s);
+    GIM_CUDA(cudaEventRecord(lev[(size_t)2 * li + 1], s));
+    for (int i = 0; i < A_COUNT; ++i) lacct[(size_t)li][(size_t)i] = ctx().acct[i].load() - a0[i];
+    liters[(size_t)li] = st.refine_iterations.load() - it0;
   }
   GIM_CUDA(cudaMemcpyAsync(out_part, cur.get(), sizeof(int) * g0.n, cudaMemcpyDeviceToDevice, s));
   GIM_CUDA(cudaEventRecord(ev[3], s));
@@ -1227,7 +1246,20 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     for (int i = 0; i < 64; ++i) {
       stats->level_n[i] = i < nl ? level_n[i] : 0;
       stats->level_m2[i] = i < nl ? level_m2[i] : 0;
+      stats->level_iters[i] = i < nl ? liters[(size_t)i] : 0;
+      stats->level_refine_ms[i] = 0.0;
+      stats->level_bytes[i] = 0.0;
+      stats->level_barriers[i] = 0;
+      if (i < nl) {
+        float lm = 0.f;
+        cudaEventElapsedTime(&lm, lev[(size_t)2 * i], lev[(size_t)2 * i + 1]);
+        stats->level_refine_ms[i] = lm;
+        stats->level_bytes[i] = s8d_refine_bytes(lacct[(size_t)i].data(), level_n[i],
+                                                 level_m2[i], (int)k, P.rho);
+        stats->level_barriers[i] = lacct[(size_t)i][A_BARRIERS];
+      }
     }
+    for (int i = 0; i < 16; ++i) stats->acct[i] = i < A_COUNT ? ctx().acct[i].load() : 0;
     stats->ms_upload = stats->ms_download = 0.0;
     stats->bytes_h2d = stats->bytes_d2h = 0;
     stats->ms_coarsen = a;
@@ -1265,6 +1297,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     stats->max_block_weight = mx;
   }
   for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& e : lev) cudaEventDestroy(e);
 }
 
 // host-array upload (graph.py:17-39 int64 CSR) -> int32 device level
@@ -1307,7 +1340,7 @@ struct UpJob {
 };
 struct UpAcc {
   long long sum_ew = 0, sum_vw = 0, h2d = 0, maxdeg = 0;
-  bool bad_range = false, bad_vw = false;
+  bool bad_range = false, bad_vw = false, bad_ew = false, bad_off = false, bad_tgt = false;
 };
 }  // namespace
 
@@ -1323,6 +1356,7 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
                               const int64_t* ew, const int64_t* vw, OwnedGraph& G,
                               cudaStream_t s) {
   GIM_CHECK(n >= 0 && n < INT32_MAX, GIM_E_OVERFLOW, "n must be < 2^31");
+  GIM_CHECK(off[0] == 0, GIM_E_INVALID, "offsets[0] must be 0");
   long long m2 = off[n];
   GIM_CHECK(m2 >= 0 && m2 < INT32_MAX, GIM_E_OVERFLOW, "2m must be < 2^31");
   G.n = (int)n;
@@ -1370,6 +1404,7 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
         if (used[slot]) GIM_CUDA(cudaEventSynchronize(done[slot]));
         long long sum = 0;
         bool bad = false, nonpos = false, same = J.kind == 1 || J.kind == 2;
+        bool badt = false, bado = false;
         if (same) {  // weights: validate, and look for a constant chunk first
           const int64_t x0 = J.src[0];
           for (long long i = 0; i < J.cnt; ++i) {
@@ -1390,13 +1425,22 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
           for (long long i = 0; i < J.cnt; ++i) {
             const int64_t x = J.src[i];
             bad |= x < INT32_MIN || x > INT32_MAX;
+            badt |= x < 0 || x >= n;  // targets: vertex ids (offsets: below)
             buf[i] = (int)x;
           }
-          if (J.kind == 3)  // row lengths inside the chunk (boundaries: below)
-            for (long long i = 1; i < J.cnt; ++i)
-              a.maxdeg = std::max<long long>(a.maxdeg, J.src[i] - J.src[i - 1]);
+          if (J.kind == 3) {  // row lengths inside the chunk (boundaries: below)
+            badt = false;
+            for (long long i = 1; i < J.cnt; ++i) {
+              const long long len = J.src[i] - J.src[i - 1];
+              bado |= len < 0;
+              a.maxdeg = std::max<long long>(a.maxdeg, len);
+            }
+          }
         }
         a.bad_range |= bad;
+        a.bad_tgt |= badt;
+        a.bad_off |= bado;
+        if (J.kind == 1) a.bad_ew |= nonpos;
         if (J.kind == 1) a.sum_ew += sum;
         if (J.kind == 2) { a.sum_vw += sum; a.bad_vw |= nonpos; }
         if (!(same && !bad)) {
@@ -1427,13 +1471,21 @@ static long long upload_graph(long long n, const int64_t* off, const int64_t* tg
     tot.sum_vw += a.sum_vw;
     tot.bad_range |= a.bad_range;
     tot.bad_vw |= a.bad_vw;
+    tot.bad_ew |= a.bad_ew;
+    tot.bad_off |= a.bad_off;
+    tot.bad_tgt |= a.bad_tgt;
     tot.h2d += a.h2d;
     tot.maxdeg = std::max(tot.maxdeg, a.maxdeg);
   }
-  for (long long b = kChunk; b <= n; b += kChunk)  // rows across chunk boundaries
+  for (long long b = kChunk; b <= n; b += kChunk) {  // rows across chunk boundaries
     tot.maxdeg = std::max<long long>(tot.maxdeg, off[b] - off[b - 1]);
+    tot.bad_off |= off[b] < off[b - 1];
+  }
   G.maxdeg = (int)std::min<long long>(tot.maxdeg, INT32_MAX);
   GIM_CHECK(!tot.bad_range, GIM_E_OVERFLOW, "CSR values must fit int32");
+  GIM_CHECK(!tot.bad_off, GIM_E_INVALID, "offsets must be nondecreasing");
+  GIM_CHECK(!tot.bad_tgt, GIM_E_INVALID, "edge targets must lie in [0, n)");
+  GIM_CHECK(!tot.bad_ew, GIM_E_INVALID, "edge weights must be positive");
   GIM_CHECK(!tot.bad_vw, GIM_E_INVALID, "vertex weights must be positive");
   GIM_CHECK(tot.sum_vw < INT32_MAX, GIM_E_OVERFLOW, "total vertex weight must be < 2^31");
   GIM_CHECK(tot.sum_ew < INT32_MAX, GIM_E_OVERFLOW, "total edge weight must be < 2^31");
@@ -1465,7 +1517,21 @@ static gim_im_params default_params() {
   p.sigma_coarse = 0.065;
   p.sigma_fine = 0.005;
   p.iw_max_finest = 10;
+  p.run_flags = GIM_RUN_DEFAULT;
   return p;
+}
+
+// the call's mode flags: explicit bits or the process defaults
+static RunFlags flags_of(const gim_im_params* P) {
+  RunFlags f = default_flags();
+  if (P && P->run_flags >= 0) {
+    f.fused = P->run_flags & GIM_RUN_FUSED;
+    f.rowwise = P->run_flags & GIM_RUN_ROWWISE;
+    f.batch = P->run_flags & GIM_RUN_BATCH;
+    f.fanout = P->run_flags & GIM_RUN_FANOUT;
+    f.prof = P->run_flags & GIM_RUN_PROFILE;
+  }
+  return f;
 }
 
 extern "C" int gim_default_params(gim_im_params* out) {
@@ -1699,6 +1765,9 @@ extern "C" int gim_hierarchical_multisection(const gim_graph* g, const gim_topol
     std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
     std::vector<long long> d(t->distances, t->distances + t->levels);
     RunStats st;
+    RunCtx rc;
+    rc.f = default_flags();
+    CtxScope scope(&rc);
     hierarchical_multisection(dg, total, h, d, eps, seed, assignment, st, s);
     GIM_CUDA(sync_stream(s));
   });
@@ -1718,6 +1787,9 @@ extern "C" int gim_hierarchical_multisection_host(int64_t n, const int64_t* offs
               "null argument");
     GIM_CHECK(n > 0, GIM_E_EMPTY, "cannot map an empty graph");
     cudaStream_t s = (cudaStream_t)stream;
+    RunCtx rc;
+    rc.f = default_flags();
+    CtxScope scope(&rc);
     OwnedGraph G;
     upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
     Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
@@ -1748,6 +1820,9 @@ extern "C" int gim_integrated_map_device(const gim_graph* g, const gim_topology*
     DevGraph dg = view(*g);
     GIM_CHECK(dg.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
     gim_im_params P = params ? *params : default_params();
+    RunCtx rc;
+    rc.f = flags_of(&P);
+    CtxScope scope(&rc);
     long long total = total_vertex_weight(dg, s);
     integrated_map_device(dg, total, *t, eps, seed, P, out_assignment,
                           reinterpret_cast<long long*>(out_block_weights), stats, s);
@@ -1765,6 +1840,9 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     GIM_CHECK(n > 0, GIM_E_EMPTY, "cannot map an empty graph");
     cudaStream_t s = (cudaStream_t)stream;
     gim_im_params P = params ? *params : default_params();
+    RunCtx rc;
+    rc.f = flags_of(&P);
+    CtxScope scope(&rc);
     OwnedGraph G;
     const auto t_up = std::chrono::steady_clock::now();
     const long long h2d = upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
@@ -1817,7 +1895,24 @@ extern "C" int64_t gim_launch_count(void) { return launches(); }
 extern "C" void gim_release_cached_memory(void) { gim::release_cached_memory(); }
 extern "C" void gim_reset_launch_count(void) { reset_launches(); }
 
-extern "C" void gim_set_fanout(int32_t on) { gim::g_fanout.store(on != 0); }
-extern "C" void gim_set_fused(int32_t on) { gim::g_fused.store(on != 0); }
-extern "C" void gim_set_batch(int32_t on) { gim::g_batch.store(on != 0); }
-extern "C" void gim_set_rowwise_contraction(int32_t on) { gim::g_rowwise.store(on != 0); }
+namespace gim {
+template <class F>
+static void update_defaults(F&& edit) {
+  RunFlags f = default_flags();
+  edit(f);
+  set_default_flags(f);
+}
+}  // namespace gim
+
+extern "C" void gim_set_fanout(int32_t on) {
+  gim::update_defaults([&](gim::RunFlags& f) { f.fanout = on != 0; });
+}
+extern "C" void gim_set_fused(int32_t on) {
+  gim::update_defaults([&](gim::RunFlags& f) { f.fused = on != 0; });
+}
+extern "C" void gim_set_batch(int32_t on) {
+  gim::update_defaults([&](gim::RunFlags& f) { f.batch = on != 0; });
+}
+extern "C" void gim_set_rowwise_contraction(int32_t on) {
+  gim::update_defaults([&](gim::RunFlags& f) { f.rowwise = on != 0; });
+}

@@ -612,7 +612,7 @@ static void ggg_seeds(const DevGraph& g, int k, int* dist, int* seeds, cudaStrea
   std::call_once(once, [] {
     GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ggg_seeds, 256, 0));
   });
-  const int G = std::max(1, std::min(kSMs * std::max(occ, 1), (int)((g.n + 255) / 256)));
+  const int G = std::max(1, std::min(device_sms() * std::max(occ, 1), (int)((g.n + 255) / 256)));
   const size_t n = (size_t)std::max(g.n, 1);
   DBuf<int> q(3 * n + 4, s);
   DBuf<unsigned long long> keys(2, s);

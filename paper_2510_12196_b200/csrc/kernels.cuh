@@ -135,6 +135,7 @@ struct FusedState {
   int status;   // 0 = finished, 1 = strong pass due (host)
   int started;  // 0 = first launch of this refinement
   int reinit;   // 1 = re-establish the per-vertex list invariants on entry
+  long long acct[16];  // Acct counters (common.cuh), summed over launches
 };
 
 struct FusedCfg {
@@ -151,6 +152,7 @@ struct FusedBuffers {
   int *bstamp = nullptr, *wdeg = nullptr, *lsmall = nullptr, *lheavy = nullptr, *lcand = nullptr;
   int *lmov0 = nullptr, *lmov1 = nullptr;
   long long lp_seen = 0, weak_seen = 0;
+  long long acct_seen[16] = {0};  // FusedState::acct already accounted
   // owned
   DBuf<long long> W, S;
   long long W_cap = 0, S_cap = 0;
@@ -159,6 +161,10 @@ struct FusedBuffers {
 };
 
 bool fused_supported(int k, int rho);
+
+// SURVEY §8(d) algorithmic bytes of refinement work described by Acct
+// counter deltas `d` on a level of n vertices / m2 slots
+double s8d_refine_bytes(const long long* d, long long n, long long m2, int k, int rho);
 
 // batched small-graph partitioner pieces (batch.cu)
 struct SmallStack {

@@ -135,6 +135,7 @@ constexpr int kEvalChunk = GIM_EVAL_CHUNK;  // row slots per load batch
 struct ThreadEval {
   long long cur, conn_own, best_gain, cost_tb;
   int best_b;
+  int nblk;  // distinct adjacent blocks found (conn-table entries, S_v)
   bool overflow;
 };
 
@@ -152,6 +153,7 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
   r.best_gain = kGainNone;
   r.best_b = -1;
   r.cost_tb = 0;
+  r.nblk = 0;
   r.overflow = false;
   int nb[TPV_DISTINCT];
   long long cw[TPV_DISTINCT];
@@ -201,6 +203,7 @@ __device__ __forceinline__ ThreadEval eval_thread(int e0, int e1, int own, const
       }
     }
   }
+  r.nblk = cnt;
   if (flatd > 0) {
     long long W = 0, ctb = 0;
 #pragma unroll

@@ -125,6 +125,13 @@ struct Ctl {
   int brk, take, strong_yield;
 };
 
+// warp-aggregated counter add: every lane of the warp must execute it
+__device__ __forceinline__ void acct_warp(long long* s_acct, int i, int x) {
+  const int t = __reduce_add_sync(0xffffffffu, x);
+  if (lane_id() == 0 && t) atomicAdd(reinterpret_cast<unsigned long long*>(&s_acct[i]),
+                                     (unsigned long long)t);
+}
+
 __device__ __forceinline__ long long block_max_bw(const long long* bw, int k) {
   __shared__ long long red[kFusedWarps];
   long long m = 0;
@@ -191,8 +198,10 @@ __device__ __forceinline__ void wq_push(WarpQueue& q, bool pred, int val, int* l
 // hardware cluster barrier with release/acquire semantics, so many
 // refinements run concurrently); large graphs as a cooperative grid.
 struct GridBarrier {
-  int mode;  // 0 one CTA, 1 cluster, 2 cooperative grid
+  int mode;            // 0 one CTA, 1 cluster, 2 cooperative grid
+  long long* counter;  // shared-memory barrier count of this CTA (accounting)
   __device__ __forceinline__ void sync() const {
+    if (threadIdx.x == 0) ++*counter;
     if (mode == 0) __syncthreads();
     else if (mode == 1) cg::this_cluster().sync();
     else cg::this_grid().sync();
@@ -374,7 +383,11 @@ __device__ __forceinline__ void hub_phase(const FusedArgs& A, const GridBarrier&
 
 template <int VW>
 __device__ __forceinline__ void refine_body(const FusedArgs& A) {
-  const GridBarrier grid{A.bar_mode};
+  // SURVEY §8(d) accounting (Acct, common.cuh): warp-aggregated (REDUX) into
+  // this CTA's shared counters, added to the FusedState once at exit
+  __shared__ long long s_acct[A_COUNT];
+  if (threadIdx.x < A_COUNT) s_acct[threadIdx.x] = 0;
+  const GridBarrier grid{A.bar_mode, &s_acct[A_BARRIERS]};
   extern __shared__ unsigned char dsm[];
   __shared__ long long s_dbit[64];
   __shared__ Ctl C;
@@ -472,6 +485,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       }
     }
     if (first) block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);
+    if (BX == 0 && threadIdx.x == 0) s_acct[A_SWEEPS] += 1;
   }
   if (first) {
     for (long long v = gt; v < n; v += GT) A.best[v] = A.part[v];
@@ -572,12 +586,14 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       if (!vcent) {
         // boundary list (unlocked): ext[v] > 0; four vertices per thread
         // per step with their loads issued together
+        int nbnd = 0;
         for (long long b0 = (gt - lane) * 4; b0 < n; b0 += GT * 4) {
           bool bnd[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const long long v = b0 + q * 32 + lane;
             bnd[q] = v < n && ext[v] > 0;
+            nbnd += bnd[q];
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -586,6 +602,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             wq_push(qa, bnd[q], (int)v, A.lsmall, cnt + C_SMALL);
           }
         }
+        acct_warp(s_acct, A_BND, nbnd);
+        if (BX == 0 && threadIdx.x == 0) s_acct[A_SCAN] += n;
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
         grid.sync();
         PHASE_MARK(1);
@@ -634,8 +652,12 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             r.best_b = q.best_b;
             r.best_gain = q.best_gain;
             r.conn_own = q.conn_own;
+            r.nblk = sz;
           }
         }
+        acct_warp(s_acct, A_EVAL_V, live);
+        acct_warp(s_acct, A_EVAL_SLOTS, live ? e1 - e0 : 0);
+        acct_warp(s_acct, A_EVAL_S, live ? r.nblk : 0);
         bool ok = false;
         if (live && r.best_b >= 0) {
           if (r.best_gain >= 0) ok = true;
@@ -663,10 +685,12 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         const bool live = idx < nc;
         const int v = live ? A.lcand[idx] : 0;
         long long fut = 0;
+        int csl = 0;
         if (live) {
           const long long gv = A.gkey[v];
           const unsigned long long oc = T.code[A.part[v]];
           const unsigned long long dc = T.code[A.dest[v]];
+          if (li == 0) csl = A.off[v + 1] - A.off[v];
           for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
             int u = A.tgt[e];
             long long gu = A.gkey[u];
@@ -679,6 +703,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
         const bool m = live && li == 0 && fut >= 0;
+        acct_warp(s_acct, A_CAND_SLOTS, csl);
         if (m) {
           mstamp[v] = cur_stamp;
           opart[v] = A.part[v];
@@ -753,13 +778,16 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         ThreadEval r{};
         r.best_b = -1;
         bool ovf = false, hub = false, big = false;
+        int osl = 0;
         if (live && ext && ext[v] == 0) {
           // interior vertex (every neighbour in its own block): no adjacent
           // candidate, cur = 0, cost(tb) = wdeg * D(tb, own) — no row walk
+          r.nblk = 1;
           if (tb >= 0)
             r.cost_tb = (long long)A.wdeg[v] * cdist(s_dbit, T.code[tb], T.code[own]);
         } else if (live) {
           const int e0 = A.off[v], e1 = A.off[v + 1];
+          osl = e1 - e0;
           if (A.hconn && (A.hub_phases & 2) && e1 - e0 > A.list_deg) {
             // evaluated by the grid after this pass
             if (e1 - e0 > A.hub_deg) big = true;
@@ -789,8 +817,12 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             r.best_gain = q.best_gain;
             r.cur = q.cur;
             r.cost_tb = ctb;
+            r.nblk = sz;
           }
         }
+        acct_warp(s_acct, A_OVL_V, live);
+        acct_warp(s_acct, A_OVL_SLOTS, osl);
+        acct_warp(s_acct, A_OVL_S, live ? r.nblk : 0);
         int target = -1;
         long long gain = 0;
         if (live && !hub && !big) {  // listed rows: decided by the grid below
@@ -1032,8 +1064,10 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       long long acc = 0;
       for (long long ib = gw * GPW; ib < nm; ib += NW * GPW) {
         const long long idx = ib + gi;
+        int msl = 0;
         if (idx < nm) {
           const int v = lmov[idx];
+          if (li == 0) msl = A.off[v + 1] - A.off[v];
           const int ov = opart[v], nv = A.dest[v];
           const unsigned long long oc = T.code[ov], nc2 = T.code[nv];
           int dext = 0;
@@ -1062,6 +1096,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
             }
           }
         }
+        acct_warp(s_acct, A_MOV_SLOTS, msl);
       }
       block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
       if (balanced_now) {
@@ -1077,6 +1112,15 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     const long long mx = block_max_bw(A.bw, k);
     if (threadIdx.x == 0) {
       const long long mv = cnt[C_MOV];
+      if (BX == 0) {
+        s_acct[A_MOV_V] += mv;
+        if (balanced_now) {
+          s_acct[A_CAND_V] += cnt[C_CAND];
+          s_acct[A_LP_IT] += 1;
+        } else {
+          s_acct[A_WEAK_IT] += 1;
+        }
+      }
       C.take = 0;
       C.iters++;
       C.stamp = stamp;
@@ -1129,6 +1173,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   }
   // ---- exit: persist the control state; on completion restore the best
   grid.sync();
+  if (threadIdx.x < A_COUNT && (threadIdx.x != A_BARRIERS || BX == 0) && s_acct[threadIdx.x])
+    atomicAdd(reinterpret_cast<unsigned long long*>(&A.st->acct[threadIdx.x]),
+              (unsigned long long)s_acct[threadIdx.x]);
   if (BX == 0 && threadIdx.x == 0) {
     FusedState& S1 = *A.st;
     S1.started = 1;
@@ -1381,6 +1428,22 @@ static int hub_phases() {
 
 bool fused_supported(int k, int rho) { return k <= 1024 && rho >= 1 && rho <= 8; }
 
+// LP pass (K9+K10) 8*S + 17n + 25*(2m_cand), with S the
+// conn-table entries of the unlocked vertices (evaluated vertices' distinct
+// adjacent blocks + one per interior vertex); rebalance (K11+K12) 8*S_over +
+// 24*n_over + 16*k*31*rho; apply (K13) 24 per mover slot; plus the entry
+// sweeps 8n + 12*m2 each (as K1)
+double s8d_refine_bytes(const long long* d, long long n, long long m2, int k, int rho) {
+  const double interior = (double)(d[A_SCAN] - d[A_BND]);
+  const double S = (double)d[A_EVAL_S] + interior;
+  double b = 8.0 * S + 17.0 * (double)n * (double)d[A_LP_IT] + 25.0 * (double)d[A_CAND_SLOTS];
+  b += 8.0 * (double)d[A_OVL_S] + 24.0 * (double)d[A_OVL_V] +
+       16.0 * (double)k * 31.0 * (double)rho * (double)d[A_WEAK_IT];
+  b += 24.0 * (double)d[A_MOV_SLOTS];
+  b += (8.0 * (double)n + 12.0 * (double)m2) * (double)d[A_SWEEPS];
+  return b;
+}
+
 // runs Alg. 4 iterations on the device until the loop ends (returns true) or a
 // strong pass is due (returns false; the host performs it and calls again)
 bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long* bw,
@@ -1511,8 +1574,8 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   }
   const long long it0 = fb.lp_seen + fb.weak_seen, lp0 = fb.lp_seen;
   {
-    // one launch = many Alg. 4 iterations; per-iteration algorithmic bytes
-    // are accounted by the host from the iteration count
+    // one launch = many Alg. 4 iterations; its algorithmic bytes come from
+    // the device counters it returns (SURVEY §8(d) formulas)
     ProfScope prof(P_LP_EVAL, 0.0, s);
     if (mode == 3) {
       void* fs = nullptr;
@@ -1545,8 +1608,12 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     count_launch();
     GIM_CUDA(cudaMemcpyAsync(fb.h_state, fb.state, sizeof(FusedState), cudaMemcpyDeviceToHost, s));
     GIM_CUDA(sync_stream(s));
-    prof.extra = (double)(fb.h_state->lp + fb.h_state->weak - fb.lp_seen - fb.weak_seen) *
-                 (12.0 * (double)g.m2 + 8.0 * (double)g.n);
+    long long d[16];
+    for (int i = 0; i < 16; ++i) {
+      d[i] = fb.h_state->acct[i] - fb.acct_seen[i];
+      fb.acct_seen[i] = fb.h_state->acct[i];
+    }
+    prof.extra = s8d_refine_bytes(d, g.n, g.m2, k, cfg.rho);
     fb.lp_seen = fb.h_state->lp;
     fb.weak_seen = fb.h_state->weak;
   }

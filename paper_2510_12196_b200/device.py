@@ -303,8 +303,16 @@ def hierarchical_multisection(dg: DeviceGraph, hierarchy, distances, eps: float,
     return out[:dg.n]
 
 
+def run_flags(fused=True, rowwise=True, batch=True, fanout=True, profile=False) -> int:
+    """GIM_RUN_* bits for one call (gim_im_params.run_flags)."""
+    return ((_lib.RUN_FUSED if fused else 0) | (_lib.RUN_ROWWISE if rowwise else 0) |
+            (_lib.RUN_BATCH if batch else 0) | (_lib.RUN_FANOUT if fanout else 0) |
+            (_lib.RUN_PROFILE if profile else 0))
+
+
 def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", jet_filter_c=0.25,
-                  sigma_coarse=0.065, sigma_fine=0.005, iw_max_finest=10) -> _lib.GimImParams:
+                  sigma_coarse=0.065, sigma_fine=0.005, iw_max_finest=10,
+                  run_flags: int = -1) -> _lib.GimImParams:
     p = _lib.GimImParams()
     p.coarsest_factor = int(coarsest_factor)
     p.phi = float(phi)
@@ -314,6 +322,7 @@ def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", j
     p.sigma_coarse = float(sigma_coarse)
     p.sigma_fine = float(sigma_fine)
     p.iw_max_finest = int(iw_max_finest)
+    p.run_flags = int(run_flags)
     return p
 
 
@@ -322,11 +331,16 @@ PROF_CLASSES = ("jeval", "hem", "contract", "lp_eval", "lp_second", "apply", "re
 
 
 def stats_dict(st: _lib.GimImStats) -> dict:
+    per_level = ("level_n", "level_m2", "level_iters", "level_refine_ms", "level_bytes",
+                 "level_barriers")
     d = {f: getattr(st, f) for f, _ in _lib.GimImStats._fields_
-         if f not in ("level_n", "level_m2", "prof_ms", "prof_bytes", "prof_count", "top_class",
-                     "top_ms", "top_bytes")}
-    d["level_n"] = [st.level_n[i] for i in range(min(st.n_levels, 64))]
-    d["level_m2"] = [st.level_m2[i] for i in range(min(st.n_levels, 64))]
+         if f not in per_level + ("prof_ms", "prof_bytes", "prof_count", "top_class",
+                                  "top_ms", "top_bytes", "acct")}
+    nl = min(st.n_levels, 64)
+    for f in per_level:
+        arr = getattr(st, f)
+        d[f] = [arr[i] for i in range(nl)]
+    d["acct"] = {name: st.acct[i] for i, name in enumerate(_lib.ACCT_NAMES)}
     prof = {}
     for i, name in enumerate(PROF_CLASSES):
         if st.prof_count[i]:
@@ -336,6 +350,12 @@ def stats_dict(st: _lib.GimImStats) -> dict:
     d["top_launch"] = ({"class": PROF_CLASSES[st.top_class], "ms": st.top_ms,
                         "bytes": st.top_bytes} if 0 <= st.top_class < len(PROF_CLASSES) else None)
     return d
+
+
+def release_cached_memory() -> None:
+    """Return the library's cached device scratch to the CUDA pools and trim
+    them (like torch.cuda.empty_cache for libgpuim's allocator)."""
+    _lib.load().gim_release_cached_memory()
 
 
 def set_profiling(on: bool) -> None:

@@ -1,0 +1,175 @@
+"""Runtime behaviour of libgpuim on the GPU: per-call run contexts (modes,
+launch counts, refinement counters), concurrent maps on separate streams,
+input validation at the boundary, the §8(d) byte accounting, device-keyed
+caches."""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+H = (4, 8, 6)
+DIST = (1, 10, 100)
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_12196_b200 import device
+    return device
+
+
+@pytest.fixture(scope="module")
+def rgg16(D):
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << 16, 0.55, 1)
+    return g, D.DeviceGraph.from_host(g)
+
+
+def test_concurrent_maps_on_streams_equal_serial(D, rgg16):
+    """Three maps at once from three host threads on three streams (config 5's
+    per-GPU concurrency) give exactly the serial mappings and stats."""
+    _, dg = rgg16
+    seeds = [0, 1, 2, 3, 4, 5]
+    serial = {}
+    for s in seeds:
+        a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, s)
+        serial[s] = (a.cpu().numpy(), bw.cpu().numpy(), st["final_j"], st["kernel_launches"])
+    got, errs = {}, []
+
+    def work(my_seeds):
+        st_ = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st_):
+                for s in my_seeds:
+                    a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, s)
+                    st_.synchronize()
+                    got[s] = (a.cpu().numpy(), bw.cpu().numpy(), st["final_j"],
+                              st["kernel_launches"])
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(seeds[i::3],)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for s in seeds:
+        assert np.array_equal(got[s][0], serial[s][0]), s
+        assert np.array_equal(got[s][1], serial[s][1]), s
+        assert got[s][2] == serial[s][2]
+        # launch counts are per call: concurrent calls do not inflate them
+        assert got[s][3] == serial[s][3]
+
+
+def test_replica_runner_on_device(D, rgg16):
+    from paper_2510_12196_b200.replicas import DeviceRunner
+    _, dg = rgg16
+    ref = {s: D.integrated_map_device(dg, H, DIST, 0.03, s)[2]["final_j"] for s in range(4)}
+    r = DeviceRunner(dg, 2)
+    r.warm()
+    out = r.run(list(range(4)))
+    assert [j["seed"] for j in out["jobs"]] == list(range(4))
+    assert all(j["balanced"] for j in out["jobs"])
+    assert {j["seed"]: j["J"] for j in out["jobs"]} == ref
+
+
+@pytest.mark.parametrize("flags", [dict(fused=False), dict(rowwise=False), dict(batch=False),
+                                   dict(fanout=False)])
+def test_per_call_run_flags_identical(D, rgg16, flags):
+    """Every mode gives the same mapping; a per-call mode does not change the
+    process defaults."""
+    _, dg = rgg16
+    a0, _, s0 = D.integrated_map_device(dg, H, DIST, 0.03, 7)
+    a1, _, s1 = D.integrated_map_device(dg, H, DIST, 0.03, 7, run_flags=D.run_flags(**flags))
+    assert np.array_equal(a0.cpu().numpy(), a1.cpu().numpy())
+    assert s0["final_j"] == s1["final_j"]
+    a2, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 7)
+    assert np.array_equal(a0.cpu().numpy(), a2.cpu().numpy())
+
+
+def test_refinement_accounting_reproduces_bytes(D, rgg16):
+    """The per-level §8(d) bytes are the formula over the emitted counters."""
+    g, dg = rgg16
+    _, _, st = D.integrated_map_device(dg, H, DIST, 0.03, 0, run_flags=D.run_flags(profile=True))
+    ac = st["acct"]
+    assert ac["lp_it"] + ac["weak_it"] > 0
+    assert ac["eval_v"] > 0 and ac["eval_slots"] >= ac["eval_v"]
+    assert ac["mov_v"] > 0 and ac["mov_slots"] >= ac["mov_v"]
+    assert 0 < ac["bnd"] <= ac["scan"]
+    assert sum(st["level_iters"]) == st["refine_iterations"]
+    assert all(b > 0 for b in st["level_bytes"])
+    assert st["level_refine_ms"][0] > 0
+    # the profile's refinement class carries the same byte model
+    assert st["profile"]["lp_eval"]["bytes"] > 0
+    k = int(np.prod(H))
+
+    def s8d(a, n, m2):
+        interior = a["scan"] - a["bnd"]
+        b = 8 * (a["eval_S"] + interior) + 17 * n * a["lp_it"] + 25 * a["cand_slots"]
+        b += 8 * a["ovl_S"] + 24 * a["ovl_v"] + 16 * k * 31 * 2 * a["weak_it"]
+        b += 24 * a["mov_slots"] + (8 * n + 12 * m2) * a["sweeps"]
+        return b
+
+    # summed over the levels the totals cannot be recombined exactly (n
+    # differs per level), but a single-level stack can: coarsest_factor huge
+    _, _, st1 = D.integrated_map_device(dg, H, DIST, 0.03, 0, coarsest_factor=1 << 20)
+    assert st1["n_levels"] == 1
+    assert st1["level_bytes"][0] == pytest.approx(s8d(st1["acct"], g.n, 2 * g.m))
+
+
+@pytest.mark.parametrize("bad", ["off0", "offdec", "tgt", "ew"])
+def test_malformed_csr_rejected(D, bad):
+    from paper_2510_12196_b200 import integrated_map
+    from paper_2510_12196_b200._lib import GimError
+    from paper_2510_12196_b200.generators import gen_grid
+    g = gen_grid(8, 8)
+    off, tgt = g.offsets.copy(), g.edge_targets.copy()
+    ew, vw = g.edge_weights.copy(), g.vertex_weights.copy()
+    if bad == "off0":
+        off = off + 1
+    elif bad == "offdec":
+        off[5], off[6] = off[6], off[5]
+    elif bad == "tgt":
+        tgt[3] = g.n + 5
+    else:
+        ew[0] = 0
+
+    class G:
+        offsets, edge_targets, edge_weights, vertex_weights = off, tgt, ew, vw
+
+    class T:
+        hierarchy, distances = (2, 2), (1, 10)
+
+    with pytest.raises(GimError):
+        integrated_map(G(), T(), 0.03, 0)
+
+
+def test_empty_cache_then_map(D, rgg16):
+    from paper_2510_12196_b200 import empty_cache
+    _, dg = rgg16
+    a0, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 3)
+    empty_cache()
+    a1, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 3)
+    assert np.array_equal(a0.cpu().numpy(), a1.cpu().numpy())
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs")
+def test_second_device_after_first(D):
+    """Topology tables, scratch caches and worker streams are per device."""
+    from paper_2510_12196_b200.generators import gen_rgg
+    g = gen_rgg(1 << 14, 0.55, 2)
+    res = []
+    for dev in (0, 1):
+        with torch.cuda.device(dev):
+            dg = D.DeviceGraph.from_host(g, device=f"cuda:{dev}")
+            a, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 0)
+            res.append(a.cpu().numpy())
+    assert np.array_equal(res[0], res[1])

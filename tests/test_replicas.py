@@ -47,3 +47,43 @@ def test_max_over_ranks_gloo():
     for _, tmax, value in res:
         assert tmax == 150.0
         assert value == pytest.approx(1000 * 4 * 2 / 0.150)
+
+
+# ---------------------------------------------------------------------------
+# config-5 replica runner (paper_2510_12196_b200/replicas.py): job split and
+# aggregation across spawned processes, no NCCL
+
+def _fake_child(rank, gpu, seeds, logn, concurrency, barrier, q):
+    """Stands in for the GPU mapper: every 'map' of seed s takes 20 ms and
+    reports J = 1000 + s; rank 1 starts late to exercise the wall span."""
+    import time
+    barrier.wait()
+    if rank == 1:
+        time.sleep(0.05)
+    t0 = time.time()
+    jobs = []
+    for s in seeds:
+        time.sleep(0.02 / max(concurrency, 1))
+        jobs.append({"seed": s, "J": 1000 + s, "ms": 20.0, "balanced": True})
+    q.put({"rank": rank, "t_start": t0, "t_end": time.time(), "jobs": jobs, "m": 500})
+
+
+def test_split_jobs_covers_every_seed_once():
+    from paper_2510_12196_b200.replicas import split_jobs
+    for g in (1, 2, 3, 4, 8):
+        parts = split_jobs(list(range(64)), g)
+        assert sorted(s for p in parts for s in p) == list(range(64))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def test_replica_runner_processes_aggregate():
+    import math
+
+    from paper_2510_12196_b200 import replicas
+    out = replicas.run(gpus=2, jobs=10, concurrency=2, logn=10, child=_fake_child)
+    assert out["maps"] == 10 and out["gpus"] == 2 and out["jobs"] == 10
+    assert out["edges_per_s"] == pytest.approx(10 * 500 / out["wall_s"])
+    assert out["wall_s"] >= 0.05  # spans the late rank
+    assert out["J_geomean"] == pytest.approx(math.exp(sum(math.log(1000 + s)
+                                                          for s in range(10)) / 10))
+    assert out["balanced"]
