@@ -41,7 +41,7 @@ extern "C" {
 #define GIM_E_FORMAT 7      /* malformed METIS file (MetisFormatError)       */
 #define GIM_E_IO 8          /* file cannot be opened / read                  */
 
-#define GIM_MAX_LEVELS 8
+#define GIM_MAX_LEVELS 32
 
 /* Device-resident CSR graph (graph.py:17-39 `Graph`, int32 on device). */
 typedef struct gim_graph {
@@ -54,12 +54,18 @@ typedef struct gim_graph {
   const int32_t* sources;   /* [m2]  edge sources (`edge_sources`, E_u)    */
 } gim_graph;
 
-/* Machine hierarchy a_1:...:a_l and integral distances d_1:...:d_l
- * (topology.py:25-58 `Topology`; integral_distances must be true). */
+/* Machine hierarchy a_1:...:a_l and distances d_1:...:d_l (topology.py:25-58
+ * `Topology`), l <= GIM_MAX_LEVELS.  Distances may be non-integral
+ * (Topology.integral_distances false): the device works on d * 2^s as exact
+ * int64 (s = the smallest shift making every d integral when the d are
+ * dyadic rationals — then every gain, J and decision equals the reference's
+ * float arithmetic — else s chosen so that J fits int64, with the d rounded:
+ * tolerance parity); gain-bucket bounds and the Jet filter are scaled by
+ * 2^s.  gim_im_stats reports s, whether it is exact, and J in float64. */
 typedef struct gim_topology {
   int32_t levels;
   int64_t hierarchy[GIM_MAX_LEVELS];
-  int64_t distances[GIM_MAX_LEVELS];
+  double distances[GIM_MAX_LEVELS];
 } gim_topology;
 
 /* Keyword arguments of integrated_map (pipelines.py:221-235). */
@@ -76,7 +82,18 @@ typedef struct gim_im_params {
    * process defaults set by gim_set_* when the call starts.  Every mode
    * gives identical results; they exist for A/B measurement and tests. */
   int32_t run_flags;
+  /* GIM_ISOLATED_KEEP (0, the reference's algorithm, bit-exact) or
+   * GIM_ISOLATED_STRIP (1): degree-0 vertices are removed before the level
+   * stack (they can never be matched, so on skewed graphs they stall the
+   * coarsening, coarsening.py:289-290), the rest is mapped with the same
+   * L_max, and the isolated vertices are water-filled into the lightest
+   * blocks.  They add nothing to J wherever they go: tolerance parity
+   * (every block <= L_max; J compared by geometric mean). */
+  int32_t isolated;
 } gim_im_params;
+
+#define GIM_ISOLATED_KEEP 0
+#define GIM_ISOLATED_STRIP 1
 
 #define GIM_RUN_DEFAULT (-1)
 #define GIM_RUN_FUSED 1    /* Alg. 4 as one persistent kernel per level     */
@@ -146,6 +163,14 @@ typedef struct gim_im_stats {
   int64_t level_barriers[64];
   /* GIM_ACCT_* counters summed over the IM levels */
   int64_t acct[16];
+  /* distances as device integers d * 2^dist_shift (exact when dist_exact);
+   * final_j above is in those units, final_j_f64 = J with the caller's
+   * float distances (mapping.py:76-91 float path) */
+  int32_t dist_shift;
+  int32_t dist_exact;
+  double final_j_f64;
+  /* isolated-vertex strip mode: vertices set aside and mapped by the fill */
+  int64_t isolated_vertices;
 } gim_im_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -154,9 +179,18 @@ const char* gim_last_error(void);
 
 /* ---- objective ---------------------------------------------------------- */
 /* J = sum over directed slots of w * D[Pi(src), Pi(tgt)]   (mapping.py:76-91).
- * *j_out (device int64) is OVERWRITTEN. */
+ * *j_out (device int64) is OVERWRITTEN, in units of 2^-s (s = the
+ * topology's distance shift, 0 for integral distances). */
 int gim_total_cost(const gim_graph* g, const int32_t* assignment,
                    const gim_topology* t, int64_t* j_out, void* stream);
+
+/* J in float64 with the topology's own distances (the reference's float J
+ * for non-integral distances); *j_out device double, OVERWRITTEN. */
+int gim_total_cost_f64(const gim_graph* g, const int32_t* assignment,
+                       const gim_topology* t, double* j_out, void* stream);
+
+/* Distance shift s of a topology and whether d * 2^s is exact (host ints). */
+int gim_topology_scale(const gim_topology* t, int32_t* shift_out, int32_t* exact_out);
 
 /* k-bin histogram of vertex weights, bw_out[k] overwritten (mapping.py:38-43). */
 int gim_block_weights(const gim_graph* g, const int32_t* assignment, int32_t k,

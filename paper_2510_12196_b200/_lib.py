@@ -10,7 +10,7 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libgpuim.so"
-MAX_LEVELS = 8
+MAX_LEVELS = 32
 
 GIM_OK = 0
 GIM_E_INVALID = 1
@@ -39,7 +39,7 @@ class GimTopology(C.Structure):
     _fields_ = [
         ("levels", C.c_int32),
         ("hierarchy", C.c_int64 * MAX_LEVELS),
-        ("distances", C.c_int64 * MAX_LEVELS),
+        ("distances", C.c_double * MAX_LEVELS),
     ]
 
 
@@ -54,6 +54,7 @@ class GimImParams(C.Structure):
         ("sigma_fine", C.c_double),
         ("iw_max_finest", C.c_int32),
         ("run_flags", C.c_int32),
+        ("isolated", C.c_int32),
     ]
 
 
@@ -98,6 +99,10 @@ class GimImStats(C.Structure):
         ("level_bytes", C.c_double * 64),
         ("level_barriers", C.c_int64 * 64),
         ("acct", C.c_int64 * 16),
+        ("dist_shift", C.c_int32),
+        ("dist_exact", C.c_int32),
+        ("final_j_f64", C.c_double),
+        ("isolated_vertices", C.c_int64),
     ]
 
 
@@ -119,6 +124,8 @@ SIGNATURES: dict[str, list] = {
     "gim_version": [],
     "gim_last_error": [],
     "gim_total_cost": [GP, P, TP, P, P],
+    "gim_total_cost_f64": [GP, P, TP, P, P],
+    "gim_topology_scale": [TP, PI32, PI32],
     "gim_block_weights": [GP, P, I32, P, P],
     "gim_hem_round": [GP, P, P, DBL, U64, PI64, P],
     "gim_match_graph": [GP, DBL, U64, P, PI64, P],
@@ -203,5 +210,7 @@ def topology_struct(hierarchy, distances) -> GimTopology:
     t.levels = len(hierarchy)
     for i, (a, d) in enumerate(zip(hierarchy, distances)):
         t.hierarchy[i] = int(a)
-        t.distances[i] = int(d)
+        t.distances[i] = float(d)
+        if int(d) == d and abs(d) >= 2**53:
+            raise OverflowError("integral distances must be < 2^53")
     return t

@@ -66,13 +66,20 @@ def _validate(phi, rho, filter_mode, sigma_coarse, sigma_fine, iw_max_finest):
 def integrated_map(g, t, eps: float, seed: int = 0, *, coarsest_factor: int = 128,
                    phi: float = 0.999, rho: int = 2, filter_mode: str = "nonneg",
                    jet_filter_c: float = 0.25, sigma_coarse: float = 0.065,
-                   sigma_fine: float = 0.005, iw_max_finest: int = 10, stats: dict | None = None):
+                   sigma_fine: float = 0.005, iw_max_finest: int = 10, stats: dict | None = None,
+                   isolated_vertices: str = "keep"):
     """GPU-IM: coarsen, map the coarsest graph, refine upward — on the B200.
 
     `g` is any object with the reference Graph's int64 CSR arrays
     (offsets, edge_targets, edge_weights, vertex_weights); `t` any object
     with `hierarchy` and `distances`.  If `stats` is a dict it receives the
     run counters (levels, iterations, device milliseconds, launches).
+
+    `isolated_vertices="strip"` (not in the reference) maps the graph without
+    its degree-0 vertices and water-fills them into the lightest blocks
+    afterwards (include/gpuim.h GIM_ISOLATED_STRIP): on skewed graphs whose
+    isolated vertices stall the coarsening (R-MAT) this is much faster; it is
+    held to tolerance parity (balanced, J by geometric mean), not bit-exact.
     """
     from . import device as D
 
@@ -84,7 +91,10 @@ def integrated_map(g, t, eps: float, seed: int = 0, *, coarsest_factor: int = 12
         g.offsets, g.edge_targets, g.edge_weights, g.vertex_weights, tuple(t.hierarchy),
         tuple(t.distances), eps, seed, coarsest_factor=coarsest_factor, phi=phi, rho=rho,
         filter_mode=filter_mode, jet_filter_c=jet_filter_c, sigma_coarse=sigma_coarse,
-        sigma_fine=sigma_fine, iw_max_finest=iw_max_finest)
+        sigma_fine=sigma_fine, iw_max_finest=iw_max_finest, isolated_vertices=isolated_vertices)
+    # J as the reference types it (mapping.py:76-91): int for integral
+    # distances, else float (the device works on d * 2^dist_shift)
+    st["J"] = st["final_j"] if D.integral_distances(t.distances) else st["final_j_f64"]
     if stats is not None:
         stats.update(st)
     m = _mapping_type()(a, bw)

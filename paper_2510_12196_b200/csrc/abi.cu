@@ -4,6 +4,9 @@
 
 #include <sched.h>
 
+#include <cmath>
+#include <cstring>
+
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -224,20 +227,51 @@ void release_cached_memory() {
 static std::mutex g_topo_mu;
 static std::map<std::vector<long long>, Topo> g_topo_cache;
 
-Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances) {
+// distance scale of a topology (gim_topology doc): the smallest shift s
+// making every d * 2^s integral (dyadic distances: exact, the reference's
+// float sums are exact too), else the largest s keeping d_max * 2^s < 2^31
+// (J = sum w * d * 2^s < 2^62 for total edge weight < 2^31), d rounded
+void topo_scale(int levels, const double* d, int* shift, int* exact) {
+  double dmax = 0.0;
+  for (int i = 0; i < levels; ++i) dmax = std::max(dmax, d[i]);
+  for (int s = 0; s <= 40; ++s) {
+    bool ok = true;
+    for (int i = 0; i < levels && ok; ++i) {
+      const double x = std::ldexp(d[i], s);
+      ok = x == std::floor(x) && x < 9.0e15;
+    }
+    if (ok && (s == 0 || std::ldexp(dmax, s) < 2147483648.0)) {
+      *shift = s;
+      *exact = 1;
+      return;
+    }
+  }
+  int s = 0;
+  while (s < 40 && std::ldexp(dmax, s + 1) < 2147483648.0) ++s;
+  *shift = s;
+  *exact = 0;
+}
+
+Topo get_topo(const gim_topology& tt) {
+  const int levels = tt.levels;
+  const int64_t* hierarchy = tt.hierarchy;
+  const double* distances = tt.distances;
   GIM_CHECK(levels >= 1 && levels <= GIM_MAX_LEVELS, GIM_E_INVALID,
             "hierarchy must have 1.." + std::to_string(GIM_MAX_LEVELS) + " levels");
   std::vector<long long> key;
   long long k = 1;
   for (int i = 0; i < levels; ++i) {
     GIM_CHECK(hierarchy[i] >= 1, GIM_E_INVALID, "hierarchy factors must be >= 1");
-    GIM_CHECK(distances[i] >= 0, GIM_E_INVALID, "distances must be nonnegative");
+    GIM_CHECK(distances[i] >= 0 && std::isfinite(distances[i]), GIM_E_INVALID,
+              "distances must be nonnegative");
     if (i) GIM_CHECK(distances[i] >= distances[i - 1], GIM_E_INVALID,
                      "distances must be nondecreasing");
     k *= hierarchy[i];
     GIM_CHECK(k < (1ll << 30), GIM_E_OVERFLOW, "k too large for int32 block ids");
+    long long dk;
+    std::memcpy(&dk, &distances[i], sizeof(dk));
     key.push_back(hierarchy[i]);
-    key.push_back(distances[i]);
+    key.push_back(dk);
   }
   int dev = 0;
   GIM_CUDA(cudaGetDevice(&dev));
@@ -245,15 +279,22 @@ Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances) {
   std::lock_guard<std::mutex> lk(g_topo_mu);
   auto it = g_topo_cache.find(key);
   if (it != g_topo_cache.end()) return it->second;
+  int dshift = 0, exact = 1;
+  topo_scale(levels, distances, &dshift, &exact);
   // bit field layout: level 0 (least significant digit) in the low bits
   int shift[GIM_MAX_LEVELS];
   int bits = 0;
   std::vector<long long> dbit(64, 0);
+  std::vector<double> dbitf(64, 0.0);
   for (int i = 0; i < levels; ++i) {
     int wdt = 0;
     while ((1ll << wdt) < hierarchy[i]) ++wdt;
     shift[i] = bits;
-    for (int b = bits; b < bits + wdt && b < 64; ++b) dbit[b] = distances[i];
+    const long long di = (long long)std::llround(std::ldexp(distances[i], dshift));
+    for (int b = bits; b < bits + wdt && b < 64; ++b) {
+      dbit[b] = di;
+      dbitf[b] = distances[i];
+    }
     bits += wdt;
   }
   GIM_CHECK(bits <= 64, GIM_E_UNSUPPORTED, "hierarchy digit codes exceed 64 bits");
@@ -268,25 +309,32 @@ Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances) {
     code[(size_t)b] = c;
   }
   void* p = nullptr;
-  size_t bytes = sizeof(unsigned long long) * (size_t)k + sizeof(long long) * 64;
+  const size_t cb = sizeof(unsigned long long) * (size_t)k;
+  size_t bytes = cb + sizeof(long long) * 64 + sizeof(double) * 64;
   GIM_CUDA(cudaMalloc(&p, bytes));
-  GIM_CUDA(cudaMemcpy(p, code.data(), sizeof(unsigned long long) * (size_t)k,
+  GIM_CUDA(cudaMemcpy(p, code.data(), cb, cudaMemcpyHostToDevice));
+  GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + cb, dbit.data(), sizeof(long long) * 64,
                       cudaMemcpyHostToDevice));
-  GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + sizeof(unsigned long long) * (size_t)k,
-                      dbit.data(), sizeof(long long) * 64, cudaMemcpyHostToDevice));
+  GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + cb + sizeof(long long) * 64, dbitf.data(),
+                      sizeof(double) * 64, cudaMemcpyHostToDevice));
   Topo t;
   t.L = levels;
   t.k = (int)k;
+  t.dshift = dshift;
+  t.exact = exact;
   t.code = static_cast<const unsigned long long*>(p);
-  t.dbit = reinterpret_cast<const long long*>(static_cast<char*>(p) +
-                                              sizeof(unsigned long long) * (size_t)k);
+  t.dbit = reinterpret_cast<const long long*>(static_cast<char*>(p) + cb);
+  t.dbitf = reinterpret_cast<const double*>(static_cast<char*>(p) + cb + sizeof(long long) * 64);
   g_topo_cache.emplace(key, t);
   return t;
 }
 
 Topo get_flat_topo(int k) {
-  int64_t h[1] = {k}, d[1] = {1};
-  return get_topo(1, h, d);
+  gim_topology t{};
+  t.levels = 1;
+  t.hierarchy[0] = k;
+  t.distances[0] = 1.0;
+  return get_topo(t);
 }
 
 // one-time pool configuration: keep freed blocks cached (no OS round trips
@@ -434,3 +482,14 @@ extern "C" int gim_version(void) {
 }
 
 extern "C" const char* gim_last_error(void) { return gim::last_error(); }
+
+extern "C" int gim_topology_scale(const gim_topology* t, int32_t* shift_out, int32_t* exact_out) {
+  return gim::guard([&] {
+    GIM_CHECK(t && shift_out && exact_out, GIM_E_INVALID, "null argument");
+    GIM_CHECK(t->levels >= 1 && t->levels <= GIM_MAX_LEVELS, GIM_E_INVALID, "bad levels");
+    int s = 0, e = 1;
+    gim::topo_scale(t->levels, t->distances, &s, &e);
+    *shift_out = s;
+    *exact_out = e;
+  });
+}

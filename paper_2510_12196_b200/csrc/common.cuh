@@ -70,16 +70,23 @@ int guard(F&& body) {
 // the highest differing digit, and dbit[bit] holds that level's distance.
 // Both tables live in one small device array (L1-resident), built once per
 // topology by get_topo() — two cached loads + xor + clz per distance.
+// Non-integral distances (topology.py:56-58) are carried as d * 2^dshift
+// in int64 (exact for dyadic d); dbitf holds the caller's float distances per
+// bit for the float64 J.
 struct Topo {
   int L;                                // hierarchy levels
   int k;                                // number of PEs
+  int dshift;                           // distance scale 2^dshift
+  int exact;                            // 1: d * 2^dshift is exactly integral
   const unsigned long long* code;       // [k]
   const long long* dbit;                // [64]
+  const double* dbitf;                  // [64] the caller's distances
 };
 
-// cached per (hierarchy, distances); device tables are never freed
-Topo get_topo(int levels, const int64_t* hierarchy, const int64_t* distances);
+// cached per (device, hierarchy, distances); device tables are never freed
+Topo get_topo(const gim_topology& t);
 Topo get_flat_topo(int k);
+void topo_scale(int levels, const double* d, int* shift, int* exact);
 
 __device__ __forceinline__ long long dist(const Topo& t, int x, int y) {
   unsigned long long c = __ldg(t.code + x) ^ __ldg(t.code + y);

@@ -14,6 +14,8 @@
 #include <cmath>
 #include <exception>
 #include <thread>
+#include <queue>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -846,7 +848,7 @@ static void internal_partitioner_batch(std::vector<BatchPartJob>& jobs, int part
 // hierarchical multisection (pipelines.py:49-110)
 
 struct MsCtx {
-  std::vector<long long> h, d;
+  std::vector<long long> h;  // the multisection only needs the hierarchy
   long long k;
   long long total;
   double eps;
@@ -1138,13 +1140,12 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
 
 static void hierarchical_multisection(const DevGraph& g, long long total,
                                       const std::vector<long long>& h,
-                                      const std::vector<long long>& d, double eps,
+                                      double eps,
                                       unsigned long long seed, int* assignment, RunStats& st,
                                       cudaStream_t s) {
   GIM_CHECK(g.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
   MsCtx C;
   C.h = h;
-  C.d = d;
   C.k = 1;
   for (long long a : h) C.k *= a;
   C.total = total;
@@ -1172,21 +1173,22 @@ struct ImTimes {
   cudaEvent_t e[4];
 };
 
+// `l_max_in` >= 0: the caller's L_max (isolated-vertex strip mode maps the
+// reduced graph against the full graph's L_max)
 static void integrated_map_device(const DevGraph& g0, long long total, const gim_topology& tt,
                                   double eps, unsigned long long seed, const gim_im_params& P,
                                   int* out_part, long long* out_bw, gim_im_stats* stats,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, double l_max_in = -1.0) {
   GIM_CHECK(g0.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
-  Topo t = get_topo(tt.levels, tt.hierarchy, tt.distances);
+  Topo t = get_topo(tt);
   std::vector<long long> h(tt.hierarchy, tt.hierarchy + tt.levels);
-  std::vector<long long> d(tt.distances, tt.distances + tt.levels);
   const long long k = t.k;
   RunStats st;
   reset_launches();
   cudaEvent_t ev[4];
   for (auto& e : ev) GIM_CUDA(cudaEventCreate(&e));
   GIM_CUDA(cudaEventRecord(ev[0], s));
-  const double l_max = (1.0 + eps) * (double)total / (double)k;
+  const double l_max = l_max_in >= 0.0 ? l_max_in : (1.0 + eps) * (double)total / (double)k;
   std::vector<Level> levels = build_level_stack(
       g0, l_max, std::max<long long>(P.coarsest_factor * k, 1), seed, s);
   const int nl = (int)levels.size();
@@ -1198,7 +1200,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   GIM_CUDA(cudaEventRecord(ev[1], s));
   DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
   st.in_initial = true;
-  hierarchical_multisection(levels.back().g, levels.size() == 1 ? total : total, h, d, eps,
+  hierarchical_multisection(levels.back().g, total, h, eps,
                             hash2(seed, 7, 7), cur.get(), st, s);
   st.in_initial = false;
   GIM_CUDA(cudaEventRecord(ev[2], s));
@@ -1243,6 +1245,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     cudaEventElapsedTime(&c, ev[2], ev[3]);
     cudaEventElapsedTime(&tot, ev[0], ev[3]);
     stats->n_levels = nl;
+    stats->isolated_vertices = 0;
     for (int i = 0; i < 64; ++i) {
       stats->level_n[i] = i < nl ? level_n[i] : 0;
       stats->level_m2[i] = i < nl ? level_m2[i] : 0;
@@ -1290,6 +1293,15 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
     DBuf<long long> dj(1, s);
     total_cost(g0, out_part, t, dj.get(), s);
     stats->final_j = read_scalar(dj.get(), s);
+    stats->dist_shift = t.dshift;
+    stats->dist_exact = t.exact;
+    if (t.exact) {
+      stats->final_j_f64 = std::ldexp((double)stats->final_j, -t.dshift);
+    } else {
+      DBuf<double> djf(1, s);
+      total_cost_f64(g0, out_part, t, djf.get(), s);
+      stats->final_j_f64 = read_scalar(djf.get(), s);
+    }
     std::vector<long long> bw((size_t)k);
     GIM_CUDA(cudaMemcpy(bw.data(), out_bw, sizeof(long long) * k, cudaMemcpyDeviceToHost));
     long long mx = 0;
@@ -1298,6 +1310,169 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (auto& e : lev) cudaEventDestroy(e);
+}
+
+// ---------------------------------------------------------------------------
+// isolated-vertex strip mode (gim_im_params.isolated, include/gpuim.h)
+
+__global__ void k_isolated_flag(int n, const int* __restrict__ off, int* __restrict__ flag) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    flag[v] = off[v + 1] == off[v];
+}
+
+// isolated vertex of rank r (vertex order) -> the block whose fill range
+// [start[b], start[b+1]) holds r
+__global__ void k_fill_isolated(int n_iso, const int* __restrict__ ids,
+                                const int* __restrict__ start, int k, int* __restrict__ part) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_iso; r += gridDim.x * blockDim.x) {
+    int lo = 0, hi = k;  // last b with start[b] <= r
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (start[mid] <= r) lo = mid;
+      else hi = mid;
+    }
+    part[ids[r]] = lo;
+  }
+}
+
+// Water-filling of `cnt` equal weights `w0` into blocks of weights bw: the
+// lowest level T with sum_b max(0, floor((T - bw_b) / w0)) >= cnt, ties of
+// the last unit to the lowest block ids.  Returns the per-block counts.
+static std::vector<long long> water_fill(const std::vector<long long>& bw, long long cnt,
+                                         long long w0) {
+  const size_t k = bw.size();
+  auto units = [&](long long T) {
+    long long u = 0;
+    for (long long b : bw) u += T > b ? (T - b) / w0 : 0;
+    return u;
+  };
+  long long lo = *std::min_element(bw.begin(), bw.end()), hi = lo + (cnt + 1) * w0;
+  while (lo < hi) {  // minimal T with units(T) >= cnt
+    const long long mid = lo + (hi - lo) / 2;
+    if (units(mid) >= cnt) hi = mid;
+    else lo = mid + 1;
+  }
+  std::vector<long long> c(k);
+  long long used = 0;
+  for (size_t b = 0; b < k; ++b) {
+    c[b] = lo - 1 > bw[b] ? (lo - 1 - bw[b]) / w0 : 0;
+    used += c[b];
+  }
+  for (size_t b = 0; b < k && used < cnt; ++b) {
+    const long long at_T = lo > bw[b] ? (lo - bw[b]) / w0 : 0;
+    if (at_T > c[b]) {
+      c[b] += 1;
+      ++used;
+    }
+  }
+  return c;
+}
+
+static void integrated_map_dispatch(const DevGraph& g0, long long total, const gim_topology& tt,
+                                    double eps, unsigned long long seed, const gim_im_params& P,
+                                    int* out_part, long long* out_bw, gim_im_stats* stats,
+                                    cudaStream_t s) {
+  integrated_map_device(g0, total, tt, eps, seed, P, out_part, out_bw, stats, s);
+}
+
+static void integrated_map_strip(const DevGraph& g0, long long total, const gim_topology& tt,
+                                 double eps, unsigned long long seed, const gim_im_params& P,
+                                 int* out_part, long long* out_bw, gim_im_stats* stats,
+                                 cudaStream_t s) {
+  Topo t = get_topo(tt);
+  const int k = t.k;
+  const int n = g0.n;
+  DBuf<int> flag((size_t)n, s);
+  k_isolated_flag<<<grid_for(n, 256), 256, 0, s>>>(n, g0.off, flag.get());
+  count_launch();
+  GIM_LAUNCH_CHECK();
+  std::vector<OwnedGraph> subs;
+  std::vector<DBuf<int>> ids;
+  extract_subgraphs(g0, flag.get(), 2, subs, ids, s);  // 0: with edges, 1: isolated
+  const OwnedGraph& R = subs[0];
+  const int n_iso = subs[1].n;
+  const double l_max = (1.0 + eps) * (double)total / (double)k;
+  gim_im_params Q = P;
+  Q.isolated = GIM_ISOLATED_KEEP;
+  if (n_iso == 0 || R.n == 0) {  // nothing to strip / nothing but isolated vertices
+    if (R.n == 0) {
+      GIM_CUDA(cudaMemsetAsync(out_part, 0, sizeof(int) * n, s));
+    } else {
+      integrated_map_device(g0, total, tt, eps, seed, Q, out_part, out_bw, stats, s);
+      return;
+    }
+  } else {
+    long long total_r = 0;
+    {
+      DBuf<long long> d(1, s);
+      GIM_CUDA(cudaMemsetAsync(d.get(), 0, sizeof(long long), s));
+      k_sum_vw<<<grid_for(R.n, 256, kSMs * 2), 256, 0, s>>>(R.n, R.vw.get(), d.get());
+      count_launch();
+      total_r = read_scalar(d.get(), s);
+    }
+    DBuf<int> rp((size_t)R.n, s);
+    integrated_map_device(R.view(), total_r, tt, eps, seed, Q, rp.get(), out_bw, stats, s, l_max);
+    leaf_scatter(R.n, ids[0].get(), rp.get(), 0, out_part, s);
+  }
+  if (n_iso > 0) {
+    // water-fill the isolated vertices into the lightest blocks
+    std::vector<long long> bw((size_t)k, 0);
+    if (R.n > 0)
+      GIM_CUDA(cudaMemcpyAsync(bw.data(), out_bw, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+    std::vector<int> iw((size_t)n_iso);
+    GIM_CUDA(cudaMemcpyAsync(iw.data(), subs[1].vw.get(), sizeof(int) * n_iso,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    const bool equal = std::all_of(iw.begin(), iw.end(), [&](int x) { return x == iw[0]; });
+    if (equal) {  // unit (equal) weights: per-block counts, rank ranges on the device
+      std::vector<long long> c = water_fill(bw, n_iso, iw[0]);
+      std::vector<int> start((size_t)k + 1, 0);
+      for (int b = 0; b < k; ++b) start[(size_t)b + 1] = start[(size_t)b] + (int)c[(size_t)b];
+      DBuf<int> ds((size_t)k + 1, s);
+      GIM_CUDA(cudaMemcpyAsync(ds.get(), start.data(), sizeof(int) * (k + 1),
+                               cudaMemcpyHostToDevice, s));
+      k_fill_isolated<<<grid_for(n_iso, 256), 256, 0, s>>>(n_iso, ids[1].get(), ds.get(), k,
+                                                           out_part);
+      count_launch();
+      GIM_LAUNCH_CHECK();
+      GIM_CUDA(sync_stream(s));
+    } else {  // general weights: heaviest first into the current lightest block (LPT)
+      std::vector<int> order((size_t)n_iso), blk((size_t)n_iso);
+      for (int i = 0; i < n_iso; ++i) order[(size_t)i] = i;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return iw[(size_t)a] > iw[(size_t)b]; });
+      using Q2 = std::pair<long long, int>;
+      std::priority_queue<Q2, std::vector<Q2>, std::greater<Q2>> heap;
+      for (int b = 0; b < k; ++b) heap.push({bw[(size_t)b], b});
+      for (int i : order) {
+        auto top = heap.top();
+        heap.pop();
+        blk[(size_t)i] = top.second;
+        top.first += iw[(size_t)i];
+        heap.push(top);
+      }
+      DBuf<int> db((size_t)n_iso, s);
+      GIM_CUDA(cudaMemcpyAsync(db.get(), blk.data(), sizeof(int) * n_iso, cudaMemcpyHostToDevice,
+                               s));
+      leaf_scatter(n_iso, ids[1].get(), db.get(), 0, out_part, s);
+      GIM_CUDA(sync_stream(s));
+    }
+  }
+  block_weights(n, g0.vw, out_part, k, out_bw, s);
+  if (stats) {
+    std::vector<long long> bw((size_t)k);
+    GIM_CUDA(cudaMemcpyAsync(bw.data(), out_bw, sizeof(long long) * k, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    stats->max_block_weight = *std::max_element(bw.begin(), bw.end());
+    stats->l_max = l_max;
+    stats->isolated_vertices = n_iso;
+    if (R.n == 0) {  // no IM run filled the stats
+      stats->n_levels = 0;
+      stats->final_j = 0;
+      stats->final_j_f64 = 0.0;
+      stats->kernel_launches = launches();
+    }
+  }
 }
 
 // host-array upload (graph.py:17-39 int64 CSR) -> int32 device level
@@ -1518,6 +1693,7 @@ static gim_im_params default_params() {
   p.sigma_fine = 0.005;
   p.iw_max_finest = 10;
   p.run_flags = GIM_RUN_DEFAULT;
+  p.isolated = GIM_ISOLATED_KEEP;
   return p;
 }
 
@@ -1609,7 +1785,7 @@ extern "C" int gim_lp_pass(const gim_graph* g, const int32_t* assignment, const 
   return guard([&] {
     GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     RefineLevel L;
     L.g = view(*g);
     prepare_level(L, tp.k, s);
@@ -1647,7 +1823,7 @@ extern "C" int gim_rebalance(const gim_graph* g, const int32_t* assignment,
     GIM_CHECK(g && t && block_weights, GIM_E_INVALID, "null argument");
     GIM_CHECK(rho >= 1, GIM_E_INVALID, "rho must be >= 1");
     cudaStream_t s = (cudaStream_t)stream;
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     const int k = tp.k;
     std::vector<long long> bw((size_t)k);
     GIM_CUDA(cudaMemcpyAsync(bw.data(), block_weights, sizeof(long long) * k,
@@ -1690,7 +1866,7 @@ extern "C" int gim_apply_moves(const gim_graph* g, int32_t* assignment, int64_t*
   return guard([&] {
     GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     RefineLevel L;
     L.g = view(*g);
     prepare_level(L, tp.k, s);
@@ -1713,7 +1889,7 @@ extern "C" int gim_refine(const gim_graph* g, const gim_topology* t, int32_t* as
   return guard([&] {
     GIM_CHECK(g && t, GIM_E_INVALID, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     RefineLevel L;
     L.g = view(*g);
     RefCfg c;
@@ -1760,15 +1936,14 @@ extern "C" int gim_hierarchical_multisection(const gim_graph* g, const gim_topol
     cudaStream_t s = (cudaStream_t)stream;
     DevGraph dg = view(*g);
     GIM_CHECK(dg.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
-    (void)get_topo(t->levels, t->hierarchy, t->distances);
+    (void)get_topo(*t);
     long long total = total_vertex_weight(dg, s);
     std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
-    std::vector<long long> d(t->distances, t->distances + t->levels);
     RunStats st;
     RunCtx rc;
     rc.f = default_flags();
     CtxScope scope(&rc);
-    hierarchical_multisection(dg, total, h, d, eps, seed, assignment, st, s);
+    hierarchical_multisection(dg, total, h, eps, seed, assignment, st, s);
     GIM_CUDA(sync_stream(s));
   });
 }
@@ -1792,14 +1967,13 @@ extern "C" int gim_hierarchical_multisection_host(int64_t n, const int64_t* offs
     CtxScope scope(&rc);
     OwnedGraph G;
     upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
-    std::vector<long long> d(t->distances, t->distances + t->levels);
     DBuf<int> part((size_t)n, s);
     DBuf<long long> bw((size_t)tp.k, s);
     RunStats st;
     reset_launches();
-    hierarchical_multisection(G.view(), G.total_vw, h, d, eps, seed, part.get(), st, s);
+    hierarchical_multisection(G.view(), G.total_vw, h, eps, seed, part.get(), st, s);
     block_weights((int)n, G.vw.get(), part.get(), tp.k, bw.get(), s);
     int* h_part = static_cast<int*>(pinned_scratch(sizeof(int) * (size_t)n));
     GIM_CUDA(cudaMemcpyAsync(h_part, part.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
@@ -1824,7 +1998,8 @@ extern "C" int gim_integrated_map_device(const gim_graph* g, const gim_topology*
     rc.f = flags_of(&P);
     CtxScope scope(&rc);
     long long total = total_vertex_weight(dg, s);
-    integrated_map_device(dg, total, *t, eps, seed, P, out_assignment,
+    (P.isolated == GIM_ISOLATED_STRIP ? integrated_map_strip : integrated_map_dispatch)(
+        dg, total, *t, eps, seed, P, out_assignment,
                           reinterpret_cast<long long*>(out_block_weights), stats, s);
   });
 }
@@ -1849,10 +2024,11 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
     GIM_CUDA(sync_stream(s));
     const double ms_up =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_up).count();
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     DBuf<int> part((size_t)n, s);
     DBuf<long long> bw((size_t)tp.k, s);
-    integrated_map_device(G.view(), G.total_vw, *t, eps, seed, P, part.get(), bw.get(), stats, s);
+    (P.isolated == GIM_ISOLATED_STRIP ? integrated_map_strip : integrated_map_dispatch)(
+        G.view(), G.total_vw, *t, eps, seed, P, part.get(), bw.get(), stats, s);
     const auto t_down = std::chrono::steady_clock::now();
     // int32 assignment -> pinned staging -> widened to int64 on the host by
     // worker threads (half the PCIe bytes, no pageable staging copy)

@@ -68,22 +68,36 @@ __device__ __forceinline__ void cta_argmax(int& a, int& b, int* sa, int* sb) {
   __syncthreads();
 }
 
+// Level-synchronous multi-source BFS (pipelines.py:113-130).  Race-free: a
+// round first READS dist and marks the next frontier in the bitmap `nxt`
+// (ceil(n/32) words, zero on entry and on exit) with atomicOr, then each
+// bitmap word's owner thread writes dist and clears the word.
 __device__ void cta_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
-                        int ns) {
+                        int ns, unsigned* nxt) {
   for (int v = threadIdx.x; v < n; v += blockDim.x) dist[v] = -1;
   __syncthreads();
   for (int i = threadIdx.x; i < ns; i += blockDim.x) dist[seeds[i]] = 0;
   __syncthreads();
+  const int nw = (n + 31) >> 5;
   for (int d = 0;; ++d) {
-    int changed = 0;
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
       if (dist[v] != d) continue;
       for (int e = off[v]; e < off[v + 1]; ++e) {
-        int u = tgt[e];
-        if (dist[u] < 0) {
-          dist[u] = d + 1;  // benign race: every writer stores d + 1
-          changed = 1;
-        }
+        const int u = tgt[e];
+        if (dist[u] < 0) atomicOr(&nxt[u >> 5], 1u << (u & 31));
+      }
+    }
+    __syncthreads();
+    int changed = 0;
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) {
+      unsigned m = nxt[w];
+      if (!m) continue;
+      nxt[w] = 0;
+      changed = 1;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        dist[(w << 5) + b] = d + 1;
       }
     }
     if (!__syncthreads_or(changed)) break;
@@ -123,10 +137,12 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   int* part = dist + n;
   int* seeds = part + n;
   int* conn = seeds + k;
+  unsigned* nxt = reinterpret_cast<unsigned*>(conn + (size_t)k * n);  // BFS frontier bitmap
   if (k == 1) {
     for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
     return;
   }
+  for (int w = threadIdx.x; w < ((n + 31) >> 5); w += blockDim.x) nxt[w] = 0;
   // small graphs: CSR staged in shared memory (every growth step walks a row
   // and reads a vertex weight on its critical path)
   const int* g_off = J.off;
@@ -134,7 +150,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   const int* g_w = J.w;
   const int* g_vw = J.vw;
   if (J.stage) {
-    int* so = conn + (size_t)k * n;
+    int* so = reinterpret_cast<int*>(nxt) + ((n + 31) >> 5);
     int* st = so + n + 1;
     int* sw = st + J.m2;
     int* sv = sw + J.m2;
@@ -153,12 +169,12 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   // seeds (pipelines.py:143-153)
   if (threadIdx.x == 0) s_v = 0;
   __syncthreads();
-  cta_bfs(n, g_off, g_tgt, dist, &s_v, 1);
+  cta_bfs(n, g_off, g_tgt, dist, &s_v, 1, nxt);
   int sv = cta_pick_seed(n, dist, sa, sb);
   if (threadIdx.x == 0) seeds[0] = sv;
   __syncthreads();
   for (int ns = 1; ns < k; ++ns) {
-    cta_bfs(n, g_off, g_tgt, dist, seeds, ns);
+    cta_bfs(n, g_off, g_tgt, dist, seeds, ns, nxt);
     sv = cta_pick_seed(n, dist, sa, sb);
     if (threadIdx.x == 0) seeds[ns] = sv;
     __syncthreads();
@@ -692,7 +708,7 @@ static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector
   std::vector<size_t> words((size_t)J);
   for (int j = 0; j < J; ++j) {
     const DevGraph& g = gs[(size_t)j];
-    words[(size_t)j] = (size_t)2 * g.n + k + (size_t)k * g.n;
+    words[(size_t)j] = (size_t)2 * g.n + k + (size_t)k * g.n + ((size_t)g.n + 31) / 32;
     max_words = std::max(max_words, words[(size_t)j]);
     max_staged = std::max(max_staged, words[(size_t)j] + (size_t)g.n + 1 + 2 * (size_t)g.m2 + g.n);
   }

@@ -51,6 +51,45 @@ void total_cost(const DevGraph& g, const int* part, const Topo& t, long long* j_
   count_launch();
 }
 
+// J with the caller's float distances (mapping.py:76-91, float path when
+// Topology.integral_distances is false): per-slot w * d in float64, reduced
+// warp -> block -> one double atomic per CTA
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_total_cost_f64(long long m2, const int* __restrict__ src,
+                                                          const int* __restrict__ tgt,
+                                                          const int* __restrict__ w,
+                                                          const int* __restrict__ part, Topo t,
+                                                          double* __restrict__ out) {
+  __shared__ double red[BLOCK / 32];
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * BLOCK + threadIdx.x; e < m2;
+       e += (long long)gridDim.x * BLOCK) {
+    const unsigned long long c = __ldg(t.code + part[src[e]]) ^ __ldg(t.code + part[tgt[e]]);
+    if (c) acc += (double)w[e] * __ldg(t.dbitf + (63 - __clzll(c)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane_id() == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int i = 0; i < BLOCK / 32; ++i) x += red[i];
+    if (x != 0.0) atomicAdd(out, x);
+  }
+}
+
+void total_cost_f64(const DevGraph& g, const int* part, const Topo& t, double* j_out,
+                    cudaStream_t s) {
+  GIM_CUDA(cudaMemsetAsync(j_out, 0, sizeof(double), s));
+  if (g.m2 == 0) return;
+  ProfScope prof(P_JEVAL, 8.0 * g.n + 12.0 * g.m2, s);
+  constexpr int B = 256;
+  k_total_cost_f64<B><<<grid_for(g.m2, B, kSMs * 8), B, 0, s>>>(g.m2, g.src, g.tgt, g.w, part,
+                                                                 t, j_out);
+  GIM_LAUNCH_CHECK();
+  count_launch();
+}
+
 // block weights: per-CTA shared histogram (k <= kSmemBins) with
 // warp-aggregated shared atomics, one global atomic per (CTA, nonzero bin)
 constexpr int kSmemBins = 8192;
@@ -119,9 +158,18 @@ extern "C" int gim_total_cost(const gim_graph* g, const int32_t* assignment,
                               const gim_topology* t, int64_t* j_out, void* stream) {
   return guard([&] {
     GIM_CHECK(g && t && j_out, GIM_E_INVALID, "null argument");
-    Topo tp = get_topo(t->levels, t->hierarchy, t->distances);
+    Topo tp = get_topo(*t);
     total_cost(view(*g), assignment, tp, reinterpret_cast<long long*>(j_out),
                (cudaStream_t)stream);
+  });
+}
+
+extern "C" int gim_total_cost_f64(const gim_graph* g, const int32_t* assignment,
+                                  const gim_topology* t, double* j_out, void* stream) {
+  return guard([&] {
+    GIM_CHECK(g && t && j_out, GIM_E_INVALID, "null argument");
+    Topo tp = get_topo(*t);
+    total_cost_f64(view(*g), assignment, tp, j_out, (cudaStream_t)stream);
   });
 }
 

@@ -55,6 +55,8 @@ struct OwnedGraph {
 // ---- jeval.cu
 void total_cost(const DevGraph& g, const int* part, const Topo& t, long long* j_out,
                 cudaStream_t s);
+void total_cost_f64(const DevGraph& g, const int* part, const Topo& t, double* j_out,
+                    cudaStream_t s);
 void block_weights(int n, const int* vw, const int* part, int k, long long* bw,
                    cudaStream_t s);
 

@@ -276,14 +276,14 @@ struct RbFlag {
 struct RbKeyOut {
   RbFlag f;
   const long long* gain;
-  int rho, k, strong;
+  int rho, k, strong, dshift;
   unsigned int* keys;
   int* vals;
   __device__ void operator()(long long v, int pos) const {
     if (!f(v)) return;
     int src = f.part[v];
     int tb = f.target[v];
-    unsigned cell = (unsigned)(slot_for_gain(gain[v]) * rho + (int)(v % rho));
+    unsigned cell = (unsigned)(slot_for_gain(gain[v], dshift) * rho + (int)(v % rho));
     unsigned ncell = 31u * (unsigned)rho;
     unsigned key = strong ? ((unsigned)tb * ncell + cell) * (unsigned)k + (unsigned)src
                           : (unsigned)src * ncell + cell;
@@ -412,7 +412,7 @@ void prepare_level(RefineLevel& L, int k, cudaStream_t s) {
 void lp_pass(const RefineLevel& L, const Topo& t, const int* part, const unsigned char* locked,
              int jet, double jet_c, RefineBuffers& rb, cudaStream_t s) {
   const DevGraph& g = L.g;
-  LpParams lp{locked, jet, jet_c};
+  LpParams lp{locked, jet, jet_c, t.dshift};
   LpOut lo{rb.cand.get(), rb.dest.get(), rb.gkey.get()};
   RbParams rp{};
   RbOut ro{};
@@ -443,7 +443,7 @@ void rebalance_pass(const RefineLevel& L, const Topo& t, const int* part, const 
   launch_eval(L, 1, t, part, lp, lo, rp, ro, rb.ctr.get(), s);
   // compaction in vertex order + keys
   RbFlag f{part, ovl, rb.dest2.get()};
-  RbKeyOut ko{f, rb.gkey.get(), rho, k, strong ? 1 : 0, rb.rkeys.get(), rb.rvals.get()};
+  RbKeyOut ko{f, rb.gkey.get(), rho, k, strong ? 1 : 0, t.dshift, rb.rkeys.get(), rb.rvals.get()};
   exclusive_scan<int>(g.n, f, ko, rb.count.get(), s);
   int cnt = 0;
   GIM_CUDA(cudaMemcpyAsync(&cnt, rb.count.get(), sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -307,6 +307,7 @@ __device__ __forceinline__ int warp_build_table(const WarpTable& wt, int k, int 
                                                 const int* __restrict__ w,
                                                 const int* __restrict__ part) {
   const int lane = lane_id();
+  __syncwarp();  // every lane is done reading the previous vertex's table
   for (int i = lane; i < k; i += 32) wt.tab[i] = 0;
   __syncwarp();
   for (int e = e0 + lane; e < e1; e += 32) atomicAdd(&wt.tab[part[tgt[e]]], w[e]);
@@ -384,14 +385,22 @@ struct LpParams {
   const unsigned char* locked;  // null = no locks
   int jet;
   double jet_c;
+  int dshift;  // distances scaled by 2^dshift (Topo::dshift)
 };
+
+// Jet filter (refinement.py:236-240): -gain < floor(c * conn(v, own)); gains
+// carry the 2^dshift distance scale, conn is a weight
+__device__ __forceinline__ bool jet_admits(long long gain, long long conn_own, double c,
+                                          int dshift) {
+  return (double)(-gain) < ldexp(floor(c * (double)conn_own), dshift);
+}
 
 __device__ __forceinline__ void lp_decide(int v, int own, const VertexEval& r,
                                           const LpParams& p, const LpOut& o) {
   bool ok = false;
   if (r.best_b >= 0) {
     if (r.best_gain >= 0) ok = true;
-    else if (p.jet) ok = (double)(-r.best_gain) < floor(p.jet_c * (double)r.conn_own);
+    else if (p.jet) ok = jet_admits(r.best_gain, r.conn_own, p.jet_c, p.dshift);
   }
   o.cand[v] = ok ? 1 : 0;
   o.dest[v] = ok ? r.best_b : own;
@@ -424,6 +433,12 @@ __device__ __forceinline__ int slot_for_gain(long long g) {
   if (x < 100) return 10 + (int)(x / 10);
   if (x < 1000) return 19 + (int)(x / 100);
   return 30;
+}
+
+// the same bucket for a gain in units of 2^-sh (scaled distances): the slot
+// bounds are integers b, and b * 2^sh <= -g  <=>  b <= floor(-g / 2^sh)
+__device__ __forceinline__ int slot_for_gain(long long g, int sh) {
+  return slot_for_gain(g > 0 ? g : -((-g) >> sh));
 }
 
 }  // namespace gim

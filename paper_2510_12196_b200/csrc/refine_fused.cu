@@ -314,7 +314,7 @@ __device__ __forceinline__ void hub_eval_one(const FusedArgs& A, int u, int sz, 
     bool ok = false;
     if (q.best_b >= 0) {
       if (q.best_gain >= 0) ok = true;
-      else if (A.jet) ok = (double)(-q.best_gain) < floor(A.jet_c * (double)q.conn_own);
+      else if (A.jet) ok = jet_admits(q.best_gain, q.conn_own, A.jet_c, A.t.dshift);
     }
     if (ok && lane == 0) {
       A.dest[u] = q.best_b;
@@ -342,7 +342,7 @@ __device__ __forceinline__ void hub_eval_one(const FusedArgs& A, int u, int sz, 
     }
     if (target >= 0 && lane == 0) {
       A.rtgt[u] = target;
-      const int cell = slot_for_gain(gain) * A.rho + u % A.rho;
+      const int cell = slot_for_gain(gain, A.t.dshift) * A.rho + u % A.rho;
       A.rcell[u] = (unsigned char)cell;
       atomicAdd(reinterpret_cast<unsigned long long*>(&A.W[(size_t)ou * NC + cell]),
                 (unsigned long long)(long long)A.vw[u]);
@@ -661,7 +661,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         bool ok = false;
         if (live && r.best_b >= 0) {
           if (r.best_gain >= 0) ok = true;
-          else if (A.jet) ok = (double)(-r.best_gain) < floor(A.jet_c * (double)r.conn_own);
+          else if (A.jet) ok = jet_admits(r.best_gain, r.conn_own, A.jet_c, A.t.dshift);
         }
         if (ok) {
           A.dest[v] = r.best_b;
@@ -839,7 +839,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         unsigned vwv = 0;
         if (isc) {
           A.rtgt[v] = target;
-          const int cell = slot_for_gain(gain) * A.rho + v % A.rho;
+          const int cell = slot_for_gain(gain, A.t.dshift) * A.rho + v % A.rho;
           A.rcell[v] = (unsigned char)cell;
           wkey = own * NC + cell;
           vwv = (unsigned)A.vw[v];

@@ -40,10 +40,22 @@ def _u8(x, device) -> torch.Tensor:
 
 
 def topology_struct(hierarchy, distances) -> _lib.GimTopology:
-    if not all(isinstance(d, (int, np.integer)) for d in distances):
-        raise NotImplementedError(
-            "the GPU path implements integral distances (Topology.integral_distances)")
+    """gim_topology of a (hierarchy, distances) pair; non-integral distances
+    run as d * 2^s device integers (include/gpuim.h)."""
     return _lib.topology_struct(hierarchy, distances)
+
+
+def integral_distances(distances) -> bool:
+    """topology.py:56-58: J and gains are Python ints iff every d is an int."""
+    return all(isinstance(d, (int, np.integer)) for d in distances)
+
+
+def topology_scale(hierarchy, distances) -> tuple[int, bool]:
+    """(s, exact): the device carries d * 2^s (exact for dyadic d)."""
+    t = topology_struct(hierarchy, distances)
+    sh, ex = C.c_int32(0), C.c_int32(0)
+    _lib.call("gim_topology_scale", C.byref(t), C.byref(sh), C.byref(ex))
+    return sh.value, bool(ex.value)
 
 
 class DeviceGraph:
@@ -115,11 +127,18 @@ class DeviceGraph:
 # ---------------------------------------------------------------------------
 # objective (mapping.py:38-91)
 
-def total_cost(dg: DeviceGraph, assignment, hierarchy, distances) -> int:
+def total_cost(dg: DeviceGraph, assignment, hierarchy, distances):
+    """mapping.py:76-91: exact int J for integral distances, else float J
+    (float64 with the caller's distances)."""
     a = _i32(assignment, dg.device)
-    out = torch.empty(1, dtype=torch.int64, device=dg.device)
     t = topology_struct(hierarchy, distances)
     g = dg.struct()
+    if not integral_distances(distances):
+        out = torch.empty(1, dtype=torch.float64, device=dg.device)
+        _lib.call("gim_total_cost_f64", C.byref(g), _ptr(a), C.byref(t), out.data_ptr(),
+                  stream_ptr(dg.device))
+        return float(out.item())
+    out = torch.empty(1, dtype=torch.int64, device=dg.device)
     _lib.call("gim_total_cost", C.byref(g), _ptr(a), C.byref(t), out.data_ptr(),
               stream_ptr(dg.device))
     return int(out.item())
@@ -312,7 +331,7 @@ def run_flags(fused=True, rowwise=True, batch=True, fanout=True, profile=False) 
 
 def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", jet_filter_c=0.25,
                   sigma_coarse=0.065, sigma_fine=0.005, iw_max_finest=10,
-                  run_flags: int = -1) -> _lib.GimImParams:
+                  run_flags: int = -1, isolated_vertices: str = "keep") -> _lib.GimImParams:
     p = _lib.GimImParams()
     p.coarsest_factor = int(coarsest_factor)
     p.phi = float(phi)
@@ -323,6 +342,9 @@ def params_struct(coarsest_factor=128, phi=0.999, rho=2, filter_mode="nonneg", j
     p.sigma_fine = float(sigma_fine)
     p.iw_max_finest = int(iw_max_finest)
     p.run_flags = int(run_flags)
+    if isolated_vertices not in ("keep", "strip"):
+        raise ValueError(f"isolated_vertices must be 'keep' or 'strip', got {isolated_vertices!r}")
+    p.isolated = 1 if isolated_vertices == "strip" else 0
     return p
 
 

@@ -15,6 +15,8 @@ ap.add_argument("--rmat-scale", type=int, default=22)
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--profile", action="store_true", help="serialised per-class device times")
+ap.add_argument("--isolated", nargs="+", default=["keep"], choices=["keep", "strip"],
+                help="isolated-vertex modes to run (R-MAT: strip = tolerance-parity mode)")
 args = ap.parse_args()
 D.set_profiling(args.profile)
 for w in args.which:
@@ -27,12 +29,13 @@ for w in args.which:
         h, d = (4, 16, 8), (1, 10, 100)
     print(f"{w}: n={g.n} m={g.m} gen {time.time() - t0:.1f}s", flush=True)
     dg = D.DeviceGraph.from_host(g)
-    for r in range(args.reps):
+    for iso, r in [(i, r) for i in args.isolated for r in range(args.reps)]:
         torch.cuda.synchronize()
         t0 = time.time()
-        a, bw, st = D.integrated_map_device(dg, h, d, 0.03, r)
+        a, bw, st = D.integrated_map_device(dg, h, d, 0.03, r, isolated_vertices=iso)
         torch.cuda.synchronize()
-        print(json.dumps({"cfg": w, "rep": r, "wall_ms": (time.time() - t0) * 1e3,
+        print(json.dumps({"cfg": w, "isolated": iso, "rep": r, "wall_ms": (time.time() - t0) * 1e3,
+                          "isolated_vertices": st["isolated_vertices"],
                           "J": st["final_j"], "maxw": st["max_block_weight"],
                           "l_max": st["l_max"], "balanced": st["max_block_weight"] <= st["l_max"],
                           "levels": st["n_levels"], "level_n": st["level_n"],
