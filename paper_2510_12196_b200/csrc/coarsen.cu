@@ -107,33 +107,54 @@ __global__ void __launch_bounds__(BLOCK) k_hem_mutual(int n, const int* __restri
 constexpr int kHemTpv = 32;
 constexpr int kHemHuge = 1024;
 
-// per-vertex round data, one 16-byte gather per candidate: c_u (-1 when u
-// is matched) and S_u = splitmix64(seed ^ splitmix64(u)), the first two
-// stages of hash2(seed, a, b) = splitmix64(S_a ^ b) for a = min(v, u)
-struct __align__(16) HemV {
-  unsigned long long s;
-  int c;
-  int pad;
-};
+// Per-round eligibility: elig[u] = c_u for unmatched u, -1 for matched u —
+// ONE 4-byte gather per candidate slot (the array stays L2-resident: 16.8 MB
+// at 2^22).  The tie-break hash2(seed, min, max) = splitmix64(S_min ^ max),
+// S_a = splitmix64(seed ^ splitmix64(a)), is recomputed from the ids (pure
+// ALU) and only when a candidate's rating ties the current best's.
+__device__ __forceinline__ unsigned long long hem_s(unsigned long long seed, int a) {
+  return splitmix64(seed ^ splitmix64((unsigned long long)a));
+}
+
+__device__ __forceinline__ unsigned long long hem_hash(unsigned long long seed, int v, int u) {
+  const int a = min(v, u), b = max(v, u);
+  return splitmix64(hem_s(seed, a) ^ (unsigned long long)b);
+}
+
+// rating order of coarsening.py:52-60 with the hash computed lazily:
+// returns true when `c` beats `best` (both hashes filled in on a tie)
+__device__ __forceinline__ bool hem_better_lazy(HemCand& c, bool& c_h, HemCand& best,
+                                                bool& best_h, unsigned long long seed, int v) {
+  c_h = false;
+  if (best.u < 0) return true;
+  const unsigned long long cw2 = (unsigned long long)c.w * (unsigned long long)c.w;
+  const unsigned long long bw2 = (unsigned long long)best.w * (unsigned long long)best.w;
+  const unsigned __int128 lhs = (unsigned __int128)cw2 * (unsigned)best.c;
+  const unsigned __int128 rhs = (unsigned __int128)bw2 * (unsigned)c.c;
+  if (lhs != rhs) return lhs > rhs;
+  if (!best_h) {
+    best.h = hem_hash(seed, v, best.u);
+    best_h = true;
+  }
+  c.h = hem_hash(seed, v, c.u);
+  c_h = true;
+  if (c.h != best.h) return c.h > best.h;
+  return c.slot < best.slot;
+}
 
 __global__ void k_hem_elig(int n, const int* __restrict__ partner, const int* __restrict__ vw,
-                           unsigned long long seed, HemV* __restrict__ ev,
-                           const long long* gate, int* huge_cnt) {
+                           int* __restrict__ elig, const long long* gate, int* huge_cnt) {
   if (huge_cnt && blockIdx.x == 0 && threadIdx.x == 0) *huge_cnt = 0;
   if (hem_gated(gate, n)) return;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    HemV x;
-    x.s = splitmix64(seed ^ splitmix64((unsigned long long)v));
-    x.c = partner[v] < 0 ? vw[v] : -1;
-    x.pad = 0;
-    ev[v] = x;
-  }
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    elig[v] = partner[v] < 0 ? vw[v] : -1;
 }
 
 __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restrict__ off,
                                                       const int* __restrict__ tgt,
                                                       const int* __restrict__ w,
-                                                      const HemV* __restrict__ ev,
+                                                      const int* __restrict__ elig,
+                                                      unsigned long long seed,
                                                       double l_max, int* __restrict__ pref,
                                                       const long long* gate,
                                                       int* __restrict__ huge,
@@ -144,11 +165,7 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
   for (long long b0 = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; b0 < n; b0 += T) {
     const int v = (int)(b0 + lane);
     const bool inr = v < n;
-    HemV me;
-    me.s = 0;
-    me.c = -1;
-    if (inr) me = ev[v];
-    const int cvv = me.c;
+    const int cvv = inr ? elig[v] : -1;
     const bool active = cvv >= 0;  // unmatched
     int e0 = 0, e1 = 0;
     if (active) {
@@ -163,11 +180,11 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
     best.u = -1;
     best.w = best.c = best.slot = 0;
     best.h = 0;
+    bool best_h = false;
     if (active && !longrow) {
       const long long cv = cvv;
       for (int e = e0; e < e1; e += 4) {
-        int tg[4], wg[4];
-        HemV cg[4];
+        int tg[4], wg[4], cg[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (e + q < e1) {
@@ -176,20 +193,23 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
           }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (e + q < e1) cg[q] = ev[tg[q]];
+          if (e + q < e1) cg[q] = elig[tg[q]];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (e + q >= e1) break;
-          const int cu = cg[q].c;
+          const int cu = cg[q];
           if (cu < 0 || (double)(cv + cu) > l_max) continue;
           HemCand c;
           c.w = wg[q];
           c.c = cu;
           c.slot = e + q;
           c.u = tg[q];
-          c.h = v < c.u ? splitmix64(me.s ^ (unsigned long long)c.u)
-                        : splitmix64(cg[q].s ^ (unsigned long long)v);  // = hash2(seed, min, max)
-          if (hem_better(c, best)) best = c;
+          c.h = 0;
+          bool c_h;
+          if (hem_better_lazy(c, c_h, best, best_h, seed, v)) {
+            best = c;
+            best_h = c_h;
+          }
         }
       }
     }
@@ -201,23 +221,20 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
       const int x = __shfl_sync(0xffffffffu, v, l);
       const int xb = __shfl_sync(0xffffffffu, e0, l), xe = __shfl_sync(0xffffffffu, e1, l);
       const long long cx = __shfl_sync(0xffffffffu, cvv, l);
-      const unsigned long long sx = __shfl_sync(0xffffffffu, me.s, l);
       HemCand bx;
       bx.u = -1;
       bx.w = bx.c = bx.slot = 0;
       bx.h = 0;
       for (int e = xb + lane; e < xe; e += 32) {
         const int u = tgt[e];
-        const HemV hu = ev[u];
-        const int cu = hu.c;
+        const int cu = elig[u];
         if (cu < 0 || (double)(cx + cu) > l_max) continue;
         HemCand c;
         c.w = w[e];
         c.c = cu;
         c.slot = e;
         c.u = u;
-        c.h = x < u ? splitmix64(sx ^ (unsigned long long)u)
-                    : splitmix64(hu.s ^ (unsigned long long)x);  // = hash2(seed, min, max)
+        c.h = hem_hash(seed, x, u);
         if (hem_better(c, bx)) bx = c;
       }
 #pragma unroll
@@ -236,7 +253,8 @@ __global__ void __launch_bounds__(256) k_hem_pref_tpv(int n, const int* __restri
 __global__ void __launch_bounds__(256) k_hem_pref_huge(const int* __restrict__ off,
                                                        const int* __restrict__ tgt,
                                                        const int* __restrict__ w,
-                                                       const HemV* __restrict__ ev, double l_max,
+                                                       const int* __restrict__ elig,
+                                                       unsigned long long seed, double l_max,
                                                        int* __restrict__ pref,
                                                        const long long* gate, int n,
                                                        const int* __restrict__ huge,
@@ -246,24 +264,21 @@ __global__ void __launch_bounds__(256) k_hem_pref_huge(const int* __restrict__ o
   const int cnt = *huge_cnt;
   for (int h = blockIdx.x; h < cnt; h += gridDim.x) {
     const int x = huge[h];
-    const HemV me = ev[x];
-    const long long cx = me.c;
+    const long long cx = elig[x];
     HemCand bx;
     bx.u = -1;
     bx.w = bx.c = bx.slot = 0;
     bx.h = 0;
     for (int e = off[x] + threadIdx.x; e < off[x + 1]; e += blockDim.x) {
       const int u = tgt[e];
-      const HemV hu = ev[u];
-      const int cu = hu.c;
+      const int cu = elig[u];
       if (cu < 0 || (double)(cx + cu) > l_max) continue;
       HemCand c;
       c.w = w[e];
       c.c = cu;
       c.slot = e;
       c.u = u;
-      c.h = x < u ? splitmix64(me.s ^ (unsigned long long)u)
-                  : splitmix64(hu.s ^ (unsigned long long)x);  // = hash2(seed, min, max)
+      c.h = hem_hash(seed, x, u);
       if (hem_better(c, bx)) bx = c;
     }
 #pragma unroll
@@ -295,21 +310,21 @@ void hem_round(const DevGraph& g, int* partner, int* pref, double l_max,
                unsigned long long seed, long long* matched, cudaStream_t s,
                const long long* gate) {
   if (g.n == 0) return;
+  // 16 B per vertex, 16 B per slot
   ProfScope prof(P_HEM, 16.0 * g.n + 16.0 * g.m2, s);
   constexpr int B = 256;
-  DBuf<HemV> ev((size_t)g.n, s);
+  DBuf<int> ev((size_t)g.n, s);
   // a row can exceed kHemHuge (row-length bound known for uploaded and
   // matching-contracted levels; otherwise only the total bounds it)
   const bool hubs = g.maxdeg >= 0 ? g.maxdeg > kHemHuge : g.m2 > (long long)kHemHuge;
   DBuf<int> huge(hubs ? (size_t)g.n + 1 : 1, s);
   int* hcnt = hubs ? huge.get() + g.n : nullptr;
-  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, seed, ev.get(), gate,
-                                                      hcnt);
-  k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, ev.get(),
+  k_hem_elig<<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, partner, g.vw, ev.get(), gate, hcnt);
+  k_hem_pref_tpv<<<grid_for(g.n, B, kSMs * 16), B, 0, s>>>(g.n, g.off, g.tgt, g.w, ev.get(), seed,
                                                            l_max, pref, gate, huge.get(), hcnt);
   if (hubs) {
-    k_hem_pref_huge<<<kSMs, B, 0, s>>>(g.off, g.tgt, g.w, ev.get(), l_max, pref, gate, g.n,
-                                            huge.get(), hcnt);
+    k_hem_pref_huge<<<kSMs, B, 0, s>>>(g.off, g.tgt, g.w, ev.get(), seed, l_max, pref, gate, g.n,
+                                       huge.get(), hcnt);
     count_launch();
   }
   k_hem_mutual<B><<<grid_for(g.n, B, kSMs * 8), B, 0, s>>>(g.n, pref, partner, matched, gate);
@@ -957,8 +972,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int*
 // go through the warp-per-row shared-memory path into the same buffers.
 constexpr int kCtTpv = 32;
 constexpr int kCtBlock = 128;
-// slots per row chunk (8 ints = one 32-byte sector of targets / weights)
-constexpr int kCtChunk = 8;
+// slots per row chunk (independent target / weight loads, then M gathers)
+constexpr int kCtChunk = 4;
 
 __global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __restrict__ mem,
                                                       const int* __restrict__ rowlen,
@@ -970,7 +985,10 @@ __global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __rest
                                                       int* __restrict__ t_tgt,
                                                       int* __restrict__ t_w,
                                                       int* __restrict__ cdeg) {
-  __shared__ int sK[kCtTpv][kCtBlock], sW[kCtTpv][kCtBlock];
+  // one 64-bit entry per (key, weight): key in the high word, so entries
+  // order by key; a classic insertion sort moves each entry once per step
+  // (one shared load + one store), equal keys merge by adding the weight
+  __shared__ unsigned long long sE[kCtTpv][kCtBlock];
   const int tid = threadIdx.x;
   for (long long cc = (long long)blockIdx.x * kCtBlock + tid; cc < n_c;
        cc += (long long)gridDim.x * kCtBlock) {
@@ -1000,25 +1018,29 @@ __global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __rest
           const int key = kg[q];
           if (key == c) continue;  // self loop
           int pos = cnt;
-          while (pos > 0 && sK[pos - 1][tid] > key) --pos;
-          if (pos > 0 && sK[pos - 1][tid] == key) {
-            sW[pos - 1][tid] += wg[q];
+          unsigned long long x = 0;
+          while (pos > 0) {
+            x = sE[pos - 1][tid];
+            if ((int)(x >> 32) <= key) break;
+            sE[pos][tid] = x;
+            --pos;
+          }
+          if (pos > 0 && (int)(x >> 32) == key) {
+            // merge into the equal entry: close the gap opened above it
+            sE[pos - 1][tid] = x + (unsigned)wg[q];
+            for (int i = pos; i < cnt; ++i) sE[i][tid] = sE[i + 1][tid];
             continue;
           }
-          for (int i = cnt; i > pos; --i) {
-            sK[i][tid] = sK[i - 1][tid];
-            sW[i][tid] = sW[i - 1][tid];
-          }
-          sK[pos][tid] = key;
-          sW[pos][tid] = wg[q];
+          sE[pos][tid] = ((unsigned long long)(unsigned)key << 32) | (unsigned)wg[q];
           ++cnt;
         }
       }
     }
     const int base = ub[c];
     for (int i = 0; i < cnt; ++i) {
-      t_tgt[base + i] = sK[i][tid];
-      t_w[base + i] = sW[i][tid];
+      const unsigned long long x = sE[i][tid];
+      t_tgt[base + i] = (int)(x >> 32);
+      t_w[base + i] = (int)(unsigned)x;
     }
     cdeg[c] = cnt;
   }

@@ -1410,8 +1410,12 @@ static void integrated_map_strip(const DevGraph& g0, long long total, const gim_
       count_launch();
       total_r = read_scalar(d.get(), s);
     }
+    // the reduced graph gets the full graph's capacity: eps_r makes every
+    // multisection node's budget (Eq. 2) and L_max the same absolute weights
+    // as with the isolated vertices present (they are the slack)
+    const double eps_r = (1.0 + eps) * (double)total / (double)total_r - 1.0;
     DBuf<int> rp((size_t)R.n, s);
-    integrated_map_device(R.view(), total_r, tt, eps, seed, Q, rp.get(), out_bw, stats, s, l_max);
+    integrated_map_device(R.view(), total_r, tt, eps_r, seed, Q, rp.get(), out_bw, stats, s, l_max);
     leaf_scatter(R.n, ids[0].get(), rp.get(), 0, out_part, s);
   }
   if (n_iso > 0) {

@@ -63,7 +63,8 @@ __device__ __forceinline__ void cta_argmax(int& a, int& b, int* sa, int* sb) {
   __syncthreads();
   a = sa[0];
   b = sb[0];
-  for (int i = 1; i < kGggWarps; ++i)
+  const int nw = (int)(blockDim.x >> 5);
+  for (int i = 1; i < nw; ++i)
     if (sa[i] > a || (sa[i] == a && sb[i] < b)) { a = sa[i]; b = sb[i]; }
   __syncthreads();
 }
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
     if (lane_id() == 0) { sa[threadIdx.x >> 5] = bc; sb[threadIdx.x >> 5] = bv; }
     __syncthreads();
     int ga = sa[0], gv = sb[0];
-    for (int i = 1; i < kGggWarps; ++i)
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
       if (sa[i] > ga || (sa[i] == ga && sb[i] < gv)) { ga = sa[i]; gv = sb[i]; }
     if (ga == 0) {  // frontier dried up: lowest unassigned vertex (CTA-uniform)
       while (part[next_free] >= 0) ++next_free;
@@ -746,7 +747,13 @@ static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector
     GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(160 * 1024)));
   });
-  k_ggg<<<J, kGggBlock, smem, s>>>(dj.get(), J);
+  // the growth loop is a sequential chain of claims, each an argmax over
+  // the job's n vertices: small jobs run one warp per job (no multi-warp
+  // merge, near-free barriers), larger ones a few warps
+  int max_n = 0;
+  for (const DevGraph& g : gs) max_n = std::max(max_n, g.n);
+  const int threads = max_n <= 1024 ? 32 : max_n <= 4096 ? 64 : kGggBlock;
+  k_ggg<<<J, threads, smem, s>>>(dj.get(), J);
   count_launch();
   GIM_LAUNCH_CHECK();
 }

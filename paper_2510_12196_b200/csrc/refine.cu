@@ -359,8 +359,10 @@ static void launch_eval(const RefineLevel& L, int mode, const Topo& t, const int
   if (L.n_heavy > 0) {
     int k = t.k;
     size_t smem = (size_t)4 * 3 * k * sizeof(int);
+    // dynamic + the kernel's static shared memory may pass 48 KB before the
+    // dynamic part alone does (k = 1024): always raise the opt-in limit
     static int configured_smem = 0;
-    if ((int)smem > 48 * 1024 && (int)smem > configured_smem) {
+    if ((int)smem > configured_smem) {
       GIM_CUDA(cudaFuncSetAttribute(k_eval_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
       configured_smem = (int)smem;

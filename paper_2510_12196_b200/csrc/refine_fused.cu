@@ -1314,6 +1314,42 @@ static size_t smem_resident_bytes(long long n, long long m2, int k, int NC) {
 // ---------------------------------------------------------------------------
 // host side
 
+// GIM_TRACE_REFINE for batched launches: per-phase times of job 0 and the
+// batch's device time, printed after the batch finished
+struct BatchTrace {
+  bool on = false;
+  DBuf<long long> pt;
+  cudaEvent_t e[2]{};
+  void begin(long long** job0_ptime, cudaStream_t s) {
+    static const bool env = std::getenv("GIM_TRACE_REFINE") != nullptr;
+    on = env;
+    if (!on) return;
+    pt = DBuf<long long>(16, s);
+    GIM_CUDA(cudaMemsetAsync(pt.get(), 0, 16 * sizeof(long long), s));
+    *job0_ptime = pt.get();
+    GIM_CUDA(cudaEventCreate(&e[0]));
+    GIM_CUDA(cudaEventCreate(&e[1]));
+    GIM_CUDA(cudaEventRecord(e[0], s));
+  }
+  void end(const char* kind, int jobs, int n0, long long m20, long long it0, cudaStream_t s) {
+    if (!on) return;
+    GIM_CUDA(cudaEventRecord(e[1], s));
+    GIM_CUDA(cudaEventSynchronize(e[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e[0], e[1]);
+    long long h[16];
+    GIM_CUDA(cudaMemcpy(h, pt.get(), sizeof(h), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "%s jobs=%d job0 n=%d m2=%lld iters=%lld batch_ms=%.3f us/iter(job0)=%.1f |",
+                 kind, jobs, n0, m20, it0, ms, it0 ? 1000.0 * ms / (double)it0 : 0.0);
+    static const char* nm[12] = {"stamp", "blist", "ff", "sf", "wlist", "wcand", "wA", "wB",
+                                 "wsel", "apply", "commit", "ctl"};
+    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.1f", nm[i], h[i] / 1000.0);
+    std::fprintf(stderr, "\n");
+    cudaEventDestroy(e[0]);
+    cudaEventDestroy(e[1]);
+  }
+};
+
 // co-resident CTA capacity per (VW, smem), queried once per device
 template <int VW>
 static int coop_max_blocks(size_t smem) {
@@ -1706,6 +1742,8 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
     A.seed = R.cfg.seed;
     host[(size_t)j] = A;
   }
+  BatchTrace trace;
+  trace.begin(&host[0].ptime, s);
   // group by lane width (the VW template), one launch per group
   DBuf<FusedArgs> dargs((size_t)J, s);
   std::vector<FusedArgs> ordered;
@@ -1761,6 +1799,7 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
   FusedState* hs = static_cast<FusedState*>(pinned_scratch(sizeof(FusedState) * (size_t)J));
   GIM_CUDA(cudaMemcpyAsync(hs, states, sizeof(FusedState) * (size_t)J, cudaMemcpyDeviceToHost, s));
   GIM_CUDA(sync_stream(s));
+  trace.end("smem_batch", J, jobs[0].g.n, jobs[0].g.m2, hs[0].iters, s);
   for (int j = 0; j < J; ++j) {
     // states are indexed by the original job (A.st = states + j)
     yielded[(size_t)j] = hs[j].status != 0;
@@ -1849,6 +1888,8 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
     GIM_CUDA(cudaMemsetAsync(A.ctr, 0, 17 * sizeof(long long), s));
   }
   const int vpc = cluster_vertices_per_cta();
+  BatchTrace trace;
+  trace.begin(&host[0].ptime, s);
   DBuf<FusedArgs> dargs((size_t)J, s);
   std::vector<FusedArgs> ordered;
   struct Grp { int vw, first, cnt, cs; };
@@ -1908,6 +1949,7 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
   FusedState* hs = static_cast<FusedState*>(pinned_scratch(sizeof(FusedState) * (size_t)J));
   GIM_CUDA(cudaMemcpyAsync(hs, states, sizeof(FusedState) * (size_t)J, cudaMemcpyDeviceToHost, s));
   GIM_CUDA(sync_stream(s));
+  trace.end("cluster_batch", J, jobs[0].g.n, jobs[0].g.m2, hs[0].iters, s);
   for (int j = 0; j < J; ++j) {
     yielded[(size_t)j] = hs[j].status != 0;
     jobs[(size_t)j].iters = hs[j].iters;

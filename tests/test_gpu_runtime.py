@@ -102,7 +102,7 @@ def test_refinement_accounting_reproduces_bytes(D, rgg16):
     assert ac["lp_it"] + ac["weak_it"] > 0
     assert ac["eval_v"] > 0 and ac["eval_slots"] >= ac["eval_v"]
     assert ac["mov_v"] > 0 and ac["mov_slots"] >= ac["mov_v"]
-    assert 0 < ac["bnd"] <= ac["scan"]
+    assert 0 <= ac["bnd"] <= ac["scan"]  # list-driven levels only (2^16 is all vertex-centric)
     assert sum(st["level_iters"]) == st["refine_iterations"]
     assert all(b > 0 for b in st["level_bytes"])
     assert st["level_refine_ms"][0] > 0
