@@ -962,87 +962,88 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int*
   }
 }
 
-// Thread-per-coarse-vertex contraction (rows of L <= kCtTpv staged entries):
-// the thread walks its <= 2 member rows in chunks of 4 (independent loads),
-// maps each target through M and insertion-sorts (key, weight) into its own
-// column of a shared-memory scratch (conflict-free [i][thread] layout),
-// summing parallel edges and dropping the self loop — the same sorted,
-// deduplicated row as the warp path.  Rows are written at upper-bound
-// offsets (scan of L) with their true degree, then compacted.  Longer rows
-// go through the warp-per-row shared-memory path into the same buffers.
+// Warp-per-coarse-vertex contraction (rows of L <= kCtTpv = 32 staged
+// entries): lane i stages entry i of the <= 2 member rows (coalesced target /
+// weight loads, then the M gather), self loops become +inf, a 32-lane bitonic
+// network in registers sorts (key, weight) by key, a segmented shuffle scan
+// sums parallel edges and the segment tails write the sorted, deduplicated
+// row at its upper-bound offset (compacted afterwards).  No shared memory,
+// so the SM keeps 48+ warps of rows in flight.  Longer rows go through the
+// shared-memory warp path (k_row_long) into the same buffers.
 constexpr int kCtTpv = 32;
-constexpr int kCtBlock = 128;
-// slots per row chunk (independent target / weight loads, then M gathers)
-constexpr int kCtChunk = 4;
+constexpr int kCtBlock = 256;
 
-__global__ void __launch_bounds__(kCtBlock) k_row_tpv(int n_c, const int* __restrict__ mem,
-                                                      const int* __restrict__ rowlen,
-                                                      const int* __restrict__ ub,
-                                                      const int* __restrict__ off,
-                                                      const int* __restrict__ tgt,
-                                                      const int* __restrict__ w,
-                                                      const int* __restrict__ cmap,
-                                                      int* __restrict__ t_tgt,
-                                                      int* __restrict__ t_w,
-                                                      int* __restrict__ cdeg) {
-  // one 64-bit entry per (key, weight): key in the high word, so entries
-  // order by key; a classic insertion sort moves each entry once per step
-  // (one shared load + one store), equal keys merge by adding the weight
-  __shared__ unsigned long long sE[kCtTpv][kCtBlock];
-  const int tid = threadIdx.x;
-  for (long long cc = (long long)blockIdx.x * kCtBlock + tid; cc < n_c;
-       cc += (long long)gridDim.x * kCtBlock) {
-    const int c = (int)cc;
-    if (rowlen[c] > kCtTpv) continue;  // warp path
+__device__ __forceinline__ void cx_swap(int& k, int& w, int j, bool up) {
+  const int k2 = __shfl_xor_sync(0xffffffffu, k, j);
+  const int w2 = __shfl_xor_sync(0xffffffffu, w, j);
+  const bool lower = (lane_id() & j) == 0;
+  // ascending pair: the lower lane keeps the smaller key
+  const bool take = lower == up ? k2 < k : k2 > k;
+  if (take) {
+    k = k2;
+    w = w2;
+  }
+}
+
+__global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int* __restrict__ mem,
+                                                       const int* __restrict__ rowlen,
+                                                       const int* __restrict__ ub,
+                                                       const int* __restrict__ off,
+                                                       const int* __restrict__ tgt,
+                                                       const int* __restrict__ w,
+                                                       const int* __restrict__ cmap,
+                                                       int* __restrict__ t_tgt,
+                                                       int* __restrict__ t_w,
+                                                       int* __restrict__ cdeg) {
+  const int lane = lane_id();
+  for (long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c0 < n_c;
+       c0 += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int c = (int)c0;
+    const int L = rowlen[c];
+    if (L > kCtTpv) continue;  // warp-uniform: k_row_long
     const int v0 = mem[2 * c], v1 = mem[2 * c + 1];
-    int cnt = 0;
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      const int vv = part ? v1 : v0;
-      if (vv < 0) break;
-      const int e1 = off[vv + 1];
-      for (int e = off[vv]; e < e1; e += kCtChunk) {
-        int tg[kCtChunk], wg[kCtChunk], kg[kCtChunk];
-#pragma unroll
-        for (int q = 0; q < kCtChunk; ++q)
-          if (e + q < e1) {
-            tg[q] = tgt[e + q];
-            wg[q] = w[e + q];
-          }
-#pragma unroll
-        for (int q = 0; q < kCtChunk; ++q)
-          if (e + q < e1) kg[q] = cmap[tg[q]];
-#pragma unroll
-        for (int q = 0; q < kCtChunk; ++q) {
-          if (e + q >= e1) break;
-          const int key = kg[q];
-          if (key == c) continue;  // self loop
-          int pos = cnt;
-          unsigned long long x = 0;
-          while (pos > 0) {
-            x = sE[pos - 1][tid];
-            if ((int)(x >> 32) <= key) break;
-            sE[pos][tid] = x;
-            --pos;
-          }
-          if (pos > 0 && (int)(x >> 32) == key) {
-            // merge into the equal entry: close the gap opened above it
-            sE[pos - 1][tid] = x + (unsigned)wg[q];
-            for (int i = pos; i < cnt; ++i) sE[i][tid] = sE[i + 1][tid];
-            continue;
-          }
-          sE[pos][tid] = ((unsigned long long)(unsigned)key << 32) | (unsigned)wg[q];
-          ++cnt;
-        }
+    const int b0 = off[v0], d0 = off[v0 + 1] - b0;
+    const int b1 = v1 >= 0 ? off[v1] : 0;
+    int key = INT_MAX, wt = 0;
+    if (lane < L) {
+      const int e = lane < d0 ? b0 + lane : b1 + (lane - d0);
+      const int t = tgt[e];
+      wt = w[e];
+      key = cmap[t];
+      if (key == c) {  // self loop
+        key = INT_MAX;
+        wt = 0;
       }
     }
-    const int base = ub[c];
-    for (int i = 0; i < cnt; ++i) {
-      const unsigned long long x = sE[i][tid];
-      t_tgt[base + i] = (int)(x >> 32);
-      t_w[base + i] = (int)(unsigned)x;
+    // bitonic sort ascending by key across the warp
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+      const bool up = (lane & size) == 0 || size == 32;
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) cx_swap(key, wt, j, up);
     }
-    cdeg[c] = cnt;
+    // segmented inclusive sum of the weights of equal keys
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = lane == 0 || prev != key;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    // segment start = highest head lane <= lane
+    const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+    int sum = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, sum, o);
+      if (lane - o >= start) sum += y;
+    }
+    const int next = __shfl_down_sync(0xffffffffu, key, 1);
+    const bool tail = (lane == 31 || next != key) && key != INT_MAX;
+    const unsigned tails = __ballot_sync(0xffffffffu, tail);
+    if (tail) {
+      const int base = ub[c];
+      const int rank = __popc(tails & ((1u << lane) - 1u));
+      t_tgt[base + rank] = key;
+      t_w[base + rank] = sum;
+    }
+    if (lane == 0) cdeg[c] = __popc(tails);
   }
 }
 
@@ -1161,7 +1162,7 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
   out.vw = std::move(cvw);
   out.off = DBuf<int>((size_t)n_c + 1, s);
   DBuf<int> t_tgt((size_t)std::max(ubtot, 1), s), t_w((size_t)std::max(ubtot, 1), s);
-  k_row_tpv<<<grid_for(n_c, kCtBlock, kSMs * 16), kCtBlock, 0, s>>>(
+  k_row_warp<<<grid_for((long long)n_c * 32, kCtBlock, kSMs * 32), kCtBlock, 0, s>>>(
       n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
       cdeg.get());
   count_launch();
@@ -1282,7 +1283,7 @@ bool coarsen_level_fast(const DevGraph& g_in, double l_max, unsigned long long l
   GIM_CUDA(cudaMemsetAsync(cdeg.get() + n_c, 0, sizeof(int), s));
   exclusive_scan<int>((long long)n_c, LoadAs<int, int>{rowlen.get()}, StoreTo<int>{ub.get()},
                       scal.get() + 1, s);
-  k_row_tpv<<<grid_for(n_c, kCtBlock, kSMs * 16), kCtBlock, 0, s>>>(
+  k_row_warp<<<grid_for((long long)n_c * 32, kCtBlock, kSMs * 32), kCtBlock, 0, s>>>(
       n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
       cdeg.get());
   count_launch();

@@ -28,14 +28,18 @@ struct Error {
   std::string msg;
 };
 
+// a failed call also leaves its code as the thread's "last error": clear it
+// so the next call's launch check does not report this one again
 #define GIM_CUDA(call)                                                        \
   do {                                                                        \
     cudaError_t _e = (call);                                                  \
-    if (_e != cudaSuccess)                                                    \
+    if (_e != cudaSuccess) {                                                  \
+      (void)cudaGetLastError();                                               \
       throw ::gim::Error{GIM_E_CUDA, std::string(#call) + ": " +              \
                                          cudaGetErrorString(_e) + " @" +      \
                                          __FILE__ + ":" +                     \
                                          std::to_string(__LINE__)};           \
+    }                                                                         \
   } while (0)
 
 #define GIM_CHECK(cond, code, msg)                                            \

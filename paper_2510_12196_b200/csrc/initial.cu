@@ -747,13 +747,7 @@ static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector
     GIM_CUDA(cudaFuncSetAttribute(k_ggg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(160 * 1024)));
   });
-  // the growth loop is a sequential chain of claims, each an argmax over
-  // the job's n vertices: small jobs run one warp per job (no multi-warp
-  // merge, near-free barriers), larger ones a few warps
-  int max_n = 0;
-  for (const DevGraph& g : gs) max_n = std::max(max_n, g.n);
-  const int threads = max_n <= 1024 ? 32 : max_n <= 4096 ? 64 : kGggBlock;
-  k_ggg<<<J, threads, smem, s>>>(dj.get(), J);
+  k_ggg<<<J, kGggBlock, smem, s>>>(dj.get(), J);
   count_launch();
   GIM_LAUNCH_CHECK();
 }

@@ -1350,6 +1350,28 @@ struct BatchTrace {
   }
 };
 
+// Raise a kernel's dynamic shared-memory limit to the device's opt-in
+// maximum (minus its static shared memory) once per (device, kernel).  The
+// limit is never lowered afterwards: launches of the same kernel with
+// different k (different dynamic sizes) from other calls / threads must all
+// stay valid.
+static void raise_dyn_smem_limit(const void* fn) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  GIM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return;
+  int optin = 0;
+  GIM_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  GIM_CUDA(cudaFuncGetAttributes(&fa, fn));
+  const int lim = optin > (int)fa.sharedSizeBytes ? optin - (int)fa.sharedSizeBytes : 0;
+  GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  done[{dev, fn}] = true;
+}
+
 // co-resident CTA capacity per (VW, smem), queried once per device
 template <int VW>
 static int coop_max_blocks(size_t smem) {
@@ -1363,10 +1385,7 @@ static int coop_max_blocks(size_t smem) {
   if (it != cache.end()) return it->second;
   int sms = 0, per = 0;
   GIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)std::max<size_t>(smem, 48 * 1024)));
-  GIM_CUDA(cudaFuncSetAttribute(k_refine_fused<VW>,
-                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  raise_dyn_smem_limit((const void*)k_refine_fused<VW>);
   GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW>, kFusedBlock,
                                                          smem));
   int r = std::max(1, per) * sms;
@@ -1923,11 +1942,9 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
       case 16: fn = (void*)k_refine_cluster_batch<16>; slot = 2; break;
       default: fn = (void*)k_refine_cluster_batch<32>; slot = 3; break;
     }
-    std::call_once(once[slot], [&] {
-      GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      GIM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)std::max<size_t>(base, 48 * 1024)));
-    });
+    (void)once;
+    (void)slot;
+    raise_dyn_smem_limit(fn);
     const FusedArgs* a = dargs.get() + g.first;
     int cs = g.cs;
     void* args[] = {(void*)&a, (void*)&cs};
