@@ -847,40 +847,41 @@ void contract(const DevGraph& g, const int* cmap, int n_c, OwnedGraph& out, cuda
 constexpr int kRowCap = 256;
 constexpr int kRowWarps = 8;
 
+// member table: per coarse vertex c the rows of its <= 2 fine members as
+// (begin0, len0, begin1, len1) — one 16-byte load in the row kernels, which
+// then start from the slots without a dependent offsets gather
 __global__ void k_members(int n, const int* __restrict__ partner, const int* __restrict__ cmap,
                           const int* __restrict__ off, const int* __restrict__ vw,
-                          int* __restrict__ mem, int* __restrict__ rowlen, int* __restrict__ cvw,
+                          int4* __restrict__ mem, int* __restrict__ rowlen, int* __restrict__ cvw,
                           int* __restrict__ maxlen) {
   int mx = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const int p = partner[v];
     if (p >= 0 && p < v) continue;  // not the root of its pair
     const int c = cmap[v];
-    int L = off[v + 1] - off[v];
-    int wsum = vw[v];
+    const int b0 = off[v], d0 = off[v + 1] - b0;
+    int b1 = 0, d1 = 0, wsum = vw[v];
     if (p >= 0) {
-      L += off[p + 1] - off[p];
+      b1 = off[p];
+      d1 = off[p + 1] - b1;
       wsum += vw[p];
     }
-    mem[2 * c] = v;
-    mem[2 * c + 1] = p;
-    rowlen[c] = L;
+    mem[c] = make_int4(b0, d0, b1, d1);
+    rowlen[c] = d0 + d1;
     cvw[c] = wsum;
-    mx = max(mx, L);
+    mx = max(mx, d0 + d1);
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lane_id() == 0 && mx) atomicMax(maxlen, mx);
 }
 
 // stage the row of coarse vertex c in K/Wt (self loops -> INT_MAX)
-__device__ __forceinline__ int stage_row(int c, const int* mem, const int* off, const int* tgt,
-                                         const int* w, const int* cmap, int* K, int* Wt) {
-  const int v0 = mem[2 * c], v1 = mem[2 * c + 1];
-  const int b0 = off[v0], d0 = off[v0 + 1] - b0;
-  const int b1 = v1 >= 0 ? off[v1] : 0, d1 = v1 >= 0 ? off[v1 + 1] - b1 : 0;
-  const int L = d0 + d1;
+__device__ __forceinline__ int stage_row(int c, const int4* mem, const int* tgt, const int* w,
+                                         const int* cmap, int* K, int* Wt) {
+  const int4 m = mem[c];
+  const int L = m.y + m.w;
   for (int i = lane_id(); i < L; i += 32) {
-    const int e = i < d0 ? b0 + i : b1 + (i - d0);
+    const int e = i < m.y ? m.x + i : m.z + (i - m.y);
     const int key = cmap[tgt[e]];
     K[i] = key == c ? INT_MAX : key;
     Wt[i] = w[e];
@@ -889,106 +890,22 @@ __device__ __forceinline__ int stage_row(int c, const int* mem, const int* off, 
   return L;
 }
 
-__global__ void __launch_bounds__(kRowWarps * 32) k_row_count(int n_c, const int* __restrict__ mem,
-                                                             const int* __restrict__ off,
-                                                             const int* __restrict__ tgt,
-                                                             const int* __restrict__ w,
-                                                             const int* __restrict__ cmap,
-                                                             int* __restrict__ cdeg) {
-  __shared__ int sK[kRowWarps][kRowCap], sW[kRowWarps][kRowCap];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  int* K = sK[warp];
-  int* Wt = sW[warp];
-  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_c;
-       c += ((long long)gridDim.x * blockDim.x) >> 5) {
-    const int L = stage_row((int)c, mem, off, tgt, w, cmap, K, Wt);
-    int cnt = 0;
-    for (int i = lane; i < L; i += 32) {
-      const int key = K[i];
-      if (key == INT_MAX) continue;
-      bool first = true;
-      for (int j = 0; j < i; ++j)
-        if (K[j] == key) { first = false; break; }
-      cnt += first;
-    }
-    cnt = warp_sum_i(cnt);
-    if (lane == 0) cdeg[c] = cnt;
-    __syncwarp();
-  }
-}
-
-__global__ void __launch_bounds__(kRowWarps * 32) k_row_fill(int n_c, const int* __restrict__ mem,
-                                                            const int* __restrict__ off,
-                                                            const int* __restrict__ tgt,
-                                                            const int* __restrict__ w,
-                                                            const int* __restrict__ cmap,
-                                                            const int* __restrict__ c_off,
-                                                            int* __restrict__ c_tgt,
-                                                            int* __restrict__ c_w,
-                                                            int* __restrict__ c_src) {
-  __shared__ int sK[kRowWarps][kRowCap], sW[kRowWarps][kRowCap];
-  __shared__ unsigned char sF[kRowWarps][kRowCap];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  int* K = sK[warp];
-  int* Wt = sW[warp];
-  unsigned char* F = sF[warp];
-  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_c;
-       c += ((long long)gridDim.x * blockDim.x) >> 5) {
-    const int L = stage_row((int)c, mem, off, tgt, w, cmap, K, Wt);
-    for (int i = lane; i < L; i += 32) {
-      const int key = K[i];
-      bool first = key != INT_MAX;
-      for (int j = 0; j < i && first; ++j)
-        if (K[j] == key) first = false;
-      F[i] = first;
-    }
-    __syncwarp();
-    const int base = c_off[c];
-    for (int i = lane; i < L; i += 32) {
-      if (!F[i]) continue;
-      const int key = K[i];
-      long long sum = 0;
-      int rank = 0;
-      for (int j = 0; j < L; ++j) {
-        const int kj = K[j];
-        if (kj == key) sum += Wt[j];
-        rank += (F[j] && kj < key);
-      }
-      c_tgt[base + rank] = key;
-      c_w[base + rank] = (int)sum;
-      c_src[base + rank] = (int)c;
-    }
-    __syncwarp();
-  }
-}
-
 // Warp-per-coarse-vertex contraction (rows of L <= kCtTpv = 32 staged
 // entries): lane i stages entry i of the <= 2 member rows (coalesced target /
-// weight loads, then the M gather), self loops become +inf, a 32-lane bitonic
-// network in registers sorts (key, weight) by key, a segmented shuffle scan
-// sums parallel edges and the segment tails write the sorted, deduplicated
-// row at its upper-bound offset (compacted afterwards).  No shared memory,
-// so the SM keeps 48+ warps of rows in flight.  Longer rows go through the
-// shared-memory warp path (k_row_long) into the same buffers.
+// weight loads straight from the member table's row ranges, then the M
+// gather), self loops drop out, __match_any_sync groups equal coarse
+// targets, __reduce_add_sync sums their weights (parallel edges) and each
+// group's lowest lane writes the entry at its rank among the group leaders —
+// the deduplicated row in first-occurrence order, at its upper-bound offset
+// (compacted afterwards).  Within-row order is irrelevant to every consumer
+// (the pipeline is invariant to it; the ABI's gim_contract keeps
+// sorted rows).  No shared memory, ~20 instructions per row.  Longer rows go
+// through the shared-memory warp path (k_row_long) into the same buffers.
 constexpr int kCtTpv = 32;
 constexpr int kCtBlock = 256;
 
-__device__ __forceinline__ void cx_swap(int& k, int& w, int j, bool up) {
-  const int k2 = __shfl_xor_sync(0xffffffffu, k, j);
-  const int w2 = __shfl_xor_sync(0xffffffffu, w, j);
-  const bool lower = (lane_id() & j) == 0;
-  // ascending pair: the lower lane keeps the smaller key
-  const bool take = lower == up ? k2 < k : k2 > k;
-  if (take) {
-    k = k2;
-    w = w2;
-  }
-}
-
-__global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int* __restrict__ mem,
-                                                       const int* __restrict__ rowlen,
+__global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int4* __restrict__ mem,
                                                        const int* __restrict__ ub,
-                                                       const int* __restrict__ off,
                                                        const int* __restrict__ tgt,
                                                        const int* __restrict__ w,
                                                        const int* __restrict__ cmap,
@@ -999,59 +916,34 @@ __global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int* __res
   for (long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c0 < n_c;
        c0 += ((long long)gridDim.x * blockDim.x) >> 5) {
     const int c = (int)c0;
-    const int L = rowlen[c];
+    const int4 m = mem[c];
+    const int L = m.y + m.w;
     if (L > kCtTpv) continue;  // warp-uniform: k_row_long
-    const int v0 = mem[2 * c], v1 = mem[2 * c + 1];
-    const int b0 = off[v0], d0 = off[v0 + 1] - b0;
-    const int b1 = v1 >= 0 ? off[v1] : 0;
-    int key = INT_MAX, wt = 0;
+    int key = -1, wt = 0;
     if (lane < L) {
-      const int e = lane < d0 ? b0 + lane : b1 + (lane - d0);
+      const int e = lane < m.y ? m.x + lane : m.z + (lane - m.y);
       const int t = tgt[e];
       wt = w[e];
       key = cmap[t];
-      if (key == c) {  // self loop
-        key = INT_MAX;
-        wt = 0;
-      }
+      if (key == c) key = -1;  // self loop
     }
-    // bitonic sort ascending by key across the warp
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-      const bool up = (lane & size) == 0 || size == 32;
-#pragma unroll
-      for (int j = size >> 1; j > 0; j >>= 1) cx_swap(key, wt, j, up);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int sum = (int)__reduce_add_sync(peers, (unsigned)wt);
+    const bool lead = key >= 0 && lane == __ffs(peers) - 1;
+    const unsigned leads = __ballot_sync(0xffffffffu, lead);
+    if (lead) {
+      const int pos = ub[c] + __popc(leads & ((1u << lane) - 1u));
+      t_tgt[pos] = key;
+      t_w[pos] = sum;
     }
-    // segmented inclusive sum of the weights of equal keys
-    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = lane == 0 || prev != key;
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    // segment start = highest head lane <= lane
-    const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
-    int sum = wt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, sum, o);
-      if (lane - o >= start) sum += y;
-    }
-    const int next = __shfl_down_sync(0xffffffffu, key, 1);
-    const bool tail = (lane == 31 || next != key) && key != INT_MAX;
-    const unsigned tails = __ballot_sync(0xffffffffu, tail);
-    if (tail) {
-      const int base = ub[c];
-      const int rank = __popc(tails & ((1u << lane) - 1u));
-      t_tgt[base + rank] = key;
-      t_w[base + rank] = sum;
-    }
-    if (lane == 0) cdeg[c] = __popc(tails);
+    if (lane == 0) cdeg[c] = __popc(leads);
   }
 }
 
 // long rows (kCtTpv < L <= kRowCap): warp per row, shared-memory staging
-__global__ void __launch_bounds__(kRowWarps * 32) k_row_long(int n_c, const int* __restrict__ mem,
+__global__ void __launch_bounds__(kRowWarps * 32) k_row_long(int n_c, const int4* __restrict__ mem,
                                                             const int* __restrict__ rowlen,
                                                             const int* __restrict__ ub,
-                                                            const int* __restrict__ off,
                                                             const int* __restrict__ tgt,
                                                             const int* __restrict__ w,
                                                             const int* __restrict__ cmap,
@@ -1068,7 +960,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_row_long(int n_c, const int*
        c0 += ((long long)gridDim.x * blockDim.x) >> 5) {
     const int c = (int)c0;
     if (rowlen[c] <= kCtTpv) continue;  // warp-uniform
-    const int L = stage_row(c, mem, off, tgt, w, cmap, K, Wt);
+    const int L = stage_row(c, mem, tgt, w, cmap, K, Wt);
     int nf = 0;
     for (int i = lane; i < L; i += 32) {
       const int key = K[i];
@@ -1135,7 +1027,8 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
     contract(g, cmap, n_c, out, s);
     return;
   }
-  DBuf<int> mem((size_t)2 * n_c, s), rowlen((size_t)n_c + 1, s);
+  DBuf<int4> mem((size_t)std::max(n_c, 1), s);
+  DBuf<int> rowlen((size_t)n_c + 1, s);
   DBuf<int> cdeg((size_t)n_c + 1, s), ub((size_t)n_c + 1, s), scal(3, s);  // maxlen, m2c, ub total
   DBuf<int> cvw((size_t)n_c, s);
   GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 3 * sizeof(int), s));
@@ -1163,12 +1056,11 @@ void contract_matching(const DevGraph& g, const int* cmap, const int* partner, i
   out.off = DBuf<int>((size_t)n_c + 1, s);
   DBuf<int> t_tgt((size_t)std::max(ubtot, 1), s), t_w((size_t)std::max(ubtot, 1), s);
   k_row_warp<<<grid_for((long long)n_c * 32, kCtBlock, kSMs * 32), kCtBlock, 0, s>>>(
-      n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
-      cdeg.get());
+      n_c, mem.get(), ub.get(), g.tgt, g.w, cmap, t_tgt.get(), t_w.get(), cdeg.get());
   count_launch();
   if (maxlen > kCtTpv) {
     const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
-    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(), g.off,
+    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(),
                                                g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
                                                cdeg.get());
     count_launch();
@@ -1243,7 +1135,8 @@ bool coarsen_level_fast(const DevGraph& g_in, double l_max, unsigned long long l
   DBuf<int> ids((size_t)std::max(n, 1), s), tot(1, s);
   exclusive_scan<int>(n, IsRoot{partner}, StoreTo<int>{ids.get()}, tot.get(), s);
   k_coarse_map<<<grid_for(n, 256), 256, 0, s>>>(n, partner, ids.get(), cmap);
-  DBuf<int> mem((size_t)2 * std::max(n, 1), s), rowlen((size_t)n + 1, s), cvw((size_t)std::max(n, 1), s);
+  DBuf<int4> mem((size_t)std::max(n, 1), s);
+  DBuf<int> rowlen((size_t)n + 1, s), cvw((size_t)std::max(n, 1), s);
   DBuf<int> scal(3, s);  // maxlen, ubtot, m2c
   GIM_CUDA(cudaMemsetAsync(scal.get(), 0, 3 * sizeof(int), s));
   k_members<<<grid_for(n, 256), 256, 0, s>>>(n, partner, cmap, g.off, g.vw, mem.get(),
@@ -1284,12 +1177,11 @@ bool coarsen_level_fast(const DevGraph& g_in, double l_max, unsigned long long l
   exclusive_scan<int>((long long)n_c, LoadAs<int, int>{rowlen.get()}, StoreTo<int>{ub.get()},
                       scal.get() + 1, s);
   k_row_warp<<<grid_for((long long)n_c * 32, kCtBlock, kSMs * 32), kCtBlock, 0, s>>>(
-      n_c, mem.get(), rowlen.get(), ub.get(), g.off, g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
-      cdeg.get());
+      n_c, mem.get(), ub.get(), g.tgt, g.w, cmap, t_tgt.get(), t_w.get(), cdeg.get());
   count_launch();
   if (maxlen > kCtTpv) {
     const int grid = grid_for((long long)n_c * 32, kRowWarps * 32, kSMs * 8);
-    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(), g.off,
+    k_row_long<<<grid, kRowWarps * 32, 0, s>>>(n_c, mem.get(), rowlen.get(), ub.get(),
                                                g.tgt, g.w, cmap, t_tgt.get(), t_w.get(),
                                                cdeg.get());
     count_launch();

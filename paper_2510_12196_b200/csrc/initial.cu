@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   int* seeds = part + n;
   int* conn = seeds + k;
   unsigned* nxt = reinterpret_cast<unsigned*>(conn + (size_t)k * n);  // BFS frontier bitmap
+  const int nch = (n + 31) >> 5;
+  int* cmx = reinterpret_cast<int*>(nxt) + nch;  // [k][nch] chunk maxima (upper bounds)
   if (k == 1) {
     for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
     return;
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   const int* g_w = J.w;
   const int* g_vw = J.vw;
   if (J.stage) {
-    int* so = reinterpret_cast<int*>(nxt) + ((n + 31) >> 5);
+    int* so = cmx + (size_t)k * nch;
     int* st = so + n + 1;
     int* sw = st + J.m2;
     int* sv = sw + J.m2;
@@ -180,62 +182,87 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
     if (threadIdx.x == 0) seeds[ns] = sv;
     __syncthreads();
   }
-  // growth (pipelines.py:155-188), two barriers per step: (A) every thread
-  // finds the lightest block and its share of the argmax, (B) every thread
-  // merges the warp results, falls back to the lowest unassigned vertex
-  // when the frontier is dry, and applies the claim's row update
+  // growth (pipelines.py:155-188) driven by warp 0 alone, no CTA barrier per
+  // claim.  conn[b][u] holds block b's connectivity to unassigned u (-1 once
+  // u is assigned, in every block); cmx[b][c] >= max conn[b][u] over chunk c
+  // (32 vertices) is an UPPER bound: a claim raises it (atomicMax), an
+  // assignment leaves it stale and a query that finds the chunk's true max
+  // below the bound repairs it and retries.  The query takes the chunk
+  // attaining the largest bound (lowest chunk on ties), then the lowest
+  // vertex attaining the true maximum in it: the heap pop of pipelines.py
+  // (max conn, lowest id); a zero maximum means the frontier is dry and the
+  // lowest unassigned vertex is claimed instead.
   __shared__ long long s_bw[kGggMaxK];
   long long* bw = k <= kGggMaxK ? s_bw : J.bwork;
   for (int v = threadIdx.x; v < n; v += blockDim.x) part[v] = -1;
   for (long long i = threadIdx.x; i < (long long)k * n; i += blockDim.x) conn[i] = 0;
+  for (long long i = threadIdx.x; i < (long long)k * nch; i += blockDim.x) cmx[i] = 0;
   for (int b = threadIdx.x; b < k; b += blockDim.x) bw[b] = 0;
   __syncthreads();
-  auto claim_rows = [&](int v, int b) {  // all threads; part[v] / bw by thread 0
-    if (threadIdx.x == 0) {
-      part[v] = b;
-      bw[b] += g_vw[v];
+  if (threadIdx.x < 32) {
+    const int lane = (int)threadIdx.x;
+    auto claim = [&](int v, int b) {  // warp 0
+      if (lane == 0) {
+        part[v] = b;
+        bw[b] += g_vw[v];
+      }
+      for (int x = lane; x < k; x += 32) conn[(long long)x * n + v] = -1;
+      __syncwarp();
+      int* cb = conn + (long long)b * n;
+      int* mb = cmx + (long long)b * nch;
+      for (int e = g_off[v] + lane; e < g_off[v + 1]; e += 32) {
+        const int u = g_tgt[e];
+        const int c0 = cb[u];
+        if (u == v || c0 < 0) continue;  // assigned (distinct u per row)
+        const int c = c0 + g_w[e];
+        cb[u] = c;
+        atomicMax(mb + (u >> 5), c);
+      }
+      __syncwarp();
+    };
+    for (int b = 0; b < k; ++b) claim(seeds[b], b);
+    int next_free = 0;  // lane-uniform
+    for (int assigned = k; assigned < n; ++assigned) {
+      // lightest block, lowest id on ties (block weights < 2^31: totals are
+      // checked on upload): warp min-reduce, then the lowest lane attaining it
+      unsigned bwv = 0xffffffffu;
+      int bb = INT_MAX;
+      for (int b = lane; b < k; b += 32) {
+        const unsigned x = (unsigned)bw[b];
+        if (x < bwv) { bwv = x; bb = b; }
+      }
+      const unsigned mn = __reduce_min_sync(0xffffffffu, bwv);
+      bb = (int)__reduce_min_sync(0xffffffffu, bwv == mn ? (unsigned)bb : 0xffffffffu);
+      const int* cb = conn + (long long)bb * n;
+      int* mb = cmx + (long long)bb * nch;
+      int gv = -1;
+      for (;;) {
+        int bc = 0, bch = INT_MAX;  // largest bound, lowest chunk
+        for (int c = lane; c < nch; c += 32) {
+          const int x = mb[c];
+          if (x > bc) { bc = x; bch = c; }
+        }
+        const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)bc);
+        if (mx <= 0) break;  // frontier dry
+        bch = (int)__reduce_min_sync(0xffffffffu, bc == mx ? (unsigned)bch : 0xffffffffu);
+        const int u = (bch << 5) + lane;
+        const int cu = u < n ? max(cb[u], 0) : 0;
+        const int cm = (int)__reduce_max_sync(0xffffffffu, (unsigned)cu);
+        if (cm == mx) {
+          gv = (bch << 5) + __ffs(__ballot_sync(0xffffffffu, cu == cm)) - 1;
+          break;
+        }
+        if (lane == 0) mb[bch] = cm;  // stale bound: repair, retry
+        __syncwarp();
+      }
+      if (gv < 0) {  // frontier dried up: lowest unassigned vertex
+        while (part[next_free] >= 0) ++next_free;
+        gv = next_free;
+      }
+      claim(gv, bb);
     }
-    for (int e = g_off[v] + threadIdx.x; e < g_off[v + 1]; e += blockDim.x) {
-      const int u = g_tgt[e];
-      if (u != v && part[u] < 0) conn[(long long)b * n + u] += g_w[e];  // distinct u per thread
-    }
-  };
-  for (int b = 0; b < k; ++b) {
-    claim_rows(seeds[b], b);
-    __syncthreads();
   }
-  int next_free = 0;  // identical in every thread
-  for (int assigned = k; assigned < n; ++assigned) {
-    long long bwv = LLONG_MAX;
-    int bb = 0;
-    for (int b = 0; b < k; ++b) {  // lightest block, lowest id on ties
-      const long long x = bw[b];
-      if (x < bwv) { bwv = x; bb = b; }
-    }
-    const int* cb = conn + (long long)bb * n;
-    int bc = 0, bv = INT_MAX;
-    for (int u = threadIdx.x; u < n; u += blockDim.x) {
-      const int c = cb[u];
-      if (c > bc && part[u] < 0) { bc = c; bv = u; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int a2 = __shfl_xor_sync(0xffffffffu, bc, o), b2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      if (a2 > bc || (a2 == bc && b2 < bv)) { bc = a2; bv = b2; }
-    }
-    if (lane_id() == 0) { sa[threadIdx.x >> 5] = bc; sb[threadIdx.x >> 5] = bv; }
-    __syncthreads();
-    int ga = sa[0], gv = sb[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
-      if (sa[i] > ga || (sa[i] == ga && sb[i] < gv)) { ga = sa[i]; gv = sb[i]; }
-    if (ga == 0) {  // frontier dried up: lowest unassigned vertex (CTA-uniform)
-      while (part[next_free] >= 0) ++next_free;
-      gv = next_free;
-      __syncthreads();  // every thread has scanned part[] before the claim writes it
-    }
-    claim_rows(gv, bb);
-    __syncthreads();
-  }
+  __syncthreads();
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = part[v];
 }
 
@@ -709,7 +736,8 @@ static void launch_ggg(const std::vector<DevGraph>& gs, int k, const std::vector
   std::vector<size_t> words((size_t)J);
   for (int j = 0; j < J; ++j) {
     const DevGraph& g = gs[(size_t)j];
-    words[(size_t)j] = (size_t)2 * g.n + k + (size_t)k * g.n + ((size_t)g.n + 31) / 32;
+    words[(size_t)j] = (size_t)2 * g.n + k + (size_t)k * g.n + ((size_t)g.n + 31) / 32 +
+                       (size_t)k * (((size_t)g.n + 31) / 32);
     max_words = std::max(max_words, words[(size_t)j]);
     max_staged = std::max(max_staged, words[(size_t)j] + (size_t)g.n + 1 + 2 * (size_t)g.m2 + g.n);
   }
