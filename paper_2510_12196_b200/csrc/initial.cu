@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
 // cost one step of the warp.
 
 constexpr int kGgCh = 256;
+constexpr int kGggMaxDry = 1024;  // known-dry flags for k up to this
 constexpr int kGgSc = 256;
 constexpr int kGgWarpRow = 128;
 
@@ -348,7 +349,13 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   __shared__ int sa[kGggWarps], sb[kGggWarps];
   __shared__ int s_cmd, s_v, s_b;
   __shared__ long long s_bw[kGggMaxK];
+  // known-dry blocks: bit b set = b's frontier was found empty and b has
+  // claimed only isolated vertices since (only b's own claims can grow b's
+  // frontier), so its next query can be skipped
+  __shared__ unsigned s_dry[(kGggMaxDry + 31) / 32];
   const int nch = (n + kGgCh - 1) / kGgCh, nsc = (nch + kGgSc - 1) / kGgSc;
+  const bool track_dry = k <= kGggMaxDry;
+  for (int i = threadIdx.x; i < (kGggMaxDry + 31) / 32; i += blockDim.x) s_dry[i] = 0;
   int* smax = J.smax_smem ? sm : J.gsmax;
   long long* bw = k <= kGggMaxK ? s_bw : J.bwork;
   if (k == 1) {
@@ -378,24 +385,22 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     if (warp == 0) {
       int cmd = 2;
       while (assigned < n) {
-        // lightest block, lowest id on ties
-        long long bwv = LLONG_MAX;
+        // lightest block, lowest id on ties (weights < 2^31: totals are
+        // checked on upload): warp min-reduce, lowest lane attaining it
+        unsigned bwv = 0xffffffffu;
         int bb = INT_MAX;
         for (int b = lane; b < k; b += 32) {
-          const long long x = bw[b];
+          const unsigned x = (unsigned)bw[b];
           if (x < bwv) { bwv = x; bb = b; }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const long long x2 = __shfl_xor_sync(0xffffffffu, bwv, o);
-          const int b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-          if (x2 < bwv || (x2 == bwv && b2 < bb)) { bwv = x2; bb = b2; }
-        }
+        const unsigned mn = __reduce_min_sync(0xffffffffu, bwv);
+        bb = (int)__reduce_min_sync(0xffffffffu, bwv == mn ? (unsigned)bb : 0xffffffffu);
         int* cb = J.conn + (size_t)bb * n;
         int* mb = J.cmax + (size_t)bb * nch;
         int* sbm = smax + (size_t)bb * nsc;
         int v = -1;
-        for (;;) {  // query with lazy repair of stale bounds
+        const bool known_dry = track_dry && ((s_dry[bb >> 5] >> (bb & 31)) & 1u);
+        for (; !known_dry;) {  // query with lazy repair of stale bounds
           int top = 0, ts = INT_MAX;
           for (int i = lane; i < nsc; i += 32) {
             const int x = J.smax_smem ? sbm[i] : __ldcg(sbm + i);
@@ -407,7 +412,11 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             const int s2 = __shfl_xor_sync(0xffffffffu, ts, o);
             if (x2 > top || (x2 == top && s2 < ts)) { top = x2; ts = s2; }
           }
-          if (top == 0) break;  // every frontier bound is empty
+          if (top == 0) {  // every frontier bound is empty
+            if (track_dry && lane == 0) s_dry[bb >> 5] |= 1u << (bb & 31);
+            __syncwarp();
+            break;
+          }
           // lowest chunk of superchunk ts whose bound equals top
           const int c0 = ts * kGgSc;
           int cm[kGgSc / 32];
@@ -505,8 +514,17 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         if (lane == 0) {
           J.part[v] = bb;
           bw[bb] += vwv;
+          // bb may have a frontier after a claim with neighbours
+          if (deg > 0 && track_dry) s_dry[bb >> 5] &= ~(1u << (bb & 31));
         }
-        for (int b2 = lane; b2 < k; b2 += 32) __stcg(J.conn + (size_t)b2 * n + v, INT_MIN);
+        // assigned marks: an isolated vertex never enters a frontier (no
+        // neighbour raises its conn), so only block 0's row — the fallback
+        // scan's "unassigned" test — needs the mark; others need all k
+        if (deg > 0) {
+          for (int b2 = lane; b2 < k; b2 += 32) __stcg(J.conn + (size_t)b2 * n + v, INT_MIN);
+        } else if (lane == 0) {
+          __stcg(J.conn + v, INT_MIN);
+        }
         ++assigned;
         __syncwarp();
         if (deg > kGgWarpRow) {  // hub row: the whole CTA updates it
