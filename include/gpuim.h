@@ -40,6 +40,7 @@ extern "C" {
 #define GIM_E_EMPTY 6       /* empty graph (reference raises ValueError)     */
 #define GIM_E_FORMAT 7      /* malformed METIS file (MetisFormatError)       */
 #define GIM_E_IO 8          /* file cannot be opened / read                  */
+#define GIM_E_CALLBACK 9    /* a caller callback returned nonzero (plugin)   */
 
 #define GIM_MAX_LEVELS 32
 
@@ -281,6 +282,38 @@ int gim_hierarchical_multisection_host(int64_t n, const int64_t* offsets, const 
                                        const int64_t* vertex_weights, const gim_topology* t,
                                        double eps, uint64_t seed, int64_t* out_assignment,
                                        int64_t* out_block_weights, void* stream);
+
+/* Plugin seam of hierarchical_multisection (pipelines.py:49-110): the
+ * caller's partitioner, called once per tree node with parts > 1 in the
+ * reference's depth-first order, receives the node's subgraph as HOST int64
+ * CSR arrays (order-preserving local ids, graph.py:357-389), the node's
+ * parts, eps_local (Eq. 2), seed and identifier, writes part[n] in
+ * [0, parts) and returns 0 — nonzero aborts the call with GIM_E_CALLBACK.
+ * NULL = the built-in GPU partitioner. */
+typedef int (*gim_partition_fn)(void* user, int64_t n, const int64_t* offsets,
+                                const int64_t* targets, const int64_t* edge_weights,
+                                const int64_t* vertex_weights, int32_t parts, double eps_local,
+                                uint64_t seed, const int32_t* ident, int32_t ident_len,
+                                int64_t* out_part);
+
+/* Trace record of one partitioning step (pipelines.py:36-47 SplitRecord,
+ * appended at :98-104): level, identifier, parts, eps_local, subgraph
+ * weight, the parts' block weights, budget met. */
+typedef void (*gim_trace_fn)(void* user, int32_t level, const int32_t* ident, int32_t ident_len,
+                             int32_t parts, double eps_local, int64_t subgraph_weight,
+                             const int64_t* block_weights, int32_t budget_met);
+
+/* hierarchical_multisection with the plugin seam and trace records, on HOST
+ * int64 CSR arrays (depth-first, the reference's node order; each node's
+ * extraction, block weights and the built-in partitioner run on the GPU).
+ * partition / trace may be NULL. */
+int gim_hierarchical_multisection_plugin(int64_t n, const int64_t* offsets,
+                                         const int64_t* targets, const int64_t* edge_weights,
+                                         const int64_t* vertex_weights, const gim_topology* t,
+                                         double eps, uint64_t seed, gim_partition_fn partition,
+                                         gim_trace_fn trace, void* user,
+                                         int64_t* out_assignment, int64_t* out_block_weights,
+                                         void* stream);
 
 /* ---- the drop-in ------------------------------------------------------- */
 /* Default keyword arguments of integrated_map. */

@@ -21,6 +21,7 @@ GIM_E_INTERNAL = 5
 GIM_E_EMPTY = 6
 GIM_E_FORMAT = 7
 GIM_E_IO = 8
+GIM_E_CALLBACK = 9
 
 
 class GimGraph(C.Structure):
@@ -142,6 +143,7 @@ SIGNATURES: dict[str, list] = {
     "gim_hierarchical_multisection": [GP, TP, DBL, U64, P, P],
     "gim_hierarchical_multisection_host": [I64, P, P, P, P, TP, DBL, U64, P, P, P],
     "gim_default_params": [PARP],
+    "gim_hierarchical_multisection_plugin": [I64, P, P, P, P, TP, DBL, U64, P, P, P, P, P, P],
     "gim_integrated_map_device": [GP, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_integrated_map": [I64, P, P, P, P, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_fill_sources": [I32, P, P, P],
@@ -164,6 +166,15 @@ RESTYPES = {"gim_last_error": C.c_char_p, "gim_launch_count": C.c_int64,
             "gim_set_rowwise_contraction": None}
 
 _lib = None
+
+
+# plugin-seam callbacks (include/gpuim.h gim_partition_fn / gim_trace_fn)
+PARTITION_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                           C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                           C.c_int32, C.c_double, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
+                           C.POINTER(C.c_int64))
+TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                       C.c_double, C.c_int64, C.POINTER(C.c_int64), C.c_int32)
 
 
 class GimError(RuntimeError):

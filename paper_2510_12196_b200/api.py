@@ -107,26 +107,108 @@ def integrated_map(g, t, eps: float, seed: int = 0, *, coarsest_factor: int = 12
     return m
 
 
+@dataclass
+class SplitRecord:
+    """Mirror of promap.pipelines.SplitRecord (pipelines.py:36-47), used when
+    the reference package is not importable."""
+
+    level: int
+    identifier: tuple
+    parts: int
+    eps_local: float
+    subgraph_weight: int
+    block_weights: list
+    budget_met: bool
+
+
+def _split_record_type():
+    try:
+        from promap.pipelines import SplitRecord as RefSplitRecord
+        return RefSplitRecord
+    except Exception:  # noqa: BLE001 - reference absent
+        return SplitRecord
+
+
+def _graph_type():
+    try:
+        from promap.graph import Graph as RefGraph
+        return RefGraph
+    except Exception:  # noqa: BLE001 - reference absent
+        from .generators import HostGraph
+        return HostGraph
+
+
 def hierarchical_multisection(g, t, eps: float, partitioner=None, seed: int = 0,
                               trace: list | None = None):
     """GPU-HM: recursive multisection along the machine hierarchy
-    (pipelines.py:49-110) of the whole graph on the B200, with the built-in
-    multilevel partitioner.  Same signature and return type as the
-    reference; `ValueError` on an empty graph.  The reference's plugin seam
-    (a Python `partitioner` callable) and `trace` records run the user's
-    Python code per tree node and are not part of the GPU path: they raise
-    NotImplementedError (use the reference package for them)."""
+    (pipelines.py:49-110) of the whole graph on the B200.  Same signature,
+    return type and errors as the reference, including its plugin seam: a
+    `partitioner(sub, parts, eps_local, seed)` callable is called per tree
+    node in the reference's depth-first order with the node's subgraph (a
+    reference `Graph`), its exceptions surface as `RuntimeError("partitioner
+    failed at hierarchy node [...]")` and invalid outputs as
+    `RuntimeError("partitioner returned an invalid assignment at node
+    [...]")`; `trace` receives one SplitRecord per partitioning step.  The
+    tree (extraction, block weights, the built-in partitioner) runs on the
+    GPU; only the caller's own partitioner runs on the host."""
+    from . import _lib
     from . import device as D
 
     n = len(g.offsets) - 1
     if n == 0:
         raise ValueError("cannot map an empty graph")
-    if partitioner is not None or trace is not None:
-        raise NotImplementedError(
-            "custom partitioners / trace records are not supported on the GPU path")
-    a, bw = D.hierarchical_multisection_host(g.offsets, g.edge_targets, g.edge_weights,
-                                             g.vertex_weights, tuple(t.hierarchy),
-                                             tuple(t.distances), eps, seed)
+    if partitioner is None and trace is None:
+        a, bw = D.hierarchical_multisection_host(g.offsets, g.edge_targets, g.edge_weights,
+                                                 g.vertex_weights, tuple(t.hierarchy),
+                                                 tuple(t.distances), eps, seed)
+        return _mapping_type()(a, bw)
+    failure: list = []
+    part_cb = trace_cb = None
+    if partitioner is not None:
+        Graph = _graph_type()
+
+        def _part(_user, nn, off, tgt, ew, vw, parts, eps_local, node_seed, ident, ilen, out):
+            try:
+                ids = [ident[i] for i in range(ilen)]
+                o = np.ctypeslib.as_array(off, shape=(nn + 1,)).copy()
+                m2 = int(o[-1])
+                arr = (lambda p: np.ctypeslib.as_array(p, shape=(m2,)).copy()) if m2 else \
+                    (lambda p: np.zeros(0, dtype=np.int64))
+                sub = Graph(o, arr(tgt), arr(ew), np.ctypeslib.as_array(vw, shape=(nn,)).copy())
+                try:
+                    part = np.asarray(partitioner(sub, int(parts), float(eps_local),
+                                                  int(node_seed)), dtype=np.int64)
+                except Exception as exc:  # noqa: BLE001 - wrapped like the reference
+                    err = RuntimeError(f"partitioner failed at hierarchy node {ids}")
+                    err.__cause__ = exc
+                    failure.append(err)
+                    return 1
+                if len(part) != nn or part.min() < 0 or part.max() >= parts:
+                    failure.append(RuntimeError(
+                        f"partitioner returned an invalid assignment at node {ids}"))
+                    return 1
+                np.ctypeslib.as_array(out, shape=(nn,))[:] = part
+                return 0
+            except BaseException as exc:  # noqa: BLE001 - re-raised after the call
+                failure.append(exc)
+                return 1
+        part_cb = _lib.PARTITION_FN(_part)
+    if trace is not None:
+        Rec = _split_record_type()
+
+        def _trace(_user, level, ident, ilen, parts, eps_local, sub_weight, bws, met):
+            trace.append(Rec(int(level), tuple(ident[i] for i in range(ilen)), int(parts),
+                             float(eps_local), int(sub_weight),
+                             [int(bws[i]) for i in range(parts)], bool(met)))
+        trace_cb = _lib.TRACE_FN(_trace)
+    try:
+        a, bw = D.hierarchical_multisection_plugin(
+            g.offsets, g.edge_targets, g.edge_weights, g.vertex_weights, tuple(t.hierarchy),
+            tuple(t.distances), eps, seed, part_cb, trace_cb)
+    except _lib.GimError as exc:
+        if exc.status == _lib.GIM_E_CALLBACK and failure:
+            raise failure[0] from failure[0].__cause__
+        raise
     return _mapping_type()(a, bw)
 
 

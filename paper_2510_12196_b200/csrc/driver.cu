@@ -990,6 +990,89 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     if (e) std::rethrow_exception(e);
 }
 
+// Plugin-seam multisection (gim_hierarchical_multisection_plugin): the
+// reference's depth-first recursion node by node (pipelines.py:72-107), so a
+// caller's partitioner sees the nodes — and trace records are produced — in
+// the reference's order.  Extraction, block weights, scatters and the
+// built-in partitioner stay on the GPU; a caller partitioner gets the
+// node's subgraph as host int64 arrays.
+struct PluginCtx {
+  MsCtx* C;
+  gim_partition_fn partition;
+  gim_trace_fn trace;
+  void* user;
+};
+
+static void descend_plugin(PluginCtx& P, const DevGraph& sub, long long sub_total, int level,
+                           std::vector<int>& ident, const int* translation,
+                           unsigned long long node_seed, cudaStream_t s) {
+  MsCtx& C = *P.C;
+  if (sub.n == 0) return;
+  if (level == 0) {
+    scatter_const(sub.n, translation, calc_id(C.h, ident), C.assignment, s);
+    return;
+  }
+  const int parts = (int)C.h[level - 1];
+  long long k_sub = 1;
+  for (int i = 0; i < level; ++i) k_sub *= C.h[i];
+  const double eps_local = adaptive_imbalance(C.eps, C.total, sub_total, C.k, k_sub, level);
+  DBuf<int> part((size_t)std::max(sub.n, 1), s);
+  if (parts == 1) {
+    GIM_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(int) * sub.n, s));
+  } else if (P.partition) {
+    // the node's subgraph to the host as int64 (graph.py:17-39 layout)
+    const size_t n = (size_t)sub.n, m2 = (size_t)sub.m2;
+    std::vector<int> o32(n + 1), t32(m2), w32(m2), v32(n);
+    GIM_CUDA(cudaMemcpyAsync(o32.data(), sub.off, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, s));
+    if (m2) {
+      GIM_CUDA(cudaMemcpyAsync(t32.data(), sub.tgt, sizeof(int) * m2, cudaMemcpyDeviceToHost, s));
+      GIM_CUDA(cudaMemcpyAsync(w32.data(), sub.w, sizeof(int) * m2, cudaMemcpyDeviceToHost, s));
+    }
+    GIM_CUDA(cudaMemcpyAsync(v32.data(), sub.vw, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    std::vector<int64_t> o(o32.begin(), o32.end()), tt(t32.begin(), t32.end()),
+        ww(w32.begin(), w32.end()), vv(v32.begin(), v32.end()), out(n, 0);
+    const int rc = P.partition(P.user, (int64_t)n, o.data(), tt.data(), ww.data(), vv.data(),
+                               parts, eps_local, node_seed, ident.data(), (int32_t)ident.size(),
+                               out.data());
+    GIM_CHECK(rc == 0, GIM_E_CALLBACK, "partitioner callback failed");
+    std::vector<int> p32(n);
+    for (size_t i = 0; i < n; ++i) {
+      GIM_CHECK(out[i] >= 0 && out[i] < parts, GIM_E_CALLBACK, "partitioner returned an invalid assignment");
+      p32[i] = (int)out[i];
+    }
+    GIM_CUDA(cudaMemcpyAsync(part.get(), p32.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    GIM_CUDA(sync_stream(s));
+  } else {
+    internal_partitioner(sub, sub_total, parts, eps_local, node_seed, part.get(), *C.st, s);
+  }
+  DBuf<long long> bw((size_t)parts, s);
+  block_weights(sub.n, sub.vw, part.get(), parts, bw.get(), s);
+  std::vector<long long> child_total((size_t)parts);
+  GIM_CUDA(cudaMemcpyAsync(child_total.data(), bw.get(), sizeof(long long) * parts,
+                           cudaMemcpyDeviceToHost, s));
+  GIM_CUDA(sync_stream(s));
+  if (P.trace) {
+    long long mx = 0;
+    for (long long x : child_total) mx = std::max(mx, x);
+    const double budget = (1.0 + eps_local) * (double)sub_total / (double)parts;
+    std::vector<int64_t> bw64(child_total.begin(), child_total.end());
+    P.trace(P.user, level, ident.data(), (int32_t)ident.size(), parts, eps_local, sub_total,
+            bw64.data(), (double)mx <= budget ? 1 : 0);
+  }
+  std::vector<OwnedGraph> subs;
+  std::vector<DBuf<int>> ids;
+  extract_subgraphs(sub, part.get(), parts, subs, ids, s);
+  for (int j = 0; j < parts; ++j) {
+    DBuf<int> tr((size_t)std::max(subs[j].n, 1), s);
+    gather(subs[j].n, ids[j].get(), translation, tr.get(), s);
+    ident.push_back(j);
+    descend_plugin(P, subs[j].view(), child_total[j], level - 1, ident, tr.get(),
+                   hash2(node_seed, (unsigned long long)level, (unsigned long long)j), s);
+    ident.pop_back();
+  }
+}
+
 // Breadth-first multisection: all nodes of one tree level are partitioned
 // together — as one batch when they are small (internal_partitioner_batch),
 // else one host thread per node — then all their children are extracted.
@@ -1985,6 +2068,52 @@ extern "C" int gim_hierarchical_multisection_host(int64_t n, const int64_t* offs
                              cudaMemcpyDeviceToHost, s));
     GIM_CUDA(sync_stream(s));
     for (long long i = 0; i < n; ++i) out_assignment[i] = h_part[i];
+  });
+}
+
+extern "C" int gim_hierarchical_multisection_plugin(
+    int64_t n, const int64_t* offsets, const int64_t* targets, const int64_t* edge_weights,
+    const int64_t* vertex_weights, const gim_topology* t, double eps, uint64_t seed,
+    gim_partition_fn partition, gim_trace_fn trace, void* user, int64_t* out_assignment,
+    int64_t* out_block_weights, void* stream) {
+  return guard([&] {
+    GIM_CHECK(t && offsets && out_assignment && out_block_weights, GIM_E_INVALID,
+              "null argument");
+    GIM_CHECK(n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+    cudaStream_t s = (cudaStream_t)stream;
+    RunCtx rc;
+    rc.f = default_flags();
+    CtxScope scope(&rc);
+    OwnedGraph G;
+    upload_graph(n, offsets, targets, edge_weights, vertex_weights, G, s);
+    Topo tp = get_topo(*t);
+    std::vector<long long> h(t->hierarchy, t->hierarchy + t->levels);
+    DBuf<int> part((size_t)n, s);
+    DBuf<long long> bw((size_t)tp.k, s);
+    RunStats st;
+    MsCtx C;
+    C.h = h;
+    C.k = tp.k;
+    C.total = G.total_vw;
+    C.eps = eps;
+    C.assignment = part.get();
+    C.st = &st;
+    C.threads = false;
+    GIM_CUDA(cudaGetDevice(&C.device));
+    GIM_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(int) * n, s));
+    DBuf<int> ident_ids((size_t)n, s);
+    k_iota<<<grid_for(n, 256), 256, 0, s>>>((int)n, ident_ids.get());
+    count_launch();
+    PluginCtx P{&C, partition, trace, user};
+    std::vector<int> ident;
+    descend_plugin(P, G.view(), G.total_vw, (int)h.size(), ident, ident_ids.get(), seed, s);
+    block_weights((int)n, G.vw.get(), part.get(), tp.k, bw.get(), s);
+    std::vector<int> hp((size_t)n);
+    GIM_CUDA(cudaMemcpyAsync(hp.data(), part.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(cudaMemcpyAsync(out_block_weights, bw.get(), sizeof(long long) * tp.k,
+                             cudaMemcpyDeviceToHost, s));
+    GIM_CUDA(sync_stream(s));
+    for (long long i = 0; i < n; ++i) out_assignment[i] = hp[(size_t)i];
   });
 }
 

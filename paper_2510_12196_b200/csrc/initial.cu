@@ -381,6 +381,13 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   }
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   int assigned = k, next_free = 0;  // warp 0's loop state (uniform in the warp)
+  // fallback window: vertices [win, win + 32) one per lane — unassigned
+  // flag, degree, weight — so runs of fallback claims (the isolated vertices
+  // of stalled R-MAT coarsest graphs) cost no global loads; every claim
+  // inside the window clears its lane's flag
+  int win = -64;
+  bool w_free = false;
+  int w_deg = 0, w_vw = 0;
   for (;;) {
     if (warp == 0) {
       int cmd = 2;
@@ -496,21 +503,32 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
           }
           __syncwarp();
         }
+        int vwv, deg;
         if (v < 0) {  // frontier dried up: lowest unassigned vertex
           for (;;) {
-            const int u = next_free + lane;
-            const bool fr = u < n && __ldcg(J.conn + u) >= 0;  // block 0's row marks assigned
-            const unsigned m = __ballot_sync(0xffffffffu, fr);
+            if (next_free < win || next_free >= win + 32) {
+              win = next_free;
+              const int u = win + lane;
+              w_free = u < n && __ldcg(J.conn + u) >= 0;  // block 0's row marks assigned
+              w_deg = u < n ? __ldg(J.off + u + 1) - __ldg(J.off + u) : 0;
+              w_vw = u < n ? __ldg(J.vw + u) : 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, w_free && win + lane >= next_free);
             if (m) {
-              v = next_free + __ffs(m) - 1;
+              const int l = __ffs(m) - 1;
+              v = win + l;
+              deg = __shfl_sync(0xffffffffu, w_deg, l);
+              vwv = __shfl_sync(0xffffffffu, w_vw, l);
               next_free = v;
               break;
             }
-            next_free += 32;
+            next_free = win + 32;
           }
+        } else {
+          vwv = __ldg(J.vw + v);
+          deg = __ldg(J.off + v + 1) - __ldg(J.off + v);
         }
-        const int vwv = __ldg(J.vw + v);
-        const int deg = __ldg(J.off + v + 1) - __ldg(J.off + v);
+        if (v >= win && v < win + 32 && lane == v - win) w_free = false;
         if (lane == 0) {
           J.part[v] = bb;
           bw[bb] += vwv;

@@ -440,6 +440,28 @@ def hierarchical_multisection_host(offsets, targets, eweights, vweights, hierarc
     return a, bw
 
 
+def hierarchical_multisection_plugin(offsets, targets, eweights, vweights, hierarchy, distances,
+                                     eps: float, seed: int, partition_cb=None, trace_cb=None):
+    """GPU-HM with the reference's plugin seam (pipelines.py:49-110): ctypes
+    callbacks (_lib.PARTITION_FN / TRACE_FN, or None) called per tree node in
+    depth-first order -> (assignment int64 np, block weights int64 np)."""
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    tgt = np.ascontiguousarray(targets, dtype=np.int64)
+    ew = np.ascontiguousarray(eweights, dtype=np.int64)
+    vw = np.ascontiguousarray(vweights, dtype=np.int64)
+    n = len(off) - 1
+    k = int(np.prod(hierarchy))
+    a = np.empty(max(n, 0), dtype=np.int64)
+    bw = np.empty(k, dtype=np.int64)
+    t = topology_struct(hierarchy, distances)
+    ptr = lambda x: x.ctypes.data if x.size else None  # noqa: E731
+    fn = lambda cb: C.cast(cb, C.c_void_p).value if cb is not None else None  # noqa: E731
+    _lib.call("gim_hierarchical_multisection_plugin", int(n), ptr(off), ptr(tgt), ptr(ew),
+              ptr(vw), C.byref(t), float(eps), int(seed) & (2**64 - 1), fn(partition_cb),
+              fn(trace_cb), None, ptr(a), ptr(bw), stream_ptr())
+    return a, bw
+
+
 def set_fanout(on: bool) -> None:
     """Sibling multisection subtrees on concurrent host threads/streams."""
     _lib.load().gim_set_fanout(1 if on else 0)

@@ -77,11 +77,16 @@ def test_cli_map_metis_on_gpu(promap, tmp_path):
         a = np.loadtxt(out, dtype=np.int64)
         st = json.loads(stats.read_text())
         assert len(a) == g.n and st["balanced"]
-        # same mapping as the reference's CPU code on the same input
+        # same mapping as the reference's own CPU code on the same input
+        from paper_2510_12196_b200 import install, uninstall
         from promap import pipelines
         t = promap.topology.Topology((2, 2, 2), (1, 10, 100))
-        cpu = (pipelines._cpu_integrated_map(g, t, 0.03, seed=1, coarsest_factor=16)
-               if algo == "im" else pipelines._cpu_hierarchical_multisection(g, t, 0.03, seed=1))
+        uninstall()
+        try:
+            cpu = (pipelines.integrated_map(g, t, 0.03, seed=1, coarsest_factor=16)
+                   if algo == "im" else pipelines.hierarchical_multisection(g, t, 0.03, seed=1))
+        finally:
+            install()
         assert np.array_equal(a, cpu.assignment)
 
 
