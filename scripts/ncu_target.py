@@ -26,9 +26,21 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", choices=["step", "lp", "refine0"], default="step")
     ap.add_argument("--logn", type=int, default=20)
+    ap.add_argument("--level", type=int, default=0,
+                    help="refine0: refine this level of the stack instead of level 0")
     args = ap.parse_args()
     g = gen_rgg(1 << args.logn, 0.55, 1)
     dg = D.DeviceGraph.from_host(g)
+    if args.mode == "refine0" and args.level > 0:
+        k0 = 1
+        for x in H:
+            k0 *= x
+        l_max0 = 1.03 * dg.total_weight / k0
+        for li in range(args.level):  # coarsen down to the requested level
+            partner = D.match_graph(dg, l_max0, 1000 + li)
+            cmap, n_c = D.coarse_map(partner)
+            dg = D.contract(dg, cmap, n_c)
+        print("level", args.level, "n", dg.n, "m2", dg.m2)
     a, bw, st = D.integrated_map_device(dg, H, DIST, 0.03, 0)
     torch.cuda.synchronize()
     prof = torch.cuda.profiler
@@ -50,8 +62,9 @@ def main():
         l_max = 1.03 * dg.total_weight / k
         torch.cuda.synchronize()
         prof.start()
-        D.refine(dg, H, DIST, a, bw2, i_max=12, i_w_max=10, sigma_fraction=0.005, seed=3,
-                 l_max=l_max)
+        D.refine(dg, H, DIST, a, bw2, i_max=12 + args.level,
+                 i_w_max=10 if args.level == 0 else 2,
+                 sigma_fraction=0.005 if args.level == 0 else 0.03, seed=3, l_max=l_max)
         torch.cuda.synchronize()
         prof.stop()
     else:

@@ -357,7 +357,9 @@ def test_gpu_hm_matches_oracle_rgg(D):
     t = O.OTopology((4, 8, 2), (1, 10, 100))
     m = hierarchical_multisection(g, t, 0.03, seed=4)
     assert np.array_equal(m.assignment, O.hierarchical_multisection(g, t, 0.03, seed=4))
-    with pytest.raises(NotImplementedError):
+    # a partitioner returning nothing fails like the reference's seam
+    # (pipelines.py:86-93): RuntimeError naming the node
+    with pytest.raises(RuntimeError, match="partitioner failed at hierarchy node"):
         hierarchical_multisection(g, t, 0.03, partitioner=lambda *a: None)
 
 
