@@ -503,6 +503,34 @@ static std::vector<Level> build_level_stack(const DevGraph& g0, double l_max, lo
 }
 
 // ---------------------------------------------------------------------------
+// GIM_TRACE_MS: host-wall ms of the multisection's tree levels and of the
+// general-path partitioner's phases (stream-synchronised; diagnostics only)
+static bool trace_ms() {
+  static const bool on = std::getenv("GIM_TRACE_MS") != nullptr;
+  return on;
+}
+
+struct MsTimer {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0;
+  MsTimer(cudaStream_t st) : on(trace_ms()), s(st) {
+    if (on) {
+      sync_stream(s);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  double lap() {
+    if (!on) return 0.0;
+    sync_stream(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+    return ms;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // internal partitioner (pipelines.py:191-218)
 
 static void internal_partitioner(const DevGraph& g, long long total, int parts, double eps_local,
@@ -520,11 +548,14 @@ static void internal_partitioner(const DevGraph& g, long long total, int parts, 
   }
   Topo tf = get_flat_topo(parts);
   const double l_max = (1.0 + eps_local) * (double)total / (double)parts;
+  MsTimer tm(s);
   std::vector<Level> levels =
       build_level_stack(g, l_max, std::max<long long>(64ll * parts, 2), seed, s);
+  const double t_stack = tm.lap();
   const int nl = (int)levels.size();
   DBuf<int> cur((size_t)std::max(levels.back().g.n, 1), s);
   greedy_graph_growing(levels.back().g, parts, cur.get(), s);
+  const double t_ggg = tm.lap();
   DBuf<long long> bw((size_t)parts, s);
   RefineBuffers rb;
   alloc_refine_buffers(rb, g.n, parts, s);  // finest level: serves all levels
@@ -542,6 +573,9 @@ static void internal_partitioner(const DevGraph& g, long long total, int parts, 
     refine(L.rl, tf, cur.get(), bw.get(), cfg, l_max, st, rb, s);
   }
   GIM_CUDA(cudaMemcpyAsync(part, cur.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  if (tm.on)
+    std::fprintf(stderr, "partitioner n=%d parts=%d levels=%d coarsest=%d | stack %.3f ms ggg %.3f ms refine %.3f ms\n",
+                 n, parts, nl, levels.back().g.n, t_stack, t_ggg, tm.lap());
 }
 
 // ---------------------------------------------------------------------------
@@ -1096,11 +1130,14 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
   nodes[0].trans = ids;
   nodes[0].total = total;
   nodes[0].seed = seed;
+  MsTimer tm(s);
   for (int level = (int)C.h.size(); level >= 1; --level) {
     const int parts = (int)C.h[level - 1];
     long long k_sub = 1;
     for (int i = 0; i < level; ++i) k_sub *= C.h[i];
     const int N = (int)nodes.size();
+    if (tm.on && level < (int)C.h.size())
+      std::fprintf(stderr, "ms extraction into tree level %d: %.3f ms\n", level, tm.lap());
     std::vector<DBuf<int>> part((size_t)N);
     for (int j = 0; j < N; ++j) part[(size_t)j] = DBuf<int>((size_t)std::max(nodes[(size_t)j].g.n, 1), s);
     bool small = parts > 1;
@@ -1153,6 +1190,16 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
       for (auto& w : workers) w.join();
       for (auto& e : errs)
         if (e) std::rethrow_exception(e);
+    }
+    if (tm.on) {
+      long long tot_n = 0;
+      int mx = 0;
+      for (const MsNode& nd : nodes) {
+        tot_n += nd.g.n;
+        mx = std::max(mx, nd.g.n);
+      }
+      std::fprintf(stderr, "ms tree level %d: %d nodes (sum n %lld, max %d, parts %d) %s: %.3f ms\n",
+                   level, N, tot_n, mx, parts, small ? "batch" : "general", tm.lap());
     }
     if (level == 1) {  // leaves (pipelines.py:78-80)
       for (int j = 0; j < N; ++j) {
