@@ -9,7 +9,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgpuim.so"
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GIM_LIB_NAME", "libgpuim.so")
 MAX_LEVELS = 32
 
 GIM_OK = 0

@@ -52,8 +52,15 @@ namespace gim {
 
 constexpr int kFusedBlock = 256;
 constexpr int kFusedWarps = kFusedBlock / 32;
-// co-resident CTAs per SM the grid kernels are compiled for (register cap)
-constexpr int kFusedMinBlocks = 3;
+// co-resident CTAs per SM the grid kernels are compiled for (register cap).
+// GIM build flag -DGIM_FUSED_MIN_BLOCKS overrides for A/B runs.
+#ifndef GIM_FUSED_MIN_BLOCKS
+#define GIM_FUSED_MIN_BLOCKS 3
+#endif
+constexpr int kFusedMinBlocks = GIM_FUSED_MIN_BLOCKS;
+// batched cluster refinements occupy a few clusters at most: compiled for 2
+// CTAs per SM, which removes the register spills (570 B per thread at 3)
+constexpr int kClusterMinBlocks = 2;
 constexpr int kMaxCluster = 16;
 // vertex-centric first filter when a level has at most this many vertex
 // groups per warp (else edge-parallel boundary pass + lists)
@@ -1211,7 +1218,7 @@ __global__ void __launch_bounds__(kFusedBlock, kFusedMinBlocks) k_refine_fused(F
 
 // one thread-block cluster per independent refinement (batched launch)
 template <int VW>
-__global__ void __launch_bounds__(kFusedBlock, kFusedMinBlocks) k_refine_cluster_batch(const FusedArgs* args,
+__global__ void __launch_bounds__(kFusedBlock, kClusterMinBlocks) k_refine_cluster_batch(const FusedArgs* args,
                                                                       int csize) {
   refine_body<VW>(args[blockIdx.x / csize]);
 }
@@ -1932,18 +1939,14 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
   }
   GIM_CUDA(cudaMemcpyAsync(dargs.get(), ordered.data(), sizeof(FusedArgs) * (size_t)J,
                            cudaMemcpyHostToDevice, s));  // pageable: staged before return
-  static std::once_flag once[4];
   for (const Grp& g : groups) {
     void* fn = nullptr;
-    int slot = 0;
     switch (g.vw) {
-      case 4: fn = (void*)k_refine_cluster_batch<4>; slot = 0; break;
-      case 8: fn = (void*)k_refine_cluster_batch<8>; slot = 1; break;
-      case 16: fn = (void*)k_refine_cluster_batch<16>; slot = 2; break;
-      default: fn = (void*)k_refine_cluster_batch<32>; slot = 3; break;
+      case 4: fn = (void*)k_refine_cluster_batch<4>; break;
+      case 8: fn = (void*)k_refine_cluster_batch<8>; break;
+      case 16: fn = (void*)k_refine_cluster_batch<16>; break;
+      default: fn = (void*)k_refine_cluster_batch<32>; break;
     }
-    (void)once;
-    (void)slot;
     raise_dyn_smem_limit(fn);
     const FusedArgs* a = dargs.get() + g.first;
     int cs = g.cs;
