@@ -591,7 +591,21 @@ struct BatchPartJob {
 };
 
 // batch-eligible: small enough that every level refines shared-memory resident
-constexpr int kBatchMaxN = 16384;
+constexpr int kBatchMaxN = 16384;  // batched extraction (CTA per node)
+// Tree levels whose nodes are all at most this large are partitioned by the
+// batched path; larger nodes run the general path, one host thread / stream
+// each.  Measured at rgg 2^22, H=4:8:6 (scripts/ab_env.sh): the six ~4K-vertex
+// nodes of tree level 2 take 10 ms batched (the slowest job's refinement
+// gates every per-level launch) and ~3 ms concurrently on the general path;
+// initial mapping 19.5 -> 15.6 ms.  GIM_BATCH_MAXN overrides.
+constexpr int kBatchPartMaxN = 2048;
+static int batch_max_n() {
+  static const int v = [] {
+    const char* e = std::getenv("GIM_BATCH_MAXN");
+    return e ? std::atoi(e) : kBatchPartMaxN;
+  }();
+  return v;
+}
 
 // jobs the batch hands back: general path, one host thread / stream each
 static void general_parallel(const std::vector<BatchPartJob*>& jobs, int parts, RunStats& st,
@@ -957,7 +971,7 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
     // the children split straight into leaves: partition all of them in one
     // batch (one launch per phase) when they are small
     bool small = true;
-    for (int j = 0; j < parts; ++j) small = small && subs[j].n <= kBatchMaxN;
+    for (int j = 0; j < parts; ++j) small = small && subs[j].n <= batch_max_n();
     if (small) {
       std::vector<BatchPartJob> jobs;
       std::vector<DBuf<int>> cparts((size_t)parts);
@@ -1141,7 +1155,7 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
     std::vector<DBuf<int>> part((size_t)N);
     for (int j = 0; j < N; ++j) part[(size_t)j] = DBuf<int>((size_t)std::max(nodes[(size_t)j].g.n, 1), s);
     bool small = parts > 1;
-    for (const MsNode& nd : nodes) small = small && nd.g.n <= kBatchMaxN;
+    for (const MsNode& nd : nodes) small = small && nd.g.n <= batch_max_n();
     if (parts == 1) {
       for (int j = 0; j < N; ++j)
         GIM_CUDA(cudaMemsetAsync(part[(size_t)j].get(), 0, sizeof(int) * nodes[(size_t)j].g.n, s));
