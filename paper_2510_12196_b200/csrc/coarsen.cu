@@ -904,6 +904,35 @@ __device__ __forceinline__ int stage_row(int c, const int4* mem, const int* tgt,
 constexpr int kCtTpv = 32;
 constexpr int kCtBlock = 256;
 
+// one row's staged entry for this lane (key -1: none / self loop)
+__device__ __forceinline__ void row_entry(const int4 m, int c, int lane, const int* __restrict__ tgt,
+                                          const int* __restrict__ w, int& t, int& wt) {
+  t = -1;
+  wt = 0;
+  if (lane < m.y + m.w) {
+    const int e = lane < m.y ? m.x + lane : m.z + (lane - m.y);
+    t = tgt[e];
+    wt = w[e];
+  }
+}
+
+__device__ __forceinline__ void row_emit(int c, int key, int wt, int lane, const int* __restrict__ ub,
+                                         int* __restrict__ t_tgt, int* __restrict__ t_w,
+                                         int* __restrict__ cdeg) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int sum = (int)__reduce_add_sync(peers, (unsigned)wt);
+  const bool lead = key >= 0 && lane == __ffs(peers) - 1;
+  const unsigned leads = __ballot_sync(0xffffffffu, lead);
+  if (lead) {
+    const int pos = ub[c] + __popc(leads & ((1u << lane) - 1u));
+    t_tgt[pos] = key;
+    t_w[pos] = sum;
+  }
+  if (lane == 0) cdeg[c] = __popc(leads);
+}
+
+// two rows per warp per step: both rows' loads are in flight together (the
+// kernel is bound by the dependent member -> slots -> M chain per row)
 __global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int4* __restrict__ mem,
                                                        const int* __restrict__ ub,
                                                        const int* __restrict__ tgt,
@@ -913,30 +942,24 @@ __global__ void __launch_bounds__(kCtBlock) k_row_warp(int n_c, const int4* __re
                                                        int* __restrict__ t_w,
                                                        int* __restrict__ cdeg) {
   const int lane = lane_id();
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c0 < n_c;
-       c0 += ((long long)gridDim.x * blockDim.x) >> 5) {
-    const int c = (int)c0;
-    const int4 m = mem[c];
-    const int L = m.y + m.w;
-    if (L > kCtTpv) continue;  // warp-uniform: k_row_long
-    int key = -1, wt = 0;
-    if (lane < L) {
-      const int e = lane < m.y ? m.x + lane : m.z + (lane - m.y);
-      const int t = tgt[e];
-      wt = w[e];
-      key = cmap[t];
-      if (key == c) key = -1;  // self loop
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int sum = (int)__reduce_add_sync(peers, (unsigned)wt);
-    const bool lead = key >= 0 && lane == __ffs(peers) - 1;
-    const unsigned leads = __ballot_sync(0xffffffffu, lead);
-    if (lead) {
-      const int pos = ub[c] + __popc(leads & ((1u << lane) - 1u));
-      t_tgt[pos] = key;
-      t_w[pos] = sum;
-    }
-    if (lane == 0) cdeg[c] = __popc(leads);
+       c0 += 2 * nw) {
+    const int ca = (int)c0;
+    const long long cbl = c0 + nw;
+    const int cb = cbl < n_c ? (int)cbl : -1;
+    const int4 ma = mem[ca];
+    const int4 mb = cb >= 0 ? mem[cb] : make_int4(0, 0, 0, 0);
+    const bool la = ma.y + ma.w <= kCtTpv, lb = cb >= 0 && mb.y + mb.w <= kCtTpv;
+    int ta = -1, wa = 0, tb = -1, wb = 0;
+    if (la) row_entry(ma, ca, lane, tgt, w, ta, wa);
+    if (lb) row_entry(mb, cb, lane, tgt, w, tb, wb);
+    int ka = ta >= 0 ? cmap[ta] : -1;
+    int kb = tb >= 0 ? cmap[tb] : -1;
+    if (ka == ca) { ka = -1; wa = 0; }  // self loops
+    if (kb == cb) { kb = -1; wb = 0; }
+    if (la) row_emit(ca, ka, wa, lane, ub, t_tgt, t_w, cdeg);  // warp-uniform
+    if (lb) row_emit(cb, kb, wb, lane, ub, t_tgt, t_w, cdeg);
   }
 }
 

@@ -55,7 +55,7 @@ constexpr int kFusedWarps = kFusedBlock / 32;
 // co-resident CTAs per SM the grid kernels are compiled for (register cap).
 // GIM build flag -DGIM_FUSED_MIN_BLOCKS overrides for A/B runs.
 #ifndef GIM_FUSED_MIN_BLOCKS
-#define GIM_FUSED_MIN_BLOCKS 2
+#define GIM_FUSED_MIN_BLOCKS 3
 #endif
 constexpr int kFusedMinBlocks = GIM_FUSED_MIN_BLOCKS;
 // batched cluster refinements occupy a few clusters at most: compiled for 2
@@ -591,41 +591,23 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       // ---- K9 first filter (refinement.py:201-244)
       long long ns = n;  // items: vertices (vcent) or the boundary list
       if (!vcent) {
-        // boundary list (unlocked): ext[v] > 0; sixteen consecutive-ish
-        // vertices per lane per step, read as four 16-byte vectors (ext) and
-        // four 8-byte vectors (move stamps), all in flight together
+        // boundary list (unlocked): ext[v] > 0; four vertices per thread
+        // per step with their loads issued together
         int nbnd = 0;
-        for (long long b0 = (gt - lane) * 16; b0 < n; b0 += GT * 16) {
-          int ex[16];
-          unsigned short ms[16];
+        for (long long b0 = (gt - lane) * 4; b0 < n; b0 += GT * 4) {
+          bool bnd[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const long long i = b0 + j * 128 + lane * 4;
-            if (i + 3 < n) {
-              const int4 x = *reinterpret_cast<const int4*>(ext + i);
-              ex[4 * j] = x.x; ex[4 * j + 1] = x.y; ex[4 * j + 2] = x.z; ex[4 * j + 3] = x.w;
-              if (use_locks) {
-                const ushort4 m = *reinterpret_cast<const ushort4*>(mstamp + i);
-                ms[4 * j] = m.x; ms[4 * j + 1] = m.y; ms[4 * j + 2] = m.z; ms[4 * j + 3] = m.w;
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                ex[4 * j + q] = i + q < n ? ext[i + q] : 0;
-                if (use_locks) ms[4 * j + q] = i + q < n ? mstamp[i + q] : 0;
-              }
-            }
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            bnd[q] = v < n && ext[v] > 0;
+            nbnd += bnd[q];
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const long long v = b0 + j * 128 + lane * 4 + q;
-              bool bnd = ex[4 * j + q] > 0;
-              nbnd += bnd;
-              if (bnd && use_locks && ms[4 * j + q] == lock_stamp) bnd = false;
-              wq_push(qa, bnd, (int)v, A.lsmall, cnt + C_SMALL);
-            }
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            if (bnd[q] && use_locks && mstamp[v] == lock_stamp) bnd[q] = false;
+            wq_push(qa, bnd[q], (int)v, A.lsmall, cnt + C_SMALL);
+          }
         }
         acct_warp(s_acct, A_BND, nbnd);
         if (BX == 0 && threadIdx.x == 0) s_acct[A_SCAN] += n;
@@ -766,28 +748,19 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       const int n_elig = s_nelig;
       incomplete = n_elig == 0;
       long long ns = n;
-      if (!vcent) {  // vertices of overloaded blocks (16 per lane per step, as above)
-        for (long long b0 = (gt - lane) * 16; b0 < n; b0 += GT * 16) {
-          int pv[16];
+      if (!vcent) {  // vertices of overloaded blocks
+        for (long long b0 = (gt - lane) * 4; b0 < n; b0 += GT * 4) {
+          int pv[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const long long i = b0 + j * 128 + lane * 4;
-            if (i + 3 < n) {
-              const int4 x = *reinterpret_cast<const int4*>(A.part + i);
-              pv[4 * j] = x.x; pv[4 * j + 1] = x.y; pv[4 * j + 2] = x.z; pv[4 * j + 3] = x.w;
-            } else {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) pv[4 * j + q] = i + q < n ? A.part[i + q] : -1;
-            }
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            pv[q] = v < n ? A.part[v] : -1;
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const long long v = b0 + j * 128 + lane * 4 + q;
-              const int p = pv[4 * j + q];
-              wq_push(qa, p >= 0 && ovl[p], (int)v, A.lsmall, cnt + C_SMALL);
-            }
+          for (int q = 0; q < 4; ++q) {
+            const long long v = b0 + q * 32 + lane;
+            wq_push(qa, pv[q] >= 0 && ovl[pv[q]], (int)v, A.lsmall, cnt + C_SMALL);
+          }
         }
         wq_flush(qa, A.lsmall, cnt + C_SMALL);
         grid.sync();
