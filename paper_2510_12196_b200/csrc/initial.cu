@@ -73,11 +73,20 @@ __device__ __forceinline__ void cta_argmax(int& a, int& b, int* sa, int* sb) {
 // round first READS dist and marks the next frontier in the bitmap `nxt`
 // (ceil(n/32) words, zero on entry and on exit) with atomicOr, then each
 // bitmap word's owner thread writes dist and clears the word.
+// `fresh`: distances from the seed set from scratch; else `dist` holds the
+// distances from seeds[0..ns-2] and only seeds[ns-1] is added: a pruned BFS
+// that lowers distances where the new seed is closer (every vertex on a
+// shortest path to an improved vertex is improved too, so the result is the
+// multi-source distance) and stops when a round improves nothing.
 __device__ void cta_bfs(int n, const int* off, const int* tgt, int* dist, const int* seeds,
-                        int ns, unsigned* nxt) {
-  for (int v = threadIdx.x; v < n; v += blockDim.x) dist[v] = -1;
-  __syncthreads();
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) dist[seeds[i]] = 0;
+                        int ns, unsigned* nxt, bool fresh = true) {
+  if (fresh) {
+    for (int v = threadIdx.x; v < n; v += blockDim.x) dist[v] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) dist[seeds[i]] = 0;
+  } else if (threadIdx.x == 0) {
+    dist[seeds[ns - 1]] = 0;
+  }
   __syncthreads();
   const int nw = (n + 31) >> 5;
   for (int d = 0;; ++d) {
@@ -85,7 +94,8 @@ __device__ void cta_bfs(int n, const int* off, const int* tgt, int* dist, const 
       if (dist[v] != d) continue;
       for (int e = off[v]; e < off[v + 1]; ++e) {
         const int u = tgt[e];
-        if (dist[u] < 0) atomicOr(&nxt[u >> 5], 1u << (u & 31));
+        const int du = dist[u];
+        if (du < 0 || du > d + 1) atomicOr(&nxt[u >> 5], 1u << (u & 31));
       }
     }
     __syncthreads();
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
   if (threadIdx.x == 0) seeds[0] = sv;
   __syncthreads();
   for (int ns = 1; ns < k; ++ns) {
-    cta_bfs(n, g_off, g_tgt, dist, seeds, ns, nxt);
+    cta_bfs(n, g_off, g_tgt, dist, seeds, ns, nxt, ns == 1);
     sv = cta_pick_seed(n, dist, sa, sb);
     if (threadIdx.x == 0) seeds[ns] = sv;
     __syncthreads();
@@ -249,7 +259,13 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
         const int cu = u < n ? max(cb[u], 0) : 0;
         const int cm = (int)__reduce_max_sync(0xffffffffu, (unsigned)cu);
         if (cm == mx) {
-          gv = (bch << 5) + __ffs(__ballot_sync(0xffffffffu, cu == cm)) - 1;
+          const int gl = __ffs(__ballot_sync(0xffffffffu, cu == cm)) - 1;
+          gv = (bch << 5) + gl;
+          // eager removal of gv from bb's bound of this chunk (its conn
+          // becomes -1 at the claim): the next query of bb needs no repair
+          const int rest = (int)__reduce_max_sync(0xffffffffu, lane == gl ? 0u : (unsigned)cu);
+          if (lane == 0) mb[bch] = rest;
+          __syncwarp();
           break;
         }
         if (lane == 0) mb[bch] = cm;  // stale bound: repair, retry
