@@ -371,6 +371,14 @@ int gim_metis_load(const char* path, void** handle, int64_t* n, int64_t* m2);
 int gim_metis_fetch(void* handle, int64_t* offsets, int64_t* targets, int64_t* eweights,
                     int64_t* vweights, int64_t* sources);
 
+/* METIS straight to a device CSR: the graph parsed by gim_metis_load is
+ * narrowed to int32 and uploaded by the multi-threaded path of
+ * gim_integrated_map (validation included) into caller DEVICE buffers
+ * offsets[n+1], targets/weights/sources[2m], vweights[n]; *total_vweight
+ * (host) = its total vertex weight.  Frees the handle. */
+int gim_metis_upload(void* handle, int32_t* offsets, int32_t* targets, int32_t* weights,
+                     int32_t* vweights, int32_t* sources, int64_t* total_vweight, void* stream);
+
 /* kernels launched by kernel-level calls (outside integrated_map /
  * multisection calls, which count their own in gim_im_stats) since the last
  * reset (evidence). */

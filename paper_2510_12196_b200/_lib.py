@@ -143,6 +143,7 @@ SIGNATURES: dict[str, list] = {
     "gim_hierarchical_multisection": [GP, TP, DBL, U64, P, P],
     "gim_hierarchical_multisection_host": [I64, P, P, P, P, TP, DBL, U64, P, P, P],
     "gim_default_params": [PARP],
+    "gim_metis_upload": [P, P, P, P, P, P, PI64, P],
     "gim_hierarchical_multisection_plugin": [I64, P, P, P, P, TP, DBL, U64, P, P, P, P, P, P],
     "gim_integrated_map_device": [GP, TP, DBL, U64, PARP, P, P, PSTP, P],
     "gim_integrated_map": [I64, P, P, P, P, TP, DBL, U64, PARP, P, P, PSTP, P],

@@ -2257,6 +2257,41 @@ extern "C" int gim_integrated_map(int64_t n, const int64_t* offsets, const int64
   });
 }
 
+namespace gim {
+bool metis_arrays(void* handle, long long* n, const long long** off, const long long** tgt,
+                  const long long** w, const long long** vw);
+void metis_free(void* handle);
+}  // namespace gim
+
+extern "C" int gim_metis_upload(void* handle, int32_t* offsets, int32_t* targets,
+                                int32_t* weights, int32_t* vweights, int32_t* sources,
+                                int64_t* total_vweight, void* stream) {
+  return guard([&] {
+    long long n = 0;
+    const long long *off = nullptr, *tgt = nullptr, *w = nullptr, *vw = nullptr;
+    GIM_CHECK(metis_arrays(handle, &n, &off, &tgt, &w, &vw), GIM_E_INVALID, "null handle");
+    struct Free {
+      void* h;
+      ~Free() { metis_free(h); }
+    } guard_free{handle};
+    GIM_CHECK(offsets && total_vweight, GIM_E_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    OwnedGraph G;
+    upload_graph(n, reinterpret_cast<const int64_t*>(off), reinterpret_cast<const int64_t*>(tgt),
+                 reinterpret_cast<const int64_t*>(w), reinterpret_cast<const int64_t*>(vw), G, s);
+    const long long m2 = G.m2;
+    GIM_CUDA(cudaMemcpyAsync(offsets, G.off.get(), sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+    if (m2) {
+      GIM_CUDA(cudaMemcpyAsync(targets, G.tgt.get(), sizeof(int) * m2, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(weights, G.w.get(), sizeof(int) * m2, cudaMemcpyDeviceToDevice, s));
+      GIM_CUDA(cudaMemcpyAsync(sources, G.src.get(), sizeof(int) * m2, cudaMemcpyDeviceToDevice, s));
+    }
+    if (n) GIM_CUDA(cudaMemcpyAsync(vweights, G.vw.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    *total_vweight = G.total_vw;
+    GIM_CUDA(sync_stream(s));
+  });
+}
+
 extern "C" int gim_fill_sources(int32_t n, const int32_t* offsets, int32_t* sources, void* stream) {
   return guard([&] { fill_sources(n, offsets, sources, (cudaStream_t)stream); });
 }

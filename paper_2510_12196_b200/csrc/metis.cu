@@ -300,6 +300,21 @@ static void parse_metis(const char* data, long long size, MetisGraph& G) {
     fail(hl, "header claims " + std::to_string(m) + " edges, file has " + std::to_string(m2 / 2));
 }
 
+// the parsed CSR of a gim_metis_load handle (driver.cu uploads it)
+bool metis_arrays(void* handle, long long* n, const long long** off, const long long** tgt,
+                  const long long** w, const long long** vw) {
+  auto* G = static_cast<MetisGraph*>(handle);
+  if (!G) return false;
+  *n = G->n;
+  *off = G->off.data();
+  *tgt = G->tgt.data();
+  *w = G->w.data();
+  *vw = G->vw.data();
+  return true;
+}
+
+void metis_free(void* handle) { delete static_cast<MetisGraph*>(handle); }
+
 }  // namespace gim
 
 using namespace gim;

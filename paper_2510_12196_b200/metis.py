@@ -49,3 +49,35 @@ def load_metis(path: str):
     except Exception:  # noqa: BLE001
         from .generators import HostGraph
         return HostGraph(off, tgt, ew, vw, src)
+
+
+def load_metis_device(path: str, device="cuda"):
+    """A METIS file straight to a device-resident CSR (`device.DeviceGraph`):
+    parsed natively (same rules and `MetisFormatError` messages as
+    `load_metis`), narrowed to int32 and uploaded by the library's
+    multi-threaded upload path — no int64 host Graph in between."""
+    import torch
+
+    from . import device as D
+    lib = _lib.load()
+    h = C.c_void_p()
+    n = C.c_int64()
+    m2 = C.c_int64()
+    rc = lib.gim_metis_load(str(path).encode(), C.byref(h), C.byref(n), C.byref(m2))
+    if rc == _lib.GIM_E_FORMAT:
+        raise _error_type()(lib.gim_last_error().decode())
+    if rc == _lib.GIM_E_IO:
+        raise FileNotFoundError(lib.gim_last_error().decode())
+    _lib.check(rc)
+    n, m2 = n.value, m2.value
+    dev = torch.device(device)
+    i32 = dict(dtype=torch.int32, device=dev)
+    off = torch.empty(n + 1, **i32)
+    tgt = torch.empty(max(m2, 1), **i32)
+    w = torch.empty(max(m2, 1), **i32)
+    vw = torch.empty(max(n, 1), **i32)
+    src = torch.empty(max(m2, 1), **i32)
+    tot = C.c_int64(0)
+    _lib.call("gim_metis_upload", h, off.data_ptr(), tgt.data_ptr(), w.data_ptr(), vw.data_ptr(),
+              src.data_ptr(), C.byref(tot), D.stream_ptr(dev))
+    return D.DeviceGraph(off, tgt[:m2], w[:m2], vw[:n], src[:m2], tot.value)

@@ -57,6 +57,17 @@ def main():
     ok = np.array_equal(mine.offsets, g.offsets) and np.array_equal(mine.edge_targets,
                                                                       g.edge_targets)
     out["native_equals_generator"] = bool(ok)
+    # straight to a device CSR (parse + narrow + upload), the mapping's input
+    import torch
+    from paper_2510_12196_b200.metis import load_metis_device
+    load_metis_device(path)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dg = load_metis_device(path)
+    torch.cuda.synchronize()
+    out["native_to_device_s"] = time.perf_counter() - t0
+    out["device_csr_equal"] = bool(np.array_equal(dg.offsets.cpu().numpy(), g.offsets) and
+                                   np.array_equal(dg.targets.cpu().numpy(), g.edge_targets))
     ref_dir = ROOT / "baseline" / "_ref"
     if not args.no_ref and (ref_dir / "promap").is_dir():
         sys.path.insert(0, str(ref_dir))

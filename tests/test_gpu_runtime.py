@@ -173,3 +173,27 @@ def test_second_device_after_first(D):
             a, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 0)
             res.append(a.cpu().numpy())
     assert np.array_equal(res[0], res[1])
+
+
+def test_metis_straight_to_device(D, tmp_path):
+    """load_metis_device (parse natively, narrow + upload) equals the host
+    loader's graph uploaded, and maps identically."""
+    from paper_2510_12196_b200 import load_metis
+    from paper_2510_12196_b200.generators import gen_rgg
+    from paper_2510_12196_b200.metis import load_metis_device
+    g = gen_rgg(1 << 12, 0.55, 5)
+    path = tmp_path / "g.metis"
+    with open(path, "w") as fh:
+        fh.write(f"{g.n} {g.m}\n")
+        for v in range(g.n):
+            fh.write(" ".join(str(int(u) + 1) for u in g.neighbors(v)) + "\n")
+    dg = load_metis_device(str(path))
+    hg = load_metis(str(path))
+    ref = D.DeviceGraph.from_host(hg)
+    for a, b in ((dg.offsets, ref.offsets), (dg.targets, ref.targets), (dg.weights, ref.weights),
+                 (dg.vweights, ref.vweights), (dg.sources, ref.sources)):
+        assert torch.equal(a, b)
+    assert dg.total_weight == hg.total_weight
+    a1, _, _ = D.integrated_map_device(dg, H, DIST, 0.03, 2)
+    a2, _, _ = D.integrated_map_device(ref, H, DIST, 0.03, 2)
+    assert torch.equal(a1, a2)
