@@ -7,6 +7,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -303,6 +305,11 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg(const GggJob* jobs, int njobs
 // are handed to the whole CTA.  Isolated vertices claimed by the fallback
 // cost one step of the warp.
 
+static bool trace_ggg() {
+  static const bool on = std::getenv("GIM_TRACE_MS") != nullptr;
+  return on;
+}
+
 constexpr int kGgCh = 256;
 constexpr int kGggMaxDry = 1024;  // known-dry flags for k up to this
 constexpr int kGgSc = 256;
@@ -327,6 +334,9 @@ struct GggLargeJob {
   int* gsmax;       // [k][nsc] (when not in shared memory), zeroed by the host
   long long* bwork; // [k]
   int smax_smem;
+  long long* stat;  // [8] diagnostics (GIM_TRACE_MS) or null: frontier claims,
+                    // fallback claims, known-dry skips, bound repairs, CTA hub
+                    // updates, cycles in queries, cycles in claims/updates
 };
 
 __device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b, int nch,
@@ -423,6 +433,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         int* sbm = smax + (size_t)bb * nsc;
         int v = -1;
         const bool known_dry = track_dry && ((s_dry[bb >> 5] >> (bb & 31)) & 1u);
+        const long long t_q0 = J.stat ? clock64() : 0;
+        if (J.stat && known_dry && lane == 0) J.stat[2] += 1;
         for (; !known_dry;) {  // query with lazy repair of stale bounds
           int top = 0, ts = INT_MAX;
           for (int i = lane; i < nsc; i += 32) {
@@ -455,6 +467,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             if (ch < 0 && m) ch = c0 + j * 32 + __ffs(m) - 1;
             smx = max(smx, cm[j]);
           }
+          if (ch < 0 && J.stat && lane == 0) J.stat[3] += 1;
           if (ch < 0) {  // stale superchunk bound: tighten it and retry
             smx = warp_max_int(smx);
             if (lane == 0) {
@@ -503,6 +516,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             break;
           }
           // stale chunk bound: tighten chunk and superchunk, retry
+          if (J.stat && lane == 0) J.stat[3] += 1;
           cmx = warp_max_int(cmx);
           const int lj = (ch - c0) >> 5, ll = (ch - c0) & 31;
 #pragma unroll
@@ -518,6 +532,11 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
             else __stcg(sbm + ts, s2);
           }
           __syncwarp();
+        }
+        const long long t_q1 = J.stat ? clock64() : 0;
+        if (J.stat && lane == 0) {
+          J.stat[v < 0 ? 1 : 0] += 1;
+          J.stat[5] += t_q1 - t_q0;
         }
         int vwv, deg;
         if (v < 0) {  // frontier dried up: lowest unassigned vertex
@@ -561,6 +580,10 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         }
         ++assigned;
         __syncwarp();
+        if (J.stat && lane == 0) {
+          J.stat[4] += deg > kGgWarpRow;
+          J.stat[6] += clock64() - t_q1;
+        }
         if (deg > kGgWarpRow) {  // hub row: the whole CTA updates it
           if (lane == 0) {
             s_v = v;
@@ -759,10 +782,24 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     q.gsmax = q.cmax + (size_t)k * nch;
     q.bwork = bwork.get() + (size_t)k * j;
     q.smax_smem = smax_smem ? 1 : 0;
+    q.stat = nullptr;
     off += words[(size_t)j];
   }
+  DBuf<long long> stat(8 * (size_t)J, s);
+  if (trace_ggg()) {
+    GIM_CUDA(cudaMemsetAsync(stat.get(), 0, sizeof(long long) * 8 * J, s));
+    for (int j = 0; j < J; ++j) hj[(size_t)j].stat = stat.get() + 8 * j;
+  }
+  const auto t_seed = std::chrono::steady_clock::now();
+  double ms_seed = 0.0;
   for (int j = 0; j < J; ++j)
     if (k > 1) ggg_seeds(gs[(size_t)j], k, hj[(size_t)j].dist, hj[(size_t)j].seeds, s);
+  if (trace_ggg()) {
+    GIM_CUDA(sync_stream(s));
+    ms_seed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_seed)
+                  .count();
+  }
+  const auto t_grow = std::chrono::steady_clock::now();
   DBuf<GggLargeJob> dj((size_t)J, s);
   GIM_CUDA(cudaMemcpyAsync(dj.get(), hj.data(), sizeof(GggLargeJob) * (size_t)J,
                            cudaMemcpyHostToDevice, s));
@@ -774,6 +811,17 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
   k_ggg_large<<<J, kGggBlock, smax_smem ? max_smax * sizeof(int) : 0, s>>>(dj.get());
   count_launch();
   GIM_LAUNCH_CHECK();
+  if (trace_ggg()) {
+    GIM_CUDA(sync_stream(s));
+    const double ms_grow = std::chrono::duration<double, std::milli>(
+                               std::chrono::steady_clock::now() - t_grow).count();
+    std::vector<long long> h(8 * (size_t)J);
+    GIM_CUDA(cudaMemcpy(h.data(), stat.get(), sizeof(long long) * 8 * J, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < J; ++j)
+      std::fprintf(stderr, "ggg_large n=%d k=%d seeds %.1f ms grow %.1f ms | frontier %lld fallback %lld dry-skips %lld repairs %lld hub-updates %lld | Mcycles query %.1f claim %.1f\n",
+                   gs[(size_t)j].n, k, ms_seed, ms_grow, h[8 * j], h[8 * j + 1], h[8 * j + 2], h[8 * j + 3],
+                   h[8 * j + 4], h[8 * j + 5] / 1e6, h[8 * j + 6] / 1e6);
+  }
 }
 
 // one CTA per graph; working set (and, when it fits, the graph) in shared
