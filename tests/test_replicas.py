@@ -27,8 +27,9 @@ def _worker(rank, world, port, q):
     local = 100.0 + 50.0 * rank          # rank 1 is the slow replica
     tmax = bench.max_over_ranks(local, world, "cpu")
     value = bench.job_throughput(1000, 4, world, tmax)
+    js = bench.gather_lists([10 * rank + i for i in range(rank + 1)], world)
     dist.barrier()
-    q.put((rank, tmax, value))
+    q.put((rank, tmax, value, js))
     dist.destroy_process_group()
 
 
@@ -44,9 +45,11 @@ def test_max_over_ranks_gloo():
         p.join(timeout=120)
         assert p.exitcode == 0
     res = sorted(q.get() for _ in range(world))
-    for _, tmax, value in res:
+    for _, tmax, value, js in res:
         assert tmax == 150.0
         assert value == pytest.approx(1000 * 4 * 2 / 0.150)
+        # config-5 results gathered over the gloo group in rank order
+        assert js == [0, 10, 11]
 
 
 # ---------------------------------------------------------------------------
