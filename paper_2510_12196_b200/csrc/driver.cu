@@ -1324,6 +1324,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
                                   int* out_part, long long* out_bw, gim_im_stats* stats,
                                   cudaStream_t s, double l_max_in = -1.0) {
   GIM_CHECK(g0.n > 0, GIM_E_EMPTY, "cannot map an empty graph");
+  const auto th0 = std::chrono::steady_clock::now();
   Topo t = get_topo(tt);
   std::vector<long long> h(tt.hierarchy, tt.hierarchy + tt.levels);
   const long long k = t.k;
@@ -1382,6 +1383,7 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   GIM_CUDA(cudaMemcpyAsync(out_part, cur.get(), sizeof(int) * g0.n, cudaMemcpyDeviceToDevice, s));
   GIM_CUDA(cudaEventRecord(ev[3], s));
   GIM_CUDA(cudaEventSynchronize(ev[3]));
+  const auto th3 = std::chrono::steady_clock::now();
   if (stats) {
     float a = 0, b = 0, c = 0, tot = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
@@ -1454,6 +1456,14 @@ static void integrated_map_device(const DevGraph& g0, long long total, const gim
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (auto& e : lev) cudaEventDestroy(e);
+  if (trace_ms()) {
+    const auto th4 = std::chrono::steady_clock::now();
+    float dev = 0.f;
+    std::fprintf(stderr, "im host ms: start->ev3 %.2f ev3->exit %.2f (seed %llu)\n",
+                 std::chrono::duration<double, std::milli>(th3 - th0).count(),
+                 std::chrono::duration<double, std::milli>(th4 - th3).count(), seed);
+    (void)dev;
+  }
 }
 
 // ---------------------------------------------------------------------------
