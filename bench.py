@@ -280,6 +280,11 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        # NVML start-up inside nvidia-smi holds the driver for tens of ms:
+        # measured, it landed in the second timed map of every run (77-109 ms
+        # instead of ~52 ms).  Wait until the sampler is past it.
+        if self.proc is not None:
+            time.sleep(2.0)
         return self
 
     def __exit__(self, *exc):
