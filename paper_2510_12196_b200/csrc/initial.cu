@@ -418,6 +418,56 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     if (warp == 0) {
       int cmd = 2;
       while (assigned < n) {
+        if (k <= 32) {
+          // Isolated run: while the lightest block is known-dry and the
+          // lowest unassigned vertex has no neighbours, each step is the
+          // general loop's fallback claim with nothing else to do (no query,
+          // no frontier change, the block stays dry) — so run it with the
+          // block weights and dry flags in lane registers: one argmin, one
+          // ballot, two stores per claim.  Stops at the first step the
+          // general loop would handle differently.
+          long long myb = lane < k ? bw[lane] : 0;
+          const unsigned dry = s_dry[0];
+          long long runs = 0;
+          for (;;) {
+            const unsigned x = lane < k ? (unsigned)myb : 0xffffffffu;
+            const unsigned mn = __reduce_min_sync(0xffffffffu, x);
+            const int bb = (int)__reduce_min_sync(0xffffffffu, x == mn ? (unsigned)lane : 32u);
+            if (!((dry >> bb) & 1u)) break;
+            if (next_free < win || next_free >= win + 32) {
+              win = next_free;
+              const int u = win + lane;
+              w_free = u < n && __ldcg(J.conn + u) >= 0;
+              w_deg = u < n ? __ldg(J.off + u + 1) - __ldg(J.off + u) : 0;
+              w_vw = u < n ? __ldg(J.vw + u) : 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, w_free && win + lane >= next_free);
+            if (!m) {
+              next_free = win + 32;
+              continue;
+            }
+            const int l = __ffs(m) - 1;
+            if (__shfl_sync(0xffffffffu, w_deg, l) != 0) break;
+            const int v = win + l;
+            const int vwv = __shfl_sync(0xffffffffu, w_vw, l);
+            if (lane == l) w_free = false;
+            if (lane == bb) myb += vwv;
+            if (lane == 0) {
+              J.part[v] = bb;
+              __stcg(J.conn + v, INT_MIN);
+            }
+            next_free = v;
+            ++runs;
+            if (++assigned >= n) break;
+          }
+          if (lane < k) bw[lane] = myb;
+          if (J.stat && lane == 0) {
+            J.stat[1] += runs;
+            J.stat[2] += runs;
+          }
+          __syncwarp();
+          if (assigned >= n) break;
+        }
         // lightest block, lowest id on ties (weights < 2^31: totals are
         // checked on upload): warp min-reduce, lowest lane attaining it
         unsigned bwv = 0xffffffffu;
@@ -592,8 +642,10 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
           cmd = 1;
           break;
         }
-        gg_row_update(J, v, bb, nch, nsc, smax, lane, 32);
-        __syncwarp();
+        if (deg > 0) {  // isolated claims (deg known) skip the offsets round trip
+          gg_row_update(J, v, bb, nch, nsc, smax, lane, 32);
+          __syncwarp();
+        }
       }
       if (lane == 0) s_cmd = cmd;
     }

@@ -400,6 +400,28 @@ def test_ggg_large_graph_matches_oracle(D, scale, k):
     assert np.array_equal(np_(part), O.greedy_graph_growing(og, k))
 
 
+@pytest.mark.parametrize("k", [2, 5, 8, 32, 40])
+def test_ggg_large_isolated_runs_match_oracle(D, monkeypatch, k):
+    """Weighted isolated vertices interleaved with small components (the
+    stalled R-MAT coarsest graphs): the register-resident run of fallback
+    claims (k <= 32) and the general loop (k > 32) both equal the
+    reference's heap growing (pipelines.py:132-188)."""
+    from paper_2510_12196_b200.generators import from_pairs
+    monkeypatch.setenv("GIM_GGG_LARGE", "1")
+    rng = np.random.default_rng(k)
+    n = 6000
+    conn = np.flatnonzero(rng.random(n) < 0.3)  # vertices with neighbours
+    u = rng.choice(conn, 4 * len(conn))
+    v = rng.choice(conn, 4 * len(conn))
+    keep = u != v
+    pairs = np.unique(np.sort(np.stack([u[keep], v[keep]], 1), axis=1), axis=0)
+    vw = rng.integers(1, 6, n)
+    g = from_pairs(n, pairs[:, 0], pairs[:, 1], rng.integers(1, 4, len(pairs)), vw)
+    assert (np.diff(g.offsets) == 0).sum() > n // 2
+    part = D.greedy_graph_growing(D.DeviceGraph.from_host(g), k)
+    assert np.array_equal(np_(part), O.greedy_graph_growing(O.as_ograph(g), k))
+
+
 def test_relatives_parallel_equals_sequential(D, monkeypatch):
     """Two-hop relatives by rounds of disjoint ready matchmakers equal the
     single-thread sequential sweep (coarsening.py:148-158) on R-MAT, where
