@@ -378,6 +378,14 @@ void count_launch(long long n) { ctx().launches.fetch_add(n, std::memory_order_r
 long long launches() { return ctx().launches.load(); }
 void reset_launches() { ctx().launches.store(0); }
 
+static thread_local bool t_concurrent = false;
+ConcurrentScope::ConcurrentScope() : prev(t_concurrent) { t_concurrent = true; }
+ConcurrentScope::~ConcurrentScope() { t_concurrent = prev; }
+int coop_blocks_per_sm(int occ) {
+  occ = std::max(occ, 1);
+  return t_concurrent && occ > 1 ? occ - 1 : occ;
+}
+
 int device_sms() {
   static std::mutex mu;
   static std::map<int, int> cache;

@@ -572,7 +572,7 @@ static void relatives_parallel(const DevGraph& g, int* partner, double l_max, lo
   std::call_once(once, [] {
     GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relatives_par, 256, 0));
   });
-  const int G = std::max(1, std::min(device_sms() * std::max(occ, 1), (int)((g.n + 255) / 256)));
+  const int G = std::max(1, std::min(device_sms() * coop_blocks_per_sm(occ), (int)((g.n + 255) / 256)));
   DBuf<int> la((size_t)std::max(g.n, 1), s), lb((size_t)std::max(g.n, 1), s), ctr(2, s);
   DBuf<unsigned long long> owner((size_t)std::max(g.n, 1), s);
   GIM_CUDA(cudaMemsetAsync(ctr.get(), 0, 2 * sizeof(int), s));

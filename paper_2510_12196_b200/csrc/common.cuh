@@ -183,6 +183,20 @@ struct CtxScope {
   CtxScope& operator=(const CtxScope&) = delete;
 };
 
+// Cooperative grids launched from concurrent multisection workers leave one
+// CTA slot per SM free, so they can start beside a sibling worker's
+// single-CTA kernels (greedy growing) instead of waiting for them to finish
+// (a cooperative launch is dispatched only when all its CTAs fit).  Results
+// do not depend on the grid size.
+int coop_blocks_per_sm(int occ);
+struct ConcurrentScope {
+  bool prev;
+  ConcurrentScope();
+  ~ConcurrentScope();
+  ConcurrentScope(const ConcurrentScope&) = delete;
+  ConcurrentScope& operator=(const ConcurrentScope&) = delete;
+};
+
 // launch accounting (current context)
 void count_launch(long long n = 1);
 long long launches();

@@ -625,6 +625,7 @@ static void general_parallel(const std::vector<BatchPartJob*>& jobs, int parts, 
   for (size_t j = 0; j < jobs.size(); ++j) {
     workers.emplace_back([&, j, pc] {
       CtxScope scope(pc);
+      ConcurrentScope conc;
       cudaStream_t cs = nullptr;
       try {
         GIM_CUDA(cudaSetDevice(dev));
@@ -1016,6 +1017,7 @@ static void descend(MsCtx& C, const DevGraph& sub, long long sub_total, int leve
   for (int j = 0; j < parts; ++j) {
     workers.emplace_back([&, j, pc] {
       CtxScope scope(pc);
+      ConcurrentScope conc;
       cudaStream_t cs = nullptr;
       try {
         GIM_CUDA(cudaSetDevice(C.device));
@@ -1183,6 +1185,7 @@ static void multisection_bfs(MsCtx& C, const DevGraph& root, long long total, co
       for (int j = 0; j < N; ++j) {
         workers.emplace_back([&, j, pc] {
           CtxScope scope(pc);
+          ConcurrentScope conc;
           cudaStream_t cs = nullptr;
           try {
             GIM_CUDA(cudaSetDevice(C.device));

@@ -336,7 +336,8 @@ struct GggLargeJob {
   int smax_smem;
   long long* stat;  // [8] diagnostics (GIM_TRACE_MS) or null: frontier claims,
                     // fallback claims, known-dry skips, bound repairs, CTA hub
-                    // updates, cycles in queries, cycles in claims/updates
+                    // updates, cycles in queries, cycles in claims/updates,
+                    // cycles in CTA hub-row updates
 };
 
 __device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b, int nch,
@@ -347,6 +348,8 @@ __device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b
   int* sb = smax + (size_t)b * nsc;
   const int e1 = __ldg(J.off + v + 1);
   // four slots per thread per step with their loads issued together
+  // (same-address atomics stay per slot: warp aggregation with
+  // __match_any_sync doubled the hub-row update time, r2j A/B)
   for (int e = __ldg(J.off + v) + t0; e < e1; e += 4 * stride) {
     int u[4], wq[4], c0[4];
 #pragma unroll
@@ -652,8 +655,10 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     __syncthreads();
     const int cmd = s_cmd;
     if (cmd == 2) break;
+    const long long t_h0 = J.stat ? clock64() : 0;
     gg_row_update(J, s_v, s_b, nch, nsc, smax, threadIdx.x, blockDim.x);
     __syncthreads();
+    if (J.stat && threadIdx.x == 0) J.stat[7] += clock64() - t_h0;
   }
 }
 
@@ -783,7 +788,7 @@ static void ggg_seeds(const DevGraph& g, int k, int* dist, int* seeds, cudaStrea
   std::call_once(once, [] {
     GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ggg_seeds, 256, 0));
   });
-  const int G = std::max(1, std::min(device_sms() * std::max(occ, 1), (int)((g.n + 255) / 256)));
+  const int G = std::max(1, std::min(device_sms() * coop_blocks_per_sm(occ), (int)((g.n + 255) / 256)));
   const size_t n = (size_t)std::max(g.n, 1);
   DBuf<int> q(3 * n + 4, s);
   DBuf<unsigned long long> keys(2, s);
@@ -870,9 +875,9 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     std::vector<long long> h(8 * (size_t)J);
     GIM_CUDA(cudaMemcpy(h.data(), stat.get(), sizeof(long long) * 8 * J, cudaMemcpyDeviceToHost));
     for (int j = 0; j < J; ++j)
-      std::fprintf(stderr, "ggg_large n=%d k=%d seeds %.1f ms grow %.1f ms | frontier %lld fallback %lld dry-skips %lld repairs %lld hub-updates %lld | Mcycles query %.1f claim %.1f\n",
+      std::fprintf(stderr, "ggg_large n=%d k=%d seeds %.1f ms grow %.1f ms | frontier %lld fallback %lld dry-skips %lld repairs %lld hub-updates %lld | Mcycles query %.1f claim %.1f hub %.1f\n",
                    gs[(size_t)j].n, k, ms_seed, ms_grow, h[8 * j], h[8 * j + 1], h[8 * j + 2], h[8 * j + 3],
-                   h[8 * j + 4], h[8 * j + 5] / 1e6, h[8 * j + 6] / 1e6);
+                   h[8 * j + 4], h[8 * j + 5] / 1e6, h[8 * j + 6] / 1e6, h[8 * j + 7] / 1e6);
   }
 }
 

@@ -1379,7 +1379,7 @@ static void raise_dyn_smem_limit(const void* fn) {
   done[{dev, fn}] = true;
 }
 
-// co-resident CTA capacity per (VW, smem), queried once per device
+// co-resident CTAs per SM for (VW, smem), queried once per device
 template <int VW>
 static int coop_max_blocks(size_t smem) {
   static std::mutex mu;
@@ -1395,7 +1395,8 @@ static int coop_max_blocks(size_t smem) {
   raise_dyn_smem_limit((const void*)k_refine_fused<VW>);
   GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW>, kFusedBlock,
                                                          smem));
-  int r = std::max(1, per) * sms;
+  (void)sms;
+  const int r = std::max(1, per);
   cache.emplace(key, r);
   return r;
 }
@@ -1515,13 +1516,14 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   const int NC = 31 * cfg.rho;
   size_t smem = (size_t)kFusedWarps * 4 * k * sizeof(int) + (size_t)k * (8 + 8 + 8 + 4 + 4 + 4 + 1 + 1);
   smem = (smem + 15) & ~(size_t)15;
-  int maxb = 0;
+  int per = 0;
   switch (L.vw) {
-    case 4: maxb = coop_max_blocks<4>(smem); break;
-    case 8: maxb = coop_max_blocks<8>(smem); break;
-    case 16: maxb = coop_max_blocks<16>(smem); break;
-    default: maxb = coop_max_blocks<32>(smem); break;
+    case 4: per = coop_max_blocks<4>(smem); break;
+    case 8: per = coop_max_blocks<8>(smem); break;
+    case 16: per = coop_max_blocks<16>(smem); break;
+    default: per = coop_max_blocks<32>(smem); break;
   }
+  const int maxb = coop_blocks_per_sm(per) * device_sms();
   // small graphs: one CTA, or one thread-block cluster of up to kMaxCluster
   // CTAs (plain launches, so the refinements of sibling subgraphs overlap);
   // otherwise ~1K vertices per CTA, at most one full co-resident wave

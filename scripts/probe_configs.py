@@ -17,12 +17,23 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--profile", action="store_true", help="serialised per-class device times")
 ap.add_argument("--isolated", nargs="+", default=["keep"], choices=["keep", "strip"],
                 help="isolated-vertex modes to run (R-MAT: strip = tolerance-parity mode)")
+ap.add_argument("--cache", default="", help="npz path: reuse the generated graph across runs")
 args = ap.parse_args()
 D.set_profiling(args.profile)
 for w in args.which:
     t0 = time.time()
     if w == "rmat":
-        g = gen_rmat(args.rmat_scale)
+        import os
+        import numpy as np
+        from paper_2510_12196_b200.generators import HostGraph
+        if args.cache and os.path.exists(args.cache):
+            z = np.load(args.cache)
+            g = HostGraph(z["o"], z["t"], z["w"], z["vw"])
+        else:
+            g = gen_rmat(args.rmat_scale)
+            if args.cache:
+                np.savez(args.cache, o=g.offsets, t=g.edge_targets, w=g.edge_weights,
+                         vw=g.vertex_weights)
         h, d = (4, 8, 8), (1, 10, 100)
     else:
         g = gen_grid3d(args.grid, args.grid, args.grid)
