@@ -310,9 +310,19 @@ static bool trace_ggg() {
   return on;
 }
 
-constexpr int kGgCh = 256;
+// chunk / superchunk sizes (GIM_GG_CH / GIM_GG_SC override for A/B builds):
+// 1024-vertex chunks keep the chunk bounds of a 2M-vertex coarsest graph in
+// shared memory for k = 8 (70 KB), so a query makes one global round trip
+// (the conn scan of its chunk) instead of two
+#ifndef GIM_GG_CH
+#define GIM_GG_CH 1024
+#endif
+#ifndef GIM_GG_SC
+#define GIM_GG_SC 32
+#endif
+constexpr int kGgCh = GIM_GG_CH;
 constexpr int kGggMaxDry = 1024;  // known-dry flags for k up to this
-constexpr int kGgSc = 256;
+constexpr int kGgSc = GIM_GG_SC;
 constexpr int kGgWarpRow = 128;
 
 __device__ __forceinline__ int warp_max_int(int v) {
@@ -334,17 +344,27 @@ struct GggLargeJob {
   int* gsmax;       // [k][nsc] (when not in shared memory), zeroed by the host
   long long* bwork; // [k]
   int smax_smem;
+  int cmax_smem;    // chunk bounds in shared memory too (after the smax words)
   long long* stat;  // [8] diagnostics (GIM_TRACE_MS) or null: frontier claims,
                     // fallback claims, known-dry skips, bound repairs, CTA hub
                     // updates, cycles in queries, cycles in claims/updates,
                     // cycles in CTA hub-row updates
 };
 
+// bound loads / stores: shared memory (volatile: other warps' atomics) or L2
+__device__ __forceinline__ int bnd_ld(const int* p, bool smem) {
+  return smem ? *reinterpret_cast<const volatile int*>(p) : __ldcg(p);
+}
+__device__ __forceinline__ void bnd_st(int* p, int x, bool smem) {
+  if (smem) *reinterpret_cast<volatile int*>(p) = x;
+  else __stcg(p, x);
+}
+
 __device__ __forceinline__ void gg_row_update(const GggLargeJob& J, int v, int b, int nch,
-                                              int nsc, int* smax, int t0, int stride) {
+                                              int nsc, int* smax, int* cmax, int t0, int stride) {
   const int n = J.n;
   int* cb = J.conn + (size_t)b * n;
-  int* mb = J.cmax + (size_t)b * nch;
+  int* mb = cmax + (size_t)b * nch;
   int* sb = smax + (size_t)b * nsc;
   const int e1 = __ldg(J.off + v + 1);
   // four slots per thread per step with their loads issued together
@@ -386,6 +406,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   const bool track_dry = k <= kGggMaxDry;
   for (int i = threadIdx.x; i < (kGggMaxDry + 31) / 32; i += blockDim.x) s_dry[i] = 0;
   int* smax = J.smax_smem ? sm : J.gsmax;
+  int* cmax = J.cmax_smem ? sm + (size_t)k * nsc : J.cmax;
   long long* bw = k <= kGggMaxK ? s_bw : J.bwork;
   if (k == 1) {
     for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = 0;
@@ -393,6 +414,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
   }
   if (J.smax_smem)
     for (int i = threadIdx.x; i < k * nsc; i += blockDim.x) smax[i] = 0;
+  if (J.cmax_smem)
+    for (int i = threadIdx.x; i < k * nch; i += blockDim.x) cmax[i] = 0;
   // seeds: k_ggg_seeds (grid-wide BFS) ran before this launch
   for (int v = threadIdx.x; v < n; v += blockDim.x) J.part[v] = -1;
   for (int b = threadIdx.x; b < k; b += blockDim.x) bw[b] = 0;
@@ -405,7 +428,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     }
     for (int b2 = threadIdx.x; b2 < k; b2 += blockDim.x) J.conn[(size_t)b2 * n + s] = INT_MIN;
     __syncthreads();
-    gg_row_update(J, s, b, nch, nsc, smax, threadIdx.x, blockDim.x);
+    gg_row_update(J, s, b, nch, nsc, smax, cmax, threadIdx.x, blockDim.x);
     __syncthreads();
   }
   const int lane = lane_id(), warp = threadIdx.x >> 5;
@@ -482,7 +505,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         const unsigned mn = __reduce_min_sync(0xffffffffu, bwv);
         bb = (int)__reduce_min_sync(0xffffffffu, bwv == mn ? (unsigned)bb : 0xffffffffu);
         int* cb = J.conn + (size_t)bb * n;
-        int* mb = J.cmax + (size_t)bb * nch;
+        int* mb = cmax + (size_t)bb * nch;
+        const bool cs = J.cmax_smem, ss = J.smax_smem;
         int* sbm = smax + (size_t)bb * nsc;
         int v = -1;
         const bool known_dry = track_dry && ((s_dry[bb >> 5] >> (bb & 31)) & 1u);
@@ -491,7 +515,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
         for (; !known_dry;) {  // query with lazy repair of stale bounds
           int top = 0, ts = INT_MAX;
           for (int i = lane; i < nsc; i += 32) {
-            const int x = J.smax_smem ? sbm[i] : __ldcg(sbm + i);
+            const int x = bnd_ld(sbm + i, ss);
             if (x > top) { top = x; ts = i; }
           }
 #pragma unroll
@@ -511,7 +535,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
 #pragma unroll
           for (int j = 0; j < kGgSc / 32; ++j) {
             const int c = c0 + j * 32 + lane;
-            cm[j] = c < nch ? __ldcg(mb + c) : 0;
+            cm[j] = c < nch ? bnd_ld(mb + c, cs) : 0;
           }
           int ch = -1, smx = 0;
 #pragma unroll
@@ -524,8 +548,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
           if (ch < 0) {  // stale superchunk bound: tighten it and retry
             smx = warp_max_int(smx);
             if (lane == 0) {
-              if (J.smax_smem) sbm[ts] = smx;
-              else __stcg(sbm + ts, smx);
+              bnd_st(sbm + ts, smx, ss);
             }
             __syncwarp();
             continue;
@@ -562,9 +585,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
               s2 = max(s2, (j == lj && lane == ll) ? c2 : cm[j]);
             s2 = warp_max_int(s2);
             if (lane == 0) {
-              __stcg(mb + ch, c2);
-              if (J.smax_smem) sbm[ts] = s2;
-              else __stcg(sbm + ts, s2);
+              bnd_st(mb + ch, c2, cs);
+              bnd_st(sbm + ts, s2, ss);
             }
             break;
           }
@@ -580,9 +602,8 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
           for (int j = 0; j < kGgSc / 32; ++j) s2 = max(s2, cm[j]);
           s2 = warp_max_int(s2);
           if (lane == 0) {
-            __stcg(mb + ch, cmx);
-            if (J.smax_smem) sbm[ts] = s2;
-            else __stcg(sbm + ts, s2);
+            bnd_st(mb + ch, cmx, cs);
+            bnd_st(sbm + ts, s2, ss);
           }
           __syncwarp();
         }
@@ -646,7 +667,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
           break;
         }
         if (deg > 0) {  // isolated claims (deg known) skip the offsets round trip
-          gg_row_update(J, v, bb, nch, nsc, smax, lane, 32);
+          gg_row_update(J, v, bb, nch, nsc, smax, cmax, lane, 32);
           __syncwarp();
         }
       }
@@ -656,7 +677,7 @@ __global__ void __launch_bounds__(kGggBlock) k_ggg_large(const GggLargeJob* jobs
     const int cmd = s_cmd;
     if (cmd == 2) break;
     const long long t_h0 = J.stat ? clock64() : 0;
-    gg_row_update(J, s_v, s_b, nch, nsc, smax, threadIdx.x, blockDim.x);
+    gg_row_update(J, s_v, s_b, nch, nsc, smax, cmax, threadIdx.x, blockDim.x);
     __syncthreads();
     if (J.stat && threadIdx.x == 0) J.stat[7] += clock64() - t_h0;
   }
@@ -803,7 +824,7 @@ static void ggg_seeds(const DevGraph& g, int k, int* dist, int* seeds, cudaStrea
 static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
                              const std::vector<int*>& parts, cudaStream_t s) {
   const int J = (int)gs.size();
-  size_t total = 0, max_smax = 0;
+  size_t total = 0, max_smax = 0, max_bnd = 0;
   std::vector<size_t> words((size_t)J);
   for (int j = 0; j < J; ++j) {
     const size_t n = (size_t)gs[(size_t)j].n;
@@ -811,9 +832,14 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     words[(size_t)j] = n + k + (size_t)k * n + (size_t)k * nch + (size_t)k * nsc;
     total += words[(size_t)j];
     max_smax = std::max(max_smax, (size_t)k * nsc);
+    max_bnd = std::max(max_bnd, (size_t)k * (nch + nsc));
   }
-  constexpr size_t kMaxSmax = 96 * 1024;
-  const bool smax_smem = max_smax * sizeof(int) <= kMaxSmax;
+  // both bound levels in shared memory when they fit, else the superchunk
+  // level alone, else both in global memory
+  constexpr size_t kMaxSmax = 200 * 1024;
+  const bool cmax_smem = max_bnd * sizeof(int) <= kMaxSmax;
+  const bool smax_smem = cmax_smem || max_smax * sizeof(int) <= kMaxSmax;
+  const size_t dyn = cmax_smem ? max_bnd * sizeof(int) : smax_smem ? max_smax * sizeof(int) : 0;
   DBuf<int> scratch(std::max<size_t>(total, 1), s);
   GIM_CUDA(cudaMemsetAsync(scratch.get(), 0, sizeof(int) * total, s));
   DBuf<long long> bwork((size_t)k * J, s);
@@ -839,6 +865,7 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     q.gsmax = q.cmax + (size_t)k * nch;
     q.bwork = bwork.get() + (size_t)k * j;
     q.smax_smem = smax_smem ? 1 : 0;
+    q.cmax_smem = cmax_smem ? 1 : 0;
     q.stat = nullptr;
     off += words[(size_t)j];
   }
@@ -865,7 +892,7 @@ static void launch_ggg_large(const std::vector<DevGraph>& gs, int k,
     GIM_CUDA(cudaFuncSetAttribute(k_ggg_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kMaxSmax));
   });
-  k_ggg_large<<<J, kGggBlock, smax_smem ? max_smax * sizeof(int) : 0, s>>>(dj.get());
+  k_ggg_large<<<J, kGggBlock, dyn, s>>>(dj.get());
   count_launch();
   GIM_LAUNCH_CHECK();
   if (trace_ggg()) {
