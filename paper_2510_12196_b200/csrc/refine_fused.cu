@@ -222,6 +222,7 @@ struct GridBarrier {
 // and after a barrier one warp per hub evaluates it from that table exactly
 // like the in-warp table path.
 constexpr int kHubSeg = 1024;
+constexpr int kSweepWarpDeg = 128;  // entry-sweep rows longer than this: whole warp
 constexpr int kHubBatch = 256;  // hubs per accumulate/evaluate round
 // rows longer than this are listed for the grid (shorter ones beyond
 // kTpvMaxDeg stay with the owner warp: no extra barrier for a few of them);
@@ -464,31 +465,74 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     // one row sweep: boundary counts of the entry mapping + weighted degrees
     // (large levels) and, on the first launch, J of the entry mapping
     // (mapping.py:76-91), four slots' loads in flight per step
+    // Rows longer than kSweepWarpDeg slots (R-MAT hubs: up to 10^5) are
+    // swept by their whole warp instead of one thread, so no thread walks a
+    // hub row alone while the grid waits at the next barrier.
     long long acc = 0;
-    for (long long v = gt; v < n; v += GT) {
-      const int pv = A.part[v];
-      const unsigned long long pc = T.code[pv];
-      const int e0 = A.off[v], e1 = A.off[v + 1];
-      int c = 0, wd = 0;
-      for (int e = e0; e < e1; e += 4) {
-        int tg[4], wg[4], pb[4];
+    for (long long vb = gt & ~31ll; vb < n; vb += GT) {  // warp-uniform
+      const long long v = vb + lane;
+      const bool live = v < n;
+      const int e0 = live ? A.off[v] : 0, e1 = live ? A.off[v + 1] : 0;
+      const bool wide = e1 - e0 > kSweepWarpDeg;
+      if (live && !wide) {
+        const int pv = A.part[v];
+        const unsigned long long pc = T.code[pv];
+        int c = 0, wd = 0;
+        for (int e = e0; e < e1; e += 4) {
+          int tg[4], wg[4], pb[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          tg[q] = e + q < e1 ? A.tgt[e + q] : -1;
-          wg[q] = e + q < e1 ? A.w[e + q] : 0;
+          for (int q = 0; q < 4; ++q) {
+            tg[q] = e + q < e1 ? A.tgt[e + q] : -1;
+            wg[q] = e + q < e1 ? A.w[e + q] : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pb[q] = tg[q] >= 0 ? A.part[tg[q]] : pv;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            c += pb[q] != pv;
+            wd += wg[q];
+            if (first && pb[q] != pv) acc += (long long)wg[q] * cdist(s_dbit, pc, T.code[pb[q]]);
+          }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pb[q] = tg[q] >= 0 ? A.part[tg[q]] : pv;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          c += pb[q] != pv;
-          wd += wg[q];
-          if (first && pb[q] != pv) acc += (long long)wg[q] * cdist(s_dbit, pc, T.code[pb[q]]);
+        if (ext) {
+          ext[v] = c;
+          A.wdeg[v] = wd;
         }
       }
-      if (ext) {
-        ext[v] = c;
-        A.wdeg[v] = wd;
+      unsigned wm = __ballot_sync(0xffffffffu, live && wide);
+      while (wm) {
+        const int l = __ffs(wm) - 1;
+        wm &= wm - 1;
+        const int u = (int)(vb + l);
+        const int f0 = __shfl_sync(0xffffffffu, e0, l), f1 = __shfl_sync(0xffffffffu, e1, l);
+        const int pu = A.part[u];
+        const unsigned long long pc = T.code[pu];
+        int c = 0, wd = 0;
+        long long a2 = 0;
+        for (int e = f0 + lane; e < f1; e += 4 * 32) {
+          int tg[4], wg[4], pb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int eq = e + 32 * q;
+            tg[q] = eq < f1 ? A.tgt[eq] : -1;
+            wg[q] = eq < f1 ? A.w[eq] : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pb[q] = tg[q] >= 0 ? A.part[tg[q]] : pu;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            c += pb[q] != pu;
+            wd += wg[q];
+            if (first && pb[q] != pu) a2 += (long long)wg[q] * cdist(s_dbit, pc, T.code[pb[q]]);
+          }
+        }
+        c = warp_sum_i(c);
+        wd = warp_sum_i(wd);
+        acc += a2;  // summed over the CTA below
+        if (ext && lane == 0) {
+          ext[u] = c;
+          A.wdeg[u] = wd;
+        }
       }
     }
     if (first) block_sum_atomic<kFusedBlock>(acc, A.ctr + 16);

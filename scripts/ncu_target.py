@@ -26,10 +26,28 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", choices=["step", "lp", "refine0"], default="step")
     ap.add_argument("--logn", type=int, default=20)
+    ap.add_argument("--graph", choices=["rgg", "rmat"], default="rgg",
+                    help="rmat: R-MAT scale --logn, H=4:8:8 (config 3)")
+    ap.add_argument("--cache", default="", help="npz cache of the generated graph")
     ap.add_argument("--level", type=int, default=0,
                     help="refine0: refine this level of the stack instead of level 0")
     args = ap.parse_args()
-    g = gen_rgg(1 << args.logn, 0.55, 1)
+    global H
+    if args.graph == "rmat":
+        import os
+        import numpy as np
+        from paper_2510_12196_b200.generators import HostGraph, gen_rmat
+        H = (4, 8, 8)
+        if args.cache and os.path.exists(args.cache):
+            z = np.load(args.cache)
+            g = HostGraph(z["o"], z["t"], z["w"], z["vw"])
+        else:
+            g = gen_rmat(args.logn)
+            if args.cache:
+                np.savez(args.cache, o=g.offsets, t=g.edge_targets, w=g.edge_weights,
+                         vw=g.vertex_weights)
+    else:
+        g = gen_rgg(1 << args.logn, 0.55, 1)
     dg = D.DeviceGraph.from_host(g)
     if args.mode == "refine0" and args.level > 0:
         k0 = 1
