@@ -308,10 +308,22 @@ Topo get_topo(const gim_topology& tt) {
     }
     code[(size_t)b] = c;
   }
+  std::vector<long long> lv(2 * (size_t)levels);
+  {
+    long long P = 1;
+    for (int i = 0; i < levels; ++i) {
+      P *= hierarchy[i];
+      lv[(size_t)i] = P;
+      lv[(size_t)(levels + i)] = (long long)std::llround(std::ldexp(distances[i], dshift));
+    }
+  }
   void* p = nullptr;
   const size_t cb = sizeof(unsigned long long) * (size_t)k;
-  size_t bytes = cb + sizeof(long long) * 64 + sizeof(double) * 64;
+  const size_t lvo = cb + sizeof(long long) * 64 + sizeof(double) * 64;
+  size_t bytes = lvo + sizeof(long long) * lv.size();
   GIM_CUDA(cudaMalloc(&p, bytes));
+  GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + lvo, lv.data(), sizeof(long long) * lv.size(),
+                      cudaMemcpyHostToDevice));
   GIM_CUDA(cudaMemcpy(p, code.data(), cb, cudaMemcpyHostToDevice));
   GIM_CUDA(cudaMemcpy(static_cast<char*>(p) + cb, dbit.data(), sizeof(long long) * 64,
                       cudaMemcpyHostToDevice));

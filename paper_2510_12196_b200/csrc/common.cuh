@@ -84,8 +84,16 @@ struct Topo {
   int exact;                            // 1: d * 2^dshift is exactly integral
   const unsigned long long* code;       // [k]
   const long long* dbit;                // [64]
-  const double* dbitf;                  // [64] the caller's distances
+  const double* dbitf;                  // [64] the caller's distances, followed
+                                        // in the same buffer by lv[2L] (topo_lv)
 };
+
+// per-level table after dbitf (get_topo): group sizes P_l = a_0*..*a_l, then
+// the scaled distances d_l — not a Topo field, so kernels passing Topo by
+// value do not grow
+__host__ __device__ __forceinline__ const long long* topo_lv(const Topo& t) {
+  return reinterpret_cast<const long long*>(t.dbitf + 64);
+}
 
 // cached per (device, hierarchy, distances); device tables are never freed
 Topo get_topo(const gim_topology& t);

@@ -328,9 +328,91 @@ __device__ __forceinline__ int warp_build_table(const WarpTable& wt, int k, int 
   return s;
 }
 
+// Wide tables (many distinct adjacent blocks, R-MAT hubs): the O(s^2)
+// candidate costs below become O(L) each.  With mixed-radix block ids the
+// blocks within distance d_l of b form the contiguous range of b's level-l
+// group (size P_l), so cost(b) = sum_l d_l * (S_l(b) - S_{l-1}(b)) with
+// S_l(b) the table's sum over that group (S_{-1}(b) = conn(b), S_{L-1} = the
+// total) — read from an in-place exclusive prefix sum of the dense table.
+// Integer regrouping of the same sum: the gains are identical.
+#ifndef GIM_GROUPED_MIN_S
+#define GIM_GROUPED_MIN_S 16
+#endif
+constexpr int kGroupedMinS = GIM_GROUPED_MIN_S;
+
+__device__ __forceinline__ long long grouped_cost(const int* pre, int k, int L,
+                                                  const long long* lv, int total, int b,
+                                                  long long cb) {
+  long long c = 0, prev = cb;
+  for (int l = 0; l < L; ++l) {
+    long long S = total;
+    if (l < L - 1) {
+      const long long P = __ldg(lv + l);
+      const long long g0 = (b / P) * P, g1 = g0 + P;
+      S = (long long)(g1 >= k ? total : pre[g1]) - pre[g0];
+    }
+    c += __ldg(lv + L + l) * (S - prev);
+    prev = S;
+  }
+  return c;
+}
+
+__device__ __forceinline__ VertexEval eval_table_grouped(int* tab, const int* lb, const int* lw,
+                                                      int s, int own, int k, int L,
+                                                      const long long* lv,
+                                                      const unsigned char* allowed) {
+  const int lane = lane_id();
+  const int conn_own = tab[own];
+  // in-place exclusive prefix of tab[0..k): contiguous chunk per lane
+  const int per = (k + 31) >> 5, c0 = min(k, lane * per), c1 = min(k, c0 + per);
+  int run = 0;
+  for (int c = c0; c < c1; ++c) run += tab[c];
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int ex = incl - run;
+  __syncwarp();
+  for (int c = c0; c < c1; ++c) {
+    const int x = tab[c];
+    tab[c] = ex;
+    ex += x;
+  }
+  __syncwarp();
+  const long long cur = grouped_cost(tab, k, L, lv, total, own, conn_own);
+  long long g = kGainNone;
+  int b = -1;
+  for (int i = lane; i < s; i += 32) {
+    const int bi = lb[i];
+    if (bi == own || (allowed && !allowed[bi])) continue;
+    const long long gi = cur - grouped_cost(tab, k, L, lv, total, bi, lw[i]);
+    if (best_better(gi, bi, g, b)) { g = gi; b = bi; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
+    int b2 = __shfl_xor_sync(0xffffffffu, b, o);
+    if (best_better(g2, b2, g, b)) { g = g2; b = b2; }
+  }
+  __syncwarp();
+  VertexEval r;
+  r.cur = cur;
+  r.conn_own = conn_own;
+  r.best_gain = g;
+  r.best_b = b;
+  return r;
+}
+
 __device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int own,
                                                  const Topo& t, const long long* s_dbit,
                                                  const unsigned char* allowed) {
+  // wide tables: O(L) per candidate (leaves wt.tab as a prefix sum; callers
+  // use only lb / lw afterwards and the next table build re-zeroes it)
+  if (s > kGroupedMinS)
+    return eval_table_grouped(wt.tab, wt.lb, wt.lw, s, own, t.k, t.L, topo_lv(t), allowed);
   const int lane = lane_id();
   const unsigned long long oc = t.code[own];
   long long cur = 0;

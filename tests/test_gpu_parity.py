@@ -152,6 +152,41 @@ def test_lp_golden(D, golden):
         assert np.array_equal(np_(tm).astype(bool), c["to_move"])
 
 
+@pytest.mark.parametrize("h,d", [((4, 8, 8), (1, 10, 100)), ((3, 5, 7), (1, 7, 40)),
+                                 ((2, 3, 4, 5), (0, 2, 3, 50)), ((64, 4), (5, 5))])
+def test_wide_tables_match_oracle(D, h, d):
+    """Vertices adjacent to many blocks (R-MAT hubs under a random mapping
+    onto k = 120..256 blocks) take the grouped O(L) candidate costs
+    (refine_dev.cuh eval_table_grouped): LP proposals and weak-rebalance
+    candidates equal the reference's (refinement.py:201-309) for mixed-radix
+    hierarchies with unequal, equal and zero distances."""
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(12)
+    og = O.as_ograph(g)
+    t = O.OTopology(h, d)
+    rng = np.random.default_rng(len(h))
+    a = rng.integers(0, t.k, g.n)
+    assert (np.diff(g.offsets) > 64).sum() > 10  # hubs: > 16 distinct blocks
+    dg = D.DeviceGraph.from_host(g)
+    locked = np.zeros(g.n, dtype=bool)
+    for jet in (False, True):
+        cand, dest, tm = D.lp_pass(dg, a, locked, h, d, jet=jet)
+        p = O.label_propagation_pass(og, t, a, locked,
+                                     O.Config(filter_mode="jet" if jet else "nonneg"))
+        assert np.array_equal(np_(cand).astype(bool), p.candidates)
+        assert np.array_equal(np_(dest), p.destinations)
+        assert np.array_equal(np_(tm).astype(bool), p.to_move)
+    bw = O.block_weights(g.vertex_weights, a, t.k)
+    l_max = float(bw.mean())  # about half the blocks overloaded
+    cfg = O.Config()
+    sigma = l_max * (1 - cfg.sigma_fraction)
+    cand, dest, tm, inc = D.rebalance(dg, a, bw, h, d, False, sigma, l_max, cfg.rho, 3, 1)
+    p = O.weak_rebalance(og, t, a, bw, sigma, l_max, O.Config(seed=3), pass_counter=1)
+    assert np.array_equal(np_(cand).astype(bool), p.candidates)
+    assert np.array_equal(np_(dest), p.destinations)
+    assert np.array_equal(np_(tm).astype(bool), p.to_move)
+
+
 def test_rebalance_golden(D, golden):
     for c in golden("rebalance"):
         g = c.graph()
