@@ -187,6 +187,27 @@ def test_wide_tables_match_oracle(D, h, d):
     assert np.array_equal(np_(tm).astype(bool), p.to_move)
 
 
+def test_wide_tables_refine_matches_oracle(D, mode):
+    """Alg. 4 end to end on an R-MAT graph under a random k = 256 mapping
+    (hub rows listed for the grid, wide tables, rebalancing): the best
+    mapping equals the reference's refine (refinement.py:389-464)."""
+    from paper_2510_12196_b200.generators import gen_rmat
+    g = gen_rmat(12)
+    h, d = (4, 8, 8), (1, 10, 100)
+    t = O.OTopology(h, d)
+    a = np.random.default_rng(9).permutation(g.n) % t.k  # balanced, random
+    cfg = O.config_for_level(0, 3, seed=4)
+    l_max = 1.25 * g.vertex_weights.sum() / t.k
+    want = O.refine(g, t, a.copy(), cfg, l_max)
+    dg = D.DeviceGraph.from_host(g)
+    at = torch.from_numpy(a.astype(np.int32)).cuda()
+    bw = torch.from_numpy(O.block_weights(g.vertex_weights, a, t.k)).cuda()
+    D.refine(dg, h, d, at, bw, phi=cfg.phi, i_max=cfg.i_max, i_w_max=cfg.i_w_max,
+             sigma_fraction=cfg.sigma_fraction, rho=cfg.rho, jet=False, jet_c=cfg.jet_filter_c,
+             seed=cfg.seed, l_max=l_max)
+    assert np.array_equal(np_(at), want)
+
+
 def test_rebalance_golden(D, golden):
     for c in golden("rebalance"):
         g = c.graph()
