@@ -68,7 +68,7 @@ constexpr int kVcSteps = 2;
 // longest row evaluated thread-per-vertex (longer rows: warp table path)
 constexpr int kTpvMaxDeg = 64;  // non-portable cluster size (B200 allows 16)
 constexpr int kCtrStride = 8;  // per-iteration-parity counters
-enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ, C_HUB, C_BIG };
+enum { C_SMALL = 0, C_HEAVY, C_CAND, C_MOV, C_DJ, C_HUB, C_BIG, C_WIDE };
 
 struct FusedArgs {
   int n;
@@ -223,6 +223,10 @@ struct GridBarrier {
 // like the in-warp table path.
 constexpr int kHubSeg = 1024;
 constexpr int kSweepWarpDeg = 128;  // entry-sweep rows longer than this: whole warp
+// movers with rows longer than this (hub mode only) have their move applied
+// by kHubSeg-slot segments spread over every warp of the grid, listed (in
+// lsmall, free by then) by the phase that selects them
+constexpr int kApplySplitDeg = 2048;
 constexpr int kHubBatch = 256;  // hubs per accumulate/evaluate round
 // rows longer than this are listed for the grid (shorter ones beyond
 // kTpvMaxDeg stay with the owner warp: no extra barrier for a few of them);
@@ -387,6 +391,75 @@ __device__ __forceinline__ void hub_phase(const FusedArgs& A, const GridBarrier&
     grid.sync();
   }
   if (nb == 0) grid.sync();
+}
+
+// the move application of the listed wide movers (A.lsmall[0, nw)), by
+// kHubSeg-slot segments over every warp of the grid (same per-slot work as
+// the mover loop in refine_body; returns this thread's share of dJ)
+__device__ __forceinline__ long long apply_wide(const FusedArgs& A, const Topo& T,
+                                             const long long* s_dbit, int* ext,
+                                             const int* opart, const unsigned short* mstamp,
+                                             unsigned short cur_stamp, long long nw,
+                                             long long gw, long long NW) {
+  __shared__ int s_pre[kHubBatch + 1];
+  __shared__ int s_wsum[kFusedWarps];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  long long acc = 0;
+  for (long long c0 = 0; c0 < nw; c0 += kHubBatch) {
+    const int nhc = (int)min((long long)kHubBatch, nw - c0);
+    int segs = 0;
+    if ((int)threadIdx.x < nhc) {
+      const int v = A.lsmall[c0 + threadIdx.x];
+      segs = (A.off[v + 1] - A.off[v] + kHubSeg - 1) / kHubSeg;
+    }
+    int incl = segs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int base = 0, tot = 0;
+    for (int w = 0; w < kFusedWarps; ++w) {
+      if (w < warp) base += s_wsum[w];
+      tot += s_wsum[w];
+    }
+    if ((int)threadIdx.x < nhc) s_pre[threadIdx.x] = base + incl - segs;
+    if (threadIdx.x == 0) s_pre[nhc] = tot;
+    __syncthreads();
+    for (long long j = gw; j < tot; j += NW) {
+      int lo = 0, hi = nhc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pre[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      const int v = A.lsmall[c0 + lo];
+      const int e1 = A.off[v + 1];
+      const int sb = A.off[v] + (int)(j - s_pre[lo]) * kHubSeg, se = min(e1, sb + kHubSeg);
+      const int ov = opart[v], nv = A.dest[v];
+      const unsigned long long oc = T.code[ov], nc2 = T.code[nv];
+      int dext = 0;
+      for (int e = sb + lane; e < se; e += 32) {
+        const int u = A.tgt[e];
+        const bool um = mstamp[u] == cur_stamp;
+        const int ou = um ? opart[u] : A.part[u];
+        const int nu = um ? A.dest[u] : ou;
+        const long long dd = cdist(s_dbit, nc2, T.code[nu]) - cdist(s_dbit, oc, T.code[ou]);
+        acc += (long long)A.w[e] * dd * (um ? 1 : 2);
+        if (ext) {
+          const int dx = (int)(nv != nu) - (int)(ov != ou);
+          dext += dx;
+          if (!um && dx) atomicAdd(&ext[u], dx);
+        }
+      }
+      dext = warp_sum_i(dext);
+      if (ext && lane == 0 && dext) atomicAdd(&ext[v], dext);
+    }
+    __syncthreads();  // s_pre / s_wsum reused by the next batch
+  }
+  return acc;
 }
 
 template <int VW>
@@ -760,6 +833,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           opart[v] = A.part[v];
         }
         wq_push(qa, m, v, lmov, cnt + C_MOV);
+        if (A.hconn)
+          warp_append(m && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall, cnt + C_WIDE);
       }
       wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
@@ -1086,6 +1161,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           A.dest[v] = A.rtgt[v];
         }
         wq_push(qa, take, v, lmov, cnt + C_MOV);
+        if (A.hconn)
+          warp_append(take && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall,
+                      cnt + C_WIDE);
       }
       const long long nc = cnt[C_CAND];
       for (long long b0 = gt - lane; b0 < nc; b0 += GT) {
@@ -1102,6 +1180,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           }
         }
         wq_push(qa, take, v, lmov, cnt + C_MOV);
+        if (A.hconn)
+          warp_append(take && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall,
+                      cnt + C_WIDE);
       }
       wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
@@ -1122,7 +1203,9 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           const int ov = opart[v], nv = A.dest[v];
           const unsigned long long oc = T.code[ov], nc2 = T.code[nv];
           int dext = 0;
-          for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
+          const int ea = A.off[v], eb = A.off[v + 1];
+          const bool split = A.hconn && eb - ea > kApplySplitDeg;  // segments below
+          for (int e = ea + li; e < (split ? ea : eb); e += VW) {
             const int u = A.tgt[e];
             const bool um = mstamp[u] == cur_stamp;
             const int ou = um ? opart[u] : A.part[u];
@@ -1149,6 +1232,8 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         }
         acct_warp(s_acct, A_MOV_SLOTS, msl);
       }
+      if (A.hconn && cnt[C_WIDE] > 0)
+        acc += apply_wide(A, T, s_dbit, ext, opart, mstamp, cur_stamp, cnt[C_WIDE], gw, NW);
       block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
       if (balanced_now) {
         for (long long i = gt; i < nc; i += GT) A.gkey[A.lcand[i]] = kGainNone;

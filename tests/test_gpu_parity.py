@@ -187,12 +187,14 @@ def test_wide_tables_match_oracle(D, h, d):
     assert np.array_equal(np_(tm).astype(bool), p.to_move)
 
 
-def test_wide_tables_refine_matches_oracle(D, mode):
+@pytest.mark.parametrize("scale", [12, 15])
+def test_wide_tables_refine_matches_oracle(D, mode, scale):
     """Alg. 4 end to end on an R-MAT graph under a random k = 256 mapping
-    (hub rows listed for the grid, wide tables, rebalancing): the best
+    (hub rows listed for the grid, wide tables, rebalancing; at scale 15
+    hub movers > 2048 slots applied by grid-wide segments): the best
     mapping equals the reference's refine (refinement.py:389-464)."""
     from paper_2510_12196_b200.generators import gen_rmat
-    g = gen_rmat(12)
+    g = gen_rmat(scale)
     h, d = (4, 8, 8), (1, 10, 100)
     t = O.OTopology(h, d)
     a = np.random.default_rng(9).permutation(g.n) % t.k  # balanced, random
