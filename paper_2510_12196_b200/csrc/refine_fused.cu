@@ -113,6 +113,8 @@ struct FusedArgs {
   int hub_deg;         // rows longer than this are hubs (cooperative grids with hconn only)
   int list_deg;        // rows longer than this are listed for the grid (<= hub_deg)
   int hub_phases;      // bit 0: first filter, bit 1: rebalance candidates
+  long long* wctr;     // [1] wide LP candidates listed (in lhub) by the second filter
+  long long* wacc;     // [cap] their future gains, accumulated by segments (zeroed)
   double l_max, sigma, phi, jet_c;
   int jet, rho, i_max, i_w_max;
   unsigned long long seed;
@@ -391,6 +393,68 @@ __device__ __forceinline__ void hub_phase(const FusedArgs& A, const GridBarrier&
     grid.sync();
   }
   if (nb == 0) grid.sync();
+}
+
+// second filter of the listed wide LP candidates (A.lhub[0, nw)): their
+// future gains (refinement.py:246-262) summed by kHubSeg-slot segments over
+// every warp of the grid into A.wacc
+__device__ __forceinline__ void sf_wide_accumulate(const FusedArgs& A, const Topo& T,
+                                                   const long long* s_dbit, long long nw,
+                                                   long long gw, long long NW) {
+  __shared__ int s_pre[kHubBatch + 1];
+  __shared__ int s_wsum[kFusedWarps];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  for (long long c0 = 0; c0 < nw; c0 += kHubBatch) {
+    const int nhc = (int)min((long long)kHubBatch, nw - c0);
+    int segs = 0;
+    if ((int)threadIdx.x < nhc) {
+      const int v = A.lhub[c0 + threadIdx.x];
+      segs = (A.off[v + 1] - A.off[v] + kHubSeg - 1) / kHubSeg;
+    }
+    int incl = segs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int base = 0, tot = 0;
+    for (int w = 0; w < kFusedWarps; ++w) {
+      if (w < warp) base += s_wsum[w];
+      tot += s_wsum[w];
+    }
+    if ((int)threadIdx.x < nhc) s_pre[threadIdx.x] = base + incl - segs;
+    if (threadIdx.x == 0) s_pre[nhc] = tot;
+    __syncthreads();
+    for (long long j = gw; j < tot; j += NW) {
+      int lo = 0, hi = nhc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pre[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      const int v = A.lhub[c0 + lo];
+      const int e1 = A.off[v + 1];
+      const int sb = A.off[v] + (int)(j - s_pre[lo]) * kHubSeg, se = min(e1, sb + kHubSeg);
+      const long long gv = A.gkey[v];
+      const unsigned long long oc = T.code[A.part[v]];
+      const unsigned long long dc = T.code[A.dest[v]];
+      long long fut = 0;
+      for (int e = sb + lane; e < se; e += 32) {
+        const int u = A.tgt[e];
+        const long long gu = A.gkey[u];
+        const bool earlier = gu > gv || (gu == gv && u < v);
+        const unsigned long long pc = T.code[earlier ? A.dest[u] : A.part[u]];
+        fut += (long long)A.w[e] * (cdist(s_dbit, oc, pc) - cdist(s_dbit, dc, pc));
+      }
+      fut = warp_sum_ll(fut);
+      if (lane == 0 && fut)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.wacc + c0 + lo),
+                  (unsigned long long)fut);
+    }
+    __syncthreads();  // s_pre / s_wsum reused by the next batch
+  }
 }
 
 // the move application of the listed wide movers (A.lsmall[0, nw)), by
@@ -810,12 +874,15 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         const int v = live ? A.lcand[idx] : 0;
         long long fut = 0;
         int csl = 0;
+        // rows over kApplySplitDeg slots: decided after the grid-wide
+        // segment pass below (hub mode only)
+        const bool wide = live && A.hconn && A.off[v + 1] - A.off[v] > kApplySplitDeg;
         if (live) {
           const long long gv = A.gkey[v];
           const unsigned long long oc = T.code[A.part[v]];
           const unsigned long long dc = T.code[A.dest[v]];
           if (li == 0) csl = A.off[v + 1] - A.off[v];
-          for (int e = A.off[v] + li; e < A.off[v + 1]; e += VW) {
+          for (int e = A.off[v] + li; e < (wide ? 0 : A.off[v + 1]); e += VW) {
             int u = A.tgt[e];
             long long gu = A.gkey[u];
             bool earlier = gu > gv || (gu == gv && u < v);
@@ -826,18 +893,40 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         }
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) fut += __shfl_xor_sync(0xffffffffu, fut, o);
-        const bool m = live && li == 0 && fut >= 0;
+        const bool m = live && !wide && li == 0 && fut >= 0;
         acct_warp(s_acct, A_CAND_SLOTS, csl);
         if (m) {
           mstamp[v] = cur_stamp;
           opart[v] = A.part[v];
         }
         wq_push(qa, m, v, lmov, cnt + C_MOV);
-        if (A.hconn)
-          warp_append(m && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall, cnt + C_WIDE);
+        if (A.hconn) warp_append(wide && li == 0, v, A.lhub, A.wctr);
       }
       wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
+      if (A.hconn) {
+        const long long nwc = __ldcg(A.wctr);
+        if (nwc > 0) {  // wide candidates: future gains by segments, then decide
+          sf_wide_accumulate(A, T, s_dbit, nwc, gw, NW);
+          grid.sync();
+          for (long long b0 = gt - lane; b0 < nwc; b0 += GT) {
+            const long long i = b0 + lane;
+            const int v = i < nwc ? A.lhub[i] : 0;
+            bool m = false;
+            if (i < nwc) {
+              m = (long long)__ldcg(reinterpret_cast<unsigned long long*>(A.wacc + i)) >= 0;
+              A.wacc[i] = 0;
+              if (m) {
+                mstamp[v] = cur_stamp;
+                opart[v] = A.part[v];
+              }
+            }
+            warp_append(m, v, lmov, cnt + C_MOV);
+            warp_append(m, v, A.lsmall, cnt + C_WIDE);  // applied by segments too
+          }
+          grid.sync();
+        }
+      }
       PHASE_MARK(3);
     } else {
       // ---- K11 weak rebalance candidates (refinement.py:273-309)
@@ -1194,6 +1283,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     {
       const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
       long long acc = 0;
+      if (A.hconn && BX == 0 && threadIdx.x == 0) *A.wctr = 0;  // read before the last barrier
       for (long long ib = gw * GPW; ib < nm; ib += NW * GPW) {
         const long long idx = ib + gi;
         int msl = 0;
@@ -1720,7 +1810,10 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.ptime = nullptr;
   // hub rows: grid-wide evaluation (cooperative grids only)
   DBuf<int> hconn;
+  DBuf<long long> wide;
   A.hconn = nullptr;
+  A.wctr = nullptr;
+  A.wacc = nullptr;
   A.lhub = nullptr;
   A.lbig = nullptr;
   A.hub_deg = 0;
@@ -1731,6 +1824,12 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
     hconn = DBuf<int>((size_t)kHubBatch * k, s);
     GIM_CUDA(cudaMemsetAsync(hconn.get(), 0, sizeof(int) * (size_t)kHubBatch * k, s));
     A.hconn = hconn.get();
+    // wide LP candidates: at most m2 / kApplySplitDeg rows
+    const size_t wcap = (size_t)(g.m2 / kApplySplitDeg + 2);
+    wide = DBuf<long long>(wcap + 1, s);
+    GIM_CUDA(cudaMemsetAsync(wide.get(), 0, sizeof(long long) * (wcap + 1), s));
+    A.wctr = wide.get();
+    A.wacc = wide.get() + 1;
     A.lhub = fb.lheavy;
     A.lbig = fb.lmov1;
     A.hub_deg = hub_deg();
@@ -1883,6 +1982,8 @@ void refine_smem_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, FusedSta
     A.vc_steps = vc_steps();
     A.ptime = nullptr;
     A.hconn = nullptr;
+    A.wctr = nullptr;
+    A.wacc = nullptr;
     A.lhub = nullptr;
     A.lbig = nullptr;
     A.hub_deg = 0;
@@ -2027,6 +2128,8 @@ void refine_cluster_batch(std::vector<SmemRefineJob>& jobs, const Topo& t, Fused
     A.solo = 0;
     A.ptime = nullptr;
     A.hconn = nullptr;
+    A.wctr = nullptr;
+    A.wacc = nullptr;
     A.lhub = nullptr;
     A.lbig = nullptr;
     A.hub_deg = 0;
