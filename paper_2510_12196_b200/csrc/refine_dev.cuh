@@ -406,12 +406,13 @@ __device__ __forceinline__ VertexEval eval_table_grouped(int* tab, const int* lb
   return r;
 }
 
+template <bool WIDE = true>
 __device__ __forceinline__ VertexEval eval_table(const WarpTable& wt, int s, int own,
                                                  const Topo& t, const long long* s_dbit,
                                                  const unsigned char* allowed) {
   // wide tables: O(L) per candidate (leaves wt.tab as a prefix sum; callers
   // use only lb / lw afterwards and the next table build re-zeroes it)
-  if (s > kGroupedMinS)
+  if (WIDE && s > kGroupedMinS)
     return eval_table_grouped(wt.tab, wt.lb, wt.lw, s, own, t.k, t.L, topo_lv(t), allowed);
   const int lane = lane_id();
   const unsigned long long oc = t.code[own];

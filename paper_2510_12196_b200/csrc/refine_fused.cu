@@ -526,7 +526,11 @@ __device__ __forceinline__ long long apply_wide(const FusedArgs& A, const Topo& 
   return acc;
 }
 
-template <int VW>
+// HUB: the skewed-degree machinery (warp entry sweeps of long rows, listed
+// hub rows, grouped wide-table scoring, grid-segmented second filter and
+// move application) is compiled in; the HUB = false instance (graphs without
+// rows over kSweepWarpDeg slots: rgg, grids) carries none of that code
+template <int VW, bool HUB>
 __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   // SURVEY §8(d) accounting (Acct, common.cuh): warp-aggregated (REDUX) into
   // this CTA's shared counters, added to the FusedState once at exit
@@ -610,7 +614,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       const long long v = vb + lane;
       const bool live = v < n;
       const int e0 = live ? A.off[v] : 0, e1 = live ? A.off[v + 1] : 0;
-      const bool wide = e1 - e0 > kSweepWarpDeg;
+      const bool wide = HUB && e1 - e0 > kSweepWarpDeg;
       if (live && !wide) {
         const int pv = A.part[v];
         const unsigned long long pc = T.code[pv];
@@ -813,7 +817,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           own = A.part[v];
           e0 = A.off[v];
           e1 = A.off[v + 1];
-          if (A.hconn && (A.hub_phases & 1) && e1 - e0 > A.list_deg) {
+          if ((HUB && A.hconn) && (A.hub_phases & 1) && e1 - e0 > A.list_deg) {
             // evaluated by the grid after this pass
             if (e1 - e0 > A.hub_deg) big = true;
             else hub = true;
@@ -835,7 +839,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           const int u = __shfl_sync(0xffffffffu, v, l);
           const int ou = __shfl_sync(0xffffffffu, own, l);
           const int sz = warp_build_table(wt, k, A.off[u], A.off[u + 1], A.tgt, A.w, A.part);
-          const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, nullptr);
+          const VertexEval q = eval_table<HUB>(wt, sz, ou, T, s_dbit, nullptr);
           if (lane == l) {
             r.best_b = q.best_b;
             r.best_gain = q.best_gain;
@@ -860,7 +864,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       wq_flush(qa, A.lcand, cnt + C_CAND);
       wq_flush(qb, A.lhub, cnt + C_HUB);
       grid.sync();
-      if (A.hconn && (A.hub_phases & 1))  // rows listed by this first filter
+      if ((HUB && A.hconn) && (A.hub_phases & 1))  // rows listed by this first filter
         hub_phase<false>(A, grid, cnt, gw, NW, wt, k, T, s_dbit, nullptr, nullptr, 0, 0, NC);
       PHASE_MARK(2);
       // every CTA has read the previous iteration's counters by now (they
@@ -876,7 +880,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         int csl = 0;
         // rows over kApplySplitDeg slots: decided after the grid-wide
         // segment pass below (hub mode only)
-        const bool wide = live && A.hconn && A.off[v + 1] - A.off[v] > kApplySplitDeg;
+        const bool wide = live && (HUB && A.hconn) && A.off[v + 1] - A.off[v] > kApplySplitDeg;
         if (live) {
           const long long gv = A.gkey[v];
           const unsigned long long oc = T.code[A.part[v]];
@@ -900,11 +904,11 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           opart[v] = A.part[v];
         }
         wq_push(qa, m, v, lmov, cnt + C_MOV);
-        if (A.hconn) warp_append(wide && li == 0, v, A.lhub, A.wctr);
+        if ((HUB && A.hconn)) warp_append(wide && li == 0, v, A.lhub, A.wctr);
       }
       wq_flush(qa, lmov, cnt + C_MOV);
       grid.sync();
-      if (A.hconn) {
+      if ((HUB && A.hconn)) {
         const long long nwc = __ldcg(A.wctr);
         if (nwc > 0) {  // wide candidates: future gains by segments, then decide
           sf_wide_accumulate(A, T, s_dbit, nwc, gw, NW);
@@ -1003,7 +1007,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         } else if (live) {
           const int e0 = A.off[v], e1 = A.off[v + 1];
           osl = e1 - e0;
-          if (A.hconn && (A.hub_phases & 2) && e1 - e0 > A.list_deg) {
+          if ((HUB && A.hconn) && (A.hub_phases & 2) && e1 - e0 > A.list_deg) {
             // evaluated by the grid after this pass
             if (e1 - e0 > A.hub_deg) big = true;
             else hub = true;
@@ -1024,7 +1028,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           const int ou = __shfl_sync(0xffffffffu, own, l);
           const int tbl = __shfl_sync(0xffffffffu, tb, l);
           const int sz = warp_build_table(wt, k, A.off[u], A.off[u + 1], A.tgt, A.w, A.part);
-          const VertexEval q = eval_table(wt, sz, ou, T, s_dbit, elig);
+          const VertexEval q = eval_table<HUB>(wt, sz, ou, T, s_dbit, elig);
           long long ctb = 0;
           if (q.best_b < 0 && tbl >= 0) ctb = cost_table(wt, sz, tbl, T, s_dbit);  // warp-uniform
           if (lane == l) {
@@ -1075,7 +1079,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
       // the lock set is cleared on every rebalance pass (refinement.py:425):
       // lock_stamp becomes 0 at the end of this iteration
       grid.sync();
-      if (A.hconn && (A.hub_phases & 2))  // rows listed by this candidate pass
+      if ((HUB && A.hconn) && (A.hub_phases & 2))  // rows listed by this candidate pass
         hub_phase<true>(A, grid, cnt, gw, NW, wt, k, T, s_dbit, elig, elist, s_nelig,
                         C.pass_counter, NC);
       PHASE_MARK(5);
@@ -1250,7 +1254,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           A.dest[v] = A.rtgt[v];
         }
         wq_push(qa, take, v, lmov, cnt + C_MOV);
-        if (A.hconn)
+        if ((HUB && A.hconn))
           warp_append(take && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall,
                       cnt + C_WIDE);
       }
@@ -1269,7 +1273,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           }
         }
         wq_push(qa, take, v, lmov, cnt + C_MOV);
-        if (A.hconn)
+        if ((HUB && A.hconn))
           warp_append(take && A.off[v + 1] - A.off[v] > kApplySplitDeg, v, A.lsmall,
                       cnt + C_WIDE);
       }
@@ -1283,7 +1287,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
     {
       const long long nm = cnt[C_MOV], nc = cnt[C_CAND];
       long long acc = 0;
-      if (A.hconn && BX == 0 && threadIdx.x == 0) *A.wctr = 0;  // read before the last barrier
+      if ((HUB && A.hconn) && BX == 0 && threadIdx.x == 0) *A.wctr = 0;  // read before the last barrier
       for (long long ib = gw * GPW; ib < nm; ib += NW * GPW) {
         const long long idx = ib + gi;
         int msl = 0;
@@ -1294,7 +1298,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
           const unsigned long long oc = T.code[ov], nc2 = T.code[nv];
           int dext = 0;
           const int ea = A.off[v], eb = A.off[v + 1];
-          const bool split = A.hconn && eb - ea > kApplySplitDeg;  // segments below
+          const bool split = (HUB && A.hconn) && eb - ea > kApplySplitDeg;  // segments below
           for (int e = ea + li; e < (split ? ea : eb); e += VW) {
             const int u = A.tgt[e];
             const bool um = mstamp[u] == cur_stamp;
@@ -1322,7 +1326,7 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
         }
         acct_warp(s_acct, A_MOV_SLOTS, msl);
       }
-      if (A.hconn && cnt[C_WIDE] > 0)
+      if ((HUB && A.hconn) && cnt[C_WIDE] > 0)
         acc += apply_wide(A, T, s_dbit, ext, opart, mstamp, cur_stamp, cnt[C_WIDE], gw, NW);
       block_sum_atomic<kFusedBlock>(acc, cnt + C_DJ);
       if (balanced_now) {
@@ -1430,16 +1434,16 @@ __device__ __forceinline__ void refine_body(const FusedArgs& A) {
   }
 }
 
-template <int VW>
+template <int VW, bool HUB>
 __global__ void __launch_bounds__(kFusedBlock, kFusedMinBlocks) k_refine_fused(FusedArgs A) {
-  refine_body<VW>(A);
+  refine_body<VW, HUB>(A);
 }
 
 // one thread-block cluster per independent refinement (batched launch)
 template <int VW>
 __global__ void __launch_bounds__(kFusedBlock, kClusterMinBlocks) k_refine_cluster_batch(const FusedArgs* args,
                                                                       int csize) {
-  refine_body<VW>(args[blockIdx.x / csize]);
+  refine_body<VW, false>(args[blockIdx.x / csize]);
 }
 
 // Shared-memory-resident refinement of a small graph: ONE CTA copies the
@@ -1507,7 +1511,7 @@ __device__ __forceinline__ void refine_smem_run(const FusedArgs& A) {
     SA.bar_mode = 0;
   }
   __syncthreads();
-  refine_body<VW>(SA);
+  refine_body<VW, false>(SA);
   __syncthreads();
   const bool yielded = A.st->status != 0;  // strong pass due: the host needs everything
   for (int v = threadIdx.x; v < n; v += blockDim.x) {
@@ -1611,9 +1615,14 @@ static int coop_max_blocks(size_t smem) {
   if (it != cache.end()) return it->second;
   int sms = 0, per = 0;
   GIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  raise_dyn_smem_limit((const void*)k_refine_fused<VW>);
-  GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW>, kFusedBlock,
-                                                         smem));
+  raise_dyn_smem_limit((const void*)k_refine_fused<VW, false>);
+  raise_dyn_smem_limit((const void*)k_refine_fused<VW, true>);
+  int per2 = 0;
+  GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine_fused<VW, false>,
+                                                         kFusedBlock, smem));
+  GIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_refine_fused<VW, true>,
+                                                         kFusedBlock, smem));
+  per = std::min(per, per2);
   (void)sms;
   const int r = std::max(1, per);
   cache.emplace(key, r);
@@ -1847,11 +1856,13 @@ bool refine_fused_run(const RefineLevel& L, const Topo& t, int* part, long long*
   A.seed = cfg.seed;
   void* args[] = {&A};
   void* fn = nullptr;
+  // rows over kSweepWarpDeg slots (or unknown maximum degree): the HUB instance
+  const bool hubk = A.hconn != nullptr || g.maxdeg < 0 || g.maxdeg > kSweepWarpDeg;
   switch (L.vw) {
-    case 4: fn = (void*)k_refine_fused<4>; break;
-    case 8: fn = (void*)k_refine_fused<8>; break;
-    case 16: fn = (void*)k_refine_fused<16>; break;
-    default: fn = (void*)k_refine_fused<32>; break;
+    case 4: fn = hubk ? (void*)k_refine_fused<4, true> : (void*)k_refine_fused<4, false>; break;
+    case 8: fn = hubk ? (void*)k_refine_fused<8, true> : (void*)k_refine_fused<8, false>; break;
+    case 16: fn = hubk ? (void*)k_refine_fused<16, true> : (void*)k_refine_fused<16, false>; break;
+    default: fn = hubk ? (void*)k_refine_fused<32, true> : (void*)k_refine_fused<32, false>; break;
   }
   static const bool trace = std::getenv("GIM_TRACE_REFINE") != nullptr;
   cudaEvent_t te[2];
