@@ -1137,7 +1137,9 @@ void extract_subgraphs(const DevGraph& g, const int* part, int parts,
     int e0 = hoff[v0], e1 = hoff[v1];
     OwnedGraph& sg = subs[j];
     sg.n = nj;
-    sg.maxdeg = -1;
+    int md = 0;  // exact longest row (offsets are on the host anyway)
+    for (int v = v0; v < v1; ++v) md = std::max(md, hoff[(size_t)v + 1] - hoff[(size_t)v]);
+    sg.maxdeg = md;
     sg.m2 = e1 - e0;
     sg.off = DBuf<int>((size_t)nj + 1, s);
     sg.tgt = DBuf<int>((size_t)std::max(e1 - e0, 1), s);
