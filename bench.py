@@ -624,7 +624,7 @@ def main():
     ap.add_argument("--logn", type=int, default=22)
     ap.add_argument("--replica-jobs", type=int, default=64,
                     help="config 5: seeds mapped by the replica runner (0: skip)")
-    ap.add_argument("--concurrency", type=int, default=3,
+    ap.add_argument("--concurrency", type=int, default=4,
                     help="config 5: concurrent maps per GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--same-config", type=int, default=1,
